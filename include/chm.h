@@ -1,0 +1,271 @@
+/*
+ * chm.h -- C ABI of the B200-native Chameleon swap hot path (arxiv 2509.11076).
+ *
+ * Two parts (BASELINE.json north_star):
+ *   (X) policy execution: descriptor-driven batched swap-out / swap-in of activation blocks
+ *       between HBM and mapped pinned host memory on a dedicated swap stream, event-fenced
+ *       against the compute stream, fired at operator indices of the
+ *       profiled eager operator sequence;
+ *   (V) policy evaluation: replay of the operator sequence's alloc/free/swap events for many
+ *       candidate swap sets -> per-operator footprint, peak HBM, estimated stall, argmin
+ *       (P:315-340 simulator, P:421 best-of-n).
+ * Host steps (recording, sequence-change detection, trace build, triggering) sit behind the
+ * same ABI.  Citations "P:<line>" are PAPER.md lines; "§8(c).k" are SURVEY.md readings,
+ * restated in DESIGN.md §"Readings".
+ *
+ * Conventions (all calls):
+ *   - Every call returns chm_status: CHM_OK (0) or a negative code.  No C++ exception
+ *     crosses the ABI.  chm_last_error() returns a thread-local message for the last failure.
+ *   - Pointers marked "host" are host memory; "device" are CUDA device pointers (or mapped
+ *     pinned host pointers usable by the device).  Inputs are borrowed for the duration of the
+ *     call; the library copies what it keeps.
+ *   - A chm_ctx is single-owner and not thread-safe: one ctx per device / rank.
+ *   - No call on the hot path synchronises the host with the device.
+ */
+#ifndef CHM_H
+#define CHM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t chm_status;
+enum {
+  CHM_OK = 0,
+  CHM_E_INVAL = -1,      /* invalid argument; *err_index names the offending item if given */
+  CHM_E_PARSE = -2,      /* reserved (trace files)                                           */
+  CHM_E_STATE = -3,      /* call not valid in the ctx's current state                        */
+  CHM_E_NOMEM = -4,      /* host or device allocation failed                                  */
+  CHM_E_CUDA = -5,       /* a CUDA runtime call failed; message has cudaGetErrorString        */
+  CHM_E_INFEASIBLE = -6, /* reserved for the greedy generator (Algo. 2 "Raise Error")  */
+  CHM_E_NOKERNEL = -7    /* the library was built without a kernel image for this device      */
+};
+
+typedef enum { CHM_FWD = 0, CHM_BWD = 1, CHM_OPT = 2 } chm_phase;
+typedef enum { CHM_WARMUP = 0, CHM_GENPOLICY = 1, CHM_STABLE = 2 } chm_stage; /* Algo. 1  */
+
+typedef struct chm_ctx chm_ctx;
+typedef struct chm_trace chm_trace;
+
+/* ------------------------------------------------------------------------------ config */
+typedef struct {
+  uint32_t m, n;              /* Algo. 1 stable iterations before GenPolicy / Stable;
+                                 defaults 2, 5                                      */
+  double len_tol, cos_tol;    /* Algo. 1 thresholds, defaults 0.05 / 0.95 */
+  uint32_t cos_mode;          /* 0: positional cosine of zero-padded token vectors (default,
+                                 reading Q1); 1: cosine of token-count histograms    */
+  uint32_t detect_bytes;      /* 1: also require |sum bytes - prev| / max < len_tol (reading
+                                 Q4, opt-in); 0: paper-literal (default)                     */
+  int32_t device;             /* CUDA device ordinal this ctx drives; -1: host-only ctx
+                                 (profiler, detection, trace build and executor tables only;
+                                 eval / swap calls return CHM_E_STATE)                       */
+  uint64_t host_arena_bytes;  /* pinned + mapped host arena for swapped blocks (0: none)      */
+  uint32_t swap_ctas;         /* CTAs of the swap copy kernel (0: default, 16)               */
+  uint32_t eval_ctas_per_sm;  /* resident CTAs per SM for the replay kernel (0: auto)        */
+  uint32_t match_window;      /* executor: max |op - a_t| for a feature match (0: half the
+                                 smallest FWD logical layer)                                 */
+} chm_config;
+
+/* fills the paper's defaults */
+void chm_config_default(chm_config *cfg);
+
+chm_status chm_create(const chm_config *cfg, chm_ctx **out);
+void chm_destroy(chm_ctx *ctx);
+const char *chm_last_error(void);
+/* library version string and the CUDA arch it was compiled for ("sm_100a") */
+const char *chm_build_info(void);
+
+/* ---------------------------------------------------------------- profiler hook (a1, a8) */
+/* Lightweight-mode tokenisation: an integer per operator name, 1, 2, ... in order
+ * of first appearance within this ctx; stable for the ctx lifetime. */
+chm_status chm_tokenize(chm_ctx *ctx, const char *name, int32_t *token);
+
+typedef struct {
+  uint64_t id;     /* storage data_ptr this iteration (may be reused after a free)   */
+  int64_t nbytes;  /* allocated block bytes                                          */
+  uint8_t dtype;   /* small dtype code (feature field)                         */
+} chm_tensor_ref;
+
+typedef struct {
+  int32_t token;                 /* >= 1                                               */
+  uint8_t phase;                 /* chm_phase; phases never interleave: FWD* BWD* OPT* */
+  uint32_t n_in, n_out, n_free;
+  const chm_tensor_ref *in;      /* host: tensors read by the op                       */
+  const chm_tensor_ref *out;     /* host: tensors allocated by the op                  */
+  const uint64_t *freed;         /* host: ids whose refcount reached 0 after the op    */
+  int64_t live_bytes;            /* measured allocator bytes at the op, or -1          */
+} chm_op_record;
+
+typedef struct { uint64_t dev, host_off, nbytes; } chm_swap_desc; /* 24 B */
+
+typedef struct {                 /* library-owned; valid until the next chm_record_op  */
+  uint32_t n_swap_out;
+  const chm_swap_desc *swap_out; /* issue (chm_swap_out) right after this op           */
+  const uint32_t *swap_out_item;
+  uint32_t n_release;
+  const uint32_t *release_item;  /* policy items whose device block may be reclaimed after
+                                    this op, once the swap stream reached the out batch
+                                    (chm_item_wait on the compute stream)      */
+  uint32_t n_swap_in;
+  const chm_swap_desc *swap_in;  /* dev == 0: the caller allocates nbytes on the compute
+                                    stream, sets dev, then calls chm_swap_in   */
+  const uint32_t *swap_in_item;
+  uint32_t n_wait;
+  const uint32_t *wait_item;     /* compute must wait for these swap-ins before this op */
+} chm_actions;
+
+/* Records one dispatched operator (P:219 hook).  Lightweight mode appends the token
+ * (P:221); Detailed mode (stage GenPolicy, or forced with chm_set_detailed) also records
+ * tensors, frees and live bytes.  If a policy is installed, App. A tensor
+ * features are updated and the op's swap actions are returned in *actions (nullable). */
+chm_status chm_record_op(chm_ctx *ctx, const chm_op_record *op, chm_actions *actions);
+/* force (1) or stop forcing (0) Detailed recording from the next chm_record_op on */
+chm_status chm_set_detailed(chm_ctx *ctx, int32_t detailed);
+
+/* Ends the iteration: Algo. 1 on this iteration's token sequence vs the
+ * previous one.  t_iter_s is the measured iteration time (kept as Eq. 1's T_iter if the
+ * iteration was recorded in Detailed mode).  Outputs are nullable. */
+chm_status chm_detect_seq_change(chm_ctx *ctx, double t_iter_s, chm_stage *stage,
+                                 int32_t *changed, double *len_diff, double *cos_sim);
+
+/* ----------------------------------------------------------------------- trace build (a3) */
+typedef struct {
+  int64_t hbm_budget;          /* bytes; excess = max(0, peak - budget)                 */
+  int64_t static_bytes;        /* M_0: bytes live at iteration start                    */
+  double t_iter_s;             /* T_iter of Eq. 1; <= 0: the recorded iteration's time */
+  double bw_bytes_per_s;       /* B of Eq. 3; must be > 0                   */
+  uint32_t groups_fwd, groups_bwd; /* logical layers per phase, >= 1        */
+  double omega;                /* overlap factor on layer budgets, 1.0 default  */
+} chm_trace_params;
+
+/* Builds the evaluation trace from the last iteration recorded in Detailed mode: tensor
+ * table (producer p, free op f, last FWD use a, first BWD use b), no-swap footprint F0,
+ * logical layers with Eq. 1 budgets, solo swap timing r_t / s_t, the
+ * swappable set in mask-bit order (ascending a_t, then production order) and the default
+ * SEEDED base (swappable tensors whose window contains the first argmax of F0).  Tables are
+ * uploaded to the ctx's device.  The trace is caller-owned: chm_trace_free. */
+chm_status chm_trace_build(chm_ctx *ctx, const chm_trace_params *params, chm_trace **out);
+void chm_trace_free(chm_trace *t);
+
+typedef struct {
+  uint32_t n_ops, n_tensors, n_swappable, n_layers, mask_words;
+  int64_t peak0;
+  uint32_t argmax0;
+  int64_t budget;
+} chm_trace_info;
+chm_status chm_trace_get_info(const chm_trace *t, chm_trace_info *info);
+/* Copies host-side tables out (each pointer nullable): f0[n_ops]; per swappable k:
+ * tensor[k] (production-order tensor index), nbytes[k], r[k], s[k], lin[k], lout[k];
+ * per layer: start[l], count[l], bud[l]; base[mask_words]. */
+chm_status chm_trace_tables(const chm_trace *t, int64_t *f0, uint32_t *tensor, int64_t *nbytes,
+                            int32_t *r, int32_t *s, int32_t *lin, int32_t *lout,
+                            int32_t *lay_start, int32_t *lay_count, double *bud, uint64_t *base);
+
+/* ------------------------------------------------------------- policy evaluation (a4-a7) */
+typedef enum {
+  CHM_CAND_EXHAUSTIVE = 0, /* swap set of candidate c = bits of c; requires K <= 63        */
+  CHM_CAND_SEEDED = 1,     /* bit t = base[t] ^ [mix(seed ^ mix(c*K + t)) < flip_thr],
+                              mix = splitmix64 finaliser                */
+  CHM_CAND_MASKS = 2       /* device masks [count][mask_words], little-endian u64 words  */
+} chm_cand_kind;
+
+typedef struct {
+  chm_cand_kind kind;
+  uint64_t first_index, count; /* global candidate ids [first_index, first_index + count)  */
+  uint64_t seed, flip_thr;     /* SEEDED                                                  */
+  const uint64_t *base_mask;   /* SEEDED, host, mask_words words; NULL: the trace's base  */
+  const uint64_t *masks;       /* MASKS, device [count][mask_words]                       */
+} chm_candidates;
+
+/* argmin key, compared lexicographically (excess, stall, swapped_bytes, index): feasibility
+ * first, then least estimated stall ("best runtime performance"), then least PCIe
+ * traffic, then lowest id -- unique, so any reduction order gives the same winner. */
+typedef struct {
+  int64_t excess;
+  double stall;
+  int64_t swapped_bytes;
+  uint64_t index;
+  int64_t peak;
+} chm_best; /* 40 B */
+
+typedef struct {
+  int64_t *peak;           /* device [count] or NULL                                    */
+  double *stall;           /* device [count] or NULL                                    */
+  int64_t *swapped;        /* device [count] or NULL                                    */
+  int64_t *footprint;      /* device [count][ld] or NULL (full mode: F_P per op)        */
+  uint32_t ld;             /* leading dimension of footprint, >= n_ops, even            */
+  chm_best *best;          /* device, 1 element (required)                              */
+} chm_eval_out;
+
+/* Evaluates candidates on `stream` (enqueue only).  For candidate P:
+ *   F_P[i] = F0[i] - sum_{t in P} S_t [r_t < i < s_t]  (event replay of §8(c).2)
+ *   peak = max_i F_P[i]; stall = sum_l max(0, load_l / B - Bud_l) ascending in l (§8(c).5)
+ * writes the per-candidate outputs and the argmin key of this batch into *best. */
+chm_status chm_eval_policies(chm_ctx *ctx, const chm_trace *t, const chm_candidates *c,
+                             const chm_eval_out *o, cudaStream_t stream);
+/* host: lexicographic min of n keys (e.g. after an all-gather across ranks) */
+chm_status chm_best_reduce(const chm_best *keys, uint32_t n, chm_best *out);
+/* host: the swap set of global candidate `index` as mask words (mask_words u64) */
+chm_status chm_candidate_mask(const chm_trace *t, const chm_candidates *c, uint64_t index,
+                              uint64_t *words);
+
+/* ----------------------------------------------------------- policy install / trigger (a8) */
+/* Installs the swap set `words` of trace t as the active policy: every selected tensor gets
+ * an item {App. A feature key after op a_t, release op r_t, swap-in op s_t, host offset in
+ * the arena}.  Feature tables (top-32 one-hot, 8-bit index) come from the recorded
+ * iteration's token frequencies.  Subsequent chm_record_op calls return the
+ * policy's actions. */
+chm_status chm_policy_install(chm_ctx *ctx, const chm_trace *t, const uint64_t *words);
+typedef struct {
+  uint32_t n_items, n_matched, n_stale, n_collisions, n_demand_swap_in;
+  uint64_t bytes_out, bytes_in;
+} chm_exec_stats;
+chm_status chm_exec_stats_get(chm_ctx *ctx, chm_exec_stats *s);
+
+/* ---------------------------------------------------------------- swap execution (a9-a11) */
+/* The ctx's pinned, device-mapped host arena (cudaHostAllocMapped|Portable). */
+chm_status chm_host_arena(chm_ctx *ctx, void **host_base, uint64_t *bytes);
+
+enum {
+  CHM_SWAP_KERNEL = 0, /* one multi-tensor gather/scatter kernel launch per <= 64 descriptors */
+  CHM_SWAP_CE = 1      /* baseline: one cudaMemcpyAsync per descriptor on the copy engines   */
+};
+
+/* Swap-out: records an event on `compute` after the last enqueued op, makes
+ * `swap` wait on it, copies every descriptor's nbytes from device address dev to
+ * arena + host_off, and records the batch's completion event on `swap`.  *batch receives
+ * the batch id for chm_batch_wait.  Fails with CHM_E_INVAL (+ *err_index) if nbytes == 0,
+ * dev == 0, host_off + nbytes exceeds the arena, or two host ranges of the batch overlap.
+ * The device blocks must not be reused until the batch completes: make the consumer stream
+ * wait with chm_batch_wait (custom recordStream). */
+chm_status chm_swap_out(chm_ctx *ctx, const chm_swap_desc *d, uint32_t n, cudaStream_t compute,
+                        cudaStream_t swap, uint32_t flags, uint64_t *batch, int64_t *err_index);
+/* Swap-in: the mirror, arena + host_off -> dev, fenced the same way. */
+chm_status chm_swap_in(chm_ctx *ctx, const chm_swap_desc *d, uint32_t n, cudaStream_t compute,
+                       cudaStream_t swap, uint32_t flags, uint64_t *batch, int64_t *err_index);
+/* Stream-ordered wait: `stream` waits for batch completion (no host polling).
+ * Batch ids stay valid for the last 4096 batches of the ctx. */
+chm_status chm_batch_wait(chm_ctx *ctx, uint64_t batch, cudaStream_t stream);
+/* Host query (tests / diagnostics only): *done = 1 if the batch completed. */
+chm_status chm_batch_query(chm_ctx *ctx, uint64_t batch, int32_t *done);
+/* Executor helpers for the actions of the last chm_record_op:
+ *   chm_issue_swap_out: one swap-out batch of every pending swap-out item;
+ *   chm_issue_swap_in:  one swap-in batch of every pending swap-in item; dev[j] is the block
+ *                       the caller allocated for actions.swap_in[j] (becomes the tensor's id);
+ *   chm_item_wait:      `stream` waits for the swap-out (swap_in = 0: release before reuse)
+ *                       or swap-in (swap_in = 1: before the first backward use) of `item`. */
+chm_status chm_issue_swap_out(chm_ctx *ctx, cudaStream_t compute, cudaStream_t swap,
+                              uint32_t flags, uint64_t *batch);
+chm_status chm_issue_swap_in(chm_ctx *ctx, const uint64_t *dev, cudaStream_t compute,
+                             cudaStream_t swap, uint32_t flags, uint64_t *batch);
+chm_status chm_item_wait(chm_ctx *ctx, uint32_t item, int32_t swap_in, cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CHM_H */

@@ -1,0 +1,285 @@
+// executor.cpp -- policy install + trigger tables (step a8): App. A multi-feature fuzzy
+// matching, swap-out right after the last FWD use, stream-
+// ordered release at the simulator's completion op (custom recordStream),
+// swap-in pre-triggered at the chosen layer start.
+#include <algorithm>
+#include <climits>
+#include <cstring>
+
+#include "internal.h"
+
+using namespace chm;
+
+static uint64_t splitmix64(uint64_t z) {  // SEEDED candidate decode, SURVEY §8(c).4
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+extern "C" chm_status chm_candidate_mask(const chm_trace *t, const chm_candidates *c,
+                                         uint64_t index, uint64_t *words) {
+  if (!t || !c || !words) CHM_FAIL(CHM_E_INVAL, "chm_candidate_mask: NULL argument");
+  const int32_t K = t->K, W = t->W;
+  std::fill(words, words + W, 0ull);
+  switch (c->kind) {
+    case CHM_CAND_EXHAUSTIVE:
+      if (K > 63) CHM_FAIL(CHM_E_INVAL, "EXHAUSTIVE needs K <= 63");
+      if (W) words[0] = index & ((K == 64) ? ~0ull : ((1ull << K) - 1));
+      return CHM_OK;
+    case CHM_CAND_SEEDED: {
+      const uint64_t *base = c->base_mask ? c->base_mask : t->base.data();
+      for (int32_t k = 0; k < K; k++) {
+        uint64_t bit = (base[k / 64] >> (k % 64)) & 1ull;
+        uint64_t h = splitmix64(c->seed ^ splitmix64(index * uint64_t(K) + uint64_t(k)));
+        bit ^= h < c->flip_thr ? 1ull : 0ull;
+        words[k / 64] |= bit << (k % 64);
+      }
+      return CHM_OK;
+    }
+    default:
+      CHM_FAIL(CHM_E_INVAL, "chm_candidate_mask: MASKS candidates live on the device");
+  }
+}
+
+// App. A tables from the recorded iteration's token frequencies: rank by count descending,
+// ties by first appearance; index = min(rank + 1, 255); one-hot for the 32 most frequent.
+static void feature_tables(const std::vector<int32_t> &tokens, std::vector<uint8_t> &index,
+                           std::vector<uint32_t> &onehot) {
+  int32_t V = 0;
+  for (auto x : tokens) V = std::max(V, x);
+  std::vector<int64_t> cnt(size_t(V) + 1, 0);
+  std::vector<int32_t> first(size_t(V) + 1, -1);
+  for (size_t i = 0; i < tokens.size(); i++) {
+    cnt[tokens[i]]++;
+    if (first[tokens[i]] < 0) first[tokens[i]] = int32_t(i);
+  }
+  std::vector<int32_t> order;
+  for (int32_t v = 0; v <= V; v++) if (cnt[v]) order.push_back(v);
+  std::sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
+    return cnt[x] != cnt[y] ? cnt[x] > cnt[y] : first[x] < first[y];
+  });
+  index.assign(size_t(V) + 1, 0);
+  onehot.assign(size_t(V) + 1, 0);
+  for (size_t rk = 0; rk < order.size(); rk++) {
+    index[order[rk]] = uint8_t(std::min<size_t>(rk + 1, 255));
+    onehot[order[rk]] = rk < 32 ? (1u << rk) : 0u;
+  }
+}
+
+static inline void feature_update(Feature &f, int32_t token, uint8_t dtype, const chm_ctx *ctx) {
+  uint8_t idx = 0;
+  uint32_t oh = 0;
+  if (token >= 0 && size_t(token) < ctx->op_index.size()) {
+    idx = ctx->op_index[token];
+    oh = ctx->op_onehot[token];
+  }
+  f.count += 1;                       // opCount++
+  f.tag |= oh;                        // opTag |= opOneHot
+  f.stack = (f.stack << 8) + idx;     // opCallStack = (opCallStack << 8) + opIndex
+  f.dtype = dtype;
+}
+
+extern "C" chm_status chm_policy_install(chm_ctx *ctx, const chm_trace *t, const uint64_t *words) {
+  if (!ctx || !t || (!words && t->W)) CHM_FAIL(CHM_E_INVAL, "chm_policy_install: NULL argument");
+  std::vector<int32_t> sel;
+  for (int32_t k = 0; k < t->K; k++)
+    if ((words[k / 64] >> (k % 64)) & 1ull) sel.push_back(k);
+  uint64_t need = 0;
+  for (int32_t k : sel) need += (uint64_t(t->sw_S[k]) + 511) & ~uint64_t(511);
+  if (ctx->device >= 0 && need > ctx->arena_bytes)  // a host-only ctx plans offsets only
+    CHM_FAIL(CHM_E_NOMEM, "chm_policy_install: policy needs %llu arena bytes, arena has %llu",
+             (unsigned long long)need, (unsigned long long)ctx->arena_bytes);
+  feature_tables(t->tokens, ctx->op_index, ctx->op_onehot);
+  // feature key of every selected tensor right after op a_t (replay of the recorded uses)
+  std::vector<int32_t> item_of_tensor(size_t(t->T), -1);
+  ctx->items.assign(sel.size(), PolicyItem());
+  uint64_t off = 0;
+  for (size_t j = 0; j < sel.size(); j++) {
+    const int32_t k = sel[j], tid = t->sw_tensor_idx[k];
+    PolicyItem &it = ctx->items[j];
+    it.a = t->a[tid];
+    it.b = t->b[tid];
+    it.r = t->sw_r[k];
+    it.s = t->sw_s[k];
+    it.nbytes = t->sw_S[k];
+    it.host_off = off;
+    off += (uint64_t(it.nbytes) + 511) & ~uint64_t(511);
+    item_of_tensor[tid] = int32_t(j);
+  }
+  std::vector<Feature> feat(size_t(t->T));
+  for (int32_t i = 0; i < t->N; i++) {
+    for (int32_t u = t->use_ptr[i]; u < t->use_ptr[i + 1]; u++) {
+      const int32_t tid = t->use_idx[u];
+      feature_update(feat[tid], t->tokens[i], t->dtype[tid], ctx);
+      const int32_t j = item_of_tensor[tid];
+      if (j >= 0 && ctx->items[j].a == i) ctx->items[j].key = feat[tid];
+    }
+  }
+  // items sharing a key (e.g. the same tensor role in every transformer layer) are consumed
+  // in a_t order: a matching live tensor takes the first untriggered item of its key
+  ctx->key_to_item.clear();
+  ctx->stats = chm_exec_stats{};
+  ctx->stats.n_items = uint32_t(sel.size());
+  for (size_t j = 0; j < ctx->items.size(); j++) ctx->key_to_item[ctx->items[j].key].items.push_back(int32_t(j));
+  // index-keyed tables: actions returned by chm_record_op(op i) happen between op i and i+1
+  const size_t N = size_t(t->N);
+  ctx->release_at.assign(N, {});
+  ctx->swapin_at.assign(N, {});
+  ctx->wait_at.assign(N, {});
+  for (size_t j = 0; j < ctx->items.size(); j++) {
+    const PolicyItem &it = ctx->items[j];
+    ctx->release_at[it.r].push_back(int32_t(j));                       // after op r_t
+    if (it.s >= 1) ctx->swapin_at[it.s - 1].push_back(int32_t(j));     // before op s_t
+    if (it.b >= 1) ctx->wait_at[it.b - 1].push_back(int32_t(j));       // before op b_t
+  }
+  // match window: half the smallest FWD logical layer (so the same role one layer away is never
+  // nearer), unless configured
+  int32_t min_fwd = INT32_MAX;
+  for (size_t l = 0; l < t->lay_n.size(); l++)
+    if (t->lay_type[l] == CHM_FWD) min_fwd = std::min(min_fwd, t->lay_n[l]);
+  ctx->match_window = ctx->cfg.match_window ? int32_t(ctx->cfg.match_window)
+                                            : std::max(1, (min_fwd == INT32_MAX ? 2 : min_fwd) / 2);
+  ctx->live.clear();
+  ctx->op_cursor = 0;
+  ctx->policy_active = true;
+  return CHM_OK;
+}
+
+chm_status executor_on_op(chm_ctx *ctx, const chm_op_record *op, int32_t i) {
+  ctx->act_out.clear(); ctx->act_out_item.clear(); ctx->act_in.clear(); ctx->act_in_item.clear();
+  ctx->act_release.clear(); ctx->act_wait.clear();
+  uint64_t seen[64];
+  uint32_t n_seen = 0;
+  auto visit = [&](const chm_tensor_ref &ref, bool is_out) {
+    for (uint32_t q = 0; q < n_seen && q < 64; q++) if (seen[q] == ref.id) return;
+    if (n_seen < 64) seen[n_seen++] = ref.id;
+    LiveTensor *lt;
+    if (is_out) {
+      lt = &(ctx->live[ref.id] = LiveTensor());
+    } else {
+      lt = &ctx->live[ref.id];
+    }
+    feature_update(lt->f, op->token, ref.dtype, ctx);
+    if (op->phase != CHM_FWD || lt->item >= 0) return;
+    auto m = ctx->key_to_item.find(lt->f);
+    if (m == ctx->key_to_item.end()) return;
+    // App. A's four fields repeat for the same tensor role in every layer of a stacked model,
+    // so position is one more matching feature (the "..." of P:517, reading in DESIGN.md):
+    // take the untriggered item of this key whose recorded a_t is nearest to the current op,
+    // if it lies within the match window.
+    KeyItems &ki = m->second;
+    int32_t j = -1, dist = INT32_MAX;
+    for (int32_t cand : ki.items) {
+      const PolicyItem &c = ctx->items[cand];
+      if (c.state != IT_IDLE) continue;
+      const int32_t dd = c.a > i ? c.a - i : i - c.a;
+      if (dd < dist) { dist = dd; j = cand; }
+    }
+    if (j < 0 || dist > ctx->match_window) { ctx->stats.n_collisions++; return; }
+    PolicyItem &it = ctx->items[j];
+    const uint64_t slot = (uint64_t(it.nbytes) + 511) & ~uint64_t(511);
+    if (uint64_t(ref.nbytes) > slot) return;  // larger than its arena slot: cannot swap
+    it.state = IT_OUT;
+    it.cur_id = ref.id;
+    it.cur_bytes = uint64_t(ref.nbytes);
+    it.has_out = it.has_in = false;
+    lt->item = j;
+    ctx->stats.n_matched++;
+    ctx->act_out.push_back({ref.id, it.host_off, uint64_t(ref.nbytes)});
+    ctx->act_out_item.push_back(uint32_t(j));
+  };
+  for (uint32_t j = 0; j < op->n_in; j++) visit(op->in[j], false);
+  for (uint32_t j = 0; j < op->n_out; j++) visit(op->out[j], true);
+  for (uint32_t j = 0; j < op->n_free; j++) ctx->live.erase(op->freed[j]);
+  if (size_t(i) < ctx->release_at.size()) {
+    for (int32_t j : ctx->release_at[i]) {
+      PolicyItem &it = ctx->items[j];
+      if (it.state != IT_OUT) continue;
+      it.state = IT_RELEASED;
+      ctx->live.erase(it.cur_id);  // the caller drops the device storage after the wait
+      ctx->act_release.push_back(uint32_t(j));
+    }
+    for (int32_t j : ctx->swapin_at[i]) {
+      PolicyItem &it = ctx->items[j];
+      if (it.state != IT_RELEASED) continue;
+      ctx->act_in.push_back({0, it.host_off, it.cur_bytes});
+      ctx->act_in_item.push_back(uint32_t(j));
+    }
+    for (int32_t j : ctx->wait_at[i]) {
+      PolicyItem &it = ctx->items[j];
+      if (it.state == IT_IN) ctx->act_wait.push_back(uint32_t(j));  // s_t < b_t: issued
+    }
+  }
+  ctx->op_cursor = i + 1;
+  return CHM_OK;
+}
+
+void executor_end_iteration(chm_ctx *ctx) {
+  if (!ctx->policy_active) return;
+  for (PolicyItem &it : ctx->items) {
+    if (it.state == IT_IDLE) ctx->stats.n_stale++;  // never matched: diagnostic
+    it.state = IT_IDLE;
+  }
+  ctx->live.clear();
+  ctx->op_cursor = 0;
+}
+
+extern "C" chm_status chm_exec_stats_get(chm_ctx *ctx, chm_exec_stats *s) {
+  if (!ctx || !s) CHM_FAIL(CHM_E_INVAL, "chm_exec_stats_get: NULL argument");
+  *s = ctx->stats;
+  return CHM_OK;
+}
+
+extern "C" chm_status chm_issue_swap_out(chm_ctx *ctx, cudaStream_t compute, cudaStream_t swap,
+                                         uint32_t flags, uint64_t *batch) {
+  if (!ctx) CHM_FAIL(CHM_E_INVAL, "chm_issue_swap_out: NULL ctx");
+  if (ctx->act_out.empty()) { if (batch) *batch = ~0ull; return CHM_OK; }
+  uint64_t b = 0;
+  int64_t err = -1;
+  chm_status st = chm_swap_out(ctx, ctx->act_out.data(), uint32_t(ctx->act_out.size()), compute,
+                               swap, flags, &b, &err);
+  if (st != CHM_OK) return st;
+  for (uint32_t j : ctx->act_out_item) {
+    ctx->items[j].out_batch = b;
+    ctx->items[j].has_out = true;
+    ctx->stats.bytes_out += ctx->items[j].cur_bytes;
+  }
+  ctx->act_out.clear();
+  if (batch) *batch = b;
+  return CHM_OK;
+}
+
+extern "C" chm_status chm_issue_swap_in(chm_ctx *ctx, const uint64_t *dev, cudaStream_t compute,
+                                        cudaStream_t swap, uint32_t flags, uint64_t *batch) {
+  if (!ctx) CHM_FAIL(CHM_E_INVAL, "chm_issue_swap_in: NULL ctx");
+  if (ctx->act_in.empty()) { if (batch) *batch = ~0ull; return CHM_OK; }
+  if (!dev) CHM_FAIL(CHM_E_INVAL, "chm_issue_swap_in: NULL destination list");
+  for (size_t j = 0; j < ctx->act_in.size(); j++) ctx->act_in[j].dev = dev[j];
+  uint64_t b = 0;
+  int64_t err = -1;
+  chm_status st = chm_swap_in(ctx, ctx->act_in.data(), uint32_t(ctx->act_in.size()), compute,
+                              swap, flags, &b, &err);
+  if (st != CHM_OK) return st;
+  for (size_t j = 0; j < ctx->act_in_item.size(); j++) {
+    PolicyItem &it = ctx->items[ctx->act_in_item[j]];
+    it.in_batch = b;
+    it.has_in = true;
+    it.state = IT_IN;
+    it.cur_id = dev[j];
+    LiveTensor &lt = ctx->live[dev[j]];
+    lt.item = int32_t(ctx->act_in_item[j]);
+    ctx->stats.bytes_in += it.cur_bytes;
+  }
+  ctx->act_in.clear();
+  if (batch) *batch = b;
+  return CHM_OK;
+}
+
+extern "C" chm_status chm_item_wait(chm_ctx *ctx, uint32_t item, int32_t swap_in, cudaStream_t stream) {
+  if (!ctx || item >= ctx->items.size()) CHM_FAIL(CHM_E_INVAL, "chm_item_wait: bad item");
+  const PolicyItem &it = ctx->items[item];
+  if (swap_in ? !it.has_in : !it.has_out)
+    CHM_FAIL(CHM_E_STATE, "chm_item_wait: item %u has no %s batch", item, swap_in ? "swap-in" : "swap-out");
+  return chm_batch_wait(ctx, swap_in ? it.in_batch : it.out_batch, stream);
+}

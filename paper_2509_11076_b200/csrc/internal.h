@@ -1,0 +1,201 @@
+// internal.h -- private structures of libchm (product side; never shared with oracle/).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/chm.h"
+
+namespace chm {
+
+// ---------------------------------------------------------------------------- errors
+void set_error(const char *fmt, ...);
+#define CHM_FAIL(code, ...)          \
+  do {                               \
+    ::chm::set_error(__VA_ARGS__);   \
+    return (code);                   \
+  } while (0)
+#define CHM_CUDA(call)                                                                  \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      CHM_FAIL(CHM_E_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+               __LINE__);                                                               \
+  } while (0)
+
+// ---------------------------------------------------------------- detailed record
+struct TensorRec {
+  int64_t nbytes = 0;
+  uint8_t dtype = 0;
+  int32_t producer = -1;  // op index, -1 = live at iteration start
+  int32_t freed = -1;     // op after which the refcount hit 0, -1 = survives
+};
+
+struct IterRecord {
+  std::vector<int32_t> tokens;
+  std::vector<uint8_t> phase;
+  std::vector<int64_t> live_bytes;
+  // per op: CSR of tensor indices it uses (in then out, deduplicated, first-seen order),
+  // produced tensors, freed tensors, and which uses are inputs
+  std::vector<int32_t> use_ptr{0}, use_idx;
+  std::vector<uint8_t> use_is_in;
+  std::vector<int32_t> out_ptr{0}, out_idx;
+  std::vector<int32_t> free_ptr{0}, free_idx;
+  std::vector<TensorRec> tensors;
+  int64_t alloc_bytes = 0;  // total bytes allocated by ops (detect_bytes, reading Q4)
+  double t_iter = 0.0;
+  bool detailed = false;
+  void clear() {
+    tokens.clear(); phase.clear(); live_bytes.clear();
+    use_ptr.assign(1, 0); use_idx.clear(); use_is_in.clear();
+    out_ptr.assign(1, 0); out_idx.clear(); free_ptr.assign(1, 0); free_idx.clear();
+    tensors.clear(); alloc_bytes = 0; t_iter = 0.0; detailed = false;
+  }
+};
+
+// --------------------------------------------------------------------------- executor
+struct Feature {  // App. A
+  uint32_t count = 0, tag = 0;
+  uint8_t dtype = 0;
+  uint64_t stack = 0;
+  bool operator==(const Feature &o) const {
+    return count == o.count && tag == o.tag && dtype == o.dtype && stack == o.stack;
+  }
+};
+struct FeatureHash {
+  size_t operator()(const Feature &f) const {
+    uint64_t h = f.stack * 0x9E3779B97F4A7C15ull;
+    h ^= (uint64_t(f.count) << 32 | f.tag) + 0x7F4A7C15ull + (h << 6) + (h >> 2);
+    return size_t(h ^ f.dtype);
+  }
+};
+
+enum ItemState : uint8_t { IT_IDLE = 0, IT_OUT = 1, IT_RELEASED = 2, IT_IN = 3 };
+
+struct PolicyItem {
+  Feature key;
+  int32_t a = 0, r = 0, s = 0, b = 0;  // recorded op indices
+  int64_t nbytes = 0;
+  uint64_t host_off = 0;
+  // per-iteration state
+  uint8_t state = IT_IDLE;
+  uint64_t cur_id = 0, cur_bytes = 0, out_batch = 0, in_batch = 0;
+  bool has_out = false, has_in = false;
+};
+
+struct KeyItems {
+  std::vector<int32_t> items;  // policy items with this key, ascending a_t
+};
+
+struct LiveTensor {
+  Feature f;
+  int32_t item = -1;  // policy item bound to this storage
+};
+
+// ---------------------------------------------------------------------------- trace
+struct DevTrace {  // device tables for the replay kernel
+  const int64_t *f0 = nullptr;
+  const int64_t *S = nullptr;
+  const int32_t *r1 = nullptr;  // r_t + 1
+  const int32_t *s = nullptr;
+  const int32_t *lin = nullptr, *lout = nullptr;
+  const double *bud = nullptr;
+  const uint64_t *base = nullptr;
+  int32_t N = 0, K = 0, L = 0, W = 0;
+  double bw = 1.0;
+  int64_t budget = 0;
+};
+
+}  // namespace chm
+
+struct chm_trace {
+  int device = 0;
+  int32_t N = 0, T = 0, K = 0, L = 0, W = 0;
+  int64_t budget = 0, M0 = 0, peak0 = 0;
+  int32_t argmax0 = 0;
+  double bw = 1.0, t_iter = 0.0;
+  std::vector<int32_t> p, f, a, b;     // per tensor
+  std::vector<int64_t> S_t;            // per tensor
+  std::vector<int64_t> F0;             // per op
+  std::vector<int32_t> lay_start, lay_n, lay_type, lay_of_op;
+  std::vector<double> bud;
+  std::vector<uint32_t> sw_t;          // swappable k -> production-order tensor rank
+  std::vector<int32_t> sw_tensor_idx;  // swappable k -> recorded tensor index
+  std::vector<int64_t> sw_S;
+  std::vector<int32_t> sw_r, sw_s, sw_lin, sw_lout;
+  std::vector<uint64_t> base;
+  // recorded iteration (for policy install: features)
+  std::vector<int32_t> tokens;
+  std::vector<int32_t> use_ptr, use_idx;
+  std::vector<uint8_t> dtype;
+  // device copies
+  void *dev_block = nullptr;
+  chm::DevTrace dev;
+};
+
+struct chm_ctx {
+  chm_config cfg;
+  int device = 0;
+  int num_sms = 148;
+  // tokenizer
+  std::unordered_map<std::string, int32_t> tokens;
+  // profiler
+  chm::IterRecord cur, last_detailed;
+  std::vector<int32_t> prev_tokens;
+  int64_t prev_alloc_bytes = -1;
+  bool stage_init = false;
+  int32_t stable_step = 0;
+  chm_stage stage = CHM_WARMUP;
+  bool force_detailed = false;
+  std::unordered_map<uint64_t, int32_t> id_to_tensor;  // detailed recording
+  // executor
+  std::vector<chm::PolicyItem> items;
+  std::unordered_map<chm::Feature, chm::KeyItems, chm::FeatureHash> key_to_item;
+  std::vector<uint8_t> op_index;   // token -> 8-bit index
+  std::vector<uint32_t> op_onehot; // token -> one-hot
+  std::unordered_map<uint64_t, chm::LiveTensor> live;
+  std::vector<std::vector<int32_t>> release_at, swapin_at, wait_at;  // by op index
+  int32_t op_cursor = 0;
+  int32_t match_window = 1;
+  chm_exec_stats stats{};
+  std::vector<chm_swap_desc> act_out, act_in;
+  std::vector<uint32_t> act_out_item, act_in_item, act_release, act_wait;
+  bool policy_active = false;
+  // swap
+  void *arena = nullptr;
+  uint64_t arena_bytes = 0;
+  std::vector<cudaEvent_t> events;  // ring of batch-completion events
+  std::vector<cudaEvent_t> fences;  // ring of compute->swap fence events
+  uint64_t next_batch = 0;
+  // eval scratch
+  void *eval_scratch = nullptr;  // per-CTA partial keys + ticket counter
+  size_t eval_scratch_bytes = 0;
+};
+
+namespace chm {
+constexpr int kEventRing = 4096;
+constexpr int kMaxDescPerLaunch = 64;
+constexpr int kMaxSeededWords = 64;  // SEEDED base mask in kernel params: K <= 4096
+
+// launchers (swap.cu / replay.cu)
+chm_status launch_swap_copy(const chm_swap_desc *d, uint32_t n, char *arena, bool to_host,
+                            int ctas, cudaStream_t stream);
+struct EvalLaunch {
+  DevTrace tr;
+  int kind = 0;
+  uint64_t first = 0, count = 0, seed = 0, flip_thr = 0;
+  uint64_t base[kMaxSeededWords] = {};
+  const uint64_t *masks = nullptr;
+  int64_t *peak = nullptr;
+  double *stall = nullptr;
+  int64_t *swapped = nullptr;
+  int64_t *footprint = nullptr;
+  uint32_t ld = 0;
+  chm_best *best = nullptr;
+};
+chm_status launch_eval(chm_ctx *ctx, const EvalLaunch &L, cudaStream_t stream);
+}  // namespace chm

@@ -1,0 +1,220 @@
+// swap.cu -- policy execution (steps a9-a11): multi-tensor gather/scatter between HBM and the
+// ctx's mapped pinned host arena, on a dedicated swap stream fenced against compute with an
+// event record/wait pair (custom recordStream; swap-in pre-trigger P:333).
+//
+// Kernel design (sm_100a, host-link bound, see DESIGN.md §"Swap kernel"): the descriptor list
+// travels in kernel parameter space (<= 64 descriptors + chunk prefix, ~2 KB); the bytes are cut
+// into 64 KiB chunks; each 512-thread CTA copies one chunk per grid-stride step with 8
+// independent 16 B loads per thread issued before the 8 stores (64 KiB in flight per CTA), so
+// a few dozen CTAs keep > 1 MB of PCIe reads in flight for swap-in.  Loads use the
+// non-coherent path without L1 allocation; stores to HBM are streaming (.cs) so an overlapped
+// compute kernel keeps its L2.
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "internal.h"
+
+namespace chm {
+namespace {
+
+constexpr int kSwapThreads = 512;
+constexpr int kUnroll = 8;
+constexpr int kChunkShift = 16;  // 64 KiB = 512 threads x 8 x 16 B
+constexpr uint64_t kChunk = 1ull << kChunkShift;
+
+struct SwapParams {
+  uint32_t n;
+  uint32_t to_host;
+  uint64_t total_chunks;
+  uint64_t src[kMaxDescPerLaunch];
+  uint64_t dst[kMaxDescPerLaunch];
+  uint64_t bytes[kMaxDescPerLaunch];
+  uint64_t chunk_begin[kMaxDescPerLaunch + 1];
+};
+
+__device__ __forceinline__ int4 ld_nc_na(const void *p) {
+  int4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_cs(void *p, int4 v) {
+  asm volatile("st.global.cs.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void st_plain(void *p, int4 v) {
+  asm volatile("st.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kSwapThreads) swap_copy_kernel(const __grid_constant__ SwapParams p) {
+  for (uint64_t c = blockIdx.x; c < p.total_chunks; c += gridDim.x) {
+    uint32_t lo = 0, hi = p.n;  // chunk_begin[lo] <= c < chunk_begin[hi]
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (p.chunk_begin[mid] <= c) lo = mid; else hi = mid;
+    }
+    const uint64_t off = (c - p.chunk_begin[lo]) << kChunkShift;
+    const uint64_t len = min(kChunk, p.bytes[lo] - off);
+    const char *s = reinterpret_cast<const char *>(p.src[lo]) + off;
+    char *d = reinterpret_cast<char *>(p.dst[lo]) + off;
+    if (((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d)) & 15) == 0) {
+      const uint32_t nvec = uint32_t(len >> 4);
+      int4 v[kUnroll];
+#pragma unroll
+      for (int k = 0; k < kUnroll; k++) {
+        const uint32_t idx = threadIdx.x + k * kSwapThreads;
+        if (idx < nvec) v[k] = ld_nc_na(s + 16ull * idx);
+      }
+#pragma unroll
+      for (int k = 0; k < kUnroll; k++) {
+        const uint32_t idx = threadIdx.x + k * kSwapThreads;
+        if (idx < nvec) {
+          if (p.to_host) st_plain(d + 16ull * idx, v[k]);
+          else st_cs(d + 16ull * idx, v[k]);
+        }
+      }
+      const uint32_t tail = uint32_t(len & 15);
+      if (threadIdx.x < tail) d[16ull * nvec + threadIdx.x] = s[16ull * nvec + threadIdx.x];
+    } else {  // misaligned view: byte path
+      for (uint64_t b = threadIdx.x; b < len; b += kSwapThreads) d[b] = s[b];
+    }
+  }
+}
+
+}  // namespace
+
+chm_status launch_swap_copy(const chm_swap_desc *desc, uint32_t n, char *arena, bool to_host,
+                            int ctas, cudaStream_t stream) {
+  for (uint32_t base = 0; base < n; base += kMaxDescPerLaunch) {
+    SwapParams p;
+    std::memset(&p, 0, sizeof p);
+    p.n = std::min<uint32_t>(kMaxDescPerLaunch, n - base);
+    p.to_host = to_host ? 1u : 0u;
+    uint64_t chunks = 0;
+    for (uint32_t j = 0; j < p.n; j++) {
+      const chm_swap_desc &d = desc[base + j];
+      const uint64_t host = reinterpret_cast<uint64_t>(arena) + d.host_off;
+      p.src[j] = to_host ? d.dev : host;
+      p.dst[j] = to_host ? host : d.dev;
+      p.bytes[j] = d.nbytes;
+      p.chunk_begin[j] = chunks;
+      chunks += (d.nbytes + kChunk - 1) >> kChunkShift;
+    }
+    p.chunk_begin[p.n] = chunks;
+    p.total_chunks = chunks;
+    const int grid = int(std::min<uint64_t>(uint64_t(ctas), chunks));
+    if (grid == 0) continue;
+    swap_copy_kernel<<<grid, kSwapThreads, 0, stream>>>(p);
+    CHM_CUDA(cudaGetLastError());
+  }
+  return CHM_OK;
+}
+
+}  // namespace chm
+
+using namespace chm;
+
+extern "C" chm_status chm_host_arena(chm_ctx *ctx, void **host_base, uint64_t *bytes) {
+  if (!ctx) CHM_FAIL(CHM_E_INVAL, "chm_host_arena: NULL ctx");
+  if (host_base) *host_base = ctx->arena;
+  if (bytes) *bytes = ctx->arena_bytes;
+  return CHM_OK;
+}
+
+static chm_status validate_batch(chm_ctx *ctx, const chm_swap_desc *d, uint32_t n, int64_t *err) {
+  if (err) *err = -1;
+  if (n && !d) CHM_FAIL(CHM_E_INVAL, "swap: NULL descriptor list");
+  if (n && !ctx->arena) CHM_FAIL(CHM_E_STATE, "swap: ctx has no host arena");
+  for (uint32_t j = 0; j < n; j++) {
+    if (d[j].nbytes == 0 || d[j].dev == 0 || d[j].host_off > ctx->arena_bytes ||
+        d[j].nbytes > ctx->arena_bytes - d[j].host_off) {
+      if (err) *err = j;
+      CHM_FAIL(CHM_E_INVAL, "swap: descriptor %u invalid (dev %llx off %llu bytes %llu, arena %llu)",
+               j, (unsigned long long)d[j].dev, (unsigned long long)d[j].host_off,
+               (unsigned long long)d[j].nbytes, (unsigned long long)ctx->arena_bytes);
+    }
+  }
+  if (n > 1) {  // host ranges of one batch must not overlap
+    std::vector<uint32_t> ord(n);
+    std::iota(ord.begin(), ord.end(), 0u);
+    std::sort(ord.begin(), ord.end(), [&](uint32_t x, uint32_t y) { return d[x].host_off < d[y].host_off; });
+    for (uint32_t j = 1; j < n; j++) {
+      const chm_swap_desc &p = d[ord[j - 1]], &q = d[ord[j]];
+      if (p.host_off + p.nbytes > q.host_off) {
+        if (err) *err = ord[j];
+        CHM_FAIL(CHM_E_INVAL, "swap: descriptor %u overlaps descriptor %u in the arena", ord[j], ord[j - 1]);
+      }
+    }
+  }
+  return CHM_OK;
+}
+
+static chm_status swap_batch(chm_ctx *ctx, const chm_swap_desc *d, uint32_t n, cudaStream_t compute,
+                             cudaStream_t swap, uint32_t flags, uint64_t *batch, int64_t *err,
+                             bool to_host) {
+  if (!ctx) CHM_FAIL(CHM_E_INVAL, "swap: NULL ctx");
+  if (ctx->device < 0) CHM_FAIL(CHM_E_STATE, "swap: host-only ctx");
+  if (flags > CHM_SWAP_CE) CHM_FAIL(CHM_E_INVAL, "swap: unknown flags %u", flags);
+  chm_status st = validate_batch(ctx, d, n, err);
+  if (st != CHM_OK) return st;
+  const uint64_t b = ctx->next_batch++;
+  const size_t slot = size_t(b % kEventRing);
+  if (compute != swap) {  // swap stream starts after everything enqueued on compute so far
+    CHM_CUDA(cudaEventRecord(ctx->fences[slot], compute));
+    CHM_CUDA(cudaStreamWaitEvent(swap, ctx->fences[slot], 0));
+  }
+  char *arena = static_cast<char *>(ctx->arena);
+  if (flags == CHM_SWAP_CE) {  // baseline: one copy-engine transfer per descriptor
+    for (uint32_t j = 0; j < n; j++) {
+      char *host = arena + d[j].host_off;
+      void *dev = reinterpret_cast<void *>(d[j].dev);
+      CHM_CUDA(cudaMemcpyAsync(to_host ? (void *)host : dev, to_host ? (const void *)dev : host,
+                               d[j].nbytes, to_host ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice,
+                               swap));
+    }
+  } else {
+    const int ctas = ctx->cfg.swap_ctas ? int(ctx->cfg.swap_ctas) : 32;
+    st = launch_swap_copy(d, n, arena, to_host, ctas, swap);
+    if (st != CHM_OK) return st;
+  }
+  CHM_CUDA(cudaEventRecord(ctx->events[slot], swap));
+  if (batch) *batch = b;
+  return CHM_OK;
+}
+
+extern "C" chm_status chm_swap_out(chm_ctx *ctx, const chm_swap_desc *d, uint32_t n,
+                                   cudaStream_t compute, cudaStream_t swap, uint32_t flags,
+                                   uint64_t *batch, int64_t *err_index) {
+  return swap_batch(ctx, d, n, compute, swap, flags, batch, err_index, true);
+}
+
+extern "C" chm_status chm_swap_in(chm_ctx *ctx, const chm_swap_desc *d, uint32_t n,
+                                  cudaStream_t compute, cudaStream_t swap, uint32_t flags,
+                                  uint64_t *batch, int64_t *err_index) {
+  return swap_batch(ctx, d, n, compute, swap, flags, batch, err_index, false);
+}
+
+extern "C" chm_status chm_batch_wait(chm_ctx *ctx, uint64_t batch, cudaStream_t stream) {
+  if (!ctx || ctx->device < 0) CHM_FAIL(CHM_E_INVAL, "chm_batch_wait: NULL or host-only ctx");
+  if (batch >= ctx->next_batch || batch + kEventRing < ctx->next_batch)
+    CHM_FAIL(CHM_E_INVAL, "chm_batch_wait: batch %llu unknown or expired", (unsigned long long)batch);
+  CHM_CUDA(cudaStreamWaitEvent(stream, ctx->events[batch % kEventRing], 0));
+  return CHM_OK;
+}
+
+extern "C" chm_status chm_batch_query(chm_ctx *ctx, uint64_t batch, int32_t *done) {
+  if (!ctx || !done || ctx->device < 0) CHM_FAIL(CHM_E_INVAL, "chm_batch_query: NULL argument / host-only ctx");
+  if (batch >= ctx->next_batch || batch + kEventRing < ctx->next_batch)
+    CHM_FAIL(CHM_E_INVAL, "chm_batch_query: batch unknown or expired");
+  cudaError_t e = cudaEventQuery(ctx->events[batch % kEventRing]);
+  if (e == cudaErrorNotReady) { *done = 0; return CHM_OK; }
+  CHM_CUDA(e);
+  *done = 1;
+  return CHM_OK;
+}

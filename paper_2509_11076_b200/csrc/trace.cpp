@@ -1,0 +1,237 @@
+// trace.cpp -- trace build (step a3): tensor table, no-swap footprint F0, logical layers
+// (Eq. 1), solo swap timing (Eq. 3, P:333 swap-in placement, P:340 swap-out completion),
+// swappable set, default SEEDED base; upload of the device tables for the replay kernel.
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+
+#include "internal.h"
+
+using namespace chm;
+
+enum { kFWD = 0, kBWD = 1, kOPT = 2 };
+
+extern "C" chm_status chm_trace_build(chm_ctx *ctx, const chm_trace_params *P, chm_trace **out) {
+  if (!ctx || !P || !out) CHM_FAIL(CHM_E_INVAL, "chm_trace_build: NULL argument");
+  *out = nullptr;
+  const IterRecord &R = ctx->last_detailed;
+  if (R.tokens.empty()) CHM_FAIL(CHM_E_STATE, "chm_trace_build: no Detailed-mode iteration recorded");
+  if (!(P->bw_bytes_per_s > 0.0)) CHM_FAIL(CHM_E_INVAL, "chm_trace_build: B must be > 0 (Eq. 3)");
+  const double t_iter = P->t_iter_s > 0.0 ? P->t_iter_s : R.t_iter;
+  if (!(t_iter >= 0.0)) CHM_FAIL(CHM_E_INVAL, "chm_trace_build: T_iter < 0");
+  const double omega = P->omega > 0.0 ? P->omega : 1.0;
+
+  chm_trace *tr = new (std::nothrow) chm_trace();
+  if (!tr) CHM_FAIL(CHM_E_NOMEM, "chm_trace_build: out of host memory");
+  const int32_t N = int32_t(R.tokens.size()), T = int32_t(R.tensors.size());
+  tr->device = ctx->device;
+  tr->N = N;
+  tr->T = T;
+  tr->budget = P->hbm_budget;
+  tr->M0 = P->static_bytes;
+  tr->bw = P->bw_bytes_per_s;
+  tr->t_iter = t_iter;
+
+  // tensor table: producer p, refcount release f (N: survives), last FWD use a (production
+  // counts), first BWD input use b
+  tr->p.assign(T, -1); tr->f.assign(T, N); tr->a.assign(T, -1); tr->b.assign(T, -1);
+  tr->S_t.resize(T);
+  for (int32_t t = 0; t < T; t++) {
+    tr->p[t] = R.tensors[t].producer;
+    tr->f[t] = R.tensors[t].freed >= 0 ? R.tensors[t].freed : N;
+    tr->S_t[t] = R.tensors[t].nbytes;
+  }
+  for (int32_t i = 0; i < N; i++) {
+    for (int32_t u = R.use_ptr[i]; u < R.use_ptr[i + 1]; u++) {
+      const int32_t t = R.use_idx[u];
+      if (R.phase[i] == kFWD) tr->a[t] = std::max(tr->a[t], i);
+      if (R.phase[i] == kBWD && R.use_is_in[u] && tr->b[t] < 0) tr->b[t] = i;
+    }
+  }
+  // F0 by a difference array: a produced tensor is live on ops [p_t, f_t]; a static tensor
+  // released during the iteration leaves after op f_t
+  {
+    std::vector<int64_t> d(size_t(N) + 1, 0);
+    for (int32_t t = 0; t < T; t++) {
+      if (tr->p[t] >= 0) {
+        d[tr->p[t]] += tr->S_t[t];
+        d[tr->f[t] + (tr->f[t] < N ? 1 : 0)] -= tr->S_t[t];
+      } else if (tr->f[t] < N) {
+        d[tr->f[t] + 1] -= tr->S_t[t];
+      }
+    }
+    tr->F0.resize(N);
+    int64_t acc = P->static_bytes;
+    for (int32_t i = 0; i < N; i++) { acc += d[i]; tr->F0[i] = acc; }
+  }
+  tr->argmax0 = 0;
+  for (int32_t i = 1; i < N; i++) if (tr->F0[i] > tr->F0[tr->argmax0]) tr->argmax0 = i;
+  tr->peak0 = tr->F0[tr->argmax0];
+
+  // logical layers: near-even contiguous groups per phase (first n mod G groups one larger),
+  // OPT one group; budget Bud = ((T_iter / N) * n_l) * omega (Eq. 1)
+  int32_t nph[3] = {0, 0, 0};
+  for (int32_t i = 0; i < N; i++) nph[R.phase[i]]++;
+  int32_t G[3] = {int32_t(P->groups_fwd), int32_t(P->groups_bwd), nph[kOPT] > 0 ? 1 : 0};
+  for (int ph = 0; ph < 2; ph++) {
+    if (nph[ph] == 0) G[ph] = 0;
+    else if (G[ph] < 1 || G[ph] > nph[ph]) {
+      delete tr;
+      CHM_FAIL(CHM_E_INVAL, "chm_trace_build: %d groups for %d ops of phase %d", G[ph], nph[ph], ph);
+    }
+  }
+  tr->L = G[0] + G[1] + G[2];
+  tr->lay_of_op.resize(N);
+  int32_t op = 0, last_fwd = -1;
+  for (int ph = 0; ph < 3; ph++) {
+    for (int32_t g = 0; g < G[ph]; g++) {
+      const int32_t n = nph[ph] / G[ph] + (g < nph[ph] % G[ph] ? 1 : 0);
+      tr->lay_start.push_back(op);
+      tr->lay_n.push_back(n);
+      tr->lay_type.push_back(ph);
+      tr->bud.push_back(((t_iter / double(N)) * double(n)) * omega);
+      for (int32_t k = op; k < op + n; k++) tr->lay_of_op[k] = int32_t(tr->lay_start.size()) - 1;
+      if (ph == kFWD) last_fwd = int32_t(tr->lay_start.size()) - 1;
+      op += n;
+    }
+  }
+
+  // solo timing + swappable set
+  std::vector<int32_t> prod_rank(T, -1);
+  {
+    int32_t rk = 0;
+    for (int32_t i = 0; i < N; i++)
+      for (int32_t j = R.out_ptr[i]; j < R.out_ptr[i + 1]; j++) prod_rank[R.out_idx[j]] = rk++;
+  }
+  struct Cand { int32_t t, r, s; };
+  std::vector<Cand> cands;
+  for (int32_t t = 0; t < T; t++) {
+    if (tr->p[t] < 0 || tr->a[t] < 0 || tr->b[t] < 0) continue;  // activations only
+    const double tswap = double(tr->S_t[t]) / tr->bw;  // Eq. 3
+    int32_t r = -1;
+    for (int32_t l = tr->lay_of_op[tr->a[t]]; l <= last_fwd; l++)  // P:340, forward search
+      if (tr->bud[l] > tswap) { r = tr->lay_start[l] + tr->lay_n[l] - 1; break; }
+    if (r < 0) r = tr->lay_start[last_fwd] + tr->lay_n[last_fwd] - 1;  // saturated
+    const int32_t lb = tr->lay_of_op[tr->b[t]];
+    if (lb < 1) continue;
+    const int32_t s = tr->lay_start[lb - 1];  // previous layer of the first BWD use
+    if (!(r + 1 < s)) continue;               // empty off-device window
+    cands.push_back({t, r, s});
+  }
+  std::sort(cands.begin(), cands.end(), [&](const Cand &x, const Cand &y) {
+    if (tr->a[x.t] != tr->a[y.t]) return tr->a[x.t] < tr->a[y.t];
+    return prod_rank[x.t] < prod_rank[y.t];
+  });
+  tr->K = int32_t(cands.size());
+  tr->W = (tr->K + 63) / 64;
+  tr->base.assign(size_t(tr->W), 0);
+  for (int32_t k = 0; k < tr->K; k++) {
+    const Cand &c = cands[k];
+    tr->sw_t.push_back(uint32_t(prod_rank[c.t]));
+    tr->sw_S.push_back(tr->S_t[c.t]);
+    tr->sw_r.push_back(c.r);
+    tr->sw_s.push_back(c.s);
+    tr->sw_lin.push_back(tr->lay_of_op[c.s]);
+    tr->sw_lout.push_back(tr->lay_of_op[c.r]);
+    if (c.r < tr->argmax0 && tr->argmax0 < c.s) tr->base[k / 64] |= 1ull << (k % 64);
+  }
+  // keep what policy install needs (App. A features over the recorded iteration)
+  tr->tokens = R.tokens;
+  tr->use_ptr = R.use_ptr;
+  tr->use_idx = R.use_idx;
+  tr->dtype.resize(T);
+  for (int32_t t = 0; t < T; t++) tr->dtype[t] = R.tensors[t].dtype;
+  // swappable k -> product tensor index (kept for install)
+  std::vector<int32_t> sw_tensor(tr->K);
+  for (int32_t k = 0; k < tr->K; k++) sw_tensor[k] = cands[k].t;
+  tr->sw_tensor_idx = std::move(sw_tensor);
+
+  // device tables in one allocation, each array 256 B aligned
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t o_f0 = 0, o_S = o_f0 + al(8 * size_t(N)), o_r1 = o_S + al(8 * size_t(tr->K)),
+               o_s = o_r1 + al(4 * size_t(tr->K)), o_lin = o_s + al(4 * size_t(tr->K)),
+               o_lout = o_lin + al(4 * size_t(tr->K)), o_bud = o_lout + al(4 * size_t(tr->K)),
+               o_base = o_bud + al(8 * size_t(tr->L)), total = o_base + al(8 * size_t(tr->W) + 8);
+  std::vector<char> host(total, 0);
+  std::memcpy(host.data() + o_f0, tr->F0.data(), 8 * size_t(N));
+  std::vector<int32_t> r1(tr->K);
+  for (int32_t k = 0; k < tr->K; k++) r1[k] = tr->sw_r[k] + 1;
+  if (tr->K) {
+    std::memcpy(host.data() + o_S, tr->sw_S.data(), 8 * size_t(tr->K));
+    std::memcpy(host.data() + o_r1, r1.data(), 4 * size_t(tr->K));
+    std::memcpy(host.data() + o_s, tr->sw_s.data(), 4 * size_t(tr->K));
+    std::memcpy(host.data() + o_lin, tr->sw_lin.data(), 4 * size_t(tr->K));
+    std::memcpy(host.data() + o_lout, tr->sw_lout.data(), 4 * size_t(tr->K));
+  }
+  if (tr->L) std::memcpy(host.data() + o_bud, tr->bud.data(), 8 * size_t(tr->L));
+  if (tr->W) std::memcpy(host.data() + o_base, tr->base.data(), 8 * size_t(tr->W));
+  if (ctx->device < 0) {  // host-only ctx: tables stay on the host
+    *out = tr;
+    return CHM_OK;
+  }
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e == cudaSuccess) e = cudaMalloc(&tr->dev_block, total);
+  if (e == cudaSuccess) e = cudaMemcpy(tr->dev_block, host.data(), total, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    chm_trace_free(tr);
+    CHM_FAIL(CHM_E_CUDA, "chm_trace_build: device upload failed: %s", cudaGetErrorString(e));
+  }
+  char *d = static_cast<char *>(tr->dev_block);
+  tr->dev.f0 = reinterpret_cast<const int64_t *>(d + o_f0);
+  tr->dev.S = reinterpret_cast<const int64_t *>(d + o_S);
+  tr->dev.r1 = reinterpret_cast<const int32_t *>(d + o_r1);
+  tr->dev.s = reinterpret_cast<const int32_t *>(d + o_s);
+  tr->dev.lin = reinterpret_cast<const int32_t *>(d + o_lin);
+  tr->dev.lout = reinterpret_cast<const int32_t *>(d + o_lout);
+  tr->dev.bud = reinterpret_cast<const double *>(d + o_bud);
+  tr->dev.base = reinterpret_cast<const uint64_t *>(d + o_base);
+  tr->dev.N = N;
+  tr->dev.K = tr->K;
+  tr->dev.L = tr->L;
+  tr->dev.W = tr->W;
+  tr->dev.bw = tr->bw;
+  tr->dev.budget = tr->budget;
+  *out = tr;
+  return CHM_OK;
+}
+
+extern "C" void chm_trace_free(chm_trace *t) {
+  if (!t) return;
+  if (t->dev_block && t->device >= 0) {
+    cudaSetDevice(t->device);
+    cudaFree(t->dev_block);
+  }
+  delete t;
+}
+
+extern "C" chm_status chm_trace_get_info(const chm_trace *t, chm_trace_info *info) {
+  if (!t || !info) CHM_FAIL(CHM_E_INVAL, "chm_trace_get_info: NULL argument");
+  info->n_ops = uint32_t(t->N);
+  info->n_tensors = uint32_t(t->T);
+  info->n_swappable = uint32_t(t->K);
+  info->n_layers = uint32_t(t->L);
+  info->mask_words = uint32_t(t->W);
+  info->peak0 = t->peak0;
+  info->argmax0 = uint32_t(t->argmax0);
+  info->budget = t->budget;
+  return CHM_OK;
+}
+
+extern "C" chm_status chm_trace_tables(const chm_trace *t, int64_t *f0, uint32_t *tensor,
+                                       int64_t *nbytes, int32_t *r, int32_t *s, int32_t *lin,
+                                       int32_t *lout, int32_t *lay_start, int32_t *lay_count,
+                                       double *bud, uint64_t *base) {
+  if (!t) CHM_FAIL(CHM_E_INVAL, "chm_trace_tables: NULL trace");
+  if (f0) std::copy(t->F0.begin(), t->F0.end(), f0);
+  if (tensor) std::copy(t->sw_t.begin(), t->sw_t.end(), tensor);
+  if (nbytes) std::copy(t->sw_S.begin(), t->sw_S.end(), nbytes);
+  if (r) std::copy(t->sw_r.begin(), t->sw_r.end(), r);
+  if (s) std::copy(t->sw_s.begin(), t->sw_s.end(), s);
+  if (lin) std::copy(t->sw_lin.begin(), t->sw_lin.end(), lin);
+  if (lout) std::copy(t->sw_lout.begin(), t->sw_lout.end(), lout);
+  if (lay_start) std::copy(t->lay_start.begin(), t->lay_start.end(), lay_start);
+  if (lay_count) std::copy(t->lay_n.begin(), t->lay_n.end(), lay_count);
+  if (bud) std::copy(t->bud.begin(), t->bud.end(), bud);
+  if (base) std::copy(t->base.begin(), t->base.end(), base);
+  return CHM_OK;
+}

@@ -1,0 +1,67 @@
+"""CPU-side checks of the product library: it loads, exports every symbol include/chm.h declares,
+and host-only calls behave (no compute without a GPU)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_2509_11076_b200 import chm
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "chm.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(chm_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_library_builds_and_loads():
+    from paper_2509_11076_b200 import build
+    path = build.build()
+    assert os.path.exists(path)
+    chm.load()
+
+
+def test_exports_every_declared_symbol():
+    declared = _declared()
+    assert len(declared) >= 20
+    out = subprocess.run(["nm", "-D", "--defined-only", chm.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (chm_\w+)", out))
+    missing = [s for s in declared if s not in exported]
+    assert not missing, missing
+    assert set(declared) == set(chm.EXPORTS)
+
+
+def test_sm100a_cubin_embedded():
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", chm.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_host_only_calls():
+    L = chm.load()
+    assert b"sm_100a" in L.chm_build_info()
+    cfg = chm.Config()
+    L.chm_config_default(ctypes.byref(cfg))
+    assert (cfg.m, cfg.n, cfg.len_tol, cfg.cos_tol) == (2, 5, 0.05, 0.95)
+    keys = np.zeros(3, chm.BEST_DTYPE)
+    keys[0] = (5, 0.0, 1, 0, 0)
+    keys[1] = (0, 2.0, 9, 1, 0)
+    keys[2] = (0, 1.0, 9, 2, 0)
+    assert chm.best_reduce(keys).index == 2
+    keys[1] = (0, 1.0, 9, 1, 0)
+    assert chm.best_reduce(keys).index == 1  # tie on (excess, stall, swapped) -> lowest index
+    with pytest.raises(chm.ChmError):
+        chm.best_reduce(np.zeros(0, chm.BEST_DTYPE))
+
+
+def test_create_without_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(chm.ChmError):
+        chm.Context(device=0)
