@@ -69,6 +69,7 @@ typedef struct {
   uint32_t eval_ctas_per_sm;  /* resident CTAs per SM for the replay kernel (0: auto)        */
   uint32_t match_window;      /* executor: max |op - a_t| for a feature match (0: half the
                                  smallest FWD logical layer)                                 */
+  uint32_t time_batches;      /* 1: time every swap batch's copy with CUDA events            */
 } chm_config;
 
 /* fills the paper's defaults */
@@ -210,6 +211,10 @@ chm_status chm_eval_policies(chm_ctx *ctx, const chm_trace *t, const chm_candida
                              const chm_eval_out *o, cudaStream_t stream);
 /* host: lexicographic min of n keys (e.g. after an all-gather across ranks) */
 chm_status chm_best_reduce(const chm_best *keys, uint32_t n, chm_best *out);
+/* device: the same min over n device keys into *out (device), enqueued on `stream` -- the
+ * step after the NCCL all-gather of per-rank keys, without a host round trip. */
+chm_status chm_best_reduce_device(chm_ctx *ctx, const chm_best *keys, uint32_t n, chm_best *out,
+                                  cudaStream_t stream);
 /* host: the swap set of global candidate `index` as mask words (mask_words u64) */
 chm_status chm_candidate_mask(const chm_trace *t, const chm_candidates *c, uint64_t index,
                               uint64_t *words);
@@ -230,6 +235,9 @@ chm_status chm_exec_stats_get(chm_ctx *ctx, chm_exec_stats *s);
 /* ---------------------------------------------------------------- swap execution (a9-a11) */
 /* The ctx's pinned, device-mapped host arena (cudaHostAllocMapped|Portable). */
 chm_status chm_host_arena(chm_ctx *ctx, void **host_base, uint64_t *bytes);
+/* Grows the arena to at least `bytes` (e.g. to the installed policy's swapped bytes).  The old
+ * arena is released: call only while no swap batch is in flight (contents are not kept). */
+chm_status chm_arena_reserve(chm_ctx *ctx, uint64_t bytes);
 
 enum {
   CHM_SWAP_KERNEL = 0, /* one multi-tensor gather/scatter kernel launch per <= 64 descriptors */
@@ -253,6 +261,10 @@ chm_status chm_swap_in(chm_ctx *ctx, const chm_swap_desc *d, uint32_t n, cudaStr
 chm_status chm_batch_wait(chm_ctx *ctx, uint64_t batch, cudaStream_t stream);
 /* Host query (tests / diagnostics only): *done = 1 if the batch completed. */
 chm_status chm_batch_query(chm_ctx *ctx, uint64_t batch, int32_t *done);
+/* With chm_config.time_batches = 1, each batch's copy (after its fence wait) is bracketed by
+ * timing events on the swap stream; *ms = its device duration.  CHM_E_STATE if the batch has
+ * not completed or timing is off. */
+chm_status chm_batch_elapsed(chm_ctx *ctx, uint64_t batch, float *ms);
 /* Executor helpers for the actions of the last chm_record_op:
  *   chm_issue_swap_out: one swap-out batch of every pending swap-out item;
  *   chm_issue_swap_in:  one swap-in batch of every pending swap-in item; dev[j] is the block

@@ -87,6 +87,7 @@ def lib():
         L.orc_splitmix64.argtypes = [C.c_uint64]
         L.orc_splitmix64.restype = C.c_uint64
         L.orc_key_less.argtypes = [C.POINTER(_Best), C.POINTER(_Best)]
+        L.orc_swap_execute.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
         L.orc_stage_init.argtypes = [C.POINTER(_Stage), C.c_int32, C.c_int32, C.c_double,
                                      C.c_double, C.c_int32]
         L.orc_stage_release.argtypes = [C.POINTER(_Stage)]
@@ -277,3 +278,12 @@ def features_after(trace, tokens, op_index, op_onehot, after: int):
                              _p(_arr(op_index, np.uint8)), _p(_arr(op_onehot, np.uint32)), after,
                              _p(cnt), _p(tag), _p(stk))
     return cnt, tag, stk
+
+
+def swap_execute(dst_ptrs, src_ptrs, nbytes):
+    """byte-exact copy of each source range to its destination (host pointers)"""
+    n = len(nbytes)
+    d = (C.c_void_p * max(n, 1))(*dst_ptrs)
+    sp = (C.c_void_p * max(n, 1))(*src_ptrs)
+    nb = (C.c_uint64 * max(n, 1))(*[int(x) for x in nbytes])
+    lib().orc_swap_execute(n, d, sp, nb)

@@ -391,6 +391,10 @@ int orc_eval(const orc_model *m, int kind, uint64_t first, uint64_t count, uint6
   return 0;
 }
 
+void orc_swap_execute(int32_t n, void *const *dst, const void *const *src, const uint64_t *nbytes) {
+  for (int32_t j = 0; j < n; j++) memcpy(dst[j], src[j], (size_t)nbytes[j]);
+}
+
 /* ---------------------------------------------------------------------------------------
  * Algo. 1, stage adjusting, with the readings of SURVEY §8(c).8 / Q1-Q3:
  *   len_diff = |n - n'| / max(n, n');  cos = positional cosine of the zero-padded token

@@ -86,6 +86,10 @@ int orc_eval(const orc_model *m, int kind, uint64_t first, uint64_t count, uint6
 uint64_t orc_splitmix64(uint64_t z);
 int orc_key_less(const orc_best *x, const orc_best *y);
 
+/* Swap execution oracle: after a swap the destination range equals the
+ * source range byte for byte.  Executed literally on host buffers (memcpy per descriptor). */
+void orc_swap_execute(int32_t n, void *const *dst, const void *const *src, const uint64_t *nbytes);
+
 /* Algo. 1 */
 typedef struct {
   int32_t m, n, cos_mode, initialized, stable_step, prev_stage;

@@ -33,7 +33,7 @@ class Config(C.Structure):
     _fields_ = [("m", C.c_uint32), ("n", C.c_uint32), ("len_tol", C.c_double), ("cos_tol", C.c_double),
                 ("cos_mode", C.c_uint32), ("detect_bytes", C.c_uint32), ("device", C.c_int32),
                 ("host_arena_bytes", C.c_uint64), ("swap_ctas", C.c_uint32), ("eval_ctas_per_sm", C.c_uint32),
-                ("match_window", C.c_uint32)]
+                ("match_window", C.c_uint32), ("time_batches", C.c_uint32)]
 
 
 class TensorRef(C.Structure):
@@ -103,9 +103,9 @@ class ExecStats(C.Structure):
 EXPORTS = [
     "chm_config_default", "chm_create", "chm_destroy", "chm_last_error", "chm_build_info", "chm_tokenize",
     "chm_record_op", "chm_set_detailed", "chm_detect_seq_change", "chm_trace_build", "chm_trace_free",
-    "chm_trace_get_info", "chm_trace_tables", "chm_eval_policies", "chm_best_reduce", "chm_candidate_mask",
+    "chm_trace_get_info", "chm_trace_tables", "chm_eval_policies", "chm_best_reduce", "chm_best_reduce_device", "chm_candidate_mask",
     "chm_policy_install", "chm_exec_stats_get", "chm_host_arena", "chm_swap_out", "chm_swap_in",
-    "chm_batch_wait", "chm_batch_query", "chm_issue_swap_out", "chm_issue_swap_in", "chm_item_wait",
+    "chm_batch_wait", "chm_batch_query", "chm_batch_elapsed", "chm_arena_reserve", "chm_issue_swap_out", "chm_issue_swap_in", "chm_item_wait",
 ]
 
 _lib = None
@@ -137,6 +137,7 @@ def load(path: str = LIB_PATH):
         "chm_trace_tables": (i32, [vp] + [vp] * 11),
         "chm_eval_policies": (i32, [vp, vp, P(Candidates), P(EvalOut), vp]),
         "chm_best_reduce": (i32, [vp, u32, P(Best)]),
+        "chm_best_reduce_device": (i32, [vp, vp, u32, vp, vp]),
         "chm_candidate_mask": (i32, [vp, P(Candidates), u64, vp]),
         "chm_policy_install": (i32, [vp, vp, vp]),
         "chm_exec_stats_get": (i32, [vp, P(ExecStats)]),
@@ -145,6 +146,8 @@ def load(path: str = LIB_PATH):
         "chm_swap_in": (i32, [vp, vp, u32, vp, vp, u32, P(u64), P(i64)]),
         "chm_batch_wait": (i32, [vp, u64, vp]),
         "chm_batch_query": (i32, [vp, u64, P(i32)]),
+        "chm_batch_elapsed": (i32, [vp, u64, P(C.c_float)]),
+        "chm_arena_reserve": (i32, [vp, u64]),
         "chm_issue_swap_out": (i32, [vp, vp, vp, u32, P(u64)]),
         "chm_issue_swap_in": (i32, [vp, vp, vp, vp, u32, P(u64)]),
         "chm_item_wait": (i32, [vp, u32, i32, vp]),
@@ -229,7 +232,7 @@ class Context:
     """One chm_ctx per device / rank (single owner, not thread-safe)."""
 
     def __init__(self, device: int = 0, host_arena_bytes: int = 0, swap_ctas: int = 0, eval_ctas_per_sm: int = 0,
-                 **algo1):
+                 time_batches: bool = False, **algo1):
         L = load()
         cfg = Config()
         L.chm_config_default(C.byref(cfg))
@@ -237,6 +240,7 @@ class Context:
         cfg.host_arena_bytes = host_arena_bytes
         cfg.swap_ctas = swap_ctas
         cfg.eval_ctas_per_sm = eval_ctas_per_sm
+        cfg.time_batches = 1 if time_batches else 0
         for k, v in algo1.items():
             setattr(cfg, k, v)
         h = C.c_void_p()
@@ -299,6 +303,9 @@ class Context:
         o = EvalOut(_ptr(peak), _ptr(stall), _ptr(swapped), _ptr(footprint), ld, _ptr(best))
         _check(load().chm_eval_policies(self.h, trace.h, C.byref(c), C.byref(o), _stream(stream)))
 
+    def best_reduce_device(self, keys, n: int, out, stream=None):
+        _check(load().chm_best_reduce_device(self.h, _ptr(keys), n, _ptr(out), _stream(stream)))
+
     # ---------------------------------------------------------------------- swap
     def host_arena(self):
         p, n = C.c_void_p(), C.c_uint64()
@@ -323,6 +330,14 @@ class Context:
 
     def batch_wait(self, batch: int, stream=None):
         _check(load().chm_batch_wait(self.h, batch, _stream(stream)))
+
+    def batch_elapsed_ms(self, batch: int) -> float:
+        ms = C.c_float()
+        _check(load().chm_batch_elapsed(self.h, batch, C.byref(ms)))
+        return ms.value
+
+    def arena_reserve(self, nbytes: int):
+        _check(load().chm_arena_reserve(self.h, int(nbytes)))
 
     def batch_query(self, batch: int) -> bool:
         d = C.c_int32()
@@ -387,3 +402,23 @@ def record_iteration(ctx: Context, trace, tokens: Optional[Sequence[int]] = None
         if on_actions is not None:
             on_actions(i, a)
     return tokens
+
+
+class PreparedIteration:
+    """Pre-marshalled chm_op_record array for one iteration of a trace (ids chosen by the caller),
+    so a replay loop only pays one ctypes call per op."""
+
+    def __init__(self, trace, ids, tokens):
+        self.recs = []
+        self._keep = []
+        nb, dt = trace.nbytes, trace.dtype
+        for i in range(trace.n_ops):
+            ins = [TensorRef(int(ids[t]), int(nb[t]), int(dt[t])) for t in trace.ins(i)]
+            outs = [TensorRef(int(ids[t]), int(nb[t]), int(dt[t])) for t in trace.outs(i)]
+            fr = [int(ids[t]) for t in trace.frees(i)]
+            a_in = (TensorRef * max(len(ins), 1))(*ins)
+            a_out = (TensorRef * max(len(outs), 1))(*outs)
+            a_fr = (C.c_uint64 * max(len(fr), 1))(*fr)
+            self._keep += [a_in, a_out, a_fr]
+            self.recs.append(OpRecord(int(tokens[i]), int(trace.phase[i]), len(ins), len(outs), len(fr),
+                                      a_in, a_out, a_fr, -1))

@@ -43,6 +43,7 @@ extern "C" void chm_config_default(chm_config *c) {
   c->swap_ctas = 0;
   c->eval_ctas_per_sm = 0;
   c->match_window = 0;
+  c->time_batches = 0;
 }
 
 extern "C" chm_status chm_create(const chm_config *cfg, chm_ctx **out) {
@@ -84,6 +85,16 @@ extern "C" chm_status chm_create(const chm_config *cfg, chm_ctx **out) {
       CHM_FAIL(CHM_E_CUDA, "chm_create: cudaEventCreate failed");
     }
   }
+  if (c.time_batches) {
+    ctx->t0.resize(kEventRing, nullptr);
+    ctx->t1.resize(kEventRing, nullptr);
+    for (int i = 0; i < kEventRing; i++) {
+      if (cudaEventCreate(&ctx->t0[i]) != cudaSuccess || cudaEventCreate(&ctx->t1[i]) != cudaSuccess) {
+        chm_destroy(ctx);
+        CHM_FAIL(CHM_E_CUDA, "chm_create: cudaEventCreate (timing) failed");
+      }
+    }
+  }
   if (c.host_arena_bytes) {
     // pinned + device-mapped host arena (portable across contexts); this box has one NUMA
     // node, so first-touch placement is NUMA-local by construction
@@ -111,6 +122,8 @@ extern "C" void chm_destroy(chm_ctx *ctx) {
   cudaSetDevice(ctx->device);
   for (auto e : ctx->events) if (e) cudaEventDestroy(e);
   for (auto e : ctx->fences) if (e) cudaEventDestroy(e);
+  for (auto e : ctx->t0) if (e) cudaEventDestroy(e);
+  for (auto e : ctx->t1) if (e) cudaEventDestroy(e);
   if (ctx->arena) cudaFreeHost(ctx->arena);
   if (ctx->eval_scratch) cudaFree(ctx->eval_scratch);
   delete ctx;

@@ -170,6 +170,7 @@ struct chm_ctx {
   uint64_t arena_bytes = 0;
   std::vector<cudaEvent_t> events;  // ring of batch-completion events
   std::vector<cudaEvent_t> fences;  // ring of compute->swap fence events
+  std::vector<cudaEvent_t> t0, t1;  // timing events per batch slot (time_batches)
   uint64_t next_batch = 0;
   // eval scratch
   void *eval_scratch = nullptr;  // per-CTA partial keys + ticket counter

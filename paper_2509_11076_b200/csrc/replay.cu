@@ -221,6 +221,23 @@ __global__ void __launch_bounds__(256) replay_kernel(const __grid_constant__ Eva
   }
 }
 
+__global__ void best_reduce_kernel(const Key *keys, uint32_t n, Key *out) {
+  Key b;
+  b.excess = LLONG_MAX; b.stall = 0.0; b.swapped = LLONG_MAX; b.index = ~0ull; b.peak = 0;
+  for (uint32_t q = threadIdx.x; q < n; q += 32) if (key_less(keys[q], b)) b = keys[q];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    Key y;
+    y.excess = __shfl_xor_sync(0xffffffffu, b.excess, o);
+    y.stall = __shfl_xor_sync(0xffffffffu, b.stall, o);
+    y.swapped = __shfl_xor_sync(0xffffffffu, b.swapped, o);
+    y.index = __shfl_xor_sync(0xffffffffu, b.index, o);
+    y.peak = __shfl_xor_sync(0xffffffffu, b.peak, o);
+    if (key_less(y, b)) b = y;
+  }
+  if (threadIdx.x == 0) *out = b;
+}
+
 }  // namespace
 
 chm_status launch_eval(chm_ctx *ctx, const EvalLaunch &L, cudaStream_t stream) {
@@ -328,4 +345,14 @@ extern "C" chm_status chm_eval_policies(chm_ctx *ctx, const chm_trace *t, const 
   L.best = o->best;
   CHM_CUDA(cudaSetDevice(ctx->device));
   return launch_eval(ctx, L, stream);
+}
+
+extern "C" chm_status chm_best_reduce_device(chm_ctx *ctx, const chm_best *keys, uint32_t n, chm_best *out,
+                                             cudaStream_t stream) {
+  if (!ctx || !keys || !out || n == 0 || ctx->device < 0)
+    CHM_FAIL(CHM_E_INVAL, "chm_best_reduce_device: bad argument");
+  CHM_CUDA(cudaSetDevice(ctx->device));
+  best_reduce_kernel<<<1, 32, 0, stream>>>(reinterpret_cast<const Key *>(keys), n, reinterpret_cast<Key *>(out));
+  CHM_CUDA(cudaGetLastError());
+  return CHM_OK;
 }

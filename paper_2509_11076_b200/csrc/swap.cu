@@ -170,6 +170,7 @@ static chm_status swap_batch(chm_ctx *ctx, const chm_swap_desc *d, uint32_t n, c
     CHM_CUDA(cudaStreamWaitEvent(swap, ctx->fences[slot], 0));
   }
   char *arena = static_cast<char *>(ctx->arena);
+  if (!ctx->t0.empty()) CHM_CUDA(cudaEventRecord(ctx->t0[slot], swap));
   if (flags == CHM_SWAP_CE) {  // baseline: one copy-engine transfer per descriptor
     for (uint32_t j = 0; j < n; j++) {
       char *host = arena + d[j].host_off;
@@ -183,6 +184,7 @@ static chm_status swap_batch(chm_ctx *ctx, const chm_swap_desc *d, uint32_t n, c
     st = launch_swap_copy(d, n, arena, to_host, ctas, swap);
     if (st != CHM_OK) return st;
   }
+  if (!ctx->t1.empty()) CHM_CUDA(cudaEventRecord(ctx->t1[slot], swap));
   CHM_CUDA(cudaEventRecord(ctx->events[slot], swap));
   if (batch) *batch = b;
   return CHM_OK;
@@ -216,5 +218,36 @@ extern "C" chm_status chm_batch_query(chm_ctx *ctx, uint64_t batch, int32_t *don
   if (e == cudaErrorNotReady) { *done = 0; return CHM_OK; }
   CHM_CUDA(e);
   *done = 1;
+  return CHM_OK;
+}
+
+extern "C" chm_status chm_batch_elapsed(chm_ctx *ctx, uint64_t batch, float *ms) {
+  if (!ctx || !ms || ctx->device < 0) CHM_FAIL(CHM_E_INVAL, "chm_batch_elapsed: NULL argument / host-only ctx");
+  if (ctx->t0.empty()) CHM_FAIL(CHM_E_STATE, "chm_batch_elapsed: ctx created without time_batches");
+  if (batch >= ctx->next_batch || batch + kEventRing < ctx->next_batch)
+    CHM_FAIL(CHM_E_INVAL, "chm_batch_elapsed: batch unknown or expired");
+  const size_t slot = size_t(batch % kEventRing);
+  cudaError_t e = cudaEventElapsedTime(ms, ctx->t0[slot], ctx->t1[slot]);
+  if (e == cudaErrorNotReady) CHM_FAIL(CHM_E_STATE, "chm_batch_elapsed: batch not complete");
+  CHM_CUDA(e);
+  return CHM_OK;
+}
+
+extern "C" chm_status chm_arena_reserve(chm_ctx *ctx, uint64_t bytes) {
+  if (!ctx || ctx->device < 0) CHM_FAIL(CHM_E_INVAL, "chm_arena_reserve: NULL or host-only ctx");
+  if (bytes <= ctx->arena_bytes) return CHM_OK;
+  CHM_CUDA(cudaSetDevice(ctx->device));
+  if (ctx->arena) {
+    CHM_CUDA(cudaFreeHost(ctx->arena));
+    ctx->arena = nullptr;
+    ctx->arena_bytes = 0;
+  }
+  cudaError_t e = cudaHostAlloc(&ctx->arena, bytes, cudaHostAllocMapped | cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    ctx->arena = nullptr;
+    CHM_FAIL(CHM_E_NOMEM, "chm_arena_reserve: cudaHostAlloc(%llu) failed: %s", (unsigned long long)bytes,
+             cudaGetErrorString(e));
+  }
+  ctx->arena_bytes = bytes;
   return CHM_OK;
 }
