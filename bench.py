@@ -314,6 +314,7 @@ def main():
         storage[t] = buf
         ids[t] = buf.data_ptr()
     item_dev = [storage[int(tb["tensor"][k])].data_ptr() for k in keep]  # swap-in destinations
+    real_ids = set(item_dev)
     check_t = [int(tb["tensor"][k]) for k in keep[:: max(1, len(keep) // 8)]]
     check_sum = {t: int(storage[t].sum().item()) for t in check_t}
     run = chm.PreparedIteration(tr, ids, tokens)
@@ -332,6 +333,9 @@ def main():
             chm._check(L.chm_record_op(h, ctypes.byref(r), ctypes.byref(act)))
             if act.n_swap_out:
                 n = act.n_swap_out
+                for j in range(n):
+                    if act.swap_out[j].dev not in real_ids:
+                        raise RuntimeError(f"executor matched a tensor outside the policy at op {len(outs)}")
                 outs.append(ctx.issue_swap_out(comp, s_out, flags))
                 launches += (n + 63) // 64 if flags == chm.SWAP_KERNEL else 0
             for j in range(act.n_release):

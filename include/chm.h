@@ -67,8 +67,8 @@ typedef struct {
   uint64_t host_arena_bytes;  /* pinned + mapped host arena for swapped blocks (0: none)      */
   uint32_t swap_ctas;         /* CTAs of the swap copy kernel (0: default, 16)               */
   uint32_t eval_ctas_per_sm;  /* resident CTAs per SM for the replay kernel (0: auto)        */
-  uint32_t match_window;      /* executor: max |op - a_t| for a feature match (0: half the
-                                 smallest FWD logical layer)                                 */
+  uint32_t match_window;      /* executor: max recorded ops skipped when aligning a run-time
+                                 op to the recorded sequence (0: 32)                         */
   uint32_t time_batches;      /* 1: time every swap batch's copy with CUDA events            */
 } chm_config;
 

@@ -67,7 +67,8 @@ static void feature_tables(const std::vector<int32_t> &tokens, std::vector<uint8
   }
 }
 
-static inline void feature_update(Feature &f, int32_t token, uint8_t dtype, const chm_ctx *ctx) {
+static inline void feature_update(Feature &f, int32_t token, uint8_t dtype, uint32_t slot,
+                                  const chm_ctx *ctx) {
   uint8_t idx = 0;
   uint32_t oh = 0;
   if (token >= 0 && size_t(token) < ctx->op_index.size()) {
@@ -78,6 +79,7 @@ static inline void feature_update(Feature &f, int32_t token, uint8_t dtype, cons
   f.tag |= oh;                        // opTag |= opOneHot
   f.stack = (f.stack << 8) + idx;     // opCallStack = (opCallStack << 8) + opIndex
   f.dtype = dtype;
+  f.slot = uint8_t(slot < 255 ? slot : 255);  // position among the op's distinct tensors
 }
 
 extern "C" chm_status chm_policy_install(chm_ctx *ctx, const chm_trace *t, const uint64_t *words) {
@@ -111,17 +113,25 @@ extern "C" chm_status chm_policy_install(chm_ctx *ctx, const chm_trace *t, const
   for (int32_t i = 0; i < t->N; i++) {
     for (int32_t u = t->use_ptr[i]; u < t->use_ptr[i + 1]; u++) {
       const int32_t tid = t->use_idx[u];
-      feature_update(feat[tid], t->tokens[i], t->dtype[tid], ctx);
+      feature_update(feat[tid], t->tokens[i], t->dtype[tid], uint32_t(u - t->use_ptr[i]), ctx);
       const int32_t j = item_of_tensor[tid];
       if (j >= 0 && ctx->items[j].a == i) ctx->items[j].key = feat[tid];
     }
   }
-  // items sharing a key (e.g. the same tensor role in every transformer layer) are consumed
-  // in a_t order: a matching live tensor takes the first untriggered item of its key
+  // key = (App. A feature after a_t, a_t): the same tensor role repeats in every layer of a
+  // stacked model with identical features, so the recorded op index is part of the key and
+  // run-time ops are aligned to the recorded sequence (align_op)
   ctx->key_to_item.clear();
   ctx->stats = chm_exec_stats{};
   ctx->stats.n_items = uint32_t(sel.size());
-  for (size_t j = 0; j < ctx->items.size(); j++) ctx->key_to_item[ctx->items[j].key].items.push_back(int32_t(j));
+  for (size_t j = 0; j < ctx->items.size(); j++) {
+    FeatureAt k;
+    k.f = ctx->items[j].key;
+    k.a = ctx->items[j].a;
+    if (!ctx->key_to_item.emplace(k, int32_t(j)).second) ctx->stats.n_collisions++;
+  }
+  ctx->rec_tokens = t->tokens;
+  ctx->align_cursor = 0;
   // index-keyed tables: actions returned by chm_record_op(op i) happen between op i and i+1
   const size_t N = size_t(t->N);
   ctx->release_at.assign(N, {});
@@ -133,26 +143,37 @@ extern "C" chm_status chm_policy_install(chm_ctx *ctx, const chm_trace *t, const
     if (it.s >= 1) ctx->swapin_at[it.s - 1].push_back(int32_t(j));     // before op s_t
     if (it.b >= 1) ctx->wait_at[it.b - 1].push_back(int32_t(j));       // before op b_t
   }
-  // match window: half the smallest FWD logical layer (so the same role one layer away is never
-  // nearer), unless configured
-  int32_t min_fwd = INT32_MAX;
-  for (size_t l = 0; l < t->lay_n.size(); l++)
-    if (t->lay_type[l] == CHM_FWD) min_fwd = std::min(min_fwd, t->lay_n[l]);
-  ctx->match_window = ctx->cfg.match_window ? int32_t(ctx->cfg.match_window)
-                                            : std::max(1, (min_fwd == INT32_MAX ? 2 : min_fwd) / 2);
+  ctx->match_window = ctx->cfg.match_window ? int32_t(ctx->cfg.match_window) : 32;
   ctx->live.clear();
   ctx->op_cursor = 0;
   ctx->policy_active = true;
   return CHM_OK;
 }
 
+// Aligns run-time op i to a recorded op index: the next recorded op if its token matches; else
+// the first match within `match_window` recorded ops ahead (recorded ops were skipped); else -1
+// (an inserted op, e.g. on-the-fly validation or a conditional branch).
+static int32_t align_op(chm_ctx *ctx, int32_t token) {
+  const int32_t n = int32_t(ctx->rec_tokens.size());
+  const int32_t j0 = ctx->align_cursor;
+  for (int32_t j = j0; j < n && j <= j0 + ctx->match_window; j++) {
+    if (ctx->rec_tokens[j] == token) {
+      ctx->align_cursor = j + 1;
+      return j;
+    }
+  }
+  return -1;
+}
+
 chm_status executor_on_op(chm_ctx *ctx, const chm_op_record *op, int32_t i) {
   ctx->act_out.clear(); ctx->act_out_item.clear(); ctx->act_in.clear(); ctx->act_in_item.clear();
   ctx->act_release.clear(); ctx->act_wait.clear();
+  const int32_t ra = align_op(ctx, op->token);
   uint64_t seen[64];
   uint32_t n_seen = 0;
   auto visit = [&](const chm_tensor_ref &ref, bool is_out) {
     for (uint32_t q = 0; q < n_seen && q < 64; q++) if (seen[q] == ref.id) return;
+    const uint32_t slot = n_seen;
     if (n_seen < 64) seen[n_seen++] = ref.id;
     LiveTensor *lt;
     if (is_out) {
@@ -160,26 +181,18 @@ chm_status executor_on_op(chm_ctx *ctx, const chm_op_record *op, int32_t i) {
     } else {
       lt = &ctx->live[ref.id];
     }
-    feature_update(lt->f, op->token, ref.dtype, ctx);
-    if (op->phase != CHM_FWD || lt->item >= 0) return;
-    auto m = ctx->key_to_item.find(lt->f);
+    feature_update(lt->f, op->token, ref.dtype, slot, ctx);
+    if (op->phase != CHM_FWD || lt->item >= 0 || ra < 0) return;
+    FeatureAt key;
+    key.f = lt->f;
+    key.a = ra;
+    auto m = ctx->key_to_item.find(key);
     if (m == ctx->key_to_item.end()) return;
-    // App. A's four fields repeat for the same tensor role in every layer of a stacked model,
-    // so position is one more matching feature (the "..." of P:517, reading in DESIGN.md):
-    // take the untriggered item of this key whose recorded a_t is nearest to the current op,
-    // if it lies within the match window.
-    KeyItems &ki = m->second;
-    int32_t j = -1, dist = INT32_MAX;
-    for (int32_t cand : ki.items) {
-      const PolicyItem &c = ctx->items[cand];
-      if (c.state != IT_IDLE) continue;
-      const int32_t dd = c.a > i ? c.a - i : i - c.a;
-      if (dd < dist) { dist = dd; j = cand; }
-    }
-    if (j < 0 || dist > ctx->match_window) { ctx->stats.n_collisions++; return; }
+    const int32_t j = m->second;
     PolicyItem &it = ctx->items[j];
-    const uint64_t slot = (uint64_t(it.nbytes) + 511) & ~uint64_t(511);
-    if (uint64_t(ref.nbytes) > slot) return;  // larger than its arena slot: cannot swap
+    if (it.state != IT_IDLE) { ctx->stats.n_collisions++; return; }  // first one wins
+    const uint64_t slot_bytes = (uint64_t(it.nbytes) + 511) & ~uint64_t(511);
+    if (uint64_t(ref.nbytes) > slot_bytes) return;  // larger than its arena slot: cannot swap
     it.state = IT_OUT;
     it.cur_id = ref.id;
     it.cur_bytes = uint64_t(ref.nbytes);
@@ -192,21 +205,21 @@ chm_status executor_on_op(chm_ctx *ctx, const chm_op_record *op, int32_t i) {
   for (uint32_t j = 0; j < op->n_in; j++) visit(op->in[j], false);
   for (uint32_t j = 0; j < op->n_out; j++) visit(op->out[j], true);
   for (uint32_t j = 0; j < op->n_free; j++) ctx->live.erase(op->freed[j]);
-  if (size_t(i) < ctx->release_at.size()) {
-    for (int32_t j : ctx->release_at[i]) {
+  if (ra >= 0 && size_t(ra) < ctx->release_at.size()) {
+    for (int32_t j : ctx->release_at[ra]) {
       PolicyItem &it = ctx->items[j];
       if (it.state != IT_OUT) continue;
       it.state = IT_RELEASED;
       ctx->live.erase(it.cur_id);  // the caller drops the device storage after the wait
       ctx->act_release.push_back(uint32_t(j));
     }
-    for (int32_t j : ctx->swapin_at[i]) {
+    for (int32_t j : ctx->swapin_at[ra]) {
       PolicyItem &it = ctx->items[j];
       if (it.state != IT_RELEASED) continue;
       ctx->act_in.push_back({0, it.host_off, it.cur_bytes});
       ctx->act_in_item.push_back(uint32_t(j));
     }
-    for (int32_t j : ctx->wait_at[i]) {
+    for (int32_t j : ctx->wait_at[ra]) {
       PolicyItem &it = ctx->items[j];
       if (it.state == IT_IN) ctx->act_wait.push_back(uint32_t(j));  // s_t < b_t: issued
     }
@@ -223,6 +236,7 @@ void executor_end_iteration(chm_ctx *ctx) {
   }
   ctx->live.clear();
   ctx->op_cursor = 0;
+  ctx->align_cursor = 0;
 }
 
 extern "C" chm_status chm_exec_stats_get(chm_ctx *ctx, chm_exec_stats *s) {

@@ -58,19 +58,19 @@ struct IterRecord {
 };
 
 // --------------------------------------------------------------------------- executor
-struct Feature {  // App. A
+struct Feature {  // App. A + argument slot at the latest use (reading in DESIGN.md)
   uint32_t count = 0, tag = 0;
-  uint8_t dtype = 0;
+  uint8_t dtype = 0, slot = 0;
   uint64_t stack = 0;
   bool operator==(const Feature &o) const {
-    return count == o.count && tag == o.tag && dtype == o.dtype && stack == o.stack;
+    return count == o.count && tag == o.tag && dtype == o.dtype && stack == o.stack && slot == o.slot;
   }
 };
 struct FeatureHash {
   size_t operator()(const Feature &f) const {
     uint64_t h = f.stack * 0x9E3779B97F4A7C15ull;
     h ^= (uint64_t(f.count) << 32 | f.tag) + 0x7F4A7C15ull + (h << 6) + (h >> 2);
-    return size_t(h ^ f.dtype);
+    return size_t(h ^ (uint64_t(f.slot) << 8 | f.dtype));
   }
 };
 
@@ -87,8 +87,15 @@ struct PolicyItem {
   bool has_out = false, has_in = false;
 };
 
-struct KeyItems {
-  std::vector<int32_t> items;  // policy items with this key, ascending a_t
+struct FeatureAt {  // policy key: feature right after the recorded op a_t, and a_t itself
+  Feature f;
+  int32_t a = 0;
+  bool operator==(const FeatureAt &o) const { return a == o.a && f == o.f; }
+};
+struct FeatureAtHash {
+  size_t operator()(const FeatureAt &k) const {
+    return FeatureHash()(k.f) ^ (size_t(uint32_t(k.a)) * 0x9E3779B1u);
+  }
 };
 
 struct LiveTensor {
@@ -154,7 +161,9 @@ struct chm_ctx {
   std::unordered_map<uint64_t, int32_t> id_to_tensor;  // detailed recording
   // executor
   std::vector<chm::PolicyItem> items;
-  std::unordered_map<chm::Feature, chm::KeyItems, chm::FeatureHash> key_to_item;
+  std::unordered_map<chm::FeatureAt, int32_t, chm::FeatureAtHash> key_to_item;
+  std::vector<int32_t> rec_tokens;  // recorded token sequence (alignment of run-time ops)
+  int32_t align_cursor = 0;
   std::vector<uint8_t> op_index;   // token -> 8-bit index
   std::vector<uint32_t> op_onehot; // token -> one-hot
   std::unordered_map<uint64_t, chm::LiveTensor> live;

@@ -201,3 +201,33 @@ def test_executor_tolerates_minor_drift(where):
     ctx.detect_seq_change(tr.t_iter)
     assert ctx.exec_stats()["n_stale"] == 0
     assert n_fwd > 0
+
+
+@pytest.mark.parametrize("name,seed", [("C1", 0), ("C2", 1), ("C2", 2), ("C5", 3), ("C3", 4)])
+def test_executor_partial_policy_swaps_exactly_the_selected_tensors(name, seed):
+    """A random partial policy: every swap-out names the selected tensor's own storage (ids are
+    reused data_ptrs, so resolve them against the live tensor at that op) -- no same-role tensor of
+    a neighbouring layer or sibling output is swapped instead."""
+    tr = W.CONFIGS[name]()
+    m = O.Model(tr)
+    ctx = host_ctx()
+    pt = product_trace(ctx, tr)
+    rng = np.random.default_rng(seed)
+    words = np.zeros(pt.W, np.uint64)
+    sel = sorted(rng.choice(pt.K, size=max(1, pt.K // 3), replace=False).tolist())
+    for k in sel:
+        words[k // 64] |= np.uint64(1 << (k % 64))
+    ctx.policy_install(pt, words)
+    sw = m.swappable()
+    p, f, a, b = m.tensor_table()
+    got = []
+
+    def on(i, act):
+        av = chm.actions_view(act)
+        for (dev, off, nb), it in zip(av["swap_out"], av["swap_out_item"]):
+            live = [t for t in range(tr.n_tensors) if int(tr.ptr[t]) == dev and p[t] <= i <= f[t] and p[t] >= 0]
+            assert len(live) == 1
+            got.append((i, it, live[0]))
+    chm.record_iteration(ctx, tr, on_actions=on)
+    exp = sorted((int(a[sw["t"][k]]), j, int(sw["t"][k])) for j, k in enumerate(sel))
+    assert sorted(got) == exp
