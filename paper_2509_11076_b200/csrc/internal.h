@@ -104,13 +104,22 @@ struct LiveTensor {
 };
 
 // ---------------------------------------------------------------------------- trace
-struct DevTrace {  // device tables for the replay kernel
-  const int64_t *f0 = nullptr;
-  const int64_t *S = nullptr;
-  const int32_t *r1 = nullptr;  // r_t + 1
-  const int32_t *s = nullptr;
-  const int32_t *lin = nullptr, *lout = nullptr;
-  const double *bud = nullptr;
+// Device image of a trace for the replay kernel: one contiguous, 16 B-aligned block staged
+// into each CTA's shared memory with TMA bulk copies.  Search mode stages [0, search_bytes);
+// full mode also stages the per-op part [search_bytes, full_bytes).
+struct DevTrace {
+  const unsigned char *image = nullptr;
+  uint32_t search_bytes = 0, full_bytes = 0;
+  // byte offsets inside the image
+  uint32_t o_mf0 = 0;   // int64 [L]  max F0 over the ops of each logical layer
+  uint32_t o_bud = 0;   // double[L]  Eq. 1 budget
+  uint32_t o_S = 0;     // int64 [K]  swappable sizes (mask-bit order)
+  uint32_t o_po = 0;    // u16   [K]  mask bits sorted by lout (release layer)
+  uint32_t o_so = 0;    // u16   [K]  lout of that order
+  uint32_t o_pi = 0;    // u16   [K]  mask bits sorted by lin (swap-in layer)
+  uint32_t o_si = 0;    // u16   [K]  lin of that order
+  uint32_t o_f0 = 0;    // int64 [N]  no-swap footprint (full mode)
+  uint32_t o_lay = 0;   // u16   [N]  logical layer of each op (full mode)
   const uint64_t *base = nullptr;
   int32_t N = 0, K = 0, L = 0, W = 0;
   double bw = 1.0;

@@ -1,21 +1,25 @@
 // replay.cu -- policy evaluation (steps a4-a7): one candidate per CTA of a persistent grid.
 //
-// For candidate P (§5.4 simulator; readings SURVEY §8(c).2-.6):
-//   d_P[r_t + 1] -= S_t, d_P[s_t] += S_t for t in P      (release after r_t, swap-in before s_t)
-//   F_P = F0 + inclusive_scan(d_P)                       (per-op footprint)
-//   peak = max F_P, excess = max(0, peak - budget)
-//   load_l = sum_{t in P} S_t ([lin_t = l] + [lout_t = l]); stall = sum_l max(0, load_l/B - Bud_l)
-// and the argmin key (excess, stall, swapped, index) ("best runtime performance").
+// For candidate P (§5.4 simulator; readings SURVEY §8(c).2-.6) the event
+// replay gives F_P[i] = F0[i] - sum_{t in P} S_t [r_t < i < s_t].  With the solo timing of the
+// trace build every release r_t is the LAST op of layer lout_t ("completed within that
+// layer", reading Q6) and every swap-in s_t the FIRST op of layer lin_t (Q7), so the
+// offset is constant over each logical layer l:
+//   in_l  = sum_{t in P, lin_t = l} S_t,   out_l = sum_{t in P, lout_t = l} S_t
+//   D_l   = sum_{l' <= l} in_l' - sum_{l' < l} out_l'          (exact int64)
+//   F_P[i] = F0[i] + D_lay(i),   peak = max_l (max_{i in l} F0[i] + D_l)
+//   load_l = in_l + out_l,       stall = sum_l max(0, load_l / B - Bud_l), ascending l
+// -- the same integers as the event replay, in O(K + L) per candidate (+ O(N) to write the
+// footprint row in full mode).  Not a contraction: no tensor cores.  Full mode is bound by
+// the 8 B/op footprint write to HBM; search mode by the SEEDED hash decode (integer pipe).
 //
-// Not a contraction: no tensor cores.  The bound is the footprint write (full mode: 8 B per op
-// and candidate to HBM) or the SM integer pipe / shared memory (search mode).  Per candidate:
-//   zero the shared-memory delta row -> shared-memory int64 atomics for the selected items ->
-//   raking scan (each thread sums E contiguous elements, E odd so 8 B accesses are bank-
-//   conflict free) + warp shuffle scan of the per-thread sums + block scan of the warp sums ->
-//   F0 + prefix written back in place, max-reduced -> one cp.async.bulk (TMA bulk copy engine)
-//   shared->global store of the whole row, double-buffered so the next candidate's scan
-//   overlaps the previous store.  Stall: warp 0, positive terms only, in ascending layer order
-//   (bit-exact with the oracle's sequential sum; IEEE div/sub/add intrinsics, no contraction).
+// Per CTA: the trace image (layer maxima, budgets, sizes, lout/lin-sorted orders, F0, op->layer)
+// is staged once into shared memory by TMA bulk copies (cp.async.bulk + mbarrier).  Per
+// candidate: decode the mask (ballot), per-layer sums over the lout- and lin-sorted orders
+// (each thread a contiguous run, one shared atomic per run segment), warp 0 scans the L layer
+// offsets and forms peak / stall / key, then (full mode) all threads stream F0 + D_lay out with
+// 16 B streaming stores.  Stall terms are summed by one lane in ascending layer order with IEEE
+// div/sub/add intrinsics: bit-identical to the oracle's sequential loop.
 #include <algorithm>
 #include <climits>
 #include <cstring>
@@ -51,9 +55,8 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {  // splitmix64 finaliser
 struct EvalParams {
   DevTrace tr;
   int kind;
-  int E;          // contiguous row elements per thread (odd)
-  int row_ld;     // shared row stride in elements (even)
-  int fp_elems;   // elements written per footprint row (even, <= ld)
+  int Ek;         // contiguous sorted positions per thread in the per-layer sums
+  uint32_t stage_bytes;
   uint64_t first, count, seed, flip_thr;
   uint64_t base[kMaxSeededWords];
   const uint64_t *masks;
@@ -62,6 +65,7 @@ struct EvalParams {
   long long *swapped;
   long long *footprint;
   uint64_t ld;
+  int row_pairs;  // 16 B stores per footprint row (ceil(N / 2))
   Key *partial;
   unsigned int *ticket;
   Key *best;
@@ -77,98 +81,144 @@ __device__ __forceinline__ bool cand_bit(const EvalParams &p, uint64_t g, uint64
   return (__ldg(p.masks + c * uint64_t(p.tr.W) + uint64_t(k >> 6)) >> (k & 63)) & 1ull;
 }
 
-template <bool kFootprint>
+__device__ __forceinline__ void st_cs_v2(long long *dst, long long a, long long b) {
+  asm volatile("st.global.cs.v2.s64 [%0], {%1, %2};" ::"l"(dst), "l"(a), "l"(b) : "memory");
+}
+
+// stages [0, bytes) of the trace image into shared memory with TMA bulk copies on one mbarrier
+__device__ __forceinline__ void stage_image(unsigned char *dst, const unsigned char *src, uint32_t bytes,
+                                            uint64_t *mbar) {
+  const unsigned bar = static_cast<unsigned>(__cvta_generic_to_shared(mbar));
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    const unsigned sdst = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    for (uint32_t off = 0; off < bytes; off += 32768u) {
+      const uint32_t n = min(32768u, bytes - off);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sdst + off),
+          "l"(src + off), "r"(n), "r"(bar)
+          : "memory");
+    }
+  }
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(bar)
+        : "memory");
+  }
+}
+
+template <bool kFull>
 __global__ void __launch_bounds__(256) replay_kernel(const __grid_constant__ EvalParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ __align__(8) uint64_t s_mbar;
+  __shared__ long long s_red[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  const int N = p.tr.N, K = p.tr.K, L = p.tr.L;
-  long long *rows = reinterpret_cast<long long *>(smem);
-  long long *s_load = rows + (kFootprint ? 2 : 1) * p.row_ld;
+  const int N = p.tr.N, K = p.tr.K, L = p.tr.L, W = p.tr.W;
+  unsigned char *img = smem;
+  const long long *mf0 = reinterpret_cast<const long long *>(img + p.tr.o_mf0);
+  const double *bud = reinterpret_cast<const double *>(img + p.tr.o_bud);
+  const long long *S = reinterpret_cast<const long long *>(img + p.tr.o_S);
+  const unsigned short *po = reinterpret_cast<const unsigned short *>(img + p.tr.o_po);
+  const unsigned short *so = reinterpret_cast<const unsigned short *>(img + p.tr.o_so);
+  const unsigned short *pi = reinterpret_cast<const unsigned short *>(img + p.tr.o_pi);
+  const unsigned short *si = reinterpret_cast<const unsigned short *>(img + p.tr.o_si);
+  const long long *f0 = reinterpret_cast<const long long *>(img + p.tr.o_f0);
+  const unsigned short *lay = reinterpret_cast<const unsigned short *>(img + p.tr.o_lay);
+  unsigned long long *s_bits = reinterpret_cast<unsigned long long *>(img + p.stage_bytes);
+  long long *s_in = reinterpret_cast<long long *>(s_bits + ((W + 1) & ~1));
   const int L2 = (L + 1) & ~1;
-  long long *s_wtot = s_load + L2;    // [32] warp totals of the scan
-  long long *s_rmax = s_wtot + 32;    // [32]
-  long long *s_rsum = s_rmax + 32;    // [32]
+  long long *s_out = s_in + L2;
+  long long *s_D = s_out + L2;
+
+  stage_image(img, p.tr.image, p.stage_bytes, &s_mbar);
 
   Key best;
   best.excess = LLONG_MAX; best.stall = 0.0; best.swapped = LLONG_MAX; best.index = ~0ull; best.peak = 0;
-  int j = 0;
-  for (uint64_t c = blockIdx.x; c < p.count; c += gridDim.x, j++) {
+  for (uint64_t c = blockIdx.x; c < p.count; c += gridDim.x) {
     const uint64_t g = p.first + c;
-    long long *row = rows + (kFootprint ? (j & 1) * p.row_ld : 0);
-    if (kFootprint && tid == 0 && j >= 2)  // the store issued 2 candidates ago read this row
-      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-    __syncthreads();  // (A)
-    {
-      int4 *r4 = reinterpret_cast<int4 *>(row);
-      const int4 z = make_int4(0, 0, 0, 0);
-      for (int q = tid; q < (p.row_ld >> 1); q += blockDim.x) r4[q] = z;
-      for (int q = tid; q < L; q += blockDim.x) s_load[q] = 0;
+    __syncthreads();  // (A) previous candidate's readers of s_bits / s_in / s_out / s_D are done
+    for (int w = warp; w < W; w += nwarps) {  // mask decode: two ballots per 64-bit word
+      const int k0 = (w << 6) + lane, k1 = k0 + 32;
+      const unsigned lo = __ballot_sync(0xffffffffu, k0 < K && cand_bit(p, g, c, k0));
+      const unsigned hi = __ballot_sync(0xffffffffu, k1 < K && cand_bit(p, g, c, k1));
+      if (lane == 0) s_bits[w] = (unsigned long long)hi << 32 | lo;
     }
+    for (int l = tid; l < L; l += blockDim.x) { s_in[l] = 0; s_out[l] = 0; }
     __syncthreads();  // (B)
-    long long sw = 0;
-    for (int k = tid; k < K; k += blockDim.x) {
-      if (!cand_bit(p, g, c, k)) continue;
-      const long long S = __ldg(p.tr.S + k);
-      atomicAdd(reinterpret_cast<unsigned long long *>(row + __ldg(p.tr.r1 + k)), (unsigned long long)(-S));
-      atomicAdd(reinterpret_cast<unsigned long long *>(row + __ldg(p.tr.s + k)), (unsigned long long)S);
-      atomicAdd(reinterpret_cast<unsigned long long *>(s_load + __ldg(p.tr.lin + k)), (unsigned long long)S);
-      atomicAdd(reinterpret_cast<unsigned long long *>(s_load + __ldg(p.tr.lout + k)), (unsigned long long)S);
-      sw += S;
+    {  // per-layer sums: thread tid owns sorted positions [tid*Ek, tid*Ek + Ek)
+      const int q0 = tid * p.Ek, q1 = min(q0 + p.Ek, K);
+      long long acc = 0;
+      int seg = -1;
+      for (int q = q0; q < q1; q++) {
+        const int k = po[q], sg = so[q];
+        if (sg != seg) {
+          if (acc) atomicAdd(reinterpret_cast<unsigned long long *>(s_out + seg), (unsigned long long)acc);
+          acc = 0;
+          seg = sg;
+        }
+        if ((s_bits[k >> 6] >> (k & 63)) & 1ull) acc += S[k];
+      }
+      if (acc) atomicAdd(reinterpret_cast<unsigned long long *>(s_out + seg), (unsigned long long)acc);
+      acc = 0;
+      seg = -1;
+      for (int q = q0; q < q1; q++) {
+        const int k = pi[q], sg = si[q];
+        if (sg != seg) {
+          if (acc) atomicAdd(reinterpret_cast<unsigned long long *>(s_in + seg), (unsigned long long)acc);
+          acc = 0;
+          seg = sg;
+        }
+        if ((s_bits[k >> 6] >> (k & 63)) & 1ull) acc += S[k];
+      }
+      if (acc) atomicAdd(reinterpret_cast<unsigned long long *>(s_in + seg), (unsigned long long)acc);
     }
     __syncthreads();  // (C)
-    // raking scan: thread tid owns [tid*E, tid*E + E) of [0, N)
-    const int b0 = tid * p.E, b1 = min(b0 + p.E, N);
-    long long tot = 0;
-    for (int q = b0; q < b1; q++) tot += row[q];
-    long long incl = tot;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const long long y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane == 31) s_wtot[warp] = incl;
-    __syncthreads();  // (D)
-    long long x = incl - tot;
-    for (int w = 0; w < warp; w++) x += s_wtot[w];
-    long long mx = LLONG_MIN;
-    for (int q = b0; q < b1; q++) {
-      x += row[q];
-      const long long F = __ldg(p.tr.f0 + q) + x;
-      if (kFootprint) row[q] = F;
-      mx = max(mx, F);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      sw += __shfl_xor_sync(0xffffffffu, sw, o);
-    }
-    if (lane == 0) { s_rmax[warp] = mx; s_rsum[warp] = sw; }
-    if (kFootprint) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();  // (E)
-    if (kFootprint && tid == 0) {
-      long long *dst = p.footprint + c * p.ld;
-      const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(row));
-      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-                   ::"l"(dst), "r"(saddr), "r"(unsigned(p.fp_elems * 8))
-                   : "memory");
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    }
     if (warp == 0) {
-      double st = 0.0;
-      for (int l0 = 0; l0 < L; l0 += 32) {
-        const int l = l0 + lane;
+      // D_l = sum_{l' <= l} in_l' - sum_{l' < l} out_l': each lane a contiguous run of layers
+      const int cs = (L + 31) >> 5, l0 = lane * cs, l1 = min(l0 + cs, L);
+      long long tot = 0, swp = 0;
+      for (int l = l0; l < l1; l++) {
+        tot += s_in[l] - (l > 0 ? s_out[l - 1] : 0);
+        swp += s_out[l];
+      }
+      long long incl = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      long long x = incl - tot, pk = LLONG_MIN;
+      for (int l = l0; l < l1; l++) {
+        x += s_in[l] - (l > 0 ? s_out[l - 1] : 0);
+        if (kFull) s_D[l] = x;
+        pk = max(pk, mf0[l] + x);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        pk = max(pk, __shfl_xor_sync(0xffffffffu, pk, o));
+        swp += __shfl_xor_sync(0xffffffffu, swp, o);
+      }
+      double st = 0.0;  // ascending layers, positive terms only
+      for (int lb = 0; lb < L; lb += 32) {
+        const int l = lb + lane;
         double term = 0.0;
-        if (l < L) term = __dsub_rn(__ddiv_rn(double(s_load[l]), p.tr.bw), __ldg(p.tr.bud + l));
+        if (l < L) term = __dsub_rn(__ddiv_rn(double(s_in[l] + s_out[l]), p.tr.bw), bud[l]);
         unsigned m = __ballot_sync(0xffffffffu, term > 0.0);
-        while (m) {  // ascending l, positive terms only
+        while (m) {
           const int bl = __ffs(m) - 1;
           st = __dadd_rn(st, __shfl_sync(0xffffffffu, term, bl));
           m &= m - 1;
         }
       }
       if (lane == 0) {
-        long long pk = s_rmax[0], swp = s_rsum[0];
-        for (int w = 1; w < nwarps; w++) { pk = max(pk, s_rmax[w]); swp += s_rsum[w]; }
         if (p.peak) p.peak[c] = pk;
         if (p.stall) p.stall[c] = st;
         if (p.swapped) p.swapped[c] = swp;
@@ -181,8 +231,17 @@ __global__ void __launch_bounds__(256) replay_kernel(const __grid_constant__ Eva
         if (key_less(k, best)) best = k;
       }
     }
+    if (kFull) {
+      __syncthreads();  // (D) s_D visible
+      long long *row = p.footprint + c * p.ld;
+      for (int q = tid; q < p.row_pairs; q += blockDim.x) {
+        const int i = q << 1;
+        const long long v0 = f0[i] + s_D[lay[i]];
+        const long long v1 = (i + 1 < N) ? f0[i + 1] + s_D[lay[i + 1]] : 0;
+        st_cs_v2(row + i, v0, v1);
+      }
+    }
   }
-  if (kFootprint && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   // per-CTA key -> the last CTA to finish reduces all of them into *best
   __shared__ unsigned int s_last;
   if (tid == 0) {
@@ -192,6 +251,7 @@ __global__ void __launch_bounds__(256) replay_kernel(const __grid_constant__ Eva
     s_last = (t == gridDim.x - 1) ? 1u : 0u;
   }
   __syncthreads();
+  (void)s_red;
   if (!s_last || warp != 0) return;
   __threadfence();
   Key b;
@@ -241,17 +301,15 @@ __global__ void best_reduce_kernel(const Key *keys, uint32_t n, Key *out) {
 }  // namespace
 
 chm_status launch_eval(chm_ctx *ctx, const EvalLaunch &L, cudaStream_t stream) {
-  const int N = L.tr.N;
-  // block size: ~8 row elements per thread, 32..256 threads
-  int threads = ((N + 7) / 8 + 31) / 32 * 32;
+  const int N = L.tr.N, K = L.tr.K, Ly = L.tr.L, W = L.tr.W;
+  // block size: ~4 mask bits / row pairs per thread, 32..256 threads
+  int threads = ((std::max(K, (N + 1) / 2) + 3) / 4 + 31) / 32 * 32;
   threads = std::max(32, std::min(256, threads));
-  int E = (N + threads - 1) / threads;
-  if (E > 1 && (E & 1) == 0) E += 1;  // odd stride: conflict-free 8 B shared accesses
-  const int row_ld = (N + 1) & ~1;
   const bool fp = L.footprint != nullptr;
-  const int L2 = (L.tr.L + 1) & ~1;
-  const size_t smem = (size_t(fp ? 2 : 1) * row_ld + L2 + 96) * sizeof(long long);
-  if (smem > 200 * 1024) CHM_FAIL(CHM_E_INVAL, "chm_eval_policies: N = %d too large for one CTA row", N);
+  const uint32_t stage = fp ? L.tr.full_bytes : L.tr.search_bytes;
+  const int L2 = (Ly + 1) & ~1;
+  const size_t smem = size_t(stage) + 8 * size_t((W + 1) & ~1) + 3 * 8 * size_t(L2);
+  if (smem > 200 * 1024) CHM_FAIL(CHM_E_INVAL, "chm_eval_policies: trace image (%zu B) exceeds shared memory", smem);
   auto kern = fp ? replay_kernel<true> : replay_kernel<false>;
   CHM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   int per_sm = 0;
@@ -273,9 +331,9 @@ chm_status launch_eval(chm_ctx *ctx, const EvalLaunch &L, cudaStream_t stream) {
   EvalParams p{};
   p.tr = L.tr;
   p.kind = L.kind;
-  p.E = E;
-  p.row_ld = row_ld;
-  p.fp_elems = fp ? int(std::min<uint64_t>(uint64_t(row_ld), L.ld)) : 0;
+  p.Ek = std::max(1, (K + threads - 1) / threads);
+  p.stage_bytes = stage;
+  p.row_pairs = (N + 1) / 2;
   p.first = L.first;
   p.count = L.count;
   p.seed = L.seed;

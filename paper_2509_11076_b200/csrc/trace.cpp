@@ -2,6 +2,7 @@
 // (Eq. 1), solo swap timing (Eq. 3, P:333 swap-in placement, P:340 swap-out completion),
 // swappable set, default SEEDED base; upload of the device tables for the replay kernel.
 #include <algorithm>
+#include <climits>
 #include <cstring>
 #include <numeric>
 
@@ -146,25 +147,61 @@ extern "C" chm_status chm_trace_build(chm_ctx *ctx, const chm_trace_params *P, c
   for (int32_t k = 0; k < tr->K; k++) sw_tensor[k] = cands[k].t;
   tr->sw_tensor_idx = std::move(sw_tensor);
 
-  // device tables in one allocation, each array 256 B aligned
-  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-  const size_t o_f0 = 0, o_S = o_f0 + al(8 * size_t(N)), o_r1 = o_S + al(8 * size_t(tr->K)),
-               o_s = o_r1 + al(4 * size_t(tr->K)), o_lin = o_s + al(4 * size_t(tr->K)),
-               o_lout = o_lin + al(4 * size_t(tr->K)), o_bud = o_lout + al(4 * size_t(tr->K)),
-               o_base = o_bud + al(8 * size_t(tr->L)), total = o_base + al(8 * size_t(tr->W) + 8);
-  std::vector<char> host(total, 0);
-  std::memcpy(host.data() + o_f0, tr->F0.data(), 8 * size_t(N));
-  std::vector<int32_t> r1(tr->K);
-  for (int32_t k = 0; k < tr->K; k++) r1[k] = tr->sw_r[k] + 1;
-  if (tr->K) {
-    std::memcpy(host.data() + o_S, tr->sw_S.data(), 8 * size_t(tr->K));
-    std::memcpy(host.data() + o_r1, r1.data(), 4 * size_t(tr->K));
-    std::memcpy(host.data() + o_s, tr->sw_s.data(), 4 * size_t(tr->K));
-    std::memcpy(host.data() + o_lin, tr->sw_lin.data(), 4 * size_t(tr->K));
-    std::memcpy(host.data() + o_lout, tr->sw_lout.data(), 4 * size_t(tr->K));
+  // replay image (see DevTrace): with solo timing every release r_t is the last op of layer
+  // lout_t and every swap-in s_t the first op of layer lin_t, so a candidate's footprint offset
+  // is constant per logical layer; the image holds what the kernel needs for that form
+  if (tr->K > 65535 || tr->L > 65535) {
+    chm_trace_free(tr);
+    CHM_FAIL(CHM_E_INVAL, "chm_trace_build: K = %d / L = %d exceed the replay image's u16 tables", tr->K, tr->L);
   }
-  if (tr->L) std::memcpy(host.data() + o_bud, tr->bud.data(), 8 * size_t(tr->L));
-  if (tr->W) std::memcpy(host.data() + o_base, tr->base.data(), 8 * size_t(tr->W));
+  auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+  DevTrace &D = tr->dev;
+  size_t o = 0;
+  D.o_mf0 = uint32_t(o); o += al(8 * size_t(tr->L));
+  D.o_bud = uint32_t(o); o += al(8 * size_t(tr->L));
+  D.o_S = uint32_t(o); o += al(8 * size_t(tr->K));
+  D.o_po = uint32_t(o); o += al(2 * size_t(tr->K));
+  D.o_so = uint32_t(o); o += al(2 * size_t(tr->K));
+  D.o_pi = uint32_t(o); o += al(2 * size_t(tr->K));
+  D.o_si = uint32_t(o); o += al(2 * size_t(tr->K));
+  D.search_bytes = uint32_t(o);
+  D.o_f0 = uint32_t(o); o += al(8 * size_t(N));
+  D.o_lay = uint32_t(o); o += al(2 * size_t(N));
+  D.full_bytes = uint32_t(o);
+  const size_t o_base = al(o);
+  const size_t total = o_base + al(8 * size_t(tr->W) + 8);
+  std::vector<unsigned char> host(total, 0);
+  unsigned char *h = host.data();
+  std::vector<int64_t> mf0(size_t(tr->L), INT64_MIN);
+  for (int32_t i = 0; i < N; i++) mf0[tr->lay_of_op[i]] = std::max(mf0[tr->lay_of_op[i]], tr->F0[i]);
+  std::memcpy(h + D.o_mf0, mf0.data(), 8 * size_t(tr->L));
+  std::memcpy(h + D.o_bud, tr->bud.data(), 8 * size_t(tr->L));
+  if (tr->K) std::memcpy(h + D.o_S, tr->sw_S.data(), 8 * size_t(tr->K));
+  std::vector<uint16_t> po(tr->K), pi(tr->K), so(tr->K), si(tr->K);
+  for (int32_t k = 0; k < tr->K; k++) po[k] = pi[k] = uint16_t(k);
+  std::stable_sort(po.begin(), po.end(), [&](uint16_t x, uint16_t y) { return tr->sw_lout[x] < tr->sw_lout[y]; });
+  std::stable_sort(pi.begin(), pi.end(), [&](uint16_t x, uint16_t y) { return tr->sw_lin[x] < tr->sw_lin[y]; });
+  for (int32_t q = 0; q < tr->K; q++) {
+    so[q] = uint16_t(tr->sw_lout[po[q]]);
+    si[q] = uint16_t(tr->sw_lin[pi[q]]);
+  }
+  if (tr->K) {
+    std::memcpy(h + D.o_po, po.data(), 2 * size_t(tr->K));
+    std::memcpy(h + D.o_so, so.data(), 2 * size_t(tr->K));
+    std::memcpy(h + D.o_pi, pi.data(), 2 * size_t(tr->K));
+    std::memcpy(h + D.o_si, si.data(), 2 * size_t(tr->K));
+  }
+  std::memcpy(h + D.o_f0, tr->F0.data(), 8 * size_t(N));
+  std::vector<uint16_t> lay16(N);
+  for (int32_t i = 0; i < N; i++) lay16[i] = uint16_t(tr->lay_of_op[i]);
+  std::memcpy(h + D.o_lay, lay16.data(), 2 * size_t(N));
+  if (tr->W) std::memcpy(h + o_base, tr->base.data(), 8 * size_t(tr->W));
+  D.N = N;
+  D.K = tr->K;
+  D.L = tr->L;
+  D.W = tr->W;
+  D.bw = tr->bw;
+  D.budget = tr->budget;
   if (ctx->device < 0) {  // host-only ctx: tables stay on the host
     *out = tr;
     return CHM_OK;
@@ -176,21 +213,8 @@ extern "C" chm_status chm_trace_build(chm_ctx *ctx, const chm_trace_params *P, c
     chm_trace_free(tr);
     CHM_FAIL(CHM_E_CUDA, "chm_trace_build: device upload failed: %s", cudaGetErrorString(e));
   }
-  char *d = static_cast<char *>(tr->dev_block);
-  tr->dev.f0 = reinterpret_cast<const int64_t *>(d + o_f0);
-  tr->dev.S = reinterpret_cast<const int64_t *>(d + o_S);
-  tr->dev.r1 = reinterpret_cast<const int32_t *>(d + o_r1);
-  tr->dev.s = reinterpret_cast<const int32_t *>(d + o_s);
-  tr->dev.lin = reinterpret_cast<const int32_t *>(d + o_lin);
-  tr->dev.lout = reinterpret_cast<const int32_t *>(d + o_lout);
-  tr->dev.bud = reinterpret_cast<const double *>(d + o_bud);
-  tr->dev.base = reinterpret_cast<const uint64_t *>(d + o_base);
-  tr->dev.N = N;
-  tr->dev.K = tr->K;
-  tr->dev.L = tr->L;
-  tr->dev.W = tr->W;
-  tr->dev.bw = tr->bw;
-  tr->dev.budget = tr->budget;
+  D.image = static_cast<const unsigned char *>(tr->dev_block);
+  D.base = reinterpret_cast<const uint64_t *>(static_cast<char *>(tr->dev_block) + o_base);
   *out = tr;
   return CHM_OK;
 }
