@@ -198,7 +198,8 @@ typedef struct {
   int64_t *peak;           /* device [count] or NULL                                    */
   double *stall;           /* device [count] or NULL                                    */
   int64_t *swapped;        /* device [count] or NULL                                    */
-  int64_t *footprint;      /* device [count][ld] or NULL (full mode: F_P per op)        */
+  int64_t *footprint;      /* device [count][ld] or NULL (full mode: F_P per op; the
+                              entries [n_ops, ld) of a row are unspecified)            */
   uint32_t ld;             /* leading dimension of footprint, >= n_ops, even            */
   chm_best *best;          /* device, 1 element (required)                              */
 } chm_eval_out;

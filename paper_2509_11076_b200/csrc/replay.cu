@@ -82,7 +82,7 @@ __device__ __forceinline__ bool cand_bit(const EvalParams &p, uint64_t g, uint64
 }
 
 __device__ __forceinline__ void st_cs_v2(long long *dst, long long a, long long b) {
-  asm volatile("st.global.cs.v2.s64 [%0], {%1, %2};" ::"l"(dst), "l"(a), "l"(b) : "memory");
+  asm volatile("st.global.cs.v2.s64 [%0], {%1, %2};" ::"l"(dst), "l"(a), "l"(b));
 }
 
 // stages [0, bytes) of the trace image into shared memory with TMA bulk copies on one mbarrier
@@ -116,105 +116,111 @@ __device__ __forceinline__ void stage_image(unsigned char *dst, const unsigned c
 }
 
 template <bool kFull>
-__global__ void __launch_bounds__(256) replay_kernel(const __grid_constant__ EvalParams p) {
+__global__ void __launch_bounds__(256, 4) replay_kernel(const __grid_constant__ EvalParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ __align__(8) uint64_t s_mbar;
-  __shared__ long long s_red[2];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  const int N = p.tr.N, K = p.tr.K, L = p.tr.L, W = p.tr.W;
+  __shared__ long long s_wtot[2][32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int N = p.tr.N, K = p.tr.K, L = p.tr.L;
   unsigned char *img = smem;
   const long long *mf0 = reinterpret_cast<const long long *>(img + p.tr.o_mf0);
   const double *bud = reinterpret_cast<const double *>(img + p.tr.o_bud);
-  const long long *S = reinterpret_cast<const long long *>(img + p.tr.o_S);
   const unsigned short *po = reinterpret_cast<const unsigned short *>(img + p.tr.o_po);
   const unsigned short *so = reinterpret_cast<const unsigned short *>(img + p.tr.o_so);
   const unsigned short *pi = reinterpret_cast<const unsigned short *>(img + p.tr.o_pi);
   const unsigned short *si = reinterpret_cast<const unsigned short *>(img + p.tr.o_si);
+  const long long *Spo = reinterpret_cast<const long long *>(img + p.tr.o_Spo);
+  const long long *Spi = reinterpret_cast<const long long *>(img + p.tr.o_Spi);
+  const int *eo = reinterpret_cast<const int *>(img + p.tr.o_eo);
+  const int *ei = reinterpret_cast<const int *>(img + p.tr.o_ei);
   const long long *f0 = reinterpret_cast<const long long *>(img + p.tr.o_f0);
   const unsigned short *lay = reinterpret_cast<const unsigned short *>(img + p.tr.o_lay);
-  unsigned long long *s_bits = reinterpret_cast<unsigned long long *>(img + p.stage_bytes);
-  long long *s_in = reinterpret_cast<long long *>(s_bits + ((W + 1) & ~1));
-  const int L2 = (L + 1) & ~1;
-  long long *s_out = s_in + L2;
-  long long *s_D = s_out + L2;
+  unsigned char *s_flag = img + p.stage_bytes;                                     // [K]
+  long long *s_Po = reinterpret_cast<long long *>(s_flag + ((K + 15) & ~15));     // [K] cumulative, lout order
+  long long *s_Pi = s_Po + ((K + 1) & ~1);                                         // [K] cumulative, lin order
+  long long *s_D = s_Pi + ((K + 1) & ~1);                                          // [L] layer offsets
 
   stage_image(img, p.tr.image, p.stage_bytes, &s_mbar);
 
+  const int q0 = tid * p.Ek, q1 = min(q0 + p.Ek, K);  // this thread's run of sorted positions
   Key best;
   best.excess = LLONG_MAX; best.stall = 0.0; best.swapped = LLONG_MAX; best.index = ~0ull; best.peak = 0;
   for (uint64_t c = blockIdx.x; c < p.count; c += gridDim.x) {
     const uint64_t g = p.first + c;
-    __syncthreads();  // (A) previous candidate's readers of s_bits / s_in / s_out / s_D are done
-    for (int w = warp; w < W; w += nwarps) {  // mask decode: two ballots per 64-bit word
-      const int k0 = (w << 6) + lane, k1 = k0 + 32;
-      const unsigned lo = __ballot_sync(0xffffffffu, k0 < K && cand_bit(p, g, c, k0));
-      const unsigned hi = __ballot_sync(0xffffffffu, k1 < K && cand_bit(p, g, c, k1));
-      if (lane == 0) s_bits[w] = (unsigned long long)hi << 32 | lo;
-    }
-    for (int l = tid; l < L; l += blockDim.x) { s_in[l] = 0; s_out[l] = 0; }
+    __syncthreads();  // (A) the previous candidate's readers are done
+    for (int k = tid; k < K; k += blockDim.x) s_flag[k] = cand_bit(p, g, c, k) ? 1 : 0;
     __syncthreads();  // (B)
-    {  // per-layer sums: thread tid owns sorted positions [tid*Ek, tid*Ek + Ek)
-      const int q0 = tid * p.Ek, q1 = min(q0 + p.Ek, K);
-      long long acc = 0;
-      int seg = -1;
-      for (int q = q0; q < q1; q++) {
-        const int k = po[q], sg = so[q];
-        if (sg != seg) {
-          if (acc) atomicAdd(reinterpret_cast<unsigned long long *>(s_out + seg), (unsigned long long)acc);
-          acc = 0;
-          seg = sg;
-        }
-        if ((s_bits[k >> 6] >> (k & 63)) & 1ull) acc += S[k];
-      }
-      if (acc) atomicAdd(reinterpret_cast<unsigned long long *>(s_out + seg), (unsigned long long)acc);
-      acc = 0;
-      seg = -1;
-      for (int q = q0; q < q1; q++) {
-        const int k = pi[q], sg = si[q];
-        if (sg != seg) {
-          if (acc) atomicAdd(reinterpret_cast<unsigned long long *>(s_in + seg), (unsigned long long)acc);
-          acc = 0;
-          seg = sg;
-        }
-        if ((s_bits[k >> 6] >> (k & 63)) & 1ull) acc += S[k];
-      }
-      if (acc) atomicAdd(reinterpret_cast<unsigned long long *>(s_in + seg), (unsigned long long)acc);
+    // inclusive scans of the selected sizes over the lout- and lin-sorted orders
+    long long to = 0, ti = 0;
+    for (int q = q0; q < q1; q++) {
+      to += s_flag[po[q]] ? Spo[q] : 0;
+      ti += s_flag[pi[q]] ? Spi[q] : 0;
     }
+    long long io = to, ii = ti;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long yo = __shfl_up_sync(0xffffffffu, io, o);
+      const long long yi = __shfl_up_sync(0xffffffffu, ii, o);
+      if (lane >= o) { io += yo; ii += yi; }
+    }
+    if (lane == 31) { s_wtot[0][warp] = io; s_wtot[1][warp] = ii; }
     __syncthreads();  // (C)
+    long long xo = io - to, xi = ii - ti;
+    for (int w = 0; w < warp; w++) { xo += s_wtot[0][w]; xi += s_wtot[1][w]; }
+    for (int q = q0; q < q1; q++) {  // keep the running sum at the end of every layer's segment
+      xo += s_flag[po[q]] ? Spo[q] : 0;
+      xi += s_flag[pi[q]] ? Spi[q] : 0;
+      const bool last = q + 1 == K;
+      if (last || so[q] != so[q + 1]) s_Po[q] = xo;
+      if (last || si[q] != si[q + 1]) s_Pi[q] = xi;
+    }
+    __syncthreads();  // (D)
+    // per layer l: CO(l) / CI(l) = selected bytes released / swapped in through layer l;
+    // in_l = CI(l) - CI(l-1), out_l = CO(l) - CO(l-1), D_l = CI(l) - CO(l-1)
+    long long pk = LLONG_MIN, swp = 0;
+    double term[4] = {0.0, 0.0, 0.0, 0.0};
     if (warp == 0) {
-      // D_l = sum_{l' <= l} in_l' - sum_{l' < l} out_l': each lane a contiguous run of layers
-      const int cs = (L + 31) >> 5, l0 = lane * cs, l1 = min(l0 + cs, L);
-      long long tot = 0, swp = 0;
-      for (int l = l0; l < l1; l++) {
-        tot += s_in[l] - (l > 0 ? s_out[l - 1] : 0);
-        swp += s_out[l];
-      }
-      long long incl = tot;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const long long y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
+      for (int j = 0; j < 4; j++) {
+        const int l = lane + 32 * j;
+        if (l < L) {
+          const long long co = eo[l] >= 0 ? s_Po[eo[l]] : 0;
+          const long long co1 = (l > 0 && eo[l - 1] >= 0) ? s_Po[eo[l - 1]] : 0;
+          const long long ci = ei[l] >= 0 ? s_Pi[ei[l]] : 0;
+          const long long ci1 = (l > 0 && ei[l - 1] >= 0) ? s_Pi[ei[l - 1]] : 0;
+          const long long d = ci - co1;
+          if (kFull) s_D[l] = d;
+          pk = max(pk, mf0[l] + d);
+          term[j] = __dsub_rn(__ddiv_rn(double((ci - ci1) + (co - co1)), p.tr.bw), bud[l]);
+        }
       }
-      long long x = incl - tot, pk = LLONG_MIN;
-      for (int l = l0; l < l1; l++) {
-        x += s_in[l] - (l > 0 ? s_out[l - 1] : 0);
-        if (kFull) s_D[l] = x;
-        pk = max(pk, mf0[l] + x);
+      for (int l = lane + 128; l < L; l += 32) {  // L > 128
+        const long long co1 = eo[l - 1] >= 0 ? s_Po[eo[l - 1]] : 0;
+        const long long ci = ei[l] >= 0 ? s_Pi[ei[l]] : 0;
+        const long long d = ci - co1;
+        if (kFull) s_D[l] = d;
+        pk = max(pk, mf0[l] + d);
       }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        pk = max(pk, __shfl_xor_sync(0xffffffffu, pk, o));
-        swp += __shfl_xor_sync(0xffffffffu, swp, o);
-      }
+      for (int o = 16; o > 0; o >>= 1) pk = max(pk, __shfl_xor_sync(0xffffffffu, pk, o));
+      swp = (K > 0 && eo[L - 1] >= 0) ? s_Po[eo[L - 1]] : 0;
+    }
+    if (kFull) __syncthreads();  // (E) s_D visible; warp 0's stall sum overlaps the row stream
+    if (warp == 0) {
       double st = 0.0;  // ascending layers, positive terms only
-      for (int lb = 0; lb < L; lb += 32) {
-        const int l = lb + lane;
-        double term = 0.0;
-        if (l < L) term = __dsub_rn(__ddiv_rn(double(s_in[l] + s_out[l]), p.tr.bw), bud[l]);
-        unsigned m = __ballot_sync(0xffffffffu, term > 0.0);
+      for (int j = 0; j * 32 < L; j++) {
+        double t = 0.0;
+        if (j < 4) t = j == 0 ? term[0] : j == 1 ? term[1] : j == 2 ? term[2] : term[3];
+        else if (j * 32 + lane < L) {  // L > 128: recompute beyond the register cache
+          const int l = j * 32 + lane;
+          const long long co = eo[l] >= 0 ? s_Po[eo[l]] : 0, co1 = eo[l - 1] >= 0 ? s_Po[eo[l - 1]] : 0;
+          const long long ci = ei[l] >= 0 ? s_Pi[ei[l]] : 0, ci1 = ei[l - 1] >= 0 ? s_Pi[ei[l - 1]] : 0;
+          t = __dsub_rn(__ddiv_rn(double((ci - ci1) + (co - co1)), p.tr.bw), bud[l]);
+        }
+        unsigned m = __ballot_sync(0xffffffffu, t > 0.0);
         while (m) {
           const int bl = __ffs(m) - 1;
-          st = __dadd_rn(st, __shfl_sync(0xffffffffu, term, bl));
+          st = __dadd_rn(st, __shfl_sync(0xffffffffu, t, bl));
           m &= m - 1;
         }
       }
@@ -232,13 +238,14 @@ __global__ void __launch_bounds__(256) replay_kernel(const __grid_constant__ Eva
       }
     }
     if (kFull) {
-      __syncthreads();  // (D) s_D visible
       long long *row = p.footprint + c * p.ld;
-      for (int q = tid; q < p.row_pairs; q += blockDim.x) {
-        const int i = q << 1;
-        const long long v0 = f0[i] + s_D[lay[i]];
-        const long long v1 = (i + 1 < N) ? f0[i + 1] + s_D[lay[i + 1]] : 0;
-        st_cs_v2(row + i, v0, v1);
+      const longlong2 *f2 = reinterpret_cast<const longlong2 *>(f0);
+      const ushort2 *l2 = reinterpret_cast<const ushort2 *>(lay);
+      const int np = p.row_pairs;
+      for (int q = tid; q < np; q += blockDim.x) {
+        const longlong2 f = f2[q];
+        const ushort2 ly = l2[q];
+        st_cs_v2(row + 2 * q, f.x + s_D[ly.x], f.y + s_D[ly.y]);
       }
     }
   }
@@ -251,7 +258,6 @@ __global__ void __launch_bounds__(256) replay_kernel(const __grid_constant__ Eva
     s_last = (t == gridDim.x - 1) ? 1u : 0u;
   }
   __syncthreads();
-  (void)s_red;
   if (!s_last || warp != 0) return;
   __threadfence();
   Key b;
@@ -307,8 +313,8 @@ chm_status launch_eval(chm_ctx *ctx, const EvalLaunch &L, cudaStream_t stream) {
   threads = std::max(32, std::min(256, threads));
   const bool fp = L.footprint != nullptr;
   const uint32_t stage = fp ? L.tr.full_bytes : L.tr.search_bytes;
-  const int L2 = (Ly + 1) & ~1;
-  const size_t smem = size_t(stage) + 8 * size_t((W + 1) & ~1) + 3 * 8 * size_t(L2);
+  const size_t smem = size_t(stage) + size_t((K + 15) & ~15) + 2 * 8 * size_t((K + 1) & ~1) + 8 * size_t(Ly + 1);
+  (void)W;
   if (smem > 200 * 1024) CHM_FAIL(CHM_E_INVAL, "chm_eval_policies: trace image (%zu B) exceeds shared memory", smem);
   auto kern = fp ? replay_kernel<true> : replay_kernel<false>;
   CHM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -332,6 +338,7 @@ chm_status launch_eval(chm_ctx *ctx, const EvalLaunch &L, cudaStream_t stream) {
   p.tr = L.tr;
   p.kind = L.kind;
   p.Ek = std::max(1, (K + threads - 1) / threads);
+  if (p.Ek > 1 && (p.Ek & 1) == 0) p.Ek += 1;  // odd run length: conflict-free 8 B shared reads
   p.stage_bytes = stage;
   p.row_pairs = (N + 1) / 2;
   p.first = L.first;

@@ -150,9 +150,13 @@ extern "C" chm_status chm_trace_build(chm_ctx *ctx, const chm_trace_params *P, c
   // replay image (see DevTrace): with solo timing every release r_t is the last op of layer
   // lout_t and every swap-in s_t the first op of layer lin_t, so a candidate's footprint offset
   // is constant per logical layer; the image holds what the kernel needs for that form
-  if (tr->K > 65535 || tr->L > 65535) {
+  // bounds of the kernel's exact 32-bit partial sums (hi = S >> 16, lo = S & 0xffff)
+  int64_t sum_S = 0;
+  for (int32_t k = 0; k < tr->K; k++) sum_S += tr->sw_S[k];
+  if (tr->K > 32767 || tr->L > 65535 || sum_S >= (int64_t(1) << 47)) {
     chm_trace_free(tr);
-    CHM_FAIL(CHM_E_INVAL, "chm_trace_build: K = %d / L = %d exceed the replay image's u16 tables", tr->K, tr->L);
+    CHM_FAIL(CHM_E_INVAL, "chm_trace_build: K = %d, L = %d, sum S = %lld exceed the replay image bounds "
+             "(K < 32768, L < 65536, sum S < 2^47)", tr->K, tr->L, (long long)sum_S);
   }
   auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
   DevTrace &D = tr->dev;
@@ -164,6 +168,10 @@ extern "C" chm_status chm_trace_build(chm_ctx *ctx, const chm_trace_params *P, c
   D.o_so = uint32_t(o); o += al(2 * size_t(tr->K));
   D.o_pi = uint32_t(o); o += al(2 * size_t(tr->K));
   D.o_si = uint32_t(o); o += al(2 * size_t(tr->K));
+  D.o_Spo = uint32_t(o); o += al(8 * size_t(tr->K));
+  D.o_Spi = uint32_t(o); o += al(8 * size_t(tr->K));
+  D.o_eo = uint32_t(o); o += al(4 * size_t(tr->L));
+  D.o_ei = uint32_t(o); o += al(4 * size_t(tr->L));
   D.search_bytes = uint32_t(o);
   D.o_f0 = uint32_t(o); o += al(8 * size_t(N));
   D.o_lay = uint32_t(o); o += al(2 * size_t(N));
@@ -185,7 +193,22 @@ extern "C" chm_status chm_trace_build(chm_ctx *ctx, const chm_trace_params *P, c
     so[q] = uint16_t(tr->sw_lout[po[q]]);
     si[q] = uint16_t(tr->sw_lin[pi[q]]);
   }
+  std::vector<int64_t> Spo(tr->K), Spi(tr->K);
+  for (int32_t q = 0; q < tr->K; q++) { Spo[q] = tr->sw_S[po[q]]; Spi[q] = tr->sw_S[pi[q]]; }
+  std::vector<int32_t> eo(size_t(tr->L), -1), ei(size_t(tr->L), -1);
+  for (int32_t l = 0, q = -1; l < tr->L; l++) {
+    while (q + 1 < tr->K && so[q + 1] <= l) q++;
+    eo[l] = q;
+  }
+  for (int32_t l = 0, q = -1; l < tr->L; l++) {
+    while (q + 1 < tr->K && si[q + 1] <= l) q++;
+    ei[l] = q;
+  }
+  std::memcpy(h + D.o_eo, eo.data(), 4 * size_t(tr->L));
+  std::memcpy(h + D.o_ei, ei.data(), 4 * size_t(tr->L));
   if (tr->K) {
+    std::memcpy(h + D.o_Spo, Spo.data(), 8 * size_t(tr->K));
+    std::memcpy(h + D.o_Spi, Spi.data(), 8 * size_t(tr->K));
     std::memcpy(h + D.o_po, po.data(), 2 * size_t(tr->K));
     std::memcpy(h + D.o_so, so.data(), 2 * size_t(tr->K));
     std::memcpy(h + D.o_pi, pi.data(), 2 * size_t(tr->K));
