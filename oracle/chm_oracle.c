@@ -102,11 +102,20 @@ static int64_t replay_items(const orc_model *m, replay_scratch *w, int32_t n_ite
 }
 
 /* ---------------------------------------------------------------------------------------
- * Estimated stall, SURVEY §8(c).5 (the paper gives no formula: reading Q11).
+ * Estimated stall, SURVEY §8(c).5 / DESIGN.md reading R-stall (the paper gives no formula,
+ * reading Q11).
  *   load_l = sum over items of S_t*([lin_t == l] + [lout_t == l])  (swap-in charged to its
  *            placement layer; swap-out to its completion layer)
- *   stall  = sum over l ascending of max(0, load_l / B - Bud_l)       ("introduce latency")
+ *   term_l = max(0, load_l / B - Bud_l)                               ("introduce latency")
+ *   stall  = pairwise sum of term_0 .. term_{L-1}: the index range, padded with +0.0 to a power
+ *            of two, is halved recursively and the two halves' sums are added.  A fixed order,
+ *            so every implementation rounds identically.
  * ------------------------------------------------------------------------------------- */
+static double pairwise_sum(const double *v, int32_t lo, int32_t n) {
+  if (n == 1) return v[lo];
+  return pairwise_sum(v, lo, n / 2) + pairwise_sum(v, lo + n / 2, n / 2);
+}
+
 static double stall_items(const orc_model *m, int64_t *load, int32_t n_items, const int32_t *t,
                           const int32_t *r, const int32_t *s) {
   for (int32_t l = 0; l < m->L; l++) load[l] = 0;
@@ -114,11 +123,15 @@ static double stall_items(const orc_model *m, int64_t *load, int32_t n_items, co
     load[m->lay_of_op[s[k]]] += m->S[t[k]];
     load[m->lay_of_op[r[k]]] += m->S[t[k]];
   }
-  double stall = 0.0;
+  int32_t P = 1;
+  while (P < m->L) P *= 2;
+  double *term = xcalloc((size_t)P, sizeof(double)); /* zero padded */
   for (int32_t l = 0; l < m->L; l++) {
-    double term = (double)load[l] / m->bw - m->bud[l];
-    if (term > 0.0) stall = stall + term;
+    double x = (double)load[l] / m->bw - m->bud[l];
+    term[l] = x > 0.0 ? x : 0.0;
   }
+  double stall = pairwise_sum(term, 0, P);
+  free(term);
   return stall;
 }
 

@@ -178,52 +178,39 @@ __global__ void __launch_bounds__(256, 4) replay_kernel(const __grid_constant__ 
     // per layer l: CO(l) / CI(l) = selected bytes released / swapped in through layer l;
     // in_l = CI(l) - CI(l-1), out_l = CO(l) - CO(l-1), D_l = CI(l) - CO(l-1)
     long long pk = LLONG_MIN, swp = 0;
-    double term[4] = {0.0, 0.0, 0.0, 0.0};
+    double st = 0.0;
     if (warp == 0) {
+      // lanes own layers l = lane + 32 j; term_l = max(0, load_l / B - Bud_l) is summed with the
+      // pairwise (recursive halving) tree of reading R-stall: xor butterflies 1..16 give the
+      // tree over each 32-layer chunk in every lane, then a fixed tree over the 8 chunks
+      double cs[8];
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
-        const int l = lane + 32 * j;
-        if (l < L) {
-          const long long co = eo[l] >= 0 ? s_Po[eo[l]] : 0;
-          const long long co1 = (l > 0 && eo[l - 1] >= 0) ? s_Po[eo[l - 1]] : 0;
-          const long long ci = ei[l] >= 0 ? s_Pi[ei[l]] : 0;
-          const long long ci1 = (l > 0 && ei[l - 1] >= 0) ? s_Pi[ei[l - 1]] : 0;
-          const long long d = ci - co1;
-          if (kFull) s_D[l] = d;
-          pk = max(pk, mf0[l] + d);
-          term[j] = __dsub_rn(__ddiv_rn(double((ci - ci1) + (co - co1)), p.tr.bw), bud[l]);
+      for (int j = 0; j < 8; j++) {
+        cs[j] = 0.0;
+        if (32 * j < L) {
+          const int l = lane + 32 * j;
+          double t = 0.0;
+          if (l < L) {
+            const long long co = eo[l] >= 0 ? s_Po[eo[l]] : 0;
+            const long long co1 = (l > 0 && eo[l - 1] >= 0) ? s_Po[eo[l - 1]] : 0;
+            const long long ci = ei[l] >= 0 ? s_Pi[ei[l]] : 0;
+            const long long ci1 = (l > 0 && ei[l - 1] >= 0) ? s_Pi[ei[l - 1]] : 0;
+            const long long d = ci - co1;
+            if (kFull) s_D[l] = d;
+            pk = max(pk, mf0[l] + d);
+            const double x = __dsub_rn(__ddiv_rn(double((ci - ci1) + (co - co1)), p.tr.bw), bud[l]);
+            t = x > 0.0 ? x : 0.0;
+          }
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) t = __dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, o));
+          cs[j] = t;
         }
       }
-      for (int l = lane + 128; l < L; l += 32) {  // L > 128
-        const long long co1 = eo[l - 1] >= 0 ? s_Po[eo[l - 1]] : 0;
-        const long long ci = ei[l] >= 0 ? s_Pi[ei[l]] : 0;
-        const long long d = ci - co1;
-        if (kFull) s_D[l] = d;
-        pk = max(pk, mf0[l] + d);
-      }
+      st = __dadd_rn(__dadd_rn(__dadd_rn(cs[0], cs[1]), __dadd_rn(cs[2], cs[3])),
+                     __dadd_rn(__dadd_rn(cs[4], cs[5]), __dadd_rn(cs[6], cs[7])));
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) pk = max(pk, __shfl_xor_sync(0xffffffffu, pk, o));
       swp = (K > 0 && eo[L - 1] >= 0) ? s_Po[eo[L - 1]] : 0;
-    }
-    if (kFull) __syncthreads();  // (E) s_D visible; warp 0's stall sum overlaps the row stream
-    if (warp == 0) {
-      double st = 0.0;  // ascending layers, positive terms only
-      for (int j = 0; j * 32 < L; j++) {
-        double t = 0.0;
-        if (j < 4) t = j == 0 ? term[0] : j == 1 ? term[1] : j == 2 ? term[2] : term[3];
-        else if (j * 32 + lane < L) {  // L > 128: recompute beyond the register cache
-          const int l = j * 32 + lane;
-          const long long co = eo[l] >= 0 ? s_Po[eo[l]] : 0, co1 = eo[l - 1] >= 0 ? s_Po[eo[l - 1]] : 0;
-          const long long ci = ei[l] >= 0 ? s_Pi[ei[l]] : 0, ci1 = ei[l - 1] >= 0 ? s_Pi[ei[l - 1]] : 0;
-          t = __dsub_rn(__ddiv_rn(double((ci - ci1) + (co - co1)), p.tr.bw), bud[l]);
-        }
-        unsigned m = __ballot_sync(0xffffffffu, t > 0.0);
-        while (m) {
-          const int bl = __ffs(m) - 1;
-          st = __dadd_rn(st, __shfl_sync(0xffffffffu, t, bl));
-          m &= m - 1;
-        }
-      }
       if (lane == 0) {
         if (p.peak) p.peak[c] = pk;
         if (p.stall) p.stall[c] = st;
@@ -238,14 +225,18 @@ __global__ void __launch_bounds__(256, 4) replay_kernel(const __grid_constant__ 
       }
     }
     if (kFull) {
-      long long *row = p.footprint + c * p.ld;
-      const longlong2 *f2 = reinterpret_cast<const longlong2 *>(f0);
-      const ushort2 *l2 = reinterpret_cast<const ushort2 *>(lay);
-      const int np = p.row_pairs;
-      for (int q = tid; q < np; q += blockDim.x) {
-        const longlong2 f = f2[q];
-        const ushort2 ly = l2[q];
-        st_cs_v2(row + 2 * q, f.x + s_D[ly.x], f.y + s_D[ly.y]);
+      __syncthreads();  // (E) s_D visible
+      const int np = p.row_pairs, bd = blockDim.x;
+      const longlong2 *fp2 = reinterpret_cast<const longlong2 *>(f0) + tid;
+      const unsigned *lp = reinterpret_cast<const unsigned *>(lay) + tid;
+      long long *out = p.footprint + c * p.ld + 2 * tid;
+      for (int q = tid; q < np; q += bd) {
+        const longlong2 f = *fp2;
+        const unsigned lz = *lp;
+        st_cs_v2(out, f.x + s_D[lz & 0xffffu], f.y + s_D[lz >> 16]);
+        fp2 += bd;
+        lp += bd;
+        out += 2 * bd;
       }
     }
   }

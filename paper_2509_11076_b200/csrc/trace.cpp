@@ -153,10 +153,10 @@ extern "C" chm_status chm_trace_build(chm_ctx *ctx, const chm_trace_params *P, c
   // bounds of the kernel's exact 32-bit partial sums (hi = S >> 16, lo = S & 0xffff)
   int64_t sum_S = 0;
   for (int32_t k = 0; k < tr->K; k++) sum_S += tr->sw_S[k];
-  if (tr->K > 32767 || tr->L > 65535 || sum_S >= (int64_t(1) << 47)) {
+  if (tr->K > 32767 || tr->L > 256 || sum_S >= (int64_t(1) << 47)) {
     chm_trace_free(tr);
     CHM_FAIL(CHM_E_INVAL, "chm_trace_build: K = %d, L = %d, sum S = %lld exceed the replay image bounds "
-             "(K < 32768, L < 65536, sum S < 2^47)", tr->K, tr->L, (long long)sum_S);
+             "(K < 32768, L <= 256, sum S < 2^47)", tr->K, tr->L, (long long)sum_S);
   }
   auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
   DevTrace &D = tr->dev;

@@ -405,3 +405,30 @@ def test_feature_callstack_S311_S313():
         exp = ((exp << 8) + int(idx9[tok9[i]])) % 2 ** 64
     assert int(stk[0]) == exp and c[0] == n
     assert (int(stk[0]) >> 56) == int(idx9[tok9[1]])  # first use (0x11) shifted out
+
+
+def test_stall_pairwise_within_error_bound_of_exact_sum():
+    """R-stall: the stall is the pairwise sum of max(0, load_l/B - Bud_l).  Pin it to the exactly
+    rounded sum of those terms (math.fsum) within pairwise summation's error bound
+    gamma_{log2 P} * sum|t| (Higham, Accuracy and Stability, §4.2) on traces with many layers."""
+    for seed in range(6):
+        tr = W.random_trace(200 + seed, n_layers=6, ops_per_layer=4, bw=1e5)
+        m = O.Model(tr)
+        st, n, ty, bud = m.layers()
+        sw = m.swappable()
+        lay = np.repeat(np.arange(m.L), n)
+        for c in range(1, 1 << min(m.K, 8)):
+            sel = [k for k in range(m.K) if (c >> k) & 1]
+            t, r, s = sw["t"][sel], sw["r"][sel], sw["s"][sel]
+            load = np.zeros(m.L, np.int64)
+            for tt, rr, ss in zip(t, r, s):
+                load[lay[ss]] += tr.nbytes[tt]
+                load[lay[rr]] += tr.nbytes[tt]
+            terms = [max(0.0, float(load[l]) / tr.bw - bud[l]) for l in range(m.L)]
+            exact = math.fsum(terms)
+            got = m.stall(t, r, s)
+            P = 1 << (m.L - 1).bit_length()
+            u = 2.0 ** -53
+            k = P.bit_length() - 1
+            bound = k * u / (1 - k * u) * sum(terms)
+            assert abs(got - exact) <= bound + 1e-300
