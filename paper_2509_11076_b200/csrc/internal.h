@@ -120,8 +120,8 @@ struct DevTrace {
   uint32_t o_si = 0;    // u16   [K]  lin of that order
   uint32_t o_Spo = 0;   // int64 [K]  S in lout order
   uint32_t o_Spi = 0;   // int64 [K]  S in lin order
-  uint32_t o_eo = 0;    // int32 [L]  last lout-sorted position with lout <= l (-1: none)
-  uint32_t o_ei = 0;    // int32 [L]  last lin-sorted position with lin <= l (-1: none)
+  uint32_t o_eo = 0;    // int16 [L]  last layer l' <= l that releases an item (lout = l'), or -1
+  uint32_t o_ei = 0;    // int16 [L]  last layer l' <= l that swaps an item in (lin = l'), or -1
   uint32_t o_f0 = 0;    // int64 [N]  no-swap footprint (full mode)
   uint32_t o_lay = 0;   // u16   [N]  logical layer of each op (full mode)
   const uint64_t *base = nullptr;

@@ -55,8 +55,9 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {  // splitmix64 finaliser
 struct EvalParams {
   DevTrace tr;
   int kind;
-  int Ek;         // contiguous sorted positions per thread in the per-layer sums
+  int Ek;         // contiguous sorted positions per lane in the per-layer sums
   uint32_t stage_bytes;
+  uint32_t warp_scratch;  // bytes of per-warp scratch after the image
   uint64_t first, count, seed, flip_thr;
   uint64_t base[kMaxSeededWords];
   const uint64_t *masks;
@@ -115,12 +116,14 @@ __device__ __forceinline__ void stage_image(unsigned char *dst, const unsigned c
   }
 }
 
+constexpr int kEvalThreads = 512;  // 16 warps per CTA, one candidate per warp
+
 template <bool kFull>
-__global__ void __launch_bounds__(256, 4) replay_kernel(const __grid_constant__ EvalParams p) {
+__global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_constant__ EvalParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ __align__(8) uint64_t s_mbar;
-  __shared__ long long s_wtot[2][32];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ Key s_best[kEvalThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int N = p.tr.N, K = p.tr.K, L = p.tr.L;
   unsigned char *img = smem;
   const long long *mf0 = reinterpret_cast<const long long *>(img + p.tr.o_mf0);
@@ -131,26 +134,29 @@ __global__ void __launch_bounds__(256, 4) replay_kernel(const __grid_constant__ 
   const unsigned short *si = reinterpret_cast<const unsigned short *>(img + p.tr.o_si);
   const long long *Spo = reinterpret_cast<const long long *>(img + p.tr.o_Spo);
   const long long *Spi = reinterpret_cast<const long long *>(img + p.tr.o_Spi);
-  const int *eo = reinterpret_cast<const int *>(img + p.tr.o_eo);
-  const int *ei = reinterpret_cast<const int *>(img + p.tr.o_ei);
+  const short *eo = reinterpret_cast<const short *>(img + p.tr.o_eo);
+  const short *ei = reinterpret_cast<const short *>(img + p.tr.o_ei);
   const long long *f0 = reinterpret_cast<const long long *>(img + p.tr.o_f0);
   const unsigned short *lay = reinterpret_cast<const unsigned short *>(img + p.tr.o_lay);
-  unsigned char *s_flag = img + p.stage_bytes;                                     // [K]
-  long long *s_Po = reinterpret_cast<long long *>(s_flag + ((K + 15) & ~15));     // [K] cumulative, lout order
-  long long *s_Pi = s_Po + ((K + 1) & ~1);                                         // [K] cumulative, lin order
-  long long *s_D = s_Pi + ((K + 1) & ~1);                                          // [L] layer offsets
+  // per-warp scratch after the image: CO[L], CI[L], D[L] (int64), flags[K] (bytes)
+  unsigned char *wscr = img + p.stage_bytes + size_t(warp) * p.warp_scratch;
+  long long *s_CO = reinterpret_cast<long long *>(wscr);
+  long long *s_CI = s_CO + L;
+  long long *s_D = s_CI + L;
+  unsigned char *s_flag = reinterpret_cast<unsigned char *>(s_D + L);
 
   stage_image(img, p.tr.image, p.stage_bytes, &s_mbar);
 
-  const int q0 = tid * p.Ek, q1 = min(q0 + p.Ek, K);  // this thread's run of sorted positions
+  const int q0 = lane * p.Ek, q1 = min(q0 + p.Ek, K);  // this lane's run of sorted positions
   Key best;
   best.excess = LLONG_MAX; best.stall = 0.0; best.swapped = LLONG_MAX; best.index = ~0ull; best.peak = 0;
-  for (uint64_t c = blockIdx.x; c < p.count; c += gridDim.x) {
+  const uint64_t wstride = uint64_t(gridDim.x) * nwarps;
+  for (uint64_t c = uint64_t(blockIdx.x) * nwarps + warp; c < p.count; c += wstride) {
     const uint64_t g = p.first + c;
-    __syncthreads();  // (A) the previous candidate's readers are done
-    for (int k = tid; k < K; k += blockDim.x) s_flag[k] = cand_bit(p, g, c, k) ? 1 : 0;
-    __syncthreads();  // (B)
-    // inclusive scans of the selected sizes over the lout- and lin-sorted orders
+    for (int k = lane; k < K; k += 32) s_flag[k] = cand_bit(p, g, c, k) ? 1 : 0;
+    __syncwarp();
+    // running sums of the selected sizes over the lout- and lin-sorted orders; the value at
+    // the end of each layer's segment is that layer's cumulative CO / CI
     long long to = 0, ti = 0;
     for (int q = q0; q < q1; q++) {
       to += s_flag[po[q]] ? Spo[q] : 0;
@@ -163,87 +169,83 @@ __global__ void __launch_bounds__(256, 4) replay_kernel(const __grid_constant__ 
       const long long yi = __shfl_up_sync(0xffffffffu, ii, o);
       if (lane >= o) { io += yo; ii += yi; }
     }
-    if (lane == 31) { s_wtot[0][warp] = io; s_wtot[1][warp] = ii; }
-    __syncthreads();  // (C)
     long long xo = io - to, xi = ii - ti;
-    for (int w = 0; w < warp; w++) { xo += s_wtot[0][w]; xi += s_wtot[1][w]; }
-    for (int q = q0; q < q1; q++) {  // keep the running sum at the end of every layer's segment
+    for (int q = q0; q < q1; q++) {
       xo += s_flag[po[q]] ? Spo[q] : 0;
       xi += s_flag[pi[q]] ? Spi[q] : 0;
       const bool last = q + 1 == K;
-      if (last || so[q] != so[q + 1]) s_Po[q] = xo;
-      if (last || si[q] != si[q + 1]) s_Pi[q] = xi;
+      if (last || so[q] != so[q + 1]) s_CO[so[q]] = xo;
+      if (last || si[q] != si[q + 1]) s_CI[si[q]] = xi;
     }
-    __syncthreads();  // (D)
-    // per layer l: CO(l) / CI(l) = selected bytes released / swapped in through layer l;
-    // in_l = CI(l) - CI(l-1), out_l = CO(l) - CO(l-1), D_l = CI(l) - CO(l-1)
-    long long pk = LLONG_MIN, swp = 0;
-    double st = 0.0;
-    if (warp == 0) {
-      // lanes own layers l = lane + 32 j; term_l = max(0, load_l / B - Bud_l) is summed with the
-      // pairwise (recursive halving) tree of reading R-stall: xor butterflies 1..16 give the
-      // tree over each 32-layer chunk in every lane, then a fixed tree over the 8 chunks
-      double cs[8];
+    __syncwarp();
+    // layer l: in_l = CI(l) - CI(l-1), out_l = CO(l) - CO(l-1), D_l = CI(l) - CO(l-1);
+    // term_l = max(0, load_l / B - Bud_l) summed with the pairwise tree of reading R-stall
+    long long pk = LLONG_MIN;
+    double cs[8];
 #pragma unroll
-      for (int j = 0; j < 8; j++) {
-        cs[j] = 0.0;
-        if (32 * j < L) {
-          const int l = lane + 32 * j;
-          double t = 0.0;
-          if (l < L) {
-            const long long co = eo[l] >= 0 ? s_Po[eo[l]] : 0;
-            const long long co1 = (l > 0 && eo[l - 1] >= 0) ? s_Po[eo[l - 1]] : 0;
-            const long long ci = ei[l] >= 0 ? s_Pi[ei[l]] : 0;
-            const long long ci1 = (l > 0 && ei[l - 1] >= 0) ? s_Pi[ei[l - 1]] : 0;
-            const long long d = ci - co1;
-            if (kFull) s_D[l] = d;
-            pk = max(pk, mf0[l] + d);
-            const double x = __dsub_rn(__ddiv_rn(double((ci - ci1) + (co - co1)), p.tr.bw), bud[l]);
-            t = x > 0.0 ? x : 0.0;
-          }
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) t = __dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, o));
-          cs[j] = t;
+    for (int j = 0; j < 8; j++) {
+      cs[j] = 0.0;
+      if (32 * j < L) {
+        const int l = lane + 32 * j;
+        double t = 0.0;
+        if (l < L) {
+          const int a = eo[l], b = ei[l];
+          const int a1 = l > 0 ? eo[l - 1] : -1, b1 = l > 0 ? ei[l - 1] : -1;
+          const long long co = a >= 0 ? s_CO[a] : 0, co1 = a1 >= 0 ? s_CO[a1] : 0;
+          const long long ci = b >= 0 ? s_CI[b] : 0, ci1 = b1 >= 0 ? s_CI[b1] : 0;
+          const long long d = ci - co1;
+          if (kFull) s_D[l] = d;
+          pk = max(pk, mf0[l] + d);
+          const double x = __dsub_rn(__ddiv_rn(double((ci - ci1) + (co - co1)), p.tr.bw), bud[l]);
+          t = x > 0.0 ? x : 0.0;
         }
-      }
-      st = __dadd_rn(__dadd_rn(__dadd_rn(cs[0], cs[1]), __dadd_rn(cs[2], cs[3])),
-                     __dadd_rn(__dadd_rn(cs[4], cs[5]), __dadd_rn(cs[6], cs[7])));
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) pk = max(pk, __shfl_xor_sync(0xffffffffu, pk, o));
-      swp = (K > 0 && eo[L - 1] >= 0) ? s_Po[eo[L - 1]] : 0;
-      if (lane == 0) {
-        if (p.peak) p.peak[c] = pk;
-        if (p.stall) p.stall[c] = st;
-        if (p.swapped) p.swapped[c] = swp;
-        Key k;
-        k.excess = pk > p.tr.budget ? pk - p.tr.budget : 0;
-        k.stall = st;
-        k.swapped = swp;
-        k.index = g;
-        k.peak = pk;
-        if (key_less(k, best)) best = k;
+        for (int o = 1; o < 32; o <<= 1) t = __dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, o));
+        cs[j] = t;
       }
+    }
+    const double st = __dadd_rn(__dadd_rn(__dadd_rn(cs[0], cs[1]), __dadd_rn(cs[2], cs[3])),
+                                __dadd_rn(__dadd_rn(cs[4], cs[5]), __dadd_rn(cs[6], cs[7])));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pk = max(pk, __shfl_xor_sync(0xffffffffu, pk, o));
+    const long long swp = (L > 0 && eo[L - 1] >= 0) ? s_CO[eo[L - 1]] : 0;
+    if (lane == 0) {
+      if (p.peak) p.peak[c] = pk;
+      if (p.stall) p.stall[c] = st;
+      if (p.swapped) p.swapped[c] = swp;
+      Key k;
+      k.excess = pk > p.tr.budget ? pk - p.tr.budget : 0;
+      k.stall = st;
+      k.swapped = swp;
+      k.index = g;
+      k.peak = pk;
+      if (key_less(k, best)) best = k;
     }
     if (kFull) {
-      __syncthreads();  // (E) s_D visible
-      const int np = p.row_pairs, bd = blockDim.x;
-      const longlong2 *fp2 = reinterpret_cast<const longlong2 *>(f0) + tid;
-      const unsigned *lp = reinterpret_cast<const unsigned *>(lay) + tid;
-      long long *out = p.footprint + c * p.ld + 2 * tid;
-      for (int q = tid; q < np; q += bd) {
+      __syncwarp();  // s_D visible to the warp
+      const int np = p.row_pairs;
+      const longlong2 *fp2 = reinterpret_cast<const longlong2 *>(f0) + lane;
+      const unsigned *lp = reinterpret_cast<const unsigned *>(lay) + lane;
+      long long *out = p.footprint + c * p.ld + 2 * lane;
+      for (int q = lane; q < np; q += 32) {
         const longlong2 f = *fp2;
         const unsigned lz = *lp;
         st_cs_v2(out, f.x + s_D[lz & 0xffffu], f.y + s_D[lz >> 16]);
-        fp2 += bd;
-        lp += bd;
-        out += 2 * bd;
+        fp2 += 32;
+        lp += 32;
+        out += 64;
       }
     }
+    __syncwarp();  // scratch reuse by the next candidate
   }
-  // per-CTA key -> the last CTA to finish reduces all of them into *best
+  // warp keys -> CTA key -> the last CTA to finish reduces all CTA keys into *best
+  if (lane == 0) s_best[warp] = best;
+  __syncthreads();
   __shared__ unsigned int s_last;
   if (tid == 0) {
-    p.partial[blockIdx.x] = best;
+    Key b = s_best[0];
+    for (int w = 1; w < nwarps; w++) if (key_less(s_best[w], b)) b = s_best[w];
+    p.partial[blockIdx.x] = b;
     __threadfence();
     const unsigned int t = atomicAdd(p.ticket, 1u);
     s_last = (t == gridDim.x - 1) ? 1u : 0u;
@@ -298,22 +300,22 @@ __global__ void best_reduce_kernel(const Key *keys, uint32_t n, Key *out) {
 }  // namespace
 
 chm_status launch_eval(chm_ctx *ctx, const EvalLaunch &L, cudaStream_t stream) {
-  const int N = L.tr.N, K = L.tr.K, Ly = L.tr.L, W = L.tr.W;
-  // block size: ~4 mask bits / row pairs per thread, 32..256 threads
-  int threads = ((std::max(K, (N + 1) / 2) + 3) / 4 + 31) / 32 * 32;
-  threads = std::max(32, std::min(256, threads));
+  const int N = L.tr.N, K = L.tr.K, Ly = L.tr.L;
+  const int threads = kEvalThreads;
   const bool fp = L.footprint != nullptr;
   const uint32_t stage = fp ? L.tr.full_bytes : L.tr.search_bytes;
-  const size_t smem = size_t(stage) + size_t((K + 15) & ~15) + 2 * 8 * size_t((K + 1) & ~1) + 8 * size_t(Ly + 1);
-  (void)W;
-  if (smem > 200 * 1024) CHM_FAIL(CHM_E_INVAL, "chm_eval_policies: trace image (%zu B) exceeds shared memory", smem);
+  const uint32_t wscr = uint32_t(3 * 8 * size_t(Ly) + ((K + 15) & ~15));
+  const uint32_t wscr16 = (wscr + 15) & ~15u;
+  const size_t smem = size_t(stage) + size_t(threads / 32) * wscr16;
+  if (smem > 220 * 1024)
+    CHM_FAIL(CHM_E_INVAL, "chm_eval_policies: trace image + scratch (%zu B) exceeds shared memory", smem);
   auto kern = fp ? replay_kernel<true> : replay_kernel<false>;
   CHM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   int per_sm = 0;
   CHM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
   if (per_sm < 1) CHM_FAIL(CHM_E_INVAL, "chm_eval_policies: kernel does not fit an SM");
   if (ctx->cfg.eval_ctas_per_sm) per_sm = std::min(per_sm, int(ctx->cfg.eval_ctas_per_sm));
-  const uint64_t grid64 = std::min<uint64_t>(uint64_t(ctx->num_sms) * per_sm, L.count);
+  const uint64_t grid64 = std::min<uint64_t>(uint64_t(ctx->num_sms) * per_sm, (L.count + threads / 32 - 1) / (threads / 32));
   const int grid = int(std::max<uint64_t>(grid64, 1));
   const size_t need = size_t(grid) * sizeof(Key) + 256;
   if (ctx->eval_scratch_bytes < need) {
@@ -328,9 +330,10 @@ chm_status launch_eval(chm_ctx *ctx, const EvalLaunch &L, cudaStream_t stream) {
   EvalParams p{};
   p.tr = L.tr;
   p.kind = L.kind;
-  p.Ek = std::max(1, (K + threads - 1) / threads);
+  p.Ek = std::max(1, (K + 31) / 32);
   if (p.Ek > 1 && (p.Ek & 1) == 0) p.Ek += 1;  // odd run length: conflict-free 8 B shared reads
   p.stage_bytes = stage;
+  p.warp_scratch = wscr16;
   p.row_pairs = (N + 1) / 2;
   p.first = L.first;
   p.count = L.count;

@@ -170,8 +170,8 @@ extern "C" chm_status chm_trace_build(chm_ctx *ctx, const chm_trace_params *P, c
   D.o_si = uint32_t(o); o += al(2 * size_t(tr->K));
   D.o_Spo = uint32_t(o); o += al(8 * size_t(tr->K));
   D.o_Spi = uint32_t(o); o += al(8 * size_t(tr->K));
-  D.o_eo = uint32_t(o); o += al(4 * size_t(tr->L));
-  D.o_ei = uint32_t(o); o += al(4 * size_t(tr->L));
+  D.o_eo = uint32_t(o); o += al(2 * size_t(tr->L));
+  D.o_ei = uint32_t(o); o += al(2 * size_t(tr->L));
   D.search_bytes = uint32_t(o);
   D.o_f0 = uint32_t(o); o += al(8 * size_t(N));
   D.o_lay = uint32_t(o); o += al(2 * size_t(N));
@@ -195,17 +195,17 @@ extern "C" chm_status chm_trace_build(chm_ctx *ctx, const chm_trace_params *P, c
   }
   std::vector<int64_t> Spo(tr->K), Spi(tr->K);
   for (int32_t q = 0; q < tr->K; q++) { Spo[q] = tr->sw_S[po[q]]; Spi[q] = tr->sw_S[pi[q]]; }
-  std::vector<int32_t> eo(size_t(tr->L), -1), ei(size_t(tr->L), -1);
+  std::vector<int16_t> eo(size_t(tr->L), -1), ei(size_t(tr->L), -1);
   for (int32_t l = 0, q = -1; l < tr->L; l++) {
     while (q + 1 < tr->K && so[q + 1] <= l) q++;
-    eo[l] = q;
+    eo[l] = q >= 0 ? int16_t(so[q]) : int16_t(-1);
   }
   for (int32_t l = 0, q = -1; l < tr->L; l++) {
     while (q + 1 < tr->K && si[q + 1] <= l) q++;
-    ei[l] = q;
+    ei[l] = q >= 0 ? int16_t(si[q]) : int16_t(-1);
   }
-  std::memcpy(h + D.o_eo, eo.data(), 4 * size_t(tr->L));
-  std::memcpy(h + D.o_ei, ei.data(), 4 * size_t(tr->L));
+  std::memcpy(h + D.o_eo, eo.data(), 2 * size_t(tr->L));
+  std::memcpy(h + D.o_ei, ei.data(), 2 * size_t(tr->L));
   if (tr->K) {
     std::memcpy(h + D.o_Spo, Spo.data(), 8 * size_t(tr->K));
     std::memcpy(h + D.o_Spi, Spi.data(), 8 * size_t(tr->K));
