@@ -114,14 +114,8 @@ struct DevTrace {
   uint32_t o_mf0 = 0;   // int64 [L]  max F0 over the ops of each logical layer
   uint32_t o_bud = 0;   // double[L]  Eq. 1 budget
   uint32_t o_S = 0;     // int64 [K]  swappable sizes (mask-bit order)
-  uint32_t o_po = 0;    // u16   [K]  mask bits sorted by lout (release layer)
-  uint32_t o_so = 0;    // u16   [K]  lout of that order
-  uint32_t o_pi = 0;    // u16   [K]  mask bits sorted by lin (swap-in layer)
-  uint32_t o_si = 0;    // u16   [K]  lin of that order
-  uint32_t o_Spo = 0;   // int64 [K]  S in lout order
-  uint32_t o_Spi = 0;   // int64 [K]  S in lin order
-  uint32_t o_eo = 0;    // int16 [L]  last layer l' <= l that releases an item (lout = l'), or -1
-  uint32_t o_ei = 0;    // int16 [L]  last layer l' <= l that swaps an item in (lin = l'), or -1
+  uint32_t o_lo = 0;    // u16   [K]  lout (release layer) per swappable, mask-bit order
+  uint32_t o_li = 0;    // u16   [K]  lin (swap-in layer) per swappable, mask-bit order
   uint32_t o_f0 = 0;    // int64 [N]  no-swap footprint (full mode)
   uint32_t o_lay = 0;   // u16   [N]  logical layer of each op (full mode)
   const uint64_t *base = nullptr;

@@ -55,7 +55,6 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {  // splitmix64 finaliser
 struct EvalParams {
   DevTrace tr;
   int kind;
-  int Ek;         // contiguous sorted positions per lane in the per-layer sums
   uint32_t stage_bytes;
   uint32_t warp_scratch;  // bytes of per-warp scratch after the image
   uint64_t first, count, seed, flip_thr;
@@ -118,87 +117,139 @@ __device__ __forceinline__ void stage_image(unsigned char *dst, const unsigned c
 
 constexpr int kEvalThreads = 512;  // 16 warps per CTA, one candidate per warp
 
+__device__ __forceinline__ long long split_sum(unsigned hi, unsigned lo) {  // exact: see trace build
+  return (long long)(int)hi * 65536 + (long long)(int)lo;
+}
+
+// per-layer hi/lo 32-bit accumulators of signed sizes: exact while |sum S| < 2^47, K < 32768
+__device__ __forceinline__ void acc_add(unsigned *hi, unsigned *lo, int l, long long v) {
+  const bool neg = v < 0;
+  const unsigned long long a = (unsigned long long)(neg ? -v : v);
+  const unsigned h = unsigned(a >> 16), w = unsigned(a & 0xffffull);
+  atomicAdd(hi + l, neg ? 0u - h : h);
+  atomicAdd(lo + l, neg ? 0u - w : w);
+}
+
 template <bool kFull>
 __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_constant__ EvalParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ __align__(8) uint64_t s_mbar;
   __shared__ Key s_best[kEvalThreads / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  const int N = p.tr.N, K = p.tr.K, L = p.tr.L;
+  const int K = p.tr.K, L = p.tr.L;
   unsigned char *img = smem;
   const long long *mf0 = reinterpret_cast<const long long *>(img + p.tr.o_mf0);
   const double *bud = reinterpret_cast<const double *>(img + p.tr.o_bud);
-  const unsigned short *po = reinterpret_cast<const unsigned short *>(img + p.tr.o_po);
-  const unsigned short *so = reinterpret_cast<const unsigned short *>(img + p.tr.o_so);
-  const unsigned short *pi = reinterpret_cast<const unsigned short *>(img + p.tr.o_pi);
-  const unsigned short *si = reinterpret_cast<const unsigned short *>(img + p.tr.o_si);
-  const long long *Spo = reinterpret_cast<const long long *>(img + p.tr.o_Spo);
-  const long long *Spi = reinterpret_cast<const long long *>(img + p.tr.o_Spi);
-  const short *eo = reinterpret_cast<const short *>(img + p.tr.o_eo);
-  const short *ei = reinterpret_cast<const short *>(img + p.tr.o_ei);
+  const long long *S = reinterpret_cast<const long long *>(img + p.tr.o_S);
+  const unsigned short *lo_ = reinterpret_cast<const unsigned short *>(img + p.tr.o_lo);
+  const unsigned short *li_ = reinterpret_cast<const unsigned short *>(img + p.tr.o_li);
   const long long *f0 = reinterpret_cast<const long long *>(img + p.tr.o_f0);
   const unsigned short *lay = reinterpret_cast<const unsigned short *>(img + p.tr.o_lay);
-  // per-warp scratch after the image: CO[L], CI[L], D[L] (int64), flags[K] (bytes)
-  unsigned char *wscr = img + p.stage_bytes + size_t(warp) * p.warp_scratch;
-  long long *s_CO = reinterpret_cast<long long *>(wscr);
-  long long *s_CI = s_CO + L;
-  long long *s_D = s_CI + L;
-  unsigned char *s_flag = reinterpret_cast<unsigned char *>(s_D + L);
+  // CTA tables of the reference mask R (the SEEDED base; empty for the other kinds):
+  // per-layer in / out sums and their cumulative sums, int64 [L] each
+  long long *s_INR = reinterpret_cast<long long *>(img + p.stage_bytes);
+  long long *s_OUTR = s_INR + L;
+  long long *s_CIR = s_OUTR + L;
+  long long *s_COR = s_CIR + L;
+  unsigned *r_hi = reinterpret_cast<unsigned *>(s_COR + L);  // [2L] R accumulators (in, out)
+  unsigned *r_lo = r_hi + 2 * L;                             // [2L]
+  // per-warp scratch: D[L] (int64) and the candidate's signed deltas vs R, split hi/lo 32-bit
+  unsigned char *wscr = reinterpret_cast<unsigned char *>(r_lo + 2 * L) + size_t(warp) * p.warp_scratch;
+  long long *s_D = reinterpret_cast<long long *>(wscr);
+  unsigned *dI_hi = reinterpret_cast<unsigned *>(s_D + L);
+  unsigned *dI_lo = dI_hi + L;
+  unsigned *dO_hi = dI_lo + L;
+  unsigned *dO_lo = dO_hi + L;
 
   stage_image(img, p.tr.image, p.stage_bytes, &s_mbar);
+  for (int l = tid; l < 2 * L; l += blockDim.x) { r_hi[l] = 0u; r_lo[l] = 0u; }
+  for (int l = lane; l < L; l += 32) { dI_hi[l] = 0u; dI_lo[l] = 0u; dO_hi[l] = 0u; dO_lo[l] = 0u; }
+  __syncthreads();
+  const bool seeded = p.kind == CHM_CAND_SEEDED;
+  if (seeded) {  // R = base
+    for (int k = tid; k < K; k += blockDim.x) {
+      if (!((p.base[k >> 6] >> (k & 63)) & 1ull)) continue;
+      acc_add(r_hi, r_lo, li_[k], S[k]);
+      acc_add(r_hi + L, r_lo + L, lo_[k], S[k]);
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {  // cumulative R sums over layers
+    long long ci = 0, co = 0;
+    for (int l0 = 0; l0 < L; l0 += 32) {
+      const int l = l0 + lane;
+      long long in_l = 0, out_l = 0;
+      if (l < L) { in_l = split_sum(r_hi[l], r_lo[l]); out_l = split_sum(r_hi[L + l], r_lo[L + l]); }
+      long long a = in_l, b = out_l;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long ya = __shfl_up_sync(0xffffffffu, a, o), yb = __shfl_up_sync(0xffffffffu, b, o);
+        if (lane >= o) { a += ya; b += yb; }
+      }
+      if (l < L) { s_INR[l] = in_l; s_OUTR[l] = out_l; s_CIR[l] = ci + a; s_COR[l] = co + b; }
+      ci += __shfl_sync(0xffffffffu, a, 31);
+      co += __shfl_sync(0xffffffffu, b, 31);
+    }
+  }
+  __syncthreads();
 
-  const int q0 = lane * p.Ek, q1 = min(q0 + p.Ek, K);  // this lane's run of sorted positions
   Key best;
   best.excess = LLONG_MAX; best.stall = 0.0; best.swapped = LLONG_MAX; best.index = ~0ull; best.peak = 0;
   const uint64_t wstride = uint64_t(gridDim.x) * nwarps;
   for (uint64_t c = uint64_t(blockIdx.x) * nwarps + warp; c < p.count; c += wstride) {
     const uint64_t g = p.first + c;
-    for (int k = lane; k < K; k += 32) s_flag[k] = cand_bit(p, g, c, k) ? 1 : 0;
-    __syncwarp();
-    // running sums of the selected sizes over the lout- and lin-sorted orders; the value at
-    // the end of each layer's segment is that layer's cumulative CO / CI
-    long long to = 0, ti = 0;
-    for (int q = q0; q < q1; q++) {
-      to += s_flag[po[q]] ? Spo[q] : 0;
-      ti += s_flag[pi[q]] ? Spi[q] : 0;
-    }
-    long long io = to, ii = ti;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const long long yo = __shfl_up_sync(0xffffffffu, io, o);
-      const long long yi = __shfl_up_sync(0xffffffffu, ii, o);
-      if (lane >= o) { io += yo; ii += yi; }
-    }
-    long long xo = io - to, xi = ii - ti;
-    for (int q = q0; q < q1; q++) {
-      xo += s_flag[po[q]] ? Spo[q] : 0;
-      xi += s_flag[pi[q]] ? Spi[q] : 0;
-      const bool last = q + 1 == K;
-      if (last || so[q] != so[q + 1]) s_CO[so[q]] = xo;
-      if (last || si[q] != si[q + 1]) s_CI[si[q]] = xi;
+    // decode: only the items whose bit differs from R add a signed delta to their layers
+    for (int k = lane; k < K; k += 32) {
+      bool diff;
+      bool set;
+      if (seeded) {
+        const uint64_t h = mix64(p.seed ^ mix64(g * uint64_t(K) + uint64_t(k)));
+        diff = h < p.flip_thr;
+        set = ((p.base[k >> 6] >> (k & 63)) & 1ull) == 0ull;  // flipped from 0 -> now set
+      } else {
+        diff = cand_bit(p, g, c, k);
+        set = true;
+      }
+      if (diff) {
+        const long long v = set ? S[k] : -S[k];
+        acc_add(dI_hi, dI_lo, li_[k], v);
+        acc_add(dO_hi, dO_lo, lo_[k], v);
+      }
     }
     __syncwarp();
-    // layer l: in_l = CI(l) - CI(l-1), out_l = CO(l) - CO(l-1), D_l = CI(l) - CO(l-1);
-    // term_l = max(0, load_l / B - Bud_l) summed with the pairwise tree of reading R-stall
-    long long pk = LLONG_MIN;
+    // layer l: in_l / out_l = R sums + deltas; CI / CO cumulative; D_l = CI(l) - CO(l) + out_l;
+    // term_l = max(0, (in_l + out_l) / B - Bud_l), pairwise tree (reading R-stall)
+    long long pk = LLONG_MIN, cci = 0, cco = 0;
     double cs[8];
 #pragma unroll
     for (int j = 0; j < 8; j++) {
       cs[j] = 0.0;
       if (32 * j < L) {
         const int l = lane + 32 * j;
+        long long din = 0, dout = 0;
+        if (l < L) {
+          din = split_sum(dI_hi[l], dI_lo[l]);
+          dout = split_sum(dO_hi[l], dO_lo[l]);
+          dI_hi[l] = 0u; dI_lo[l] = 0u; dO_hi[l] = 0u; dO_lo[l] = 0u;  // ready for the next candidate
+        }
+        long long a = din, b = dout;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const long long ya = __shfl_up_sync(0xffffffffu, a, o), yb = __shfl_up_sync(0xffffffffu, b, o);
+          if (lane >= o) { a += ya; b += yb; }
+        }
         double t = 0.0;
         if (l < L) {
-          const int a = eo[l], b = ei[l];
-          const int a1 = l > 0 ? eo[l - 1] : -1, b1 = l > 0 ? ei[l - 1] : -1;
-          const long long co = a >= 0 ? s_CO[a] : 0, co1 = a1 >= 0 ? s_CO[a1] : 0;
-          const long long ci = b >= 0 ? s_CI[b] : 0, ci1 = b1 >= 0 ? s_CI[b1] : 0;
-          const long long d = ci - co1;
+          const long long in_l = s_INR[l] + din, out_l = s_OUTR[l] + dout;
+          const long long ci = s_CIR[l] + cci + a, co = s_COR[l] + cco + b;
+          const long long d = ci - co + out_l;
           if (kFull) s_D[l] = d;
           pk = max(pk, mf0[l] + d);
-          const double x = __dsub_rn(__ddiv_rn(double((ci - ci1) + (co - co1)), p.tr.bw), bud[l]);
+          const double x = __dsub_rn(__ddiv_rn(double(in_l + out_l), p.tr.bw), bud[l]);
           t = x > 0.0 ? x : 0.0;
         }
+        cci += __shfl_sync(0xffffffffu, a, 31);
+        cco += __shfl_sync(0xffffffffu, b, 31);
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) t = __dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, o));
         cs[j] = t;
@@ -208,7 +259,7 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
                                 __dadd_rn(__dadd_rn(cs[4], cs[5]), __dadd_rn(cs[6], cs[7])));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) pk = max(pk, __shfl_xor_sync(0xffffffffu, pk, o));
-    const long long swp = (L > 0 && eo[L - 1] >= 0) ? s_CO[eo[L - 1]] : 0;
+    const long long swp = (L > 0 ? s_COR[L - 1] : 0) + cco;  // total bytes released = swapped
     if (lane == 0) {
       if (p.peak) p.peak[c] = pk;
       if (p.stall) p.stall[c] = st;
@@ -300,13 +351,13 @@ __global__ void best_reduce_kernel(const Key *keys, uint32_t n, Key *out) {
 }  // namespace
 
 chm_status launch_eval(chm_ctx *ctx, const EvalLaunch &L, cudaStream_t stream) {
-  const int N = L.tr.N, K = L.tr.K, Ly = L.tr.L;
+  const int N = L.tr.N, Ly = L.tr.L;
   const int threads = kEvalThreads;
   const bool fp = L.footprint != nullptr;
   const uint32_t stage = fp ? L.tr.full_bytes : L.tr.search_bytes;
-  const uint32_t wscr = uint32_t(3 * 8 * size_t(Ly) + ((K + 15) & ~15));
-  const uint32_t wscr16 = (wscr + 15) & ~15u;
-  const size_t smem = size_t(stage) + size_t(threads / 32) * wscr16;
+  const uint32_t wscr16 = uint32_t((8 * size_t(Ly) + 16 * size_t(Ly) + 15) & ~size_t(15));
+  const size_t cta_tab = (32 * size_t(Ly) + 16 * size_t(Ly) + 15) & ~size_t(15);
+  const size_t smem = size_t(stage) + cta_tab + size_t(threads / 32) * wscr16;
   if (smem > 220 * 1024)
     CHM_FAIL(CHM_E_INVAL, "chm_eval_policies: trace image + scratch (%zu B) exceeds shared memory", smem);
   auto kern = fp ? replay_kernel<true> : replay_kernel<false>;
@@ -330,8 +381,6 @@ chm_status launch_eval(chm_ctx *ctx, const EvalLaunch &L, cudaStream_t stream) {
   EvalParams p{};
   p.tr = L.tr;
   p.kind = L.kind;
-  p.Ek = std::max(1, (K + 31) / 32);
-  if (p.Ek > 1 && (p.Ek & 1) == 0) p.Ek += 1;  // odd run length: conflict-free 8 B shared reads
   p.stage_bytes = stage;
   p.warp_scratch = wscr16;
   p.row_pairs = (N + 1) / 2;

@@ -164,14 +164,8 @@ extern "C" chm_status chm_trace_build(chm_ctx *ctx, const chm_trace_params *P, c
   D.o_mf0 = uint32_t(o); o += al(8 * size_t(tr->L));
   D.o_bud = uint32_t(o); o += al(8 * size_t(tr->L));
   D.o_S = uint32_t(o); o += al(8 * size_t(tr->K));
-  D.o_po = uint32_t(o); o += al(2 * size_t(tr->K));
-  D.o_so = uint32_t(o); o += al(2 * size_t(tr->K));
-  D.o_pi = uint32_t(o); o += al(2 * size_t(tr->K));
-  D.o_si = uint32_t(o); o += al(2 * size_t(tr->K));
-  D.o_Spo = uint32_t(o); o += al(8 * size_t(tr->K));
-  D.o_Spi = uint32_t(o); o += al(8 * size_t(tr->K));
-  D.o_eo = uint32_t(o); o += al(2 * size_t(tr->L));
-  D.o_ei = uint32_t(o); o += al(2 * size_t(tr->L));
+  D.o_lo = uint32_t(o); o += al(2 * size_t(tr->K));
+  D.o_li = uint32_t(o); o += al(2 * size_t(tr->K));
   D.search_bytes = uint32_t(o);
   D.o_f0 = uint32_t(o); o += al(8 * size_t(N));
   D.o_lay = uint32_t(o); o += al(2 * size_t(N));
@@ -185,34 +179,14 @@ extern "C" chm_status chm_trace_build(chm_ctx *ctx, const chm_trace_params *P, c
   std::memcpy(h + D.o_mf0, mf0.data(), 8 * size_t(tr->L));
   std::memcpy(h + D.o_bud, tr->bud.data(), 8 * size_t(tr->L));
   if (tr->K) std::memcpy(h + D.o_S, tr->sw_S.data(), 8 * size_t(tr->K));
-  std::vector<uint16_t> po(tr->K), pi(tr->K), so(tr->K), si(tr->K);
-  for (int32_t k = 0; k < tr->K; k++) po[k] = pi[k] = uint16_t(k);
-  std::stable_sort(po.begin(), po.end(), [&](uint16_t x, uint16_t y) { return tr->sw_lout[x] < tr->sw_lout[y]; });
-  std::stable_sort(pi.begin(), pi.end(), [&](uint16_t x, uint16_t y) { return tr->sw_lin[x] < tr->sw_lin[y]; });
-  for (int32_t q = 0; q < tr->K; q++) {
-    so[q] = uint16_t(tr->sw_lout[po[q]]);
-    si[q] = uint16_t(tr->sw_lin[pi[q]]);
+  std::vector<uint16_t> lo16(tr->K), li16(tr->K);
+  for (int32_t k = 0; k < tr->K; k++) {
+    lo16[k] = uint16_t(tr->sw_lout[k]);
+    li16[k] = uint16_t(tr->sw_lin[k]);
   }
-  std::vector<int64_t> Spo(tr->K), Spi(tr->K);
-  for (int32_t q = 0; q < tr->K; q++) { Spo[q] = tr->sw_S[po[q]]; Spi[q] = tr->sw_S[pi[q]]; }
-  std::vector<int16_t> eo(size_t(tr->L), -1), ei(size_t(tr->L), -1);
-  for (int32_t l = 0, q = -1; l < tr->L; l++) {
-    while (q + 1 < tr->K && so[q + 1] <= l) q++;
-    eo[l] = q >= 0 ? int16_t(so[q]) : int16_t(-1);
-  }
-  for (int32_t l = 0, q = -1; l < tr->L; l++) {
-    while (q + 1 < tr->K && si[q + 1] <= l) q++;
-    ei[l] = q >= 0 ? int16_t(si[q]) : int16_t(-1);
-  }
-  std::memcpy(h + D.o_eo, eo.data(), 2 * size_t(tr->L));
-  std::memcpy(h + D.o_ei, ei.data(), 2 * size_t(tr->L));
   if (tr->K) {
-    std::memcpy(h + D.o_Spo, Spo.data(), 8 * size_t(tr->K));
-    std::memcpy(h + D.o_Spi, Spi.data(), 8 * size_t(tr->K));
-    std::memcpy(h + D.o_po, po.data(), 2 * size_t(tr->K));
-    std::memcpy(h + D.o_so, so.data(), 2 * size_t(tr->K));
-    std::memcpy(h + D.o_pi, pi.data(), 2 * size_t(tr->K));
-    std::memcpy(h + D.o_si, si.data(), 2 * size_t(tr->K));
+    std::memcpy(h + D.o_lo, lo16.data(), 2 * size_t(tr->K));
+    std::memcpy(h + D.o_li, li16.data(), 2 * size_t(tr->K));
   }
   std::memcpy(h + D.o_f0, tr->F0.data(), 8 * size_t(N));
   std::vector<uint16_t> lay16(N);
