@@ -170,8 +170,9 @@ chm_status chm_trace_tables(const chm_trace *t, int64_t *f0, uint32_t *tensor, i
 /* ------------------------------------------------------------- policy evaluation (a4-a7) */
 typedef enum {
   CHM_CAND_EXHAUSTIVE = 0, /* swap set of candidate c = bits of c; requires K <= 63        */
-  CHM_CAND_SEEDED = 1,     /* bit t = base[t] ^ [mix(seed ^ mix(c*K + t)) < flip_thr],
-                              mix = splitmix64 finaliser                */
+  CHM_CAND_SEEDED = 1,     /* bit t = base[t] ^ [f_t < flip_thr >> 48], f_t = 16-bit field
+                              t mod 4 of w = mix(seed ^ mix(c*J + t/4)), J = ceil(K/4),
+                              mix = splitmix64 finaliser (reading R-seeded)     */
   CHM_CAND_MASKS = 2       /* device masks [count][mask_words], little-endian u64 words  */
 } chm_cand_kind;
 

@@ -341,10 +341,15 @@ static int cand_bit(const eval_job *j, uint64_t c, uint64_t idx, int32_t k) {
   const orc_model *m = j->m;
   if (j->kind == ORC_EXHAUSTIVE) return (int)((c >> k) & 1ull);
   if (j->kind == ORC_SEEDED) {
+    /* DESIGN.md reading R-seeded: candidate c draws J = ceil(K/4) words
+     * w_q = mix(seed ^ mix(c*J + q)); item k flips iff its 16-bit field
+     * (w_{k/4} >> 16*(k mod 4)) & 0xffff is below flip_thr >> 48 */
     const uint64_t *base = j->words ? j->words : m->base;
     int b = (int)((base[k / 64] >> (k % 64)) & 1ull);
-    uint64_t h = orc_splitmix64(j->seed ^ orc_splitmix64(c * (uint64_t)m->K + (uint64_t)k));
-    return b ^ (h < j->flip_thr ? 1 : 0);
+    uint64_t J = ((uint64_t)m->K + 3) / 4;
+    uint64_t w = orc_splitmix64(j->seed ^ orc_splitmix64(c * J + (uint64_t)(k / 4)));
+    uint64_t field = (w >> (16 * (k % 4))) & 0xffffull;
+    return b ^ (field < (j->flip_thr >> 48) ? 1 : 0);
   }
   return (int)((j->words[idx * (uint64_t)m->W + (uint64_t)(k / 64)] >> (k % 64)) & 1ull);
 }

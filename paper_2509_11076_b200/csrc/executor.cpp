@@ -29,10 +29,11 @@ extern "C" chm_status chm_candidate_mask(const chm_trace *t, const chm_candidate
       return CHM_OK;
     case CHM_CAND_SEEDED: {
       const uint64_t *base = c->base_mask ? c->base_mask : t->base.data();
+      const uint64_t J = (uint64_t(K) + 3) / 4, thr16 = c->flip_thr >> 48;
       for (int32_t k = 0; k < K; k++) {
         uint64_t bit = (base[k / 64] >> (k % 64)) & 1ull;
-        uint64_t h = splitmix64(c->seed ^ splitmix64(index * uint64_t(K) + uint64_t(k)));
-        bit ^= h < c->flip_thr ? 1ull : 0ull;
+        const uint64_t w = splitmix64(c->seed ^ splitmix64(index * J + uint64_t(k / 4)));
+        bit ^= ((w >> (16 * (k % 4))) & 0xffffull) < thr16 ? 1ull : 0ull;
         words[k / 64] |= bit << (k % 64);
       }
       return CHM_OK;

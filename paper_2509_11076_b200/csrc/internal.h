@@ -117,7 +117,7 @@ struct DevTrace {
   uint32_t o_lo = 0;    // u16   [K]  lout (release layer) per swappable, mask-bit order
   uint32_t o_li = 0;    // u16   [K]  lin (swap-in layer) per swappable, mask-bit order
   uint32_t o_f0 = 0;    // int64 [N]  no-swap footprint (full mode)
-  uint32_t o_lay = 0;   // u16   [N]  logical layer of each op (full mode)
+  uint32_t o_lay = 0;   // u16   [N]  8 x logical layer of each op (byte offset into D, full mode)
   const uint64_t *base = nullptr;
   int32_t N = 0, K = 0, L = 0, W = 0;
   double bw = 1.0;

@@ -75,8 +75,9 @@ __device__ __forceinline__ bool cand_bit(const EvalParams &p, uint64_t g, uint64
   if (p.kind == CHM_CAND_EXHAUSTIVE) return (g >> k) & 1ull;
   if (p.kind == CHM_CAND_SEEDED) {
     const bool b = (p.base[k >> 6] >> (k & 63)) & 1ull;
-    const uint64_t h = mix64(p.seed ^ mix64(g * uint64_t(p.tr.K) + uint64_t(k)));
-    return b != (h < p.flip_thr);
+    const uint64_t J = (uint64_t(p.tr.K) + 3) >> 2;
+    const uint64_t w = mix64(p.seed ^ mix64(g * J + uint64_t(k >> 2)));
+    return b != (((w >> (16 * (k & 3))) & 0xffffull) < (p.flip_thr >> 48));
   }
   return (__ldg(p.masks + c * uint64_t(p.tr.W) + uint64_t(k >> 6)) >> (k & 63)) & 1ull;
 }
@@ -144,7 +145,7 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
   const unsigned short *lo_ = reinterpret_cast<const unsigned short *>(img + p.tr.o_lo);
   const unsigned short *li_ = reinterpret_cast<const unsigned short *>(img + p.tr.o_li);
   const long long *f0 = reinterpret_cast<const long long *>(img + p.tr.o_f0);
-  const unsigned short *lay = reinterpret_cast<const unsigned short *>(img + p.tr.o_lay);
+  const unsigned short *lay = reinterpret_cast<const unsigned short *>(img + p.tr.o_lay);  // 8 x layer
   // CTA tables of the reference mask R (the SEEDED base; empty for the other kinds):
   // per-layer in / out sums and their cumulative sums, int64 [L] each
   long long *s_INR = reinterpret_cast<long long *>(img + p.stage_bytes);
@@ -199,21 +200,31 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
   for (uint64_t c = uint64_t(blockIdx.x) * nwarps + warp; c < p.count; c += wstride) {
     const uint64_t g = p.first + c;
     // decode: only the items whose bit differs from R add a signed delta to their layers
-    for (int k = lane; k < K; k += 32) {
-      bool diff;
-      bool set;
-      if (seeded) {
-        const uint64_t h = mix64(p.seed ^ mix64(g * uint64_t(K) + uint64_t(k)));
-        diff = h < p.flip_thr;
-        set = ((p.base[k >> 6] >> (k & 63)) & 1ull) == 0ull;  // flipped from 0 -> now set
-      } else {
-        diff = cand_bit(p, g, c, k);
-        set = true;
+    if (seeded) {  // one hash word per 4 items (reading R-seeded); flips are ~flip_thr rare
+      const uint64_t J = (uint64_t(K) + 3) >> 2;
+      const unsigned thr16 = unsigned(p.flip_thr >> 48);
+      for (int q = lane; q < int(J); q += 32) {
+        const uint64_t w = mix64(p.seed ^ mix64(g * J + uint64_t(q)));
+        unsigned f4 = 0;
+#pragma unroll
+        for (int e = 0; e < 4; e++) f4 |= (unsigned((w >> (16 * e)) & 0xffffull) < thr16 ? 1u : 0u) << e;
+        while (f4) {
+          const int e = __ffs(f4) - 1;
+          f4 &= f4 - 1;
+          const int k = 4 * q + e;
+          if (k >= K) break;
+          const bool was = (p.base[k >> 6] >> (k & 63)) & 1ull;
+          const long long v = was ? -S[k] : S[k];
+          acc_add(dI_hi, dI_lo, li_[k], v);
+          acc_add(dO_hi, dO_lo, lo_[k], v);
+        }
       }
-      if (diff) {
-        const long long v = set ? S[k] : -S[k];
-        acc_add(dI_hi, dI_lo, li_[k], v);
-        acc_add(dO_hi, dO_lo, lo_[k], v);
+    } else {
+      for (int k = lane; k < K; k += 32) {
+        if (cand_bit(p, g, c, k)) {
+          acc_add(dI_hi, dI_lo, li_[k], S[k]);
+          acc_add(dO_hi, dO_lo, lo_[k], S[k]);
+        }
       }
     }
     __syncwarp();
@@ -274,16 +285,22 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
     }
     if (kFull) {
       __syncwarp();  // s_D visible to the warp
+      // F_P[i] = F0[i] + D[lay(i)], two ops per 16 B streaming store; 32-bit shared addresses
       const int np = p.row_pairs;
-      const longlong2 *fp2 = reinterpret_cast<const longlong2 *>(f0) + lane;
-      const unsigned *lp = reinterpret_cast<const unsigned *>(lay) + lane;
+      const unsigned sD = static_cast<unsigned>(__cvta_generic_to_shared(s_D));
+      unsigned sF = static_cast<unsigned>(__cvta_generic_to_shared(f0)) + 16u * lane;
+      unsigned sL = static_cast<unsigned>(__cvta_generic_to_shared(lay)) + 4u * lane;
       long long *out = p.footprint + c * p.ld + 2 * lane;
       for (int q = lane; q < np; q += 32) {
-        const longlong2 f = *fp2;
-        const unsigned lz = *lp;
-        st_cs_v2(out, f.x + s_D[lz & 0xffffu], f.y + s_D[lz >> 16]);
-        fp2 += 32;
-        lp += 32;
+        long long fx, fy, d0, d1;
+        unsigned lz;
+        asm("ld.shared.v2.s64 {%0, %1}, [%2];" : "=l"(fx), "=l"(fy) : "r"(sF));
+        asm("ld.shared.u32 %0, [%1];" : "=r"(lz) : "r"(sL));
+        asm("ld.shared.s64 %0, [%1];" : "=l"(d0) : "r"(sD + (lz & 0xffffu)));
+        asm("ld.shared.s64 %0, [%1];" : "=l"(d1) : "r"(sD + (lz >> 16)));
+        st_cs_v2(out, fx + d0, fy + d1);
+        sF += 512u;
+        sL += 128u;
         out += 64;
       }
     }

@@ -190,7 +190,7 @@ extern "C" chm_status chm_trace_build(chm_ctx *ctx, const chm_trace_params *P, c
   }
   std::memcpy(h + D.o_f0, tr->F0.data(), 8 * size_t(N));
   std::vector<uint16_t> lay16(N);
-  for (int32_t i = 0; i < N; i++) lay16[i] = uint16_t(tr->lay_of_op[i]);
+  for (int32_t i = 0; i < N; i++) lay16[i] = uint16_t(8 * tr->lay_of_op[i]);  // byte offset into D[L]
   std::memcpy(h + D.o_lay, lay16.data(), 2 * size_t(N));
   if (tr->W) std::memcpy(h + o_base, tr->base.data(), 8 * size_t(tr->W));
   D.N = N;

@@ -285,11 +285,13 @@ def test_seeded_bits_and_masks_agree():
     seed, thr = 7, int(0.3 * 2 ** 64)
     res = m.eval(O.SEEDED, 5, 50, seed=seed, flip_thr=thr, words=base)
     masks = np.zeros((50, Wd), np.uint64)
+    J = (K + 3) // 4
     for j in range(50):
         c = 5 + j
         for k in range(K):
-            h = O.splitmix64(seed ^ O.splitmix64((c * K + k) % 2 ** 64))
-            bit = int((int(base[k // 64]) >> (k % 64)) & 1) ^ int(h < thr)
+            w = O.splitmix64(seed ^ O.splitmix64((c * J + k // 4) % 2 ** 64))
+            field = (w >> (16 * (k % 4))) & 0xFFFF
+            bit = int((int(base[k // 64]) >> (k % 64)) & 1) ^ int(field < (thr >> 48))
             if bit:
                 masks[j, k // 64] |= np.uint64(1 << (k % 64))
     res2 = m.eval(O.MASKS, 5, 50, words=masks)
@@ -432,3 +434,15 @@ def test_stall_pairwise_within_error_bound_of_exact_sum():
             k = P.bit_length() - 1
             bound = k * u / (1 - k * u) * sum(terms)
             assert abs(got - exact) <= bound + 1e-300
+
+
+def test_seeded_flip_rate():
+    """R-seeded: the flip probability is (flip_thr >> 48) / 2^16 per item."""
+    tr = W.gpt2_xl()
+    m = O.Model(tr)
+    base = m.base_mask()
+    thr = int(0.02 * 2 ** 64)
+    res = m.eval(O.SEEDED, 0, 400, seed=2, flip_thr=thr, words=np.zeros_like(base), nthreads=4)
+    p_hat = res["swapped"].sum() / (400 * tr.nbytes[m.swappable()["t"]].sum())
+    # swapped-bytes-weighted rate is an unbiased estimate of the flip probability
+    assert abs(p_hat - (thr >> 48) / 65536) < 0.004
