@@ -189,8 +189,10 @@ struct chm_ctx {
   std::vector<cudaEvent_t> t0, t1;  // timing events per batch slot (time_batches)
   uint64_t next_batch = 0;
   // eval scratch
-  void *eval_scratch = nullptr;  // per-CTA partial keys + ticket counter
+  void *eval_scratch = nullptr;  // per-CTA partial keys + ticket / work counters
   size_t eval_scratch_bytes = 0;
+  size_t eval_attr_smem[2] = {0, 0};  // cached kernel attribute / occupancy per variant
+  int eval_per_sm[2] = {0, 0};
 };
 
 namespace chm {

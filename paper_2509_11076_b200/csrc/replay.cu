@@ -68,6 +68,7 @@ struct EvalParams {
   int row_pairs;  // 16 B stores per footprint row (ceil(N / 2))
   Key *partial;
   unsigned int *ticket;
+  unsigned long long *work;  // candidate counter for dynamic distribution
   Key *best;
 };
 
@@ -196,8 +197,13 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
 
   Key best;
   best.excess = LLONG_MAX; best.stall = 0.0; best.swapped = LLONG_MAX; best.index = ~0ull; best.peak = 0;
-  const uint64_t wstride = uint64_t(gridDim.x) * nwarps;
-  for (uint64_t c = uint64_t(blockIdx.x) * nwarps + warp; c < p.count; c += wstride) {
+  // dynamic distribution: each warp takes the next candidate from a global counter (fetched
+  // one candidate ahead), so warps the scheduler favours do more and none idles at the end
+  unsigned long long nxt = 0;
+  if (lane == 0) nxt = atomicAdd(p.work, 1ull);
+  uint64_t c = __shfl_sync(0xffffffffu, nxt, 0);
+  while (c < p.count) {
+    if (lane == 0) nxt = atomicAdd(p.work, 1ull);
     const uint64_t g = p.first + c;
     // decode: only the items whose bit differs from R add a signed delta to their layers
     if (seeded) {  // one hash word per 4 items (reading R-seeded); flips are ~flip_thr rare
@@ -305,6 +311,7 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
       }
     }
     __syncwarp();  // scratch reuse by the next candidate
+    c = __shfl_sync(0xffffffffu, nxt, 0);
   }
   // warp keys -> CTA key -> the last CTA to finish reduces all CTA keys into *best
   if (lane == 0) s_best[warp] = best;
@@ -345,6 +352,7 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
   if (lane == 0) {
     *p.best = b;
     *p.ticket = 0u;  // ready for the next launch
+    *p.work = 0ull;
   }
 }
 
@@ -378,9 +386,15 @@ chm_status launch_eval(chm_ctx *ctx, const EvalLaunch &L, cudaStream_t stream) {
   if (smem > 220 * 1024)
     CHM_FAIL(CHM_E_INVAL, "chm_eval_policies: trace image + scratch (%zu B) exceeds shared memory", smem);
   auto kern = fp ? replay_kernel<true> : replay_kernel<false>;
-  CHM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   int per_sm = 0;
-  CHM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+  if (ctx->eval_attr_smem[fp] == smem) {
+    per_sm = ctx->eval_per_sm[fp];
+  } else {
+    CHM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    CHM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+    ctx->eval_attr_smem[fp] = smem;
+    ctx->eval_per_sm[fp] = per_sm;
+  }
   if (per_sm < 1) CHM_FAIL(CHM_E_INVAL, "chm_eval_policies: kernel does not fit an SM");
   if (ctx->cfg.eval_ctas_per_sm) per_sm = std::min(per_sm, int(ctx->cfg.eval_ctas_per_sm));
   const uint64_t grid64 = std::min<uint64_t>(uint64_t(ctx->num_sms) * per_sm, (L.count + threads / 32 - 1) / (threads / 32));
@@ -413,6 +427,7 @@ chm_status launch_eval(chm_ctx *ctx, const EvalLaunch &L, cudaStream_t stream) {
   p.footprint = reinterpret_cast<long long *>(L.footprint);
   p.ld = L.ld;
   p.ticket = reinterpret_cast<unsigned int *>(ctx->eval_scratch);
+  p.work = reinterpret_cast<unsigned long long *>(static_cast<char *>(ctx->eval_scratch) + 64);
   p.partial = reinterpret_cast<Key *>(static_cast<char *>(ctx->eval_scratch) + 256);
   p.best = reinterpret_cast<Key *>(L.best);
   kern<<<grid, threads, smem, stream>>>(p);
