@@ -392,6 +392,16 @@ def main():
         ce_d2h.append(sum(ctx.batch_elapsed_ms(b) for b in outs))
         ce_h2d.append(sum(ctx.batch_elapsed_ms(b) for b in ins))
     ok = ok and all(int(storage[t].sum().item()) == check_sum[t] for t in check_t)
+    # ---- AUTO engine selection (tensors >= 4 MiB on the copy engines, the rest in the kernel)
+    auto_ms = []
+    for step in range(args.ce_steps):
+        torch.cuda.synchronize()
+        ev[0].record(comp)
+        execute(chm.SWAP_AUTO)
+        ev[3].record(comp)
+        torch.cuda.synchronize()
+        auto_ms.append(ev[0].elapsed_time(ev[3]))
+    ok = ok and all(int(storage[t].sum().item()) == check_sum[t] for t in check_t)
     # ---- e2e: the GenPolicy loop through the public API from host records
     e2e_ms = []
     table_bytes = 8 * pt.N + 28 * pt.K + 8 * pt.L + 8 * pt.W
@@ -482,6 +492,11 @@ def main():
             "d2h_GBps": bytes_swap / (np.mean(ce_d2h) * 1e-3) / 1e9 if ce_d2h else None,
             "h2d_GBps": bytes_swap / (np.mean(ce_h2d) * 1e-3) / 1e9 if ce_h2d else None,
             "GBps": 2 * bytes_swap / (np.mean(ce_ms) * 1e-3) / 1e9 if ce_ms else None,
+        },
+        "auto_mode": {
+            "what": "CHM_SWAP_AUTO: tensors >= 4 MiB on the copy engines, the rest in the kernel",
+            "ms_per_step": float(np.mean(auto_ms)) if auto_ms else None,
+            "GBps": 2 * bytes_swap / (np.mean(auto_ms) * 1e-3) / 1e9 if auto_ms else None,
         },
         "e2e": {"value": tot_bytes / (e2e_t * 1e-3) / 1e9 if e2e_t else None, "unit": "GB/s",
                 "h2d_bytes_per_step": bytes_swap + table_bytes, "d2h_bytes_per_step": bytes_swap + 40,

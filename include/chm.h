@@ -70,6 +70,10 @@ typedef struct {
   uint32_t match_window;      /* executor: max recorded ops skipped when aligning a run-time
                                  op to the recorded sequence (0: 32)                         */
   uint32_t time_batches;      /* 1: time every swap batch's copy with CUDA events            */
+  uint64_t ce_min_bytes;      /* CHM_SWAP_AUTO threshold (0: 4 MiB)                          */
+  uint32_t swap_variant;      /* swap kernel: 0 16 B ld/st (default), 1 + L2::256B prefetch
+                                 on loads, 2 TMA bulk copies staged through shared memory
+                                 (16 B-aligned batches; others fall back to 0)              */
 } chm_config;
 
 /* fills the paper's defaults */
@@ -243,7 +247,9 @@ chm_status chm_arena_reserve(chm_ctx *ctx, uint64_t bytes);
 
 enum {
   CHM_SWAP_KERNEL = 0, /* one multi-tensor gather/scatter kernel launch per <= 64 descriptors */
-  CHM_SWAP_CE = 1      /* baseline: one cudaMemcpyAsync per descriptor on the copy engines   */
+  CHM_SWAP_CE = 1,     /* baseline: one cudaMemcpyAsync per descriptor on the copy engines   */
+  CHM_SWAP_AUTO = 2    /* descriptors >= chm_config.ce_min_bytes on the copy engines (256 B
+                          PCIe payloads), the rest in one kernel launch (no per-copy cost)   */
 };
 
 /* Swap-out: records an event on `compute` after the last enqueued op, makes

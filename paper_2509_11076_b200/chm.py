@@ -20,7 +20,7 @@ CHM_OK, CHM_E_INVAL, CHM_E_PARSE, CHM_E_STATE, CHM_E_NOMEM, CHM_E_CUDA, CHM_E_IN
 FWD, BWD, OPT = 0, 1, 2
 WARMUP, GENPOLICY, STABLE = 0, 1, 2
 EXHAUSTIVE, SEEDED, MASKS = 0, 1, 2
-SWAP_KERNEL, SWAP_CE = 0, 1
+SWAP_KERNEL, SWAP_CE, SWAP_AUTO = 0, 1, 2
 
 
 class ChmError(RuntimeError):
@@ -33,7 +33,8 @@ class Config(C.Structure):
     _fields_ = [("m", C.c_uint32), ("n", C.c_uint32), ("len_tol", C.c_double), ("cos_tol", C.c_double),
                 ("cos_mode", C.c_uint32), ("detect_bytes", C.c_uint32), ("device", C.c_int32),
                 ("host_arena_bytes", C.c_uint64), ("swap_ctas", C.c_uint32), ("eval_ctas_per_sm", C.c_uint32),
-                ("match_window", C.c_uint32), ("time_batches", C.c_uint32)]
+                ("match_window", C.c_uint32), ("time_batches", C.c_uint32),
+                ("ce_min_bytes", C.c_uint64), ("swap_variant", C.c_uint32)]
 
 
 class TensorRef(C.Structure):
@@ -232,7 +233,7 @@ class Context:
     """One chm_ctx per device / rank (single owner, not thread-safe)."""
 
     def __init__(self, device: int = 0, host_arena_bytes: int = 0, swap_ctas: int = 0, eval_ctas_per_sm: int = 0,
-                 time_batches: bool = False, **algo1):
+                 time_batches: bool = False, swap_variant: int = 0, ce_min_bytes: int = 0, **algo1):
         L = load()
         cfg = Config()
         L.chm_config_default(C.byref(cfg))
@@ -241,6 +242,8 @@ class Context:
         cfg.swap_ctas = swap_ctas
         cfg.eval_ctas_per_sm = eval_ctas_per_sm
         cfg.time_batches = 1 if time_batches else 0
+        cfg.swap_variant = swap_variant
+        cfg.ce_min_bytes = ce_min_bytes
         for k, v in algo1.items():
             setattr(cfg, k, v)
         h = C.c_void_p()

@@ -44,6 +44,8 @@ extern "C" void chm_config_default(chm_config *c) {
   c->eval_ctas_per_sm = 0;
   c->match_window = 0;
   c->time_batches = 0;
+  c->swap_variant = 0;
+  c->ce_min_bytes = 0;
 }
 
 extern "C" chm_status chm_create(const chm_config *cfg, chm_ctx **out) {
@@ -51,7 +53,7 @@ extern "C" chm_status chm_create(const chm_config *cfg, chm_ctx **out) {
   *out = nullptr;
   chm_config c;
   if (cfg) c = *cfg; else chm_config_default(&c);
-  if (c.len_tol <= 0 || c.cos_tol <= 0 || c.cos_tol > 1 || c.cos_mode > 1)
+  if (c.len_tol <= 0 || c.cos_tol <= 0 || c.cos_tol > 1 || c.cos_mode > 1 || c.swap_variant > 2)
     CHM_FAIL(CHM_E_INVAL, "chm_create: invalid Algo. 1 thresholds / cos_mode");
   if (c.device < 0) {  // host-only ctx: profiler, detection, trace build, executor tables
     if (c.host_arena_bytes) CHM_FAIL(CHM_E_INVAL, "chm_create: a host-only ctx has no arena");

@@ -188,6 +188,7 @@ struct chm_ctx {
   std::vector<cudaEvent_t> fences;  // ring of compute->swap fence events
   std::vector<cudaEvent_t> t0, t1;  // timing events per batch slot (time_batches)
   uint64_t next_batch = 0;
+  std::vector<chm_swap_desc> kernel_descs;  // per-batch scratch (CHM_SWAP_AUTO split)
   // eval scratch
   void *eval_scratch = nullptr;  // per-CTA partial keys + ticket / work counters
   size_t eval_scratch_bytes = 0;
@@ -202,7 +203,7 @@ constexpr int kMaxSeededWords = 64;  // SEEDED base mask in kernel params: K <= 
 
 // launchers (swap.cu / replay.cu)
 chm_status launch_swap_copy(const chm_swap_desc *d, uint32_t n, char *arena, bool to_host,
-                            int ctas, cudaStream_t stream);
+                            int ctas, int variant, cudaStream_t stream);
 struct EvalLaunch {
   DevTrace tr;
   int kind = 0;

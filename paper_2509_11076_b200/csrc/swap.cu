@@ -41,6 +41,13 @@ __device__ __forceinline__ int4 ld_nc_na(const void *p) {
                : "l"(p));
   return v;
 }
+__device__ __forceinline__ int4 ld_nc_na_256(const void *p) {  // + 256 B L2 prefetch hint
+  int4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
 __device__ __forceinline__ void st_cs(void *p, int4 v) {
   asm volatile("st.global.cs.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
                "r"(v.w)
@@ -52,6 +59,7 @@ __device__ __forceinline__ void st_plain(void *p, int4 v) {
                : "memory");
 }
 
+template <bool kPrefetch256>
 __global__ void __launch_bounds__(kSwapThreads) swap_copy_kernel(const __grid_constant__ SwapParams p) {
   for (uint64_t c = blockIdx.x; c < p.total_chunks; c += gridDim.x) {
     uint32_t lo = 0, hi = p.n;  // chunk_begin[lo] <= c < chunk_begin[hi]
@@ -69,7 +77,7 @@ __global__ void __launch_bounds__(kSwapThreads) swap_copy_kernel(const __grid_co
 #pragma unroll
       for (int k = 0; k < kUnroll; k++) {
         const uint32_t idx = threadIdx.x + k * kSwapThreads;
-        if (idx < nvec) v[k] = ld_nc_na(s + 16ull * idx);
+        if (idx < nvec) v[k] = kPrefetch256 ? ld_nc_na_256(s + 16ull * idx) : ld_nc_na(s + 16ull * idx);
       }
 #pragma unroll
       for (int k = 0; k < kUnroll; k++) {
@@ -87,30 +95,123 @@ __global__ void __launch_bounds__(kSwapThreads) swap_copy_kernel(const __grid_co
   }
 }
 
+// TMA bulk-copy variant: one thread per CTA drives a kBulkStages-deep pipeline of
+// cp.async.bulk global->shared (mbarrier completion) and shared->global (bulk group) copies of
+// kBulkStage bytes.  Requires 16 B-aligned addresses and sizes (checked by the launcher).
+constexpr int kBulkStage = 16384;
+constexpr int kBulkStages = 4;
+
+__device__ __forceinline__ void bulk_load(unsigned sdst, const void *src, unsigned n, unsigned bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(n) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sdst),
+               "l"(src), "r"(n), "r"(bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_wait(unsigned bar, unsigned parity) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+
+__global__ void __launch_bounds__(32) swap_bulk_kernel(const __grid_constant__ SwapParams p) {
+  extern __shared__ __align__(128) unsigned char buf[];
+  __shared__ __align__(8) uint64_t mbar[kBulkStages];
+  if (threadIdx.x != 0) return;
+  const unsigned sbuf = static_cast<unsigned>(__cvta_generic_to_shared(buf));
+  unsigned bars[kBulkStages];
+  for (int s = 0; s < kBulkStages; s++) {
+    bars[s] = static_cast<unsigned>(__cvta_generic_to_shared(&mbar[s]));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bars[s]) : "memory");
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  // this CTA's pieces: piece j = global piece blockIdx.x + j * gridDim.x, pieces of kBulkStage B
+  const uint64_t total = p.total_chunks;  // in kBulkStage pieces (launcher)
+  const uint64_t n = total > blockIdx.x ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  auto piece = [&](uint64_t j, const char *&src, char *&dst, unsigned &len) {
+    const uint64_t c = blockIdx.x + j * gridDim.x;
+    uint32_t lo = 0, hi = p.n;
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (p.chunk_begin[mid] <= c) lo = mid; else hi = mid;
+    }
+    const uint64_t off = (c - p.chunk_begin[lo]) * uint64_t(kBulkStage);
+    len = unsigned(min(uint64_t(kBulkStage), p.bytes[lo] - off));
+    src = reinterpret_cast<const char *>(p.src[lo]) + off;
+    dst = reinterpret_cast<char *>(p.dst[lo]) + off;
+  };
+  const char *src;
+  char *dst;
+  unsigned len;
+  for (uint64_t j = 0; j < n && j < kBulkStages - 1; j++) {
+    piece(j, src, dst, len);
+    bulk_load(sbuf + unsigned(j % kBulkStages) * kBulkStage, src, len, bars[j % kBulkStages]);
+  }
+  for (uint64_t it = 0; it < n; it++) {
+    const int s = int(it % kBulkStages);
+    bulk_wait(bars[s], unsigned((it / kBulkStages) & 1));
+    piece(it, src, dst, len);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"(sbuf + unsigned(s) * kBulkStage), "r"(len)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    const uint64_t jn = it + kBulkStages - 1;
+    if (jn < n) {
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // store it-1 left its stage
+      piece(jn, src, dst, len);
+      bulk_load(sbuf + unsigned(jn % kBulkStages) * kBulkStage, src, len, bars[jn % kBulkStages]);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 }  // namespace
 
 chm_status launch_swap_copy(const chm_swap_desc *desc, uint32_t n, char *arena, bool to_host,
-                            int ctas, cudaStream_t stream) {
+                            int ctas, int variant, cudaStream_t stream) {
   for (uint32_t base = 0; base < n; base += kMaxDescPerLaunch) {
     SwapParams p;
     std::memset(&p, 0, sizeof p);
     p.n = std::min<uint32_t>(kMaxDescPerLaunch, n - base);
     p.to_host = to_host ? 1u : 0u;
-    uint64_t chunks = 0;
+    bool aligned = true;
     for (uint32_t j = 0; j < p.n; j++) {
       const chm_swap_desc &d = desc[base + j];
       const uint64_t host = reinterpret_cast<uint64_t>(arena) + d.host_off;
       p.src[j] = to_host ? d.dev : host;
       p.dst[j] = to_host ? host : d.dev;
       p.bytes[j] = d.nbytes;
+      aligned = aligned && ((p.src[j] | p.dst[j] | p.bytes[j]) & 15) == 0;
+    }
+    const bool bulk = variant == 2 && aligned;
+    const uint64_t piece = bulk ? uint64_t(kBulkStage) : kChunk;
+    uint64_t chunks = 0;
+    for (uint32_t j = 0; j < p.n; j++) {
       p.chunk_begin[j] = chunks;
-      chunks += (d.nbytes + kChunk - 1) >> kChunkShift;
+      chunks += (p.bytes[j] + piece - 1) / piece;
     }
     p.chunk_begin[p.n] = chunks;
     p.total_chunks = chunks;
     const int grid = int(std::min<uint64_t>(uint64_t(ctas), chunks));
     if (grid == 0) continue;
-    swap_copy_kernel<<<grid, kSwapThreads, 0, stream>>>(p);
+    if (bulk) {
+      static bool attr = false;
+      if (!attr) {
+        CHM_CUDA(cudaFuncSetAttribute(swap_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kBulkStage * kBulkStages));
+        attr = true;
+      }
+      swap_bulk_kernel<<<grid, 32, kBulkStage * kBulkStages, stream>>>(p);
+    } else if (variant == 1) {
+      swap_copy_kernel<true><<<grid, kSwapThreads, 0, stream>>>(p);
+    } else {
+      swap_copy_kernel<false><<<grid, kSwapThreads, 0, stream>>>(p);
+    }
     CHM_CUDA(cudaGetLastError());
   }
   return CHM_OK;
@@ -160,7 +261,7 @@ static chm_status swap_batch(chm_ctx *ctx, const chm_swap_desc *d, uint32_t n, c
                              bool to_host) {
   if (!ctx) CHM_FAIL(CHM_E_INVAL, "swap: NULL ctx");
   if (ctx->device < 0) CHM_FAIL(CHM_E_STATE, "swap: host-only ctx");
-  if (flags > CHM_SWAP_CE) CHM_FAIL(CHM_E_INVAL, "swap: unknown flags %u", flags);
+  if (flags > CHM_SWAP_AUTO) CHM_FAIL(CHM_E_INVAL, "swap: unknown flags %u", flags);
   chm_status st = validate_batch(ctx, d, n, err);
   if (st != CHM_OK) return st;
   const uint64_t b = ctx->next_batch++;
@@ -171,17 +272,22 @@ static chm_status swap_batch(chm_ctx *ctx, const chm_swap_desc *d, uint32_t n, c
   }
   char *arena = static_cast<char *>(ctx->arena);
   if (!ctx->t0.empty()) CHM_CUDA(cudaEventRecord(ctx->t0[slot], swap));
-  if (flags == CHM_SWAP_CE) {  // baseline: one copy-engine transfer per descriptor
-    for (uint32_t j = 0; j < n; j++) {
-      char *host = arena + d[j].host_off;
-      void *dev = reinterpret_cast<void *>(d[j].dev);
-      CHM_CUDA(cudaMemcpyAsync(to_host ? (void *)host : dev, to_host ? (const void *)dev : host,
-                               d[j].nbytes, to_host ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice,
-                               swap));
-    }
-  } else {
+  const uint64_t ce_min = ctx->cfg.ce_min_bytes ? ctx->cfg.ce_min_bytes : (4ull << 20);
+  auto on_ce = [&](const chm_swap_desc &x) {
+    return flags == CHM_SWAP_CE || (flags == CHM_SWAP_AUTO && x.nbytes >= ce_min);
+  };
+  std::vector<chm_swap_desc> &kd = ctx->kernel_descs;
+  kd.clear();
+  for (uint32_t j = 0; j < n; j++) {
+    if (!on_ce(d[j])) { kd.push_back(d[j]); continue; }
+    char *host = arena + d[j].host_off;  // copy engine: one transfer per descriptor
+    void *dev = reinterpret_cast<void *>(d[j].dev);
+    CHM_CUDA(cudaMemcpyAsync(to_host ? (void *)host : dev, to_host ? (const void *)dev : host,
+                             d[j].nbytes, to_host ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice, swap));
+  }
+  if (!kd.empty()) {
     const int ctas = ctx->cfg.swap_ctas ? int(ctx->cfg.swap_ctas) : 32;
-    st = launch_swap_copy(d, n, arena, to_host, ctas, swap);
+    st = launch_swap_copy(kd.data(), uint32_t(kd.size()), arena, to_host, ctas, int(ctx->cfg.swap_variant), swap);
     if (st != CHM_OK) return st;
   }
   if (!ctx->t1.empty()) CHM_CUDA(cudaEventRecord(ctx->t1[slot], swap));

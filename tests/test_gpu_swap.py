@@ -34,7 +34,7 @@ def rand_bytes(n, seed):
     return torch.randint(0, 256, (n,), dtype=torch.uint8, device="cuda", generator=g)
 
 
-@pytest.mark.parametrize("flags", [chm.SWAP_KERNEL, chm.SWAP_CE])
+@pytest.mark.parametrize("flags", [chm.SWAP_KERNEL, chm.SWAP_CE, chm.SWAP_AUTO])
 def test_round_trip_sizes_and_alignments(ctx, flags):
     sizes = [1, 15, 16, 17, 511, 4096, 65535, 65536, 65537, (4 << 20) + 3, (33 << 20) + 7]
     dev_offs = [0, 1, 16, 3, 0, 8, 0, 5, 16, 0, 2]
@@ -190,3 +190,24 @@ def test_executor_swaps_real_buffers(ctx):
     st = ctx.exec_stats()
     assert n_out == n_in == pt.K == st["n_matched"]
     assert st["bytes_out"] == st["bytes_in"] == int(sum(tr.nbytes[t] for t in item_tensor.values()))
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+def test_round_trip_kernel_variants(variant):
+    """L2::256B-prefetch and TMA bulk-copy variants: byte-exact, incl. a misaligned descriptor
+    (the bulk variant falls back to the 16 B path for a batch that is not 16 B aligned)."""
+    c = chm.Context(device=0, host_arena_bytes=64 << 20, swap_ctas=8, swap_variant=variant)
+    comp, s = torch.cuda.current_stream(), torch.cuda.Stream()
+    for sizes, offs in (([1 << 20, 3 << 20, 48 << 10], [0, 0, 0]), ([1 << 20, (3 << 20) + 5], [0, 3])):
+        bufs = [rand_bytes(n + 16, 7 + j) for j, n in enumerate(sizes)]
+        src = [b[o:o + n] for b, n, o in zip(bufs, sizes, offs)]
+        descs, off = [], 0
+        for x in src:
+            descs.append((x.data_ptr(), off, x.numel()))
+            off += (x.numel() + 511) // 512 * 512
+        c.batch_wait(c.swap_out(descs, comp, s), comp)
+        dst = [torch.zeros_like(x) for x in src]
+        c.batch_wait(c.swap_in([(d.data_ptr(), o, n) for d, (_, o, n) in zip(dst, descs)], comp, s), comp)
+        torch.cuda.synchronize()
+        assert all(torch.equal(a, b) for a, b in zip(dst, src))
+    c.close()
