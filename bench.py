@@ -429,6 +429,28 @@ def main():
         pt2.free()
     ok = ok and all(int(storage[t].sum().item()) == check_sum[t] for t in check_t)
 
+    # ---- re-plan with the paper's generator (NEXT-1): Algo. 2 for a grid of (C, rem_scale) on the
+    # host, then the best of n by a GPU replay of the EXPLICIT item lists
+    t0 = time.perf_counter()
+    gen_lists = [pt.generate_policy(cc, rr)[0] for cc in (0.0, 0.5, 1.0, 2.0) for rr in (0.5, 1.0, 2.0)]
+    t_gen = time.perf_counter() - t0
+    off = np.zeros(len(gen_lists) + 1, np.uint64)
+    off[1:] = np.cumsum([len(x) for x in gen_lists])
+    g_items = np.concatenate(gen_lists)
+    g_peak = torch.empty(len(gen_lists), dtype=torch.int64, device=dev)
+    g_stall = torch.empty(len(gen_lists), dtype=torch.float64, device=dev)
+    g_best = torch.empty(5, dtype=torch.int64, device=dev)
+    torch.cuda.synchronize()
+    ev[0].record(comp)
+    ctx.eval_policies(pt, chm.EXPLICIT, 0, len(gen_lists), best=g_best, peak=g_peak, stall=g_stall,
+                      item_offsets=off, items=g_items, stream=comp)
+    ev[3].record(comp)
+    torch.cuda.synchronize()
+    gb = g_best.cpu().numpy().view(chm.BEST_DTYPE)[0]
+    generator = {"policies": len(gen_lists), "host_generate_ms": t_gen * 1e3,
+                 "gpu_eval_ms": ev[0].elapsed_time(ev[3]), "best_index": int(gb["index"]),
+                 "best_peak": int(gb["peak"]), "best_excess": int(gb["excess"]), "best_stall_s": float(gb["stall"]),
+                 "seeded_best_excess": int(bk["excess"]), "seeded_best_stall_s": float(bk["stall"])}
     # ---- aggregate (max over ranks of time, sum of work)
     t_step = max_over_ranks(float(np.mean(step_ms)))
     t_eval = max_over_ranks(float(np.mean(eval_ms)))
@@ -498,6 +520,7 @@ def main():
             "ms_per_step": float(np.mean(auto_ms)) if auto_ms else None,
             "GBps": 2 * bytes_swap / (np.mean(auto_ms) * 1e-3) / 1e9 if auto_ms else None,
         },
+        "generator": generator,
         "e2e": {"value": tot_bytes / (e2e_t * 1e-3) / 1e9 if e2e_t else None, "unit": "GB/s",
                 "h2d_bytes_per_step": bytes_swap + table_bytes, "d2h_bytes_per_step": bytes_swap + 40,
                 "ms_per_step": e2e_t},

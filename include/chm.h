@@ -172,12 +172,25 @@ chm_status chm_trace_tables(const chm_trace *t, int64_t *f0, uint32_t *tensor, i
                             int32_t *lay_start, int32_t *lay_count, double *bud, uint64_t *base);
 
 /* ------------------------------------------------------------- policy evaluation (a4-a7) */
+/* One swap item of an EXPLICIT candidate: tensor t = production-order index of a produced
+ * activation (the trace's tensor numbering), released after op r, swapped in before op s. */
+typedef struct {
+  uint32_t t;
+  int32_t r, s;
+  uint32_t flags; /* generator output: bit 0 highest-score fallback, bit 1 saturated
+                     swap-out (no layer had T_remaining > T_swap)                      */
+} chm_item;
+
 typedef enum {
   CHM_CAND_EXHAUSTIVE = 0, /* swap set of candidate c = bits of c; requires K <= 63        */
   CHM_CAND_SEEDED = 1,     /* bit t = base[t] ^ [f_t < flip_thr >> 48], f_t = 16-bit field
                               t mod 4 of w = mix(seed ^ mix(c*J + t/4)), J = ceil(K/4),
                               mix = splitmix64 finaliser (reading R-seeded)     */
-  CHM_CAND_MASKS = 2       /* device masks [count][mask_words], little-endian u64 words  */
+  CHM_CAND_MASKS = 2,      /* device masks [count][mask_words], little-endian u64 words  */
+  CHM_CAND_EXPLICIT = 3    /* host item lists: candidate c = items[item_offsets[c] ..
+                              item_offsets[c+1]); validated (CHM_E_INVAL + err_index = item):
+                              t a produced activation, a_t <= r, r + 1 < s <= b_t, no
+                              repeated t within a candidate                             */
 } chm_cand_kind;
 
 typedef struct {
@@ -186,6 +199,8 @@ typedef struct {
   uint64_t seed, flip_thr;     /* SEEDED                                                  */
   const uint64_t *base_mask;   /* SEEDED, host, mask_words words; NULL: the trace's base  */
   const uint64_t *masks;       /* MASKS, device [count][mask_words]                       */
+  const uint64_t *item_offsets;/* EXPLICIT, host [count + 1]                              */
+  const chm_item *items;       /* EXPLICIT, host                                          */
 } chm_candidates;
 
 /* argmin key, compared lexicographically (excess, stall, swapped_bytes, index): feasibility
@@ -215,12 +230,29 @@ typedef struct {
  * writes the per-candidate outputs and the argmin key of this batch into *best. */
 chm_status chm_eval_policies(chm_ctx *ctx, const chm_trace *t, const chm_candidates *c,
                              const chm_eval_out *o, cudaStream_t stream);
+/* chm_eval_policies with the index of the offending EXPLICIT item on CHM_E_INVAL */
+chm_status chm_eval_policies_ex(chm_ctx *ctx, const chm_trace *t, const chm_candidates *c,
+                                const chm_eval_out *o, cudaStream_t stream, int64_t *err_index);
 /* host: lexicographic min of n keys (e.g. after an all-gather across ranks) */
 chm_status chm_best_reduce(const chm_best *keys, uint32_t n, chm_best *out);
 /* device: the same min over n device keys into *out (device), enqueued on `stream` -- the
  * step after the NCCL all-gather of per-rank keys, without a host round trip. */
 chm_status chm_best_reduce_device(chm_ctx *ctx, const chm_best *keys, uint32_t n, chm_best *out,
                                   cudaStream_t stream);
+/* Algo. 2 policy generation on the trace's recorded iteration: MRL -> candidate
+ * list with Eq. 2 scores -> simulated swap-in placement, backward search with the
+ * highest-score fallback -> SetFreeTime forward search.  Writes up to
+ * `cap` items (sorted by a_t, then t) and *n_items; *feasible = 0 when the MRL could not be
+ * cleared (Algo. 2 "Raise Error"; the items chosen so far are still returned).  Host only.
+ * C weighs size against MRE coverage in Eq. 2 (the paper gives no value); rem_scale scales
+ * every layer's initial T_remaining (1 = Eq. 1 budget x omega).  Readings R-gen in DESIGN.md. */
+typedef struct {
+  double C;
+  double rem_scale;
+} chm_gen_params;
+chm_status chm_generate_policy(const chm_trace *t, const chm_gen_params *p, chm_item *items,
+                               uint32_t cap, uint32_t *n_items, int32_t *feasible);
+
 /* host: the swap set of global candidate `index` as mask words (mask_words u64) */
 chm_status chm_candidate_mask(const chm_trace *t, const chm_candidates *c, uint64_t index,
                               uint64_t *words);
@@ -232,6 +264,10 @@ chm_status chm_candidate_mask(const chm_trace *t, const chm_candidates *c, uint6
  * iteration's token frequencies.  Subsequent chm_record_op calls return the
  * policy's actions. */
 chm_status chm_policy_install(chm_ctx *ctx, const chm_trace *t, const uint64_t *words);
+/* the same for an explicit item list (e.g. chm_generate_policy's output): releases after r,
+ * swap-ins before s as given */
+chm_status chm_policy_install_items(chm_ctx *ctx, const chm_trace *t, const chm_item *items,
+                                    uint32_t n);
 typedef struct {
   uint32_t n_items, n_matched, n_stale, n_collisions, n_demand_swap_in;
   uint64_t bytes_out, bytes_in;

@@ -88,6 +88,11 @@ def lib():
         L.orc_splitmix64.restype = C.c_uint64
         L.orc_key_less.argtypes = [C.POINTER(_Best), C.POINTER(_Best)]
         L.orc_swap_execute.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.orc_generate.argtypes = [C.c_void_p, C.c_int64, C.c_double, C.c_double, C.c_int32] + [C.c_void_p] * 5
+        L.orc_generate.restype = C.c_int32
+        L.orc_eval_explicit.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.c_int64, C.c_uint64, C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.c_void_p, C.POINTER(_Best)]
         L.orc_stage_init.argtypes = [C.POINTER(_Stage), C.c_int32, C.c_int32, C.c_double,
                                      C.c_double, C.c_int32]
         L.orc_stage_release.argtypes = [C.POINTER(_Stage)]
@@ -205,6 +210,34 @@ class Model:
         if rc != 0:
             raise ValueError(lib().orc_error().decode())
         return dict(peak=peak, stall=stall, swapped=swapped, footprint=F, best=best)
+
+
+def generate(model: "Model", budget: int = None, C_coef: float = 1.0, rem_scale: float = 1.0):
+    """Algo. 2: returns dict(t, r, s, fallback, saturated, feasible)."""
+    cap = model.T + 1
+    out = [np.zeros(cap, np.int32) for _ in range(5)]
+    b = int(model.trace.budget if budget is None else budget)
+    n = lib().orc_generate(model._h, b, float(C_coef), float(rem_scale), cap, *[_p(x) for x in out])
+    feasible = n >= 0
+    n = n if n >= 0 else -1 - n
+    return dict(zip(["t", "r", "s", "fallback", "saturated"], [x[:n] for x in out]), feasible=feasible)
+
+
+def eval_explicit(model: "Model", lists, budget: int = None, first_index: int = 0, footprint: bool = False):
+    """lists: sequence of (t, r, s) arrays per candidate"""
+    off = np.zeros(len(lists) + 1, np.int64)
+    off[1:] = np.cumsum([len(x[0]) for x in lists])
+    t = np.concatenate([np.asarray(x[0], np.int32) for x in lists] + [np.zeros(0, np.int32)])
+    r = np.concatenate([np.asarray(x[1], np.int32) for x in lists] + [np.zeros(0, np.int32)])
+    s = np.concatenate([np.asarray(x[2], np.int32) for x in lists] + [np.zeros(0, np.int32)])
+    n = len(lists)
+    peak, stall, sw = np.zeros(n, np.int64), np.zeros(n, np.float64), np.zeros(n, np.int64)
+    F = np.zeros((n, model.N), np.int64) if footprint else None
+    best = _Best()
+    lib().orc_eval_explicit(model._h, n, _p(off), _p(t), _p(r), _p(s),
+                            int(model.trace.budget if budget is None else budget), first_index,
+                            _p(peak), _p(stall), _p(sw), _p(F), C.byref(best))
+    return dict(peak=peak, stall=stall, swapped=sw, footprint=F, best=best)
 
 
 def splitmix64(z: int) -> int:

@@ -526,3 +526,156 @@ void orc_features_after(const int32_t *tokens, int32_t n_ops, const int32_t *use
     }
   }
 }
+
+/* ---------------------------------------------------------------------------------------
+ * Algo. 2, policy generation, step by step:
+ *   MRL <- per-op required reduction F0[i] - budget where positive
+ *   while MRL not empty:
+ *     CL <- unselected activations whose span [a_t, b_t) holds an MRE
+ *           Score = N_MRE/max N_MRE + C * S/max S, descending                  (Eq. 2)
+ *           (ties: larger S, smaller a_t, smaller t)
+ *     if CL empty: Raise Error
+ *     simulate swap-in: per candidate, T_swap = S/B (Eq. 3); from the layer before the one
+ *       holding b_t, search backward, not past the layer of the first MRE op in the span nor
+ *       into the swap-out layer, for a layer with T_remaining > T_swap; place the swap-in at
+ *       its first op, T_remaining -= T_swap, decrement S from the MREs of the ops the tensor is
+ *       off device for (a_t, s_t)
+ *       if no candidate fits: the highest-score one goes to the layer before its first BWD use
+ *   SetFreeTime: in swap-out order, from the layer of a_t search forward (up to two layers
+ *     before the swap-in layer) for T_remaining > T_swap; release after its last op, charge
+ *     T_swap; none fits: the last such layer (saturated)
+ * ------------------------------------------------------------------------------------- */
+typedef struct { int32_t t; double score; } gen_cand;
+
+static int gen_cand_before(const orc_model *m, const gen_cand *x, const gen_cand *y) {
+  if (x->score != y->score) return x->score > y->score;
+  if (m->S[x->t] != m->S[y->t]) return m->S[x->t] > m->S[y->t];
+  if (m->a[x->t] != m->a[y->t]) return m->a[x->t] < m->a[y->t];
+  return x->t < y->t;
+}
+
+int32_t orc_generate(const orc_model *m, int64_t budget, double C, double rem_scale, int32_t cap,
+                     int32_t *t_out, int32_t *r_out, int32_t *s_out, int32_t *fb_out, int32_t *sat_out) {
+  int32_t N = m->N, T = m->T, L = m->L;
+  int64_t *mre = xcalloc((size_t)N + 1, sizeof(int64_t));
+  double *rem = xcalloc((size_t)L + 1, sizeof(double));
+  int32_t *sel = xcalloc((size_t)T + 1, sizeof(int32_t));
+  gen_cand *cl = xcalloc((size_t)T + 1, sizeof(gen_cand));
+  int32_t *it_t = xcalloc((size_t)T + 1, sizeof(int32_t)), *it_s = xcalloc((size_t)T + 1, sizeof(int32_t));
+  int32_t *it_fb = xcalloc((size_t)T + 1, sizeof(int32_t));
+  int32_t n = 0, status = 0;
+  for (int32_t i = 0; i < N; i++) mre[i] = m->F0[i] > budget ? m->F0[i] - budget : 0;
+  for (int32_t l = 0; l < L; l++) rem[l] = m->bud[l] * rem_scale;
+  for (;;) {
+    int32_t mrl_empty = 1;
+    for (int32_t i = 0; i < N; i++) if (mre[i] > 0) { mrl_empty = 0; break; }
+    if (mrl_empty) break;
+    /* candidate list with Eq. 2 scores */
+    int32_t ncl = 0, max_n = 0;
+    int64_t max_s = 0;
+    for (int32_t t = 0; t < T; t++) {
+      if (sel[t] || m->p[t] < 0 || m->a[t] < 0 || m->b[t] < 0) continue;
+      int32_t cnt = 0;
+      for (int32_t i = m->a[t]; i < m->b[t]; i++) if (mre[i] > 0) cnt++;
+      if (cnt == 0) continue;
+      cl[ncl].t = t; cl[ncl].score = (double)cnt; ncl++;
+      if (cnt > max_n) max_n = cnt;
+      if (m->S[t] > max_s) max_s = m->S[t];
+    }
+    if (ncl == 0) { status = -1; break; }
+    for (int32_t k = 0; k < ncl; k++)
+      cl[k].score = cl[k].score / (double)max_n + C * ((double)m->S[cl[k].t] / (double)max_s);
+    for (int32_t k = 1; k < ncl; k++) { /* insertion sort, descending score */
+      gen_cand x = cl[k];
+      int32_t j = k - 1;
+      while (j >= 0 && gen_cand_before(m, &x, &cl[j])) { cl[j + 1] = cl[j]; j--; }
+      cl[j + 1] = x;
+    }
+    /* simulate swap-in */
+    int32_t placed = 0;
+    for (int32_t k = 0; k < ncl; k++) {
+      int32_t t = cl[k].t;
+      double tswap = (double)m->S[t] / m->bw;
+      int32_t first_mre = -1;
+      for (int32_t i = m->a[t]; i < m->b[t]; i++) if (mre[i] > 0) { first_mre = i; break; }
+      if (first_mre < 0) continue; /* its MREs were cleared by an earlier candidate */
+      int32_t lo = m->lay_of_op[first_mre];
+      if (lo < m->lay_of_op[m->a[t]] + 1) lo = m->lay_of_op[m->a[t]] + 1;
+      int32_t found = -1;
+      for (int32_t l = m->lay_of_op[m->b[t]] - 1; l >= lo; l--)
+        if (rem[l] > tswap) { found = l; break; }
+      if (found < 0) continue;
+      int32_t sp = m->lay_start[found];
+      rem[found] -= tswap;
+      sel[t] = 1;
+      it_t[n] = t; it_s[n] = sp; it_fb[n] = 0; n++;
+      for (int32_t i = m->a[t] + 1; i < sp; i++) { mre[i] -= m->S[t]; if (mre[i] < 0) mre[i] = 0; }
+      placed = 1;
+      int32_t empty = 1;
+      for (int32_t i = 0; i < N; i++) if (mre[i] > 0) { empty = 0; break; }
+      if (empty) break;
+    }
+    if (!placed) { /* prioritise the highest-score candidate anyway */
+      int32_t t = cl[0].t;
+      double tswap = (double)m->S[t] / m->bw;
+      int32_t l = m->lay_of_op[m->b[t]] - 1;
+      sel[t] = 1;
+      if (l > m->lay_of_op[m->a[t]]) {
+        int32_t sp = m->lay_start[l];
+        rem[l] -= tswap;
+        it_t[n] = t; it_s[n] = sp; it_fb[n] = 1; n++;
+        for (int32_t i = m->a[t] + 1; i < sp; i++) { mre[i] -= m->S[t]; if (mre[i] < 0) mre[i] = 0; }
+      }
+    }
+  }
+  /* SetFreeTime, in swap-out order (a_t, t) */
+  int32_t *ord = xcalloc((size_t)n + 1, sizeof(int32_t));
+  for (int32_t k = 0; k < n; k++) ord[k] = k;
+  for (int32_t k = 1; k < n; k++) {
+    int32_t x = ord[k], j = k - 1;
+    while (j >= 0 && (m->a[it_t[ord[j]]] > m->a[it_t[x]] ||
+                      (m->a[it_t[ord[j]]] == m->a[it_t[x]] && it_t[ord[j]] > it_t[x]))) {
+      ord[j + 1] = ord[j]; j--;
+    }
+    ord[j + 1] = x;
+  }
+  int32_t w = 0;
+  for (int32_t q = 0; q < n; q++) {
+    int32_t k = ord[q], t = it_t[k], sp = it_s[k];
+    double tswap = (double)m->S[t] / m->bw;
+    int32_t lhi = m->lay_of_op[sp] - 2, r = -1, sat = 0;
+    for (int32_t l = m->lay_of_op[m->a[t]]; l <= lhi; l++)
+      if (rem[l] > tswap) { r = m->lay_start[l] + m->lay_n[l] - 1; rem[l] -= tswap; break; }
+    if (r < 0) {
+      sat = 1;
+      r = lhi >= m->lay_of_op[m->a[t]] ? m->lay_start[lhi] + m->lay_n[lhi] - 1 : sp - 2;
+    }
+    if (r < m->a[t] || !(r + 1 < sp)) continue; /* no off-device window */
+    if (w < cap) { t_out[w] = t; r_out[w] = r; s_out[w] = sp; fb_out[w] = it_fb[k]; sat_out[w] = sat; }
+    w++;
+  }
+  free(ord); free(mre); free(rem); free(sel); free(cl); free(it_t); free(it_s); free(it_fb);
+  return status < 0 ? -1 - w : w;
+}
+
+int orc_eval_explicit(const orc_model *m, int32_t count, const int64_t *off, const int32_t *t,
+                      const int32_t *r, const int32_t *s, int64_t budget, uint64_t first_index,
+                      int64_t *peak, double *stall, int64_t *swapped, int64_t *footprint,
+                      orc_best *best) {
+  int have = 0;
+  orc_best b = {0, 0.0, 0, 0, 0};
+  for (int32_t c = 0; c < count; c++) {
+    int32_t n = (int32_t)(off[c + 1] - off[c]);
+    const int32_t *tt = t + off[c], *rr = r + off[c], *ss = s + off[c];
+    int64_t out_b;
+    int64_t pk = orc_replay(m, n, tt, rr, ss, footprint ? footprint + (size_t)c * (size_t)m->N : NULL, &out_b, NULL);
+    double st = orc_stall(m, n, tt, rr, ss);
+    if (peak) peak[c] = pk;
+    if (stall) stall[c] = st;
+    if (swapped) swapped[c] = out_b;
+    orc_best key = { pk > budget ? pk - budget : 0, st, out_b, first_index + (uint64_t)c, pk };
+    if (!have || orc_key_less(&key, &b)) { b = key; have = 1; }
+  }
+  if (best) *best = b;
+  return 0;
+}

@@ -86,6 +86,20 @@ int orc_eval(const orc_model *m, int kind, uint64_t first, uint64_t count, uint6
 uint64_t orc_splitmix64(uint64_t z);
 int orc_key_less(const orc_best *x, const orc_best *y);
 
+/* Algo. 2 policy generation with the simulator of P:315-340; readings R-gen in
+ * DESIGN.md.  Items are (tensor, release op r, swap-in op s) sorted by (a_t, t).  Returns the
+ * number of items, or -1 if the MRL cannot be cleared ("Raise Error") -- the items chosen
+ * so far are still written.  fallback[k] = 1 if item k was placed by the highest-score fallback
+ * (P:333), saturated[k] = 1 if its swap-out found no layer with enough remaining time.
+ * rem_scale scales the layers' initial T_remaining (1 = Eq. 1 budgets x omega). */
+int32_t orc_generate(const orc_model *m, int64_t budget, double C, double rem_scale, int32_t cap,
+                     int32_t *t, int32_t *r, int32_t *s, int32_t *fallback, int32_t *saturated);
+/* Evaluate explicit item lists: candidate c = items [off[c], off[c+1]); outputs nullable */
+int orc_eval_explicit(const orc_model *m, int32_t count, const int64_t *off, const int32_t *t,
+                      const int32_t *r, const int32_t *s, int64_t budget, uint64_t first_index,
+                      int64_t *peak, double *stall, int64_t *swapped, int64_t *footprint,
+                      orc_best *best);
+
 /* Swap execution oracle: after a swap the destination range equals the
  * source range byte for byte.  Executed literally on host buffers (memcpy per descriptor). */
 void orc_swap_execute(int32_t n, void *const *dst, const void *const *src, const uint64_t *nbytes);

@@ -19,7 +19,7 @@ CHM_OK, CHM_E_INVAL, CHM_E_PARSE, CHM_E_STATE, CHM_E_NOMEM, CHM_E_CUDA, CHM_E_IN
     0, -1, -2, -3, -4, -5, -6, -7
 FWD, BWD, OPT = 0, 1, 2
 WARMUP, GENPOLICY, STABLE = 0, 1, 2
-EXHAUSTIVE, SEEDED, MASKS = 0, 1, 2
+EXHAUSTIVE, SEEDED, MASKS, EXPLICIT = 0, 1, 2, 3
 SWAP_KERNEL, SWAP_CE, SWAP_AUTO = 0, 1, 2
 
 
@@ -75,7 +75,19 @@ class TraceInfo(C.Structure):
 
 class Candidates(C.Structure):
     _fields_ = [("kind", C.c_int), ("first_index", C.c_uint64), ("count", C.c_uint64), ("seed", C.c_uint64),
-                ("flip_thr", C.c_uint64), ("base_mask", C.c_void_p), ("masks", C.c_void_p)]
+                ("flip_thr", C.c_uint64), ("base_mask", C.c_void_p), ("masks", C.c_void_p),
+                ("item_offsets", C.c_void_p), ("items", C.c_void_p)]
+
+
+class Item(C.Structure):
+    _fields_ = [("t", C.c_uint32), ("r", C.c_int32), ("s", C.c_int32), ("flags", C.c_uint32)]
+
+
+ITEM_DTYPE = np.dtype([("t", np.uint32), ("r", np.int32), ("s", np.int32), ("flags", np.uint32)])
+
+
+class GenParams(C.Structure):
+    _fields_ = [("C", C.c_double), ("rem_scale", C.c_double)]
 
 
 class Best(C.Structure):
@@ -104,8 +116,8 @@ class ExecStats(C.Structure):
 EXPORTS = [
     "chm_config_default", "chm_create", "chm_destroy", "chm_last_error", "chm_build_info", "chm_tokenize",
     "chm_record_op", "chm_set_detailed", "chm_detect_seq_change", "chm_trace_build", "chm_trace_free",
-    "chm_trace_get_info", "chm_trace_tables", "chm_eval_policies", "chm_best_reduce", "chm_best_reduce_device", "chm_candidate_mask",
-    "chm_policy_install", "chm_exec_stats_get", "chm_host_arena", "chm_swap_out", "chm_swap_in",
+    "chm_trace_get_info", "chm_trace_tables", "chm_eval_policies", "chm_eval_policies_ex", "chm_best_reduce", "chm_best_reduce_device", "chm_candidate_mask",
+    "chm_policy_install", "chm_policy_install_items", "chm_generate_policy", "chm_exec_stats_get", "chm_host_arena", "chm_swap_out", "chm_swap_in",
     "chm_batch_wait", "chm_batch_query", "chm_batch_elapsed", "chm_arena_reserve", "chm_issue_swap_out", "chm_issue_swap_in", "chm_item_wait",
 ]
 
@@ -137,6 +149,9 @@ def load(path: str = LIB_PATH):
         "chm_trace_get_info": (i32, [vp, P(TraceInfo)]),
         "chm_trace_tables": (i32, [vp] + [vp] * 11),
         "chm_eval_policies": (i32, [vp, vp, P(Candidates), P(EvalOut), vp]),
+        "chm_eval_policies_ex": (i32, [vp, vp, P(Candidates), P(EvalOut), vp, P(i64)]),
+        "chm_generate_policy": (i32, [vp, P(GenParams), vp, u32, P(u32), P(i32)]),
+        "chm_policy_install_items": (i32, [vp, vp, vp, u32]),
         "chm_best_reduce": (i32, [vp, u32, P(Best)]),
         "chm_best_reduce_device": (i32, [vp, vp, u32, vp, vp]),
         "chm_candidate_mask": (i32, [vp, P(Candidates), u64, vp]),
@@ -209,11 +224,20 @@ class Trace:
         out["base"] = out["base"][:W]
         return out
 
+    def generate_policy(self, C_coef: float = 1.0, rem_scale: float = 1.0):
+        """Algo. 2 -> (items ITEM_DTYPE array, feasible)"""
+        cap = self.T + 1
+        out = np.zeros(cap, ITEM_DTYPE)
+        n, feas = C.c_uint32(), C.c_int32()
+        _check(load().chm_generate_policy(self.h, C.byref(GenParams(C_coef, rem_scale)), out.ctypes.data, cap,
+                                          C.byref(n), C.byref(feas)))
+        return out[:n.value], bool(feas.value)
+
     def candidate_mask(self, kind: int, index: int, seed: int = 0, flip_thr: int = 0,
                        base: Optional[np.ndarray] = None) -> np.ndarray:
         w = np.zeros(max(self.W, 1), np.uint64)
         b = np.ascontiguousarray(base, np.uint64) if base is not None else None
-        c = Candidates(kind, 0, 1, seed, flip_thr, _ptr(b), None)
+        c = Candidates(kind, 0, 1, seed, flip_thr, _ptr(b), None, None, None)
         _check(load().chm_candidate_mask(self.h, C.byref(c), index, w.ctypes.data))
         return w[:self.W]
 
@@ -300,11 +324,23 @@ class Context:
     # ------------------------------------------------------------ policy evaluation
     def eval_policies(self, trace: Trace, kind: int, first: int, count: int, *, best, seed: int = 0,
                       flip_thr: int = 0, base: Optional[np.ndarray] = None, masks=None, peak=None, stall=None,
-                      swapped=None, footprint=None, ld: int = 0, stream=None):
+                      swapped=None, footprint=None, ld: int = 0, stream=None, item_offsets=None, items=None):
         b = np.ascontiguousarray(base, np.uint64) if base is not None else None
-        c = Candidates(kind, first, count, seed, flip_thr, _ptr(b), _ptr(masks))
+        off = np.ascontiguousarray(item_offsets, np.uint64) if item_offsets is not None else None
+        its = np.ascontiguousarray(items, ITEM_DTYPE) if items is not None else None
+        c = Candidates(kind, first, count, seed, flip_thr, _ptr(b), _ptr(masks), _ptr(off),
+                       _ptr(its) if its is not None and its.size else None)
         o = EvalOut(_ptr(peak), _ptr(stall), _ptr(swapped), _ptr(footprint), ld, _ptr(best))
-        _check(load().chm_eval_policies(self.h, trace.h, C.byref(c), C.byref(o), _stream(stream)))
+        e = C.c_int64()
+        rc = load().chm_eval_policies_ex(self.h, trace.h, C.byref(c), C.byref(o), _stream(stream), C.byref(e))
+        if rc != CHM_OK:
+            err = ChmError(rc, (load().chm_last_error() or b"").decode())
+            err.index = e.value
+            raise err
+
+    def policy_install_items(self, trace: Trace, items):
+        its = np.ascontiguousarray(items, ITEM_DTYPE)
+        _check(load().chm_policy_install_items(self.h, trace.h, its.ctypes.data if its.size else None, len(its)))
 
     def best_reduce_device(self, keys, n: int, out, stream=None):
         _check(load().chm_best_reduce_device(self.h, _ptr(keys), n, _ptr(out), _stream(stream)))

@@ -83,13 +83,16 @@ static inline void feature_update(Feature &f, int32_t token, uint8_t dtype, uint
   f.slot = uint8_t(slot < 255 ? slot : 255);  // position among the op's distinct tensors
 }
 
-extern "C" chm_status chm_policy_install(chm_ctx *ctx, const chm_trace *t, const uint64_t *words) {
-  if (!ctx || !t || (!words && t->W)) CHM_FAIL(CHM_E_INVAL, "chm_policy_install: NULL argument");
-  std::vector<int32_t> sel;
-  for (int32_t k = 0; k < t->K; k++)
-    if ((words[k / 64] >> (k % 64)) & 1ull) sel.push_back(k);
+namespace {
+struct InstallItem {
+  int32_t tid, r, s;
+  int64_t nbytes;
+};
+}  // namespace
+
+static chm_status install_items(chm_ctx *ctx, const chm_trace *t, const std::vector<InstallItem> &sel) {
   uint64_t need = 0;
-  for (int32_t k : sel) need += (uint64_t(t->sw_S[k]) + 511) & ~uint64_t(511);
+  for (const InstallItem &x : sel) need += (uint64_t(x.nbytes) + 511) & ~uint64_t(511);
   if (ctx->device >= 0 && need > ctx->arena_bytes)  // a host-only ctx plans offsets only
     CHM_FAIL(CHM_E_NOMEM, "chm_policy_install: policy needs %llu arena bytes, arena has %llu",
              (unsigned long long)need, (unsigned long long)ctx->arena_bytes);
@@ -99,13 +102,13 @@ extern "C" chm_status chm_policy_install(chm_ctx *ctx, const chm_trace *t, const
   ctx->items.assign(sel.size(), PolicyItem());
   uint64_t off = 0;
   for (size_t j = 0; j < sel.size(); j++) {
-    const int32_t k = sel[j], tid = t->sw_tensor_idx[k];
+    const int32_t tid = sel[j].tid;
     PolicyItem &it = ctx->items[j];
     it.a = t->a[tid];
     it.b = t->b[tid];
-    it.r = t->sw_r[k];
-    it.s = t->sw_s[k];
-    it.nbytes = t->sw_S[k];
+    it.r = sel[j].r;
+    it.s = sel[j].s;
+    it.nbytes = sel[j].nbytes;
     it.host_off = off;
     off += (uint64_t(it.nbytes) + 511) & ~uint64_t(511);
     item_of_tensor[tid] = int32_t(j);
@@ -149,6 +152,37 @@ extern "C" chm_status chm_policy_install(chm_ctx *ctx, const chm_trace *t, const
   ctx->op_cursor = 0;
   ctx->policy_active = true;
   return CHM_OK;
+}
+
+extern "C" chm_status chm_policy_install(chm_ctx *ctx, const chm_trace *t, const uint64_t *words) {
+  if (!ctx || !t || (!words && t->W)) CHM_FAIL(CHM_E_INVAL, "chm_policy_install: NULL argument");
+  std::vector<InstallItem> sel;
+  for (int32_t k = 0; k < t->K; k++)
+    if ((words[k / 64] >> (k % 64)) & 1ull)
+      sel.push_back({t->sw_tensor_idx[k], t->sw_r[k], t->sw_s[k], t->sw_S[k]});
+  return install_items(ctx, t, sel);
+}
+
+extern "C" chm_status chm_policy_install_items(chm_ctx *ctx, const chm_trace *t, const chm_item *items,
+                                               uint32_t n) {
+  if (!ctx || !t || (n && !items)) CHM_FAIL(CHM_E_INVAL, "chm_policy_install_items: NULL argument");
+  const int32_t n_prod = int32_t(t->rank_to_tensor.size());
+  std::vector<InstallItem> sel;
+  std::vector<char> seen(size_t(n_prod), 0);
+  for (uint32_t j = 0; j < n; j++) {
+    const chm_item &it = items[j];
+    if (int64_t(it.t) >= n_prod) CHM_FAIL(CHM_E_INVAL, "chm_policy_install_items: item %u: bad tensor", j);
+    const int32_t tid = t->rank_to_tensor[it.t];
+    if (t->a[tid] < 0 || t->b[tid] < 0 || it.r < t->a[tid] || !(it.r + 1 < it.s) || it.s > t->b[tid] || seen[it.t])
+      CHM_FAIL(CHM_E_INVAL, "chm_policy_install_items: item %u (t %u, r %d, s %d) invalid", j, it.t, it.r, it.s);
+    seen[it.t] = 1;
+    sel.push_back({tid, it.r, it.s, t->S_t[tid]});
+  }
+  std::stable_sort(sel.begin(), sel.end(), [&](const InstallItem &x, const InstallItem &y) {
+    if (t->a[x.tid] != t->a[y.tid]) return t->a[x.tid] < t->a[y.tid];
+    return t->tensor_rank[x.tid] < t->tensor_rank[y.tid];
+  });
+  return install_items(ctx, t, sel);
 }
 
 // Aligns run-time op i to a recorded op index: the next recorded op if its token matches; else

@@ -139,6 +139,8 @@ struct chm_trace {
   std::vector<double> bud;
   std::vector<uint32_t> sw_t;          // swappable k -> production-order tensor rank
   std::vector<int32_t> sw_tensor_idx;  // swappable k -> recorded tensor index
+  std::vector<int32_t> rank_to_tensor;  // production rank -> recorded tensor index
+  std::vector<int32_t> tensor_rank;     // recorded tensor index -> production rank (-1: static)
   std::vector<int64_t> sw_S;
   std::vector<int32_t> sw_r, sw_s, sw_lin, sw_lout;
   std::vector<uint64_t> base;
@@ -192,6 +194,8 @@ struct chm_ctx {
   // eval scratch
   void *eval_scratch = nullptr;  // per-CTA partial keys + ticket / work counters
   size_t eval_scratch_bytes = 0;
+  void *explicit_scratch = nullptr;  // EXPLICIT candidates: items + offsets + keys (device)
+  size_t explicit_scratch_bytes = 0;
   size_t eval_attr_smem[2] = {0, 0};  // cached kernel attribute / occupancy per variant
   int eval_per_sm[2] = {0, 0};
 };
@@ -218,4 +222,7 @@ struct EvalLaunch {
   chm_best *best = nullptr;
 };
 chm_status launch_eval(chm_ctx *ctx, const EvalLaunch &L, cudaStream_t stream);
+// explicit.cu: generic replay of explicit item lists (arbitrary r, s)
+chm_status launch_eval_explicit(chm_ctx *ctx, const chm_trace *t, const chm_candidates *c,
+                                const chm_eval_out *o, cudaStream_t stream, int64_t *err_index);
 }  // namespace chm

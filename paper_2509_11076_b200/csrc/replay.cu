@@ -441,6 +441,12 @@ using namespace chm;
 
 extern "C" chm_status chm_eval_policies(chm_ctx *ctx, const chm_trace *t, const chm_candidates *c,
                                         const chm_eval_out *o, cudaStream_t stream) {
+  return chm_eval_policies_ex(ctx, t, c, o, stream, nullptr);
+}
+
+extern "C" chm_status chm_eval_policies_ex(chm_ctx *ctx, const chm_trace *t, const chm_candidates *c,
+                                           const chm_eval_out *o, cudaStream_t stream, int64_t *err_index) {
+  if (err_index) *err_index = -1;
   if (!ctx || !t || !c || !o) CHM_FAIL(CHM_E_INVAL, "chm_eval_policies: NULL argument");
   if (!o->best) CHM_FAIL(CHM_E_INVAL, "chm_eval_policies: out.best is required");
   if (c->count == 0) CHM_FAIL(CHM_E_INVAL, "chm_eval_policies: empty candidate range");
@@ -468,6 +474,11 @@ extern "C" chm_status chm_eval_policies(chm_ctx *ctx, const chm_trace *t, const 
       if (!c->masks && t->W) CHM_FAIL(CHM_E_INVAL, "MASKS candidates need a device mask array");
       L.masks = c->masks;
       break;
+    case CHM_CAND_EXPLICIT:
+      if (o->footprint && (o->ld < uint32_t(t->N) || (o->ld & 1u)))
+        CHM_FAIL(CHM_E_INVAL, "chm_eval_policies: footprint ld %u must be even and >= n_ops %d", o->ld, t->N);
+      CHM_CUDA(cudaSetDevice(ctx->device));
+      return launch_eval_explicit(ctx, t, c, o, stream, err_index);
     default:
       CHM_FAIL(CHM_E_INVAL, "chm_eval_policies: unknown candidate kind %d", int(c->kind));
   }

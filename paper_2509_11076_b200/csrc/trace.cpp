@@ -142,6 +142,9 @@ extern "C" chm_status chm_trace_build(chm_ctx *ctx, const chm_trace_params *P, c
   tr->use_idx = R.use_idx;
   tr->dtype.resize(T);
   for (int32_t t = 0; t < T; t++) tr->dtype[t] = R.tensors[t].dtype;
+  tr->tensor_rank = prod_rank;
+  tr->rank_to_tensor.assign(size_t(R.out_idx.size()), -1);
+  for (int32_t t = 0; t < T; t++) if (prod_rank[t] >= 0) tr->rank_to_tensor[prod_rank[t]] = t;
   // swappable k -> product tensor index (kept for install)
   std::vector<int32_t> sw_tensor(tr->K);
   for (int32_t k = 0; k < tr->K; k++) sw_tensor[k] = cands[k].t;

@@ -215,3 +215,76 @@ def test_algo1_parity_random_schedule(ctx):
         assert got["len_diff"] == exp["len_diff"] and got["cos"] == exp["cos"]
         assert got["changed"] == (not exp["stable"])
     c.close()
+
+
+# ------------------------------------------------------------------- EXPLICIT (NEXT-1)
+def run_explicit(ctx, pt, lists, footprint=True):
+    dev = torch.device("cuda:0")
+    n = len(lists)
+    off = np.zeros(n + 1, np.uint64)
+    off[1:] = np.cumsum([len(x) for x in lists])
+    items = np.concatenate([np.asarray(x, chm.ITEM_DTYPE) for x in lists] + [np.zeros(0, chm.ITEM_DTYPE)])
+    peak = torch.empty(n, dtype=torch.int64, device=dev)
+    stall = torch.empty(n, dtype=torch.float64, device=dev)
+    swapped = torch.empty(n, dtype=torch.int64, device=dev)
+    best = torch.empty(5, dtype=torch.int64, device=dev)
+    ld = (pt.N + 1) // 2 * 2
+    fp = torch.empty((n, ld), dtype=torch.int64, device=dev) if footprint else None
+    ctx.eval_policies(pt, chm.EXPLICIT, 0, n, best=best, peak=peak, stall=stall, swapped=swapped, footprint=fp,
+                      ld=ld if footprint else 0, item_offsets=off, items=items)
+    torch.cuda.synchronize()
+    return dict(peak=peak.cpu().numpy(), stall=stall.cpu().numpy(), swapped=swapped.cpu().numpy(),
+                footprint=fp[:, :pt.N].cpu().numpy() if footprint else None,
+                best=best.cpu().numpy().view(chm.BEST_DTYPE)[0])
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C5"])
+def test_explicit_generator_policies(ctx, name):
+    """best-of-n over Algo. 2 policies for a grid of (C, rem_scale): GPU replay of the
+    EXPLICIT item lists vs the oracle's event replay, bit-exact."""
+    tr = W.CONFIGS[name]()
+    pt = product_trace(ctx, tr)
+    m = O.Model(tr)
+    lists, ref_lists = [], []
+    for C_coef in (0.0, 0.5, 1.0, 2.0):
+        for rem in (0.5, 1.0, 2.0):
+            items, _ = pt.generate_policy(C_coef, rem)
+            lists.append(items)
+            ref_lists.append((items["t"].astype(np.int32), items["r"], items["s"]))
+    res = run_explicit(ctx, pt, lists)
+    ref = O.eval_explicit(m, ref_lists, footprint=True)
+    assert_same(res, ref, tr.budget)
+
+
+def test_explicit_random_windows_and_empty(ctx):
+    tr = W.gpt2_xl()
+    pt = product_trace(ctx, tr)
+    m = O.Model(tr)
+    p, f, a, b = m.tensor_table()
+    rng = np.random.default_rng(4)
+    acts = [t for t in range(tr.n_produced) if a[t] >= 0 and b[t] >= 0 and b[t] - a[t] >= 3]
+    lists, ref_lists = [], []
+    for c in range(40):
+        sel = rng.choice(acts, size=int(rng.integers(0, 60)), replace=False)
+        its = []
+        for t in sel:
+            r = int(rng.integers(a[t], b[t] - 1))
+            s = int(rng.integers(r + 2, b[t] + 1))
+            its.append((t, r, s, 0))
+        arr = np.array(its, chm.ITEM_DTYPE) if its else np.zeros(0, chm.ITEM_DTYPE)
+        lists.append(arr)
+        ref_lists.append((arr["t"].astype(np.int32), arr["r"], arr["s"]))
+    res = run_explicit(ctx, pt, lists)
+    ref = O.eval_explicit(m, ref_lists, footprint=True)
+    assert_same(res, ref, tr.budget)
+
+
+def test_explicit_validation_error_index(ctx):
+    tr = W.tiny()
+    pt = product_trace(ctx, tr)
+    items, _ = pt.generate_policy(1.0, 1.0)
+    bad = items.copy()
+    bad["r"][1] = bad["s"][1]  # r + 1 < s violated on item 1
+    with pytest.raises(chm.ChmError) as e:
+        run_explicit(ctx, pt, [items, bad])
+    assert e.value.code == chm.CHM_E_INVAL and e.value.index == len(items) + 1
