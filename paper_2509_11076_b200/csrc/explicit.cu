@@ -203,7 +203,7 @@ chm_status launch_eval_explicit(chm_ctx *ctx, const chm_trace *t, const chm_cand
   unsigned char *d = static_cast<unsigned char *>(ctx->explicit_scratch);
   CHM_CUDA(cudaMemcpyAsync(d, host.data(), host.size(), cudaMemcpyHostToDevice, stream));
   XParams p{};
-  p.f0 = reinterpret_cast<const long long *>(t->dev.image + t->dev.o_f0);
+  p.f0 = reinterpret_cast<const long long *>(t->dev.image + t->dev.o_f0w);
   p.lay8 = reinterpret_cast<const unsigned short *>(t->dev.image + t->dev.o_lay);
   p.bud = reinterpret_cast<const double *>(t->dev.image + t->dev.o_bud);
   p.S_rank = reinterpret_cast<const long long *>(d);

@@ -116,7 +116,11 @@ struct DevTrace {
   uint32_t o_S = 0;     // int64 [K]  swappable sizes (mask-bit order)
   uint32_t o_lo = 0;    // u16   [K]  lout (release layer) per swappable, mask-bit order
   uint32_t o_li = 0;    // u16   [K]  lin (swap-in layer) per swappable, mask-bit order
-  uint32_t o_f0 = 0;    // int64 [N]  no-swap footprint (full mode)
+  uint32_t o_f0 = 0;    // [N] no-swap footprint (full mode): int32 units of 2^f0_shift B if
+                        // f0_narrow, else int64
+  uint32_t o_f0w = 0;   // int64 [N] no-swap footprint, global only (not staged; EXPLICIT replay)
+  int32_t f0_shift = 0;
+  int32_t f0_narrow = 0;
   uint32_t o_lay = 0;   // u16   [N]  8 x logical layer of each op (byte offset into D, full mode)
   const uint64_t *base = nullptr;
   int32_t N = 0, K = 0, L = 0, W = 0;
@@ -196,8 +200,8 @@ struct chm_ctx {
   size_t eval_scratch_bytes = 0;
   void *explicit_scratch = nullptr;  // EXPLICIT candidates: items + offsets + keys (device)
   size_t explicit_scratch_bytes = 0;
-  size_t eval_attr_smem[2] = {0, 0};  // cached kernel attribute / occupancy per variant
-  int eval_per_sm[2] = {0, 0};
+  size_t eval_attr_smem[3] = {0, 0, 0};  // cached kernel attribute / occupancy per variant
+  int eval_per_sm[3] = {0, 0, 0};
 };
 
 namespace chm {

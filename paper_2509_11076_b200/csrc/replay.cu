@@ -132,7 +132,7 @@ __device__ __forceinline__ void acc_add(unsigned *hi, unsigned *lo, int l, long 
   atomicAdd(lo + l, neg ? 0u - w : w);
 }
 
-template <bool kFull>
+template <bool kFull, bool kNarrow>
 __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_constant__ EvalParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ __align__(8) uint64_t s_mbar;
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
   const long long *S = reinterpret_cast<const long long *>(img + p.tr.o_S);
   const unsigned short *lo_ = reinterpret_cast<const unsigned short *>(img + p.tr.o_lo);
   const unsigned short *li_ = reinterpret_cast<const unsigned short *>(img + p.tr.o_li);
-  const long long *f0 = reinterpret_cast<const long long *>(img + p.tr.o_f0);
+  const unsigned char *f0 = img + p.tr.o_f0;  // int32 units (kNarrow) or int64
   const unsigned short *lay = reinterpret_cast<const unsigned short *>(img + p.tr.o_lay);  // 8 x layer
   // CTA tables of the reference mask R (the SEEDED base; empty for the other kinds):
   // per-layer in / out sums and their cumulative sums, int64 [L] each
@@ -292,20 +292,31 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
     if (kFull) {
       __syncwarp();  // s_D visible to the warp
       // F_P[i] = F0[i] + D[lay(i)], two ops per 16 B streaming store; 32-bit shared addresses
-      const int np = p.row_pairs;
+      const int np = p.row_pairs, sh = p.tr.f0_shift;
       const unsigned sD = static_cast<unsigned>(__cvta_generic_to_shared(s_D));
-      unsigned sF = static_cast<unsigned>(__cvta_generic_to_shared(f0)) + 16u * lane;
+      unsigned sF = static_cast<unsigned>(__cvta_generic_to_shared(f0)) + (kNarrow ? 8u : 16u) * lane;
       unsigned sL = static_cast<unsigned>(__cvta_generic_to_shared(lay)) + 4u * lane;
       long long *out = p.footprint + c * p.ld + 2 * lane;
       for (int q = lane; q < np; q += 32) {
         long long fx, fy, d0, d1;
         unsigned lz;
-        asm("ld.shared.v2.s64 {%0, %1}, [%2];" : "=l"(fx), "=l"(fy) : "r"(sF));
+        if (kNarrow) {
+          int ux, uy;
+          asm("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(ux), "=r"(uy) : "r"(sF));
+          fx = (long long)ux << sh;
+          fy = (long long)uy << sh;
+        } else {
+          asm("ld.shared.v2.s64 {%0, %1}, [%2];" : "=l"(fx), "=l"(fy) : "r"(sF));
+        }
         asm("ld.shared.u32 %0, [%1];" : "=r"(lz) : "r"(sL));
         asm("ld.shared.s64 %0, [%1];" : "=l"(d0) : "r"(sD + (lz & 0xffffu)));
-        asm("ld.shared.s64 %0, [%1];" : "=l"(d1) : "r"(sD + (lz >> 16)));
+        if ((lz >> 16) == (lz & 0xffffu)) {
+          d1 = d0;  // both ops of the pair in one layer: one lookup
+        } else {
+          asm("ld.shared.s64 %0, [%1];" : "=l"(d1) : "r"(sD + (lz >> 16)));
+        }
         st_cs_v2(out, fx + d0, fy + d1);
-        sF += 512u;
+        sF += kNarrow ? 256u : 512u;
         sL += 128u;
         out += 64;
       }
@@ -385,15 +396,17 @@ chm_status launch_eval(chm_ctx *ctx, const EvalLaunch &L, cudaStream_t stream) {
   const size_t smem = size_t(stage) + cta_tab + size_t(threads / 32) * wscr16;
   if (smem > 220 * 1024)
     CHM_FAIL(CHM_E_INVAL, "chm_eval_policies: trace image + scratch (%zu B) exceeds shared memory", smem);
-  auto kern = fp ? replay_kernel<true> : replay_kernel<false>;
+  const bool narrow = L.tr.f0_narrow != 0;
+  auto kern = fp ? (narrow ? replay_kernel<true, true> : replay_kernel<true, false>) : replay_kernel<false, false>;
+  const int var = fp ? (narrow ? 2 : 1) : 0;
   int per_sm = 0;
-  if (ctx->eval_attr_smem[fp] == smem) {
-    per_sm = ctx->eval_per_sm[fp];
+  if (ctx->eval_attr_smem[var] == smem) {
+    per_sm = ctx->eval_per_sm[var];
   } else {
     CHM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     CHM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
-    ctx->eval_attr_smem[fp] = smem;
-    ctx->eval_per_sm[fp] = per_sm;
+    ctx->eval_attr_smem[var] = smem;
+    ctx->eval_per_sm[var] = per_sm;
   }
   if (per_sm < 1) CHM_FAIL(CHM_E_INVAL, "chm_eval_policies: kernel does not fit an SM");
   if (ctx->cfg.eval_ctas_per_sm) per_sm = std::min(per_sm, int(ctx->cfg.eval_ctas_per_sm));

@@ -170,9 +170,22 @@ extern "C" chm_status chm_trace_build(chm_ctx *ctx, const chm_trace_params *P, c
   D.o_lo = uint32_t(o); o += al(2 * size_t(tr->K));
   D.o_li = uint32_t(o); o += al(2 * size_t(tr->K));
   D.search_bytes = uint32_t(o);
-  D.o_f0 = uint32_t(o); o += al(8 * size_t(N));
+  // F0 in int32 units of 2^g bytes when every value is a multiple of 2^g (g <= 9, the allocator
+  // block) and fits: halves the row stream's shared-memory reads
+  int g = 9;
+  int64_t fmax = 0;
+  bool nonneg = true;
+  for (int32_t i = 0; i < N; i++) {
+    while (g > 0 && (tr->F0[i] & ((int64_t(1) << g) - 1))) g--;
+    fmax = std::max(fmax, tr->F0[i]);
+    nonneg = nonneg && tr->F0[i] >= 0;
+  }
+  D.f0_narrow = nonneg && (fmax >> g) < (int64_t(1) << 31) ? 1 : 0;
+  D.f0_shift = g;
+  D.o_f0 = uint32_t(o); o += al((D.f0_narrow ? 4 : 8) * size_t(N));
   D.o_lay = uint32_t(o); o += al(2 * size_t(N));
   D.full_bytes = uint32_t(o);
+  D.o_f0w = uint32_t(o); o += al(8 * size_t(N));
   const size_t o_base = al(o);
   const size_t total = o_base + al(8 * size_t(tr->W) + 8);
   std::vector<unsigned char> host(total, 0);
@@ -191,7 +204,14 @@ extern "C" chm_status chm_trace_build(chm_ctx *ctx, const chm_trace_params *P, c
     std::memcpy(h + D.o_lo, lo16.data(), 2 * size_t(tr->K));
     std::memcpy(h + D.o_li, li16.data(), 2 * size_t(tr->K));
   }
-  std::memcpy(h + D.o_f0, tr->F0.data(), 8 * size_t(N));
+  if (D.f0_narrow) {
+    std::vector<int32_t> f0u(N);
+    for (int32_t i = 0; i < N; i++) f0u[i] = int32_t(tr->F0[i] >> D.f0_shift);
+    std::memcpy(h + D.o_f0, f0u.data(), 4 * size_t(N));
+  } else {
+    std::memcpy(h + D.o_f0, tr->F0.data(), 8 * size_t(N));
+  }
+  std::memcpy(h + D.o_f0w, tr->F0.data(), 8 * size_t(N));
   std::vector<uint16_t> lay16(N);
   for (int32_t i = 0; i < N; i++) lay16[i] = uint16_t(8 * tr->lay_of_op[i]);  // byte offset into D[L]
   std::memcpy(h + D.o_lay, lay16.data(), 2 * size_t(N));

@@ -88,9 +88,11 @@ def test_trace_build_random(ctx, seed):
 
 
 # ---------------------------------------------------------------------------- eval
-@pytest.mark.parametrize("bw", [40.0, 15.0])
-def test_w1_all_masks(ctx, bw):
-    tr, _ = w1_trace(bw)
+@pytest.mark.parametrize("bw,scale", [(40.0, 1), (15.0, 1), (40.0, (1 << 28) + 1)])
+def test_w1_all_masks(ctx, bw, scale):
+    # scale 2^28 + 1: F0 up to 200 * (2^28 + 1) B, not a multiple of 8 -> the kernel's wide
+    # (int64) F0 path; scale 1 exercises the narrow path with a 4 B unit
+    tr, _ = w1_trace(bw, scale=scale)
     pt = product_trace(ctx, tr)
     m = O.Model(tr)
     check_trace_tables(pt, m)
