@@ -231,3 +231,24 @@ def test_executor_partial_policy_swaps_exactly_the_selected_tensors(name, seed):
     chm.record_iteration(ctx, tr, on_actions=on)
     exp = sorted((int(a[sw["t"][k]]), j, int(sw["t"][k])) for j, k in enumerate(sel))
     assert sorted(got) == exp
+
+
+def test_c4_dynamic_schedule_detection():
+    """C4: s 2048 (it 0-29) -> 8192 (30-59) -> 2048 (60-89) through the profiler hook.  Positional
+    cosine (default) detects both switches; the stage machine then walks WarmUp (3 iterations) ->
+    GenPolicy (6) -> Stable, as Algo. 1 with m = 2, n = 5 prescribes."""
+    import json
+    import subprocess
+    import sys
+    out = subprocess.run([sys.executable, "tools/c4_dynamic.py", "--host-only"], capture_output=True, text=True,
+                         cwd=__import__("os").path.dirname(__import__("os").path.dirname(__file__)), timeout=300)
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    assert d["detections"] == [30, 60]
+    st = d["stages"]
+    for start in (0, 30, 60):
+        off = 0 if start == 0 else 1  # the first call initialises PrevOpSeq (stable with itself)
+        warm = 2 if start == 0 else 3
+        assert st[start:start + warm] == [0] * warm
+        assert st[start + warm:start + warm + 6] == [1] * 6
+        assert st[start + warm + 6] == 2
+        del off
