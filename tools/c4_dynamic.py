@@ -48,6 +48,7 @@ def main():
     if not args.host_only:
         import torch
         dev_t = torch.device("cuda:0")
+    stage_before = chm.WARMUP
     for it, tr in enumerate(schedule):
         t0 = time.perf_counter()
         for r in preps[tr.name].recs:
@@ -56,9 +57,11 @@ def main():
         d = ctx.detect_seq_change(tr.t_iter)
         log.append(dict(it=it, seq=int(tr.meta["shape"]["seq"]), stage=d["stage"], changed=d["changed"],
                         len_diff=round(d["len_diff"], 5), cos=round(d["cos"], 5), record_ms=round(t_rec * 1e3, 2)))
-        # a Detailed iteration was just recorded (stage GenPolicy): re-plan once per phase
+        # this iteration ran in GenPolicy, i.e. was recorded in Detailed mode: re-plan once per phase
         phase = it // 30
-        if d["stage"] == chm.GENPOLICY and not any(rp["phase"] == phase for rp in replans) and not args.host_only:
+        detailed = stage_before == chm.GENPOLICY
+        stage_before = d["stage"]
+        if detailed and not any(rp["phase"] == phase for rp in replans) and not args.host_only:
             rp = dict(phase=phase, iteration=it, seq=int(tr.meta["shape"]["seq"]))
             t0 = time.perf_counter()
             pt = ctx.trace_build(tr.budget, tr.static_bytes, tr.bw, tr.groups_fwd, tr.groups_bwd, t_iter=tr.t_iter)
@@ -96,8 +99,9 @@ def main():
         pt8, _ = policies[8192]
         out["stale_policy_on_8192"] = dict(peak_gib=pt8.peak0 / 2 ** 30, budget_gib=pt8.budget / 2 ** 30,
                                            excess_gib=max(0, pt8.peak0 - pt8.budget) / 2 ** 30,
-                                           note="the 2048 plan swaps nothing; on 8192 the no-swap peak exceeds "
-                                                "the budget: the undersized-swap failure (P:126)")
+                                           note="s=2048 fits without swapping (Algo. 2 plans nothing); kept "
+                                                "on s=8192 that plan leaves the no-swap peak above the budget: "
+                                                "the undersized-swap failure of P:126 that re-planning avoids")
     print(json.dumps(out))
 
 
