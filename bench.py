@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--candidates", type=int, default=100_000)
     ap.add_argument("--search-mode", action="store_true", help="no footprint rows (peak/stall/argmin only)")
-    ap.add_argument("--swap-ctas", type=int, default=32)
+    ap.add_argument("--swap-ctas", type=int, default=8)
     ap.add_argument("--host-frac", type=float, default=0.6, help="max fraction of host RAM pinned per node")
     ap.add_argument("--ce-steps", type=int, default=1, help="steps of the copy-engine baseline")
     ap.add_argument("--e2e-steps", type=int, default=2)

@@ -65,7 +65,8 @@ typedef struct {
                                  (profiler, detection, trace build and executor tables only;
                                  eval / swap calls return CHM_E_STATE)                       */
   uint64_t host_arena_bytes;  /* pinned + mapped host arena for swapped blocks (0: none)      */
-  uint32_t swap_ctas;         /* CTAs of the swap copy kernel (0: default, 16)               */
+  uint32_t swap_ctas;         /* CTAs of the swap copy kernel (0: default 8: the link is full at
+                                 4, fewer CTAs steal less from overlapped compute)           */
   uint32_t eval_ctas_per_sm;  /* resident CTAs per SM for the replay kernel (0: auto)        */
   uint32_t match_window;      /* executor: max recorded ops skipped when aligning a run-time
                                  op to the recorded sequence (0: 32)                         */

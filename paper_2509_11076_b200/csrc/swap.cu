@@ -286,7 +286,7 @@ static chm_status swap_batch(chm_ctx *ctx, const chm_swap_desc *d, uint32_t n, c
                              d[j].nbytes, to_host ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice, swap));
   }
   if (!kd.empty()) {
-    const int ctas = ctx->cfg.swap_ctas ? int(ctx->cfg.swap_ctas) : 32;
+    const int ctas = ctx->cfg.swap_ctas ? int(ctx->cfg.swap_ctas) : 8;
     st = launch_swap_copy(kd.data(), uint32_t(kd.size()), arena, to_host, ctas, int(ctx->cfg.swap_variant), swap);
     if (st != CHM_OK) return st;
   }
