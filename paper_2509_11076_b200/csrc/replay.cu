@@ -151,9 +151,9 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
   // per-layer in / out sums and their cumulative sums, int64 [L] each
   long long *s_INR = reinterpret_cast<long long *>(img + p.stage_bytes);
   long long *s_OUTR = s_INR + L;
-  long long *s_CIR = s_OUTR + L;
-  long long *s_COR = s_CIR + L;
-  unsigned *r_hi = reinterpret_cast<unsigned *>(s_COR + L);  // [2L] R accumulators (in, out)
+  long long *s_DR = s_OUTR + L;   // D_R(l) = CIR(l) - COR(l) + OUTR(l)
+  long long *s_SWR = s_DR + L;    // [L] (entry 0: total bytes of R)
+  unsigned *r_hi = reinterpret_cast<unsigned *>(s_SWR + L);  // [2L] R accumulators (in, out)
   unsigned *r_lo = r_hi + 2 * L;                             // [2L]
   // per-warp scratch: D[L] (int64) and the candidate's signed deltas vs R, split hi/lo 32-bit
   unsigned char *wscr = reinterpret_cast<unsigned char *>(r_lo + 2 * L) + size_t(warp) * p.warp_scratch;
@@ -188,10 +188,11 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
         const long long ya = __shfl_up_sync(0xffffffffu, a, o), yb = __shfl_up_sync(0xffffffffu, b, o);
         if (lane >= o) { a += ya; b += yb; }
       }
-      if (l < L) { s_INR[l] = in_l; s_OUTR[l] = out_l; s_CIR[l] = ci + a; s_COR[l] = co + b; }
+      if (l < L) { s_INR[l] = in_l; s_OUTR[l] = out_l; s_DR[l] = (ci + a) - (co + b) + out_l; }
       ci += __shfl_sync(0xffffffffu, a, 31);
       co += __shfl_sync(0xffffffffu, b, 31);
     }
+    if (lane == 0) s_SWR[0] = co;
   }
   __syncthreads();
 
@@ -199,11 +200,12 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
   best.excess = LLONG_MAX; best.stall = 0.0; best.swapped = LLONG_MAX; best.index = ~0ull; best.peak = 0;
   // dynamic distribution: each warp takes the next candidate from a global counter (fetched
   // one candidate ahead), so warps the scheduler favours do more and none idles at the end
+  constexpr unsigned kGrab = 4;  // candidates per counter fetch
   unsigned long long nxt = 0;
-  if (lane == 0) nxt = atomicAdd(p.work, 1ull);
-  uint64_t c = __shfl_sync(0xffffffffu, nxt, 0);
+  if (lane == 0) nxt = atomicAdd(p.work, (unsigned long long)kGrab);
+  uint64_t c0 = __shfl_sync(0xffffffffu, nxt, 0), c = c0;
   while (c < p.count) {
-    if (lane == 0) nxt = atomicAdd(p.work, 1ull);
+    if (lane == 0 && c == c0) nxt = atomicAdd(p.work, (unsigned long long)kGrab);
     const uint64_t g = p.first + c;
     // decode: only the items whose bit differs from R add a signed delta to their layers
     if (seeded) {  // one hash word per 4 items (reading R-seeded); flips are ~flip_thr rare
@@ -236,7 +238,9 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
     __syncwarp();
     // layer l: in_l / out_l = R sums + deltas; CI / CO cumulative; D_l = CI(l) - CO(l) + out_l;
     // term_l = max(0, (in_l + out_l) / B - Bud_l), pairwise tree (reading R-stall)
-    long long pk = LLONG_MIN, cci = 0, cco = 0;
+    // D_l = D_R(l) + sum_{l' <= l} (din_l' - dout_{l'-1}) with D_R(l) = CIR(l) - COR(l) + OUTR(l):
+    // one warp scan per 32-layer chunk; load_l = in_l + out_l per layer
+    long long pk = LLONG_MIN, carry = 0, prev_dout = 0, swd = 0;
     double cs[8];
 #pragma unroll
     for (int j = 0; j < 8; j++) {
@@ -249,24 +253,24 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
           dout = split_sum(dO_hi[l], dO_lo[l]);
           dI_hi[l] = 0u; dI_lo[l] = 0u; dO_hi[l] = 0u; dO_lo[l] = 0u;  // ready for the next candidate
         }
-        long long a = din, b = dout;
+        const long long up = __shfl_up_sync(0xffffffffu, dout, 1);
+        long long e = din - (lane == 0 ? prev_dout : up);
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-          const long long ya = __shfl_up_sync(0xffffffffu, a, o), yb = __shfl_up_sync(0xffffffffu, b, o);
-          if (lane >= o) { a += ya; b += yb; }
+          const long long y = __shfl_up_sync(0xffffffffu, e, o);
+          if (lane >= o) e += y;
         }
         double t = 0.0;
         if (l < L) {
-          const long long in_l = s_INR[l] + din, out_l = s_OUTR[l] + dout;
-          const long long ci = s_CIR[l] + cci + a, co = s_COR[l] + cco + b;
-          const long long d = ci - co + out_l;
+          const long long d = s_DR[l] + carry + e;
           if (kFull) s_D[l] = d;
           pk = max(pk, mf0[l] + d);
-          const double x = __dsub_rn(__ddiv_rn(double(in_l + out_l), p.tr.bw), bud[l]);
+          const double x = __dsub_rn(__ddiv_rn(double(s_INR[l] + din + s_OUTR[l] + dout), p.tr.bw), bud[l]);
           t = x > 0.0 ? x : 0.0;
         }
-        cci += __shfl_sync(0xffffffffu, a, 31);
-        cco += __shfl_sync(0xffffffffu, b, 31);
+        swd += dout;
+        carry += __shfl_sync(0xffffffffu, e, 31);
+        prev_dout = __shfl_sync(0xffffffffu, dout, 31);
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) t = __dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, o));
         cs[j] = t;
@@ -275,8 +279,11 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
     const double st = __dadd_rn(__dadd_rn(__dadd_rn(cs[0], cs[1]), __dadd_rn(cs[2], cs[3])),
                                 __dadd_rn(__dadd_rn(cs[4], cs[5]), __dadd_rn(cs[6], cs[7])));
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) pk = max(pk, __shfl_xor_sync(0xffffffffu, pk, o));
-    const long long swp = (L > 0 ? s_COR[L - 1] : 0) + cco;  // total bytes released = swapped
+    for (int o = 16; o > 0; o >>= 1) {
+      pk = max(pk, __shfl_xor_sync(0xffffffffu, pk, o));
+      swd += __shfl_xor_sync(0xffffffffu, swd, o);
+    }
+    const long long swp = s_SWR[0] + swd;  // total bytes released = swapped
     if (lane == 0) {
       if (p.peak) p.peak[c] = pk;
       if (p.stall) p.stall[c] = st;
@@ -322,7 +329,7 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
       }
     }
     __syncwarp();  // scratch reuse by the next candidate
-    c = __shfl_sync(0xffffffffu, nxt, 0);
+    if (++c == c0 + kGrab) c = c0 = __shfl_sync(0xffffffffu, nxt, 0);
   }
   // warp keys -> CTA key -> the last CTA to finish reduces all CTA keys into *best
   if (lane == 0) s_best[warp] = best;
