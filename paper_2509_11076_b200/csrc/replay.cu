@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
   best.excess = LLONG_MAX; best.stall = 0.0; best.swapped = LLONG_MAX; best.index = ~0ull; best.peak = 0;
   // dynamic distribution: each warp takes the next candidate from a global counter (fetched
   // one candidate ahead), so warps the scheduler favours do more and none idles at the end
-  constexpr unsigned kGrab = 4;  // candidates per counter fetch
+  constexpr unsigned kGrab = 1;  // candidates per counter fetch (more grows the tail)
   unsigned long long nxt = 0;
   if (lane == 0) nxt = atomicAdd(p.work, (unsigned long long)kGrab);
   uint64_t c0 = __shfl_sync(0xffffffffu, nxt, 0), c = c0;
