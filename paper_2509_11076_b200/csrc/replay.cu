@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
     if (kFull) {
       __syncwarp();  // s_D visible to the warp
       // F_P[i] = F0[i] + D[lay(i)], two ops per 16 B streaming store; 32-bit shared addresses
-      const int np = p.row_pairs, sh = p.tr.f0_shift;
+      const int np = p.row_pairs, unit = 1 << p.tr.f0_shift;
       const unsigned sD = static_cast<unsigned>(__cvta_generic_to_shared(s_D));
       unsigned sF = static_cast<unsigned>(__cvta_generic_to_shared(f0)) + (kNarrow ? 8u : 16u) * lane;
       unsigned sL = static_cast<unsigned>(__cvta_generic_to_shared(lay)) + 4u * lane;
@@ -310,18 +310,14 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
         if (kNarrow) {
           int ux, uy;
           asm("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(ux), "=r"(uy) : "r"(sF));
-          fx = (long long)ux << sh;
-          fy = (long long)uy << sh;
+          fx = (long long)ux * unit;  // IMAD.WIDE, exact: |F0| < 2^31 units
+          fy = (long long)uy * unit;
         } else {
           asm("ld.shared.v2.s64 {%0, %1}, [%2];" : "=l"(fx), "=l"(fy) : "r"(sF));
         }
         asm("ld.shared.u32 %0, [%1];" : "=r"(lz) : "r"(sL));
         asm("ld.shared.s64 %0, [%1];" : "=l"(d0) : "r"(sD + (lz & 0xffffu)));
-        if ((lz >> 16) == (lz & 0xffffu)) {
-          d1 = d0;  // both ops of the pair in one layer: one lookup
-        } else {
-          asm("ld.shared.s64 %0, [%1];" : "=l"(d1) : "r"(sD + (lz >> 16)));
-        }
+        asm("ld.shared.s64 %0, [%1];" : "=l"(d1) : "r"(sD + (lz >> 16)));
         st_cs_v2(out, fx + d0, fy + d1);
         sF += kNarrow ? 256u : 512u;
         sL += 128u;
