@@ -260,7 +260,7 @@ def main():
     lo, hi = rank * C // P, (rank + 1) * C // P
     cnt = hi - lo
     full = not args.search_mode
-    ld = (pt.N + 3) // 4 * 4
+    ld = (pt.N + 1) // 2 * 2
     peak = torch.empty(cnt, dtype=torch.int64, device=dev)
     stall = torch.empty(cnt, dtype=torch.float64, device=dev)
     fp = torch.empty((cnt, ld), dtype=torch.int64, device=dev) if full else None

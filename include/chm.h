@@ -221,8 +221,7 @@ typedef struct {
   int64_t *swapped;        /* device [count] or NULL                                    */
   int64_t *footprint;      /* device [count][ld] or NULL (full mode: F_P per op; the
                               entries [n_ops, ld) of a row are unspecified)            */
-  uint32_t ld;             /* leading dimension of footprint, >= n_ops, even; a multiple
-                              of 4 with a 32 B-aligned footprint enables 32 B stores     */
+  uint32_t ld;             /* leading dimension of footprint, >= n_ops, even            */
   chm_best *best;          /* device, 1 element (required)                              */
 } chm_eval_out;
 

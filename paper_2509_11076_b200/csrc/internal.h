@@ -200,8 +200,8 @@ struct chm_ctx {
   size_t eval_scratch_bytes = 0;
   void *explicit_scratch = nullptr;  // EXPLICIT candidates: items + offsets + keys (device)
   size_t explicit_scratch_bytes = 0;
-  size_t eval_attr_smem[4] = {0, 0, 0, 0};  // cached kernel attribute / occupancy per variant
-  int eval_per_sm[4] = {0, 0, 0, 0};
+  size_t eval_attr_smem[3] = {0, 0, 0};  // cached kernel attribute / occupancy per variant
+  int eval_per_sm[3] = {0, 0, 0};
 };
 
 namespace chm {

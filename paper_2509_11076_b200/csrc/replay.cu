@@ -132,11 +132,7 @@ __device__ __forceinline__ void acc_add(unsigned *hi, unsigned *lo, int l, long 
   atomicAdd(lo + l, neg ? 0u - w : w);
 }
 
-__device__ __forceinline__ void st_cs_v4(long long *dst, long long a, long long b, long long c, long long d) {
-  asm volatile("st.global.cs.v4.s64 [%0], {%1, %2, %3, %4};" ::"l"(dst), "l"(a), "l"(b), "l"(c), "l"(d));
-}
-
-template <bool kFull, bool kNarrow, bool kQuad>
+template <bool kFull, bool kNarrow>
 __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_constant__ EvalParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ __align__(8) uint64_t s_mbar;
@@ -307,28 +303,6 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
       const unsigned sD = static_cast<unsigned>(__cvta_generic_to_shared(s_D));
       unsigned sF = static_cast<unsigned>(__cvta_generic_to_shared(f0)) + (kNarrow ? 8u : 16u) * lane;
       unsigned sL = static_cast<unsigned>(__cvta_generic_to_shared(lay)) + 4u * lane;
-      if (kQuad) {  // 4 ops per lane: 16 B of F0 units, 8 B of layer offsets, one 32 B store
-        const int nq = (np + 1) >> 1;
-        unsigned sF4 = static_cast<unsigned>(__cvta_generic_to_shared(f0)) + 16u * lane;
-        unsigned sL4 = static_cast<unsigned>(__cvta_generic_to_shared(lay)) + 8u * lane;
-        long long *o4 = p.footprint + c * p.ld + 4 * lane;
-        for (int q = lane; q < nq; q += 32) {
-          int u0, u1, u2, u3;
-          unsigned la, lb;
-          long long d0, d1, d2, d3;
-          asm("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(u0), "=r"(u1), "=r"(u2), "=r"(u3) : "r"(sF4));
-          asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(la), "=r"(lb) : "r"(sL4));
-          asm("ld.shared.s64 %0, [%1];" : "=l"(d0) : "r"(sD + (la & 0xffffu)));
-          asm("ld.shared.s64 %0, [%1];" : "=l"(d1) : "r"(sD + (la >> 16)));
-          asm("ld.shared.s64 %0, [%1];" : "=l"(d2) : "r"(sD + (lb & 0xffffu)));
-          asm("ld.shared.s64 %0, [%1];" : "=l"(d3) : "r"(sD + (lb >> 16)));
-          st_cs_v4(o4, (long long)u0 * unit + d0, (long long)u1 * unit + d1, (long long)u2 * unit + d2,
-                   (long long)u3 * unit + d3);
-          sF4 += 512u;
-          sL4 += 256u;
-          o4 += 128;
-        }
-      } else {
       long long *out = p.footprint + c * p.ld + 2 * lane;
       for (int q = lane; q < np; q += 32) {
         long long fx, fy, d0, d1;
@@ -348,7 +322,6 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
         sF += kNarrow ? 256u : 512u;
         sL += 128u;
         out += 64;
-      }
       }
     }
     __syncwarp();  // scratch reuse by the next candidate
@@ -427,11 +400,8 @@ chm_status launch_eval(chm_ctx *ctx, const EvalLaunch &L, cudaStream_t stream) {
   if (smem > 220 * 1024)
     CHM_FAIL(CHM_E_INVAL, "chm_eval_policies: trace image + scratch (%zu B) exceeds shared memory", smem);
   const bool narrow = L.tr.f0_narrow != 0;
-  const bool quad = fp && narrow && (L.ld % 4 == 0) && (reinterpret_cast<uintptr_t>(L.footprint) % 32 == 0);
-  auto kern = !fp ? replay_kernel<false, false, false>
-              : !narrow ? replay_kernel<true, false, false>
-              : quad ? replay_kernel<true, true, true> : replay_kernel<true, true, false>;
-  const int var = !fp ? 0 : !narrow ? 1 : quad ? 3 : 2;
+  auto kern = fp ? (narrow ? replay_kernel<true, true> : replay_kernel<true, false>) : replay_kernel<false, false>;
+  const int var = fp ? (narrow ? 2 : 1) : 0;
   int per_sm = 0;
   if (ctx->eval_attr_smem[var] == smem) {
     per_sm = ctx->eval_per_sm[var];

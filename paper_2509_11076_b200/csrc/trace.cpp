@@ -182,9 +182,8 @@ extern "C" chm_status chm_trace_build(chm_ctx *ctx, const chm_trace_params *P, c
   }
   D.f0_narrow = nonneg && (fmax >> g) < (int64_t(1) << 31) ? 1 : 0;
   D.f0_shift = g;
-  const size_t N4 = (size_t(N) + 3) & ~size_t(3);  // quads of ops (padding: unit 0, layer 0)
-  D.o_f0 = uint32_t(o); o += al((D.f0_narrow ? 4 : 8) * N4);
-  D.o_lay = uint32_t(o); o += al(2 * N4);
+  D.o_f0 = uint32_t(o); o += al((D.f0_narrow ? 4 : 8) * size_t(N));
+  D.o_lay = uint32_t(o); o += al(2 * size_t(N));
   D.full_bytes = uint32_t(o);
   D.o_f0w = uint32_t(o); o += al(8 * size_t(N));
   const size_t o_base = al(o);

@@ -24,7 +24,7 @@ def main():
     ctx.detect_seq_change(tr.t_iter)
     pt = ctx.trace_build(tr.budget, tr.static_bytes, tr.bw, tr.groups_fwd, tr.groups_bwd, t_iter=tr.t_iter)
     n = 100_000
-    ld = (pt.N + 3) // 4 * 4
+    ld = (pt.N + 1) // 2 * 2
     dev = torch.device("cuda:0")
     peak = torch.empty(n, dtype=torch.int64, device=dev)
     stall = torch.empty(n, dtype=torch.float64, device=dev)
