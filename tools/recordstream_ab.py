@@ -39,7 +39,8 @@ def run(tr, sel, variant, op_us, cycles_per_us):
     chm.record_iteration(ctx, tr, tokens=tok)
     ctx.detect_seq_change(tr.t_iter)
     ctx.set_detailed(False)
-    pt = ctx.trace_build(tr.budget, tr.static_bytes, tr.bw, tr.groups_fwd, tr.groups_bwd, t_iter=tr.t_iter)
+    t_iter = tr.n_ops * op_us * 1e-6  # Eq. 1's T_iter = the stand-in compute of the iteration
+    pt = ctx.trace_build(tr.budget, tr.static_bytes, tr.bw, tr.groups_fwd, tr.groups_bwd, t_iter=t_iter)
     words = np.zeros(max(pt.W, 1), np.uint64)
     for k in sel:
         words[k // 64] |= np.uint64(1 << (k % 64))
@@ -105,11 +106,11 @@ def run(tr, sel, variant, op_us, cycles_per_us):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--batch", type=int, default=1)
-    ap.add_argument("--op-us", type=float, default=40.0)
+    ap.add_argument("--op-us", type=float, default=1000.0)
     ap.add_argument("--policy-candidates", type=int, default=2000)
     args = ap.parse_args()
     tr = W.gpt2_xl(batch=args.batch)
-    m = O.Model(tr)
+    m = O.Model(tr, t_iter=tr.n_ops * args.op_us * 1e-6)
     sd = W.SEEDED["C2"]
     best = m.eval(O.SEEDED, 0, args.policy_candidates, seed=sd["seed"], flip_thr=sd["flip_thr"], nthreads=16)["best"]
     J = (m.K + 3) // 4
@@ -133,12 +134,16 @@ def main():
     allocs = {}
     for variant in ("custom", "naive"):
         res[variant], allocs[variant] = run(tr, sel, variant, args.op_us, cycles_per_us)
+        res[variant]["reserved_over_policy_peak"] = None
     swapped = sum(int(tr.nbytes[t]) for t in sel.values())
     extra = np.maximum(allocs["naive"] - allocs["custom"], 0)
     res["naive_extra_residency_ops_per_swapped_byte"] = float(extra.sum() / max(swapped, 1))
     res["naive_peak_extra_bytes"] = int(extra.max())
     res["config"] = dict(trace=tr.name, batch=args.batch, ops=tr.n_ops, swapped_items=len(sel), swapped_bytes=swapped,
-                         op_us=args.op_us)
+                         op_us=args.op_us, t_iter_s=tr.n_ops * args.op_us * 1e-6,
+                         no_swap_peak_bytes=int(m.f0().max() - tr.static_bytes),
+                         policy_peak_bytes=int(m.eval(O.SEEDED, best.index, 1, seed=sd["seed"], flip_thr=sd["flip_thr"])["peak"][0]
+                                               - tr.static_bytes))
     print(json.dumps(res))
 
 
