@@ -147,6 +147,10 @@ typedef struct {
   double bw_bytes_per_s;       /* B of Eq. 3; must be > 0                   */
   uint32_t groups_fwd, groups_bwd; /* logical layers per phase, >= 1        */
   double omega;                /* overlap factor on layer budgets, 1.0 default  */
+  uint32_t f0_source;          /* 0: F0 from the recorded alloc/free events (+ static_bytes);
+                                  1: Fig. 3 reconstruction: the recorded
+                                  live_bytes of every op plus the bytes that were swapped out
+                                  at that op (swap log of the recorded iteration)           */
 } chm_trace_params;
 
 /* Builds the evaluation trace from the last iteration recorded in Detailed mode: tensor
@@ -274,6 +278,46 @@ typedef struct {
   uint64_t bytes_out, bytes_in;
 } chm_exec_stats;
 chm_status chm_exec_stats_get(chm_ctx *ctx, chm_exec_stats *s);
+
+/* ------------------------------------------------ WarmUp OOM handling (NEXT-4, Algo. 3) */
+/* Algo. 3, called by the allocator hook when an allocation fails in the
+ * WarmUp stage (or when a policy undershoots):
+ *   chm_oom_release:   steps (i)-(ii): every policy item whose swap-out was issued but whose
+ *                      release point has not come yet is released now -- `compute` waits for its
+ *                      swap-out batch (event record/wait, no host sync); *items (cap entries, count
+ *                      in *n_items; CHM_E_INVAL if more than cap) receives them; the caller drops
+ *                      their device blocks and retries.  CHM_E_STATE on a host-only ctx.
+ *   chm_passive_swap:  step (iv): swaps out the resident produced tensor (reported as an output of
+ *                      chm_record_op and not freed since; not bound to a policy item) whose size
+ *                      is closest to `need`: the smallest one of at least `need` bytes, else the
+ *                      largest; ties: the older.  `exclude` (n_exclude ids, e.g. the current op's
+ *                      inputs) is skipped.  Copy goes to the arena above the installed policy's
+ *                      slots (first fit); `compute` waits for it; *out names the tensor (`id`) and
+ *                      a unique `handle`; the caller drops the block and retries.  CHM_E_NOMEM if
+ *                      no tensor is eligible or the arena has no room.
+ *   chm_passive_restore: demand swap-in (reading Q20) of `handle` into the caller's new block
+ *                      `dev` before an op reads it; `compute` waits; from now on the tensor is
+ *                      known by id `dev`.  dev == 0: the tensor died while out (its last use has
+ *                      been recorded) -- the host copy is dropped, no copy is made.
+ * The caller tracks its swapped tensors by handle (a freed block's id may be reused by a new
+ * tensor at once).  Passive swaps, their restores and the policy's releases / swap-ins are
+ * logged per recorded iteration: the swap log of Fig. 3's reconstruction
+ * (chm_trace_params.f0_source = 1).  Policy install fails (CHM_E_STATE) while passive swaps are
+ * outstanding.  Use one swap stream for passive swaps: an arena range freed by a restore is
+ * rewritten only by later copies in that stream's order. */
+typedef struct {
+  uint64_t handle;   /* unique per passive swap                                   */
+  uint64_t id;       /* the swapped tensor's id (its device address) when it left  */
+  int64_t nbytes;
+  uint64_t host_off; /* arena offset of the host copy                              */
+  uint64_t batch;    /* swap-out batch (chm_batch_wait / query / elapsed)          */
+} chm_passive;
+chm_status chm_oom_release(chm_ctx *ctx, cudaStream_t compute, uint32_t *items, uint32_t cap,
+                           uint32_t *n_items);
+chm_status chm_passive_swap(chm_ctx *ctx, int64_t need, const uint64_t *exclude, uint32_t n_exclude,
+                            cudaStream_t compute, cudaStream_t swap, chm_passive *out);
+chm_status chm_passive_restore(chm_ctx *ctx, uint64_t handle, uint64_t dev, cudaStream_t compute,
+                               cudaStream_t swap);
 
 /* ---------------------------------------------------------------- swap execution (a9-a11) */
 /* The ctx's pinned, device-mapped host arena (cudaHostAllocMapped|Portable). */

@@ -64,7 +64,7 @@ class Actions(C.Structure):
 class TraceParams(C.Structure):
     _fields_ = [("hbm_budget", C.c_int64), ("static_bytes", C.c_int64), ("t_iter_s", C.c_double),
                 ("bw_bytes_per_s", C.c_double), ("groups_fwd", C.c_uint32), ("groups_bwd", C.c_uint32),
-                ("omega", C.c_double)]
+                ("omega", C.c_double), ("f0_source", C.c_uint32)]
 
 
 class TraceInfo(C.Structure):
@@ -113,12 +113,18 @@ class ExecStats(C.Structure):
                 ("bytes_out", C.c_uint64), ("bytes_in", C.c_uint64)]
 
 
+class Passive(C.Structure):
+    _fields_ = [("handle", C.c_uint64), ("id", C.c_uint64), ("nbytes", C.c_int64), ("host_off", C.c_uint64),
+                ("batch", C.c_uint64)]
+
+
 EXPORTS = [
     "chm_config_default", "chm_create", "chm_destroy", "chm_last_error", "chm_build_info", "chm_tokenize",
     "chm_record_op", "chm_set_detailed", "chm_detect_seq_change", "chm_trace_build", "chm_trace_free",
     "chm_trace_get_info", "chm_trace_tables", "chm_eval_policies", "chm_eval_policies_ex", "chm_best_reduce", "chm_best_reduce_device", "chm_candidate_mask",
     "chm_policy_install", "chm_policy_install_items", "chm_generate_policy", "chm_exec_stats_get", "chm_host_arena", "chm_swap_out", "chm_swap_in",
     "chm_batch_wait", "chm_batch_query", "chm_batch_elapsed", "chm_arena_reserve", "chm_issue_swap_out", "chm_issue_swap_in", "chm_item_wait",
+    "chm_oom_release", "chm_passive_swap", "chm_passive_restore",
 ]
 
 _lib = None
@@ -167,6 +173,9 @@ def load(path: str = LIB_PATH):
         "chm_issue_swap_out": (i32, [vp, vp, vp, u32, P(u64)]),
         "chm_issue_swap_in": (i32, [vp, vp, vp, vp, u32, P(u64)]),
         "chm_item_wait": (i32, [vp, u32, i32, vp]),
+        "chm_oom_release": (i32, [vp, vp, vp, u32, P(u32)]),
+        "chm_passive_swap": (i32, [vp, i64, vp, u32, vp, vp, P(Passive)]),
+        "chm_passive_restore": (i32, [vp, u64, u64, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -314,9 +323,9 @@ class Context:
 
     # ------------------------------------------------------------------ trace build
     def trace_build(self, budget: int, static_bytes: int, bw: float, groups_fwd: int, groups_bwd: int,
-                    t_iter: float = 0.0, omega: float = 1.0) -> Trace:
+                    t_iter: float = 0.0, omega: float = 1.0, f0_source: int = 0) -> Trace:
         p = TraceParams(int(budget), int(static_bytes), float(t_iter), float(bw), int(groups_fwd), int(groups_bwd),
-                        float(omega))
+                        float(omega), int(f0_source))
         h = C.c_void_p()
         _check(load().chm_trace_build(self.h, C.byref(p), C.byref(h)))
         return Trace(self, h)
@@ -401,6 +410,29 @@ class Context:
 
     def item_wait(self, item: int, swap_in: bool, stream=None):
         _check(load().chm_item_wait(self.h, item, 1 if swap_in else 0, _stream(stream)))
+
+    # ------------------------------------------------------------ OOM handling (Algo. 3)
+    def oom_release(self, stream=None, cap: int = 4096) -> list:
+        """(i)-(ii): release every marked block (swap-out issued, release point not reached) behind
+        an event pair; returns the policy items whose device storage the caller drops now"""
+        buf = (C.c_uint32 * cap)()
+        n = C.c_uint32()
+        _check(load().chm_oom_release(self.h, _stream(stream), buf, cap, C.byref(n)))
+        return list(buf[:n.value])
+
+    def passive_swap(self, need: int, exclude=(), compute=None, swap=None) -> dict:
+        """(iv): swap out the resident tensor closest in size to `need`; the caller drops its
+        storage (the compute stream already waits for the copy)"""
+        ex = np.ascontiguousarray(list(exclude), np.uint64)
+        out = Passive()
+        _check(load().chm_passive_swap(self.h, int(need), _ptr(ex) if ex.size else None, int(ex.size),
+                                       _stream(compute), _stream(swap), C.byref(out)))
+        return {k: getattr(out, k) for k, _ in Passive._fields_}
+
+    def passive_restore(self, handle: int, dev: int, compute=None, swap=None):
+        """demand swap-in of passive swap `handle` into `dev` before its next use; dev = 0: the
+        tensor died while out (drop the host copy)"""
+        _check(load().chm_passive_restore(self.h, int(handle), int(dev), _stream(compute), _stream(swap)))
 
     def exec_stats(self) -> dict:
         s = ExecStats()

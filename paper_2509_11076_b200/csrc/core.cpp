@@ -4,6 +4,7 @@
 // -> integer tensor), P:250-252 (Detailed mode: tensors, data_ptr, dtype, iteration time),
 // P:263 (memory in use per op), P:224-248 (Algo. 1 stage adjusting), P:421 (m = 2, n = 5).
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -213,6 +214,9 @@ extern "C" chm_status chm_record_op(chm_ctx *ctx, const chm_op_record *op, chm_a
     R.out_ptr.push_back(int32_t(R.out_idx.size()));
     R.free_ptr.push_back(int32_t(R.free_idx.size()));
   }
+  // resident produced tensors: the candidates of a passive swap (Algo. 3 (iv))
+  for (uint32_t j = 0; j < op->n_out; j++) ctx->resident[op->out[j].id] = {op->out[j].nbytes, ctx->resident_seq++};
+  for (uint32_t j = 0; j < op->n_free; j++) ctx->resident.erase(op->freed[j]);
   if (act) std::memset(act, 0, sizeof *act);
   if (ctx->policy_active) {
     chm_status st = executor_on_op(ctx, op, i);
@@ -309,6 +313,12 @@ extern "C" chm_status chm_detect_seq_change(chm_ctx *ctx, double t_iter_s, chm_s
   }
   ctx->cur.clear();
   ctx->id_to_tensor.clear();
+  for (auto &kv : ctx->passive) {  // still passively out: off the device from op 0 on
+    ctx->cur.swaps.push_back({0, INT32_MAX, kv.second.nbytes, kv.second.id});
+    kv.second.span = int32_t(ctx->cur.swaps.size()) - 1;
+    kv.second.tensor = -1;  // a tensor of the previous iteration's record
+    kv.second.has_live = false;
+  }
   executor_end_iteration(ctx);
   if (stage) *stage = ctx->stage;
   if (changed) *changed = stable ? 0 : 1;

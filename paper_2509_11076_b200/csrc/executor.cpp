@@ -99,6 +99,8 @@ static chm_status install_items(chm_ctx *ctx, const chm_trace *t, const std::vec
   feature_tables(t->tokens, ctx->op_index, ctx->op_onehot);
   // feature key of every selected tensor right after op a_t (replay of the recorded uses)
   std::vector<int32_t> item_of_tensor(size_t(t->T), -1);
+  if (!ctx->passive.empty())
+    CHM_FAIL(CHM_E_STATE, "policy install: %zu passive swaps outstanding (restore them first)", ctx->passive.size());
   ctx->items.assign(sel.size(), PolicyItem());
   uint64_t off = 0;
   for (size_t j = 0; j < sel.size(); j++) {
@@ -113,6 +115,8 @@ static chm_status install_items(chm_ctx *ctx, const chm_trace *t, const std::vec
     off += (uint64_t(it.nbytes) + 511) & ~uint64_t(511);
     item_of_tensor[tid] = int32_t(j);
   }
+  ctx->passive_base = off;  // passive swaps (Algo. 3) use the arena above the policy's slots
+  ctx->passive_free.clear();
   std::vector<Feature> feat(size_t(t->T));
   for (int32_t i = 0; i < t->N; i++) {
     for (int32_t u = t->use_ptr[i]; u < t->use_ptr[i + 1]; u++) {
@@ -200,6 +204,15 @@ static int32_t align_op(chm_ctx *ctx, int32_t token) {
   return -1;
 }
 
+// A released block's address may name a new tensor at once: the Detailed record keeps the
+// swapped tensor's index on the item until its swap-in re-aliases it to the new address.
+void chm::stash_record(chm_ctx *ctx, PolicyItem &it) {
+  auto tt = ctx->id_to_tensor.find(it.cur_id);
+  if (tt == ctx->id_to_tensor.end()) return;
+  it.rec_tensor = tt->second;
+  ctx->id_to_tensor.erase(tt);
+}
+
 chm_status executor_on_op(chm_ctx *ctx, const chm_op_record *op, int32_t i) {
   ctx->act_out.clear(); ctx->act_out_item.clear(); ctx->act_in.clear(); ctx->act_in_item.clear();
   ctx->act_release.clear(); ctx->act_wait.clear();
@@ -232,6 +245,8 @@ chm_status executor_on_op(chm_ctx *ctx, const chm_op_record *op, int32_t i) {
     it.cur_id = ref.id;
     it.cur_bytes = uint64_t(ref.nbytes);
     it.has_out = it.has_in = false;
+    it.span = -1;
+    it.rec_tensor = -1;
     lt->item = j;
     ctx->stats.n_matched++;
     ctx->act_out.push_back({ref.id, it.host_off, uint64_t(ref.nbytes)});
@@ -246,11 +261,16 @@ chm_status executor_on_op(chm_ctx *ctx, const chm_op_record *op, int32_t i) {
       if (it.state != IT_OUT) continue;
       it.state = IT_RELEASED;
       ctx->live.erase(it.cur_id);  // the caller drops the device storage after the wait
+      ctx->resident.erase(it.cur_id);
+      stash_record(ctx, it);
+      ctx->cur.swaps.push_back({i + 1, INT32_MAX, int64_t(it.cur_bytes), it.cur_id});  // off from op i+1
+      it.span = int32_t(ctx->cur.swaps.size()) - 1;
       ctx->act_release.push_back(uint32_t(j));
     }
     for (int32_t j : ctx->swapin_at[ra]) {
       PolicyItem &it = ctx->items[j];
       if (it.state != IT_RELEASED) continue;
+      if (it.span >= 0 && size_t(it.span) < ctx->cur.swaps.size()) ctx->cur.swaps[it.span].to = i + 1;
       ctx->act_in.push_back({0, it.host_off, it.cur_bytes});
       ctx->act_in_item.push_back(uint32_t(j));
     }
@@ -316,6 +336,7 @@ extern "C" chm_status chm_issue_swap_in(chm_ctx *ctx, const uint64_t *dev, cudaS
     it.has_in = true;
     it.state = IT_IN;
     it.cur_id = dev[j];
+    if (it.rec_tensor >= 0) ctx->id_to_tensor[dev[j]] = it.rec_tensor;  // same recorded tensor
     LiveTensor &lt = ctx->live[dev[j]];
     lt.item = int32_t(ctx->act_in_item[j]);
     ctx->stats.bytes_in += it.cur_bytes;

@@ -47,13 +47,16 @@ struct IterRecord {
   std::vector<int32_t> free_ptr{0}, free_idx;
   std::vector<TensorRec> tensors;
   int64_t alloc_bytes = 0;  // total bytes allocated by ops (detect_bytes, reading Q4)
+  // swap log (Fig. 3): bytes off device over ops [from, to), to = INT32_MAX while still out
+  struct SwapSpan { int32_t from, to; int64_t nbytes; uint64_t id; };
+  std::vector<SwapSpan> swaps;
   double t_iter = 0.0;
   bool detailed = false;
   void clear() {
     tokens.clear(); phase.clear(); live_bytes.clear();
     use_ptr.assign(1, 0); use_idx.clear(); use_is_in.clear();
     out_ptr.assign(1, 0); out_idx.clear(); free_ptr.assign(1, 0); free_idx.clear();
-    tensors.clear(); alloc_bytes = 0; t_iter = 0.0; detailed = false;
+    tensors.clear(); alloc_bytes = 0; t_iter = 0.0; detailed = false; swaps.clear();
   }
 };
 
@@ -85,6 +88,8 @@ struct PolicyItem {
   uint8_t state = IT_IDLE;
   uint64_t cur_id = 0, cur_bytes = 0, out_batch = 0, in_batch = 0;
   bool has_out = false, has_in = false;
+  int32_t span = -1;  // swap-log entry of the current release (Fig. 3)
+  int32_t rec_tensor = -1;  // Detailed record's tensor index while released (re-aliased at swap-in)
 };
 
 struct FeatureAt {  // policy key: feature right after the recorded op a_t, and a_t itself
@@ -187,6 +192,24 @@ struct chm_ctx {
   std::vector<chm_swap_desc> act_out, act_in;
   std::vector<uint32_t> act_out_item, act_in_item, act_release, act_wait;
   bool policy_active = false;
+  // resident tensors (for passive swaps): id -> bytes, first-seen sequence
+  struct Resident { int64_t nbytes; uint64_t seq; };
+  std::unordered_map<uint64_t, Resident> resident;
+  uint64_t resident_seq = 0;
+  // passive swaps: handle -> record; arena region [passive_base, arena_bytes), first-fit free list
+  struct Passive {
+    uint64_t id;
+    int64_t nbytes;
+    uint64_t host_off, batch;
+    int32_t span;        // swap-log entry of the current iteration
+    int32_t tensor;      // Detailed record's tensor index (-1: none)
+    bool has_live;       // executor feature state, restored with the tensor
+    chm::LiveTensor live;
+  };
+  std::unordered_map<uint64_t, Passive> passive;
+  std::vector<std::pair<uint64_t, uint64_t>> passive_free;  // (offset, bytes), sorted by offset
+  uint64_t passive_base = 0;
+  uint64_t passive_next = 1;  // next handle
   // swap
   void *arena = nullptr;
   uint64_t arena_bytes = 0;
@@ -208,6 +231,9 @@ namespace chm {
 constexpr int kEventRing = 4096;
 constexpr int kMaxDescPerLaunch = 64;
 constexpr int kMaxSeededWords = 64;  // SEEDED base mask in kernel params: K <= 4096
+
+// executor.cpp: moves a released item's Detailed-record tensor index off its old address
+void stash_record(chm_ctx *ctx, PolicyItem &it);
 
 // launchers (swap.cu / replay.cu)
 chm_status launch_swap_copy(const chm_swap_desc *d, uint32_t n, char *arena, bool to_host,

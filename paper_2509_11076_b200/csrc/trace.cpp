@@ -65,6 +65,27 @@ extern "C" chm_status chm_trace_build(chm_ctx *ctx, const chm_trace_params *P, c
     int64_t acc = P->static_bytes;
     for (int32_t i = 0; i < N; i++) { acc += d[i]; tr->F0[i] = acc; }
   }
+  if (P->f0_source == 1) {
+    // Fig. 3: the no-swap footprint is the measured footprint of every op plus
+    // the bytes the swap log has off the device at that op (span [from, to))
+    if (R.live_bytes.size() != size_t(N)) { delete tr; CHM_FAIL(CHM_E_STATE, "chm_trace_build: no live bytes recorded"); }
+    std::vector<int64_t> d(size_t(N) + 1, 0);
+    for (const auto &sp : R.swaps) {
+      const int32_t a = std::max(sp.from, 0), b = std::min(sp.to, N);
+      if (a >= b) continue;
+      d[a] += sp.nbytes;
+      d[b] -= sp.nbytes;
+    }
+    int64_t acc = 0;
+    for (int32_t i = 0; i < N; i++) {
+      if (R.live_bytes[i] < 0) { delete tr; CHM_FAIL(CHM_E_INVAL, "chm_trace_build: op %d has live_bytes < 0", i); }
+      acc += d[i];
+      tr->F0[i] = R.live_bytes[i] + acc;
+    }
+  } else if (P->f0_source != 0) {
+    delete tr;
+    CHM_FAIL(CHM_E_INVAL, "chm_trace_build: f0_source %u", P->f0_source);
+  }
   tr->argmax0 = 0;
   for (int32_t i = 1; i < N; i++) if (tr->F0[i] > tr->F0[tr->argmax0]) tr->argmax0 = i;
   tr->peak0 = tr->F0[tr->argmax0];
