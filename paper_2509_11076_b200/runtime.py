@@ -1,0 +1,477 @@
+"""PyTorch integration of the executor: Chameleon on an eager training loop.
+
+    rt = Runtime(device=0, hbm_budget=..., groups_fwd=L, groups_bwd=L)
+    for batch in data:
+        with rt.step():
+            loss = model(batch); loss.backward(); opt.step(); opt.zero_grad()
+
+What the paper does in the framework, and where it happens here:
+
+* profiler hook at op dispatch: a TorchDispatchMode reports every aten op to
+  `chm_record_op` -- its token (operator name), phase (FWD / BWD while the autograd
+  engine runs / OPT after it), and the storages it reads and creates (App. A's tensor identity is
+  the storage's device address).  Detailed iterations (the stage machine's GenPolicy,
+  P:224-248) also report frees -- polled through storage weak references between ops -- and the
+  allocator's bytes in use.  An op's record is sent when the next op arrives (or the step
+  ends), so frees that happen between two ops belong to the earlier one and the autograd pack
+  hooks of the op have run before its swap actions are carried out.
+* stage machine + re-plan (Algo. 1): `chm_detect_seq_change` at the end of every
+  step; after the Detailed iteration the runtime builds the trace (M_0 = bytes allocated when the
+  step began, T_iter = the step's time), evaluates SEEDED candidates on the GPU plus the Algo. 2
+  generator's item lists (EXPLICIT) and installs the best key's policy.  A detected
+  sequence change uninstalls the policy (the undersized-swap failure of P:126 is avoided by
+  re-planning, not by running a stale plan).
+* policy execution: the executor's actions -- swap-out after `a_t`, release after
+  `r_t` behind an event pair (custom recordStream), swap-in before `s_t`, wait before `b_t` --
+  are carried out on storages that autograd saved for backward: `saved_tensors_hooks` hand
+  autograd a box instead of the tensor; a release drops the box's device reference (the block
+  returns to PyTorch's stream-ordered allocator when nothing else holds it), a swap-in fills a
+  fresh block and the box rebuilds the saved view over it when backward unpacks it.  A box
+  unpacked before its swap-in was issued is swapped in on demand (reading Q20), never a crash.
+
+No tensor data passes through Python: copies are the swap kernels behind the C ABI.  Host-only
+mode (`device=None`) runs the hook, the stage machine, the generator and the executor's matching
+on CPU tensors (no copies): the CPU tests use it.
+"""
+from __future__ import annotations
+
+import contextlib
+import time
+import weakref
+from typing import Optional
+
+import numpy as np
+import torch
+from torch.utils._python_dispatch import TorchDispatchMode
+from torch.utils._pytree import tree_flatten
+
+from . import chm
+
+_DTYPE_CODE = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2, torch.int64: 3, torch.int32: 4,
+               torch.uint8: 5, torch.bool: 6, torch.int8: 7, torch.float64: 8, torch.int16: 9}
+
+
+def _dtype_code(dt) -> int:
+    return _DTYPE_CODE.get(dt, 15)
+
+
+class _Holder:
+    """one swapped (or swappable) storage: the device block while resident, its swap state"""
+    __slots__ = ("storage", "nbytes", "item", "host_off", "released", "in_issued", "in_waited", "boxes",
+                 "__weakref__")
+
+    def __init__(self, storage, nbytes):
+        self.storage = storage
+        self.nbytes = nbytes
+        self.item = -1
+        self.host_off = -1
+        self.released = False
+        self.in_issued = False
+        self.in_waited = False
+        self.boxes = weakref.WeakSet()
+
+
+class _Box:
+    """what autograd saves instead of an activation: a view description over a holder"""
+    __slots__ = ("holder", "t", "dtype", "size", "stride", "offset", "__weakref__")
+
+    def __init__(self, holder, t):
+        self.holder = holder
+        self.t = t
+        self.dtype = t.dtype
+        self.size = tuple(t.size())
+        self.stride = tuple(t.stride())
+        self.offset = t.storage_offset()
+
+
+class _Mode(TorchDispatchMode):
+    def __init__(self, rt: "Runtime"):
+        super().__init__()
+        self.rt = rt
+
+    def __torch_dispatch__(self, func, types, args=(), kwargs=None):
+        kwargs = kwargs or {}
+        rt = self.rt
+        if rt._internal:  # the runtime's own allocations / views (autograd unpack hook)
+            return func(*args, **kwargs)
+        rt._flush()
+        out = func(*args, **kwargs)
+        rt._stage(func, args, kwargs, out)
+        return out
+
+
+class Runtime:
+    """Chameleon's runtime for one device (one process per GPU).
+
+    hbm_budget: bytes the step may occupy (weights, optimizer state and activations); bw: host
+    link bytes/s of Eq. 3 (default: measured once with the swap kernel); groups_fwd/groups_bwd:
+    logical layers per phase; candidates: SEEDED candidates per re-plan."""
+
+    def __init__(self, device: Optional[int] = 0, *, hbm_budget: int, bw: Optional[float] = None,
+                 groups_fwd: int = 8, groups_bwd: int = 8, omega: float = 1.0, candidates: int = 1 << 16,
+                 seed: int = 1, flip_frac: float = 0.02, generator: bool = True, swap_ctas: int = 0,
+                 min_swap_bytes: int = 0, **algo1):
+        self.host_only = device is None
+        self.dev = torch.device("cpu") if self.host_only else torch.device("cuda", device)
+        self.ctx = chm.Context(device=-1 if self.host_only else device, swap_ctas=swap_ctas,
+                               host_arena_bytes=0 if self.host_only else 1 << 20, **algo1)
+        self.hbm_budget = int(hbm_budget)
+        self.groups = (int(groups_fwd), int(groups_bwd))
+        self.omega = omega
+        self.candidates = int(candidates)
+        self.seed = seed
+        self.flip_thr = int(flip_frac * 2 ** 64)
+        self.use_generator = generator
+        self.min_swap_bytes = min_swap_bytes
+        self._tok = {}
+        self.stage = chm.WARMUP
+        self.need_plan = True
+        self.record_log = False  # per-op log of the next steps (tests)
+        self.log = []
+        self.policy = None  # (trace, description)
+        self.plans = []
+        self.stats = dict(steps=0, ops=0, swap_out=0, release=0, released_bytes=0, swap_in=0, demand_swap_in=0,
+                          unheld=0, plan_ms=0.0)
+        if not self.host_only:
+            self.s_out = torch.cuda.Stream(self.dev)
+            self.s_in = torch.cuda.Stream(self.dev)
+        self.bw = float(bw) if bw else (50e9 if self.host_only else self._measure_bw())
+        self._in_step = False
+        self._internal = False
+
+    # ------------------------------------------------------------------ step
+    @contextlib.contextmanager
+    def step(self):
+        """one training iteration (forward, backward, optimizer) under the runtime"""
+        if self._in_step:
+            raise RuntimeError("Runtime.step is not reentrant")
+        self._begin()
+        mode = _Mode(self)
+        try:
+            with torch.autograd.graph.saved_tensors_hooks(self._pack, self._unpack), mode:
+                yield self
+                self._flush()
+        finally:
+            self._in_step = False
+        self._end()
+
+    def _begin(self):
+        self._in_step = True
+        self.detailed = self.stage == chm.GENPOLICY
+        self.produced = set()  # storage addresses created by ops of this step
+        self.holders = weakref.WeakValueDictionary()  # address -> _Holder (owned by autograd's boxes)
+        self.pending = None    # (token, phase, ins, outs, live_bytes) of the last op
+        self.bwd_seen = False
+        self.last_phase = chm.FWD
+        self.weak = {}         # Detailed: address -> storage weak ref, for free polling
+        self.item_holder = {}  # policy item -> (weak holder, address, host offset, bytes)
+        self.n_ops = 0
+        self.log = []
+        if not self.host_only:
+            torch.cuda.synchronize(self.dev)
+            self.m0 = torch.cuda.memory_allocated(self.dev)
+        else:
+            self.m0 = 0
+        self.t0 = time.perf_counter()
+
+    def _end(self):
+        if not self.host_only:
+            torch.cuda.synchronize(self.dev)
+        t_iter = time.perf_counter() - self.t0
+        stage_before = self.stage
+        d = self.ctx.detect_seq_change(t_iter)
+        self.stage = d["stage"]
+        for ref in self.weak.values():
+            torch.UntypedStorage._free_weak_ref(ref)
+        self.weak = {}
+        self.holders = weakref.WeakValueDictionary()
+        self.item_holder = {}
+        self.stats["steps"] += 1
+        self.stats["ops"] += self.n_ops
+        self.last_step = dict(t_iter=t_iter, changed=d["changed"], stage=self.stage, ops=self.n_ops)
+        if d["changed"]:
+            if self.policy is not None:
+                self._uninstall()
+            self.need_plan = True
+        if stage_before == chm.GENPOLICY and self.detailed and self.need_plan and not d["changed"]:
+            self._plan(t_iter)  # once per stable phase, after its first Detailed iteration
+            self.need_plan = False
+
+    # ------------------------------------------------------------------ hook
+    def _token(self, func) -> int:
+        t = self._tok.get(func)
+        if t is None:
+            t = self._tok[func] = self.ctx.tokenize(func.name())
+        return t
+
+    def _storages(self, objs):
+        """(address, nbytes, dtype code, storage) of the device tensors among objs, deduplicated"""
+        seen, res = set(), []
+        for x in objs:
+            if not isinstance(x, torch.Tensor) or x.device != self.dev or x.is_sparse:
+                continue
+            try:
+                st = x.untyped_storage()
+            except (RuntimeError, NotImplementedError):
+                continue
+            p = st.data_ptr()
+            nb = st.nbytes()
+            if nb <= 0 or p in seen:
+                continue
+            seen.add(p)
+            res.append((p, nb, _dtype_code(x.dtype), st))
+        return res
+
+    def _stage(self, func, args, kwargs, out):
+        """called after op dispatch: stash the op's record (sent when the next op arrives)"""
+        flat_in, _ = tree_flatten((args, kwargs))
+        flat_out, _ = tree_flatten(out)
+        ins = self._storages(flat_in)
+        in_ptrs = {p for p, _, _, _ in ins}
+        outs = [o for o in self._storages(flat_out) if o[0] not in in_ptrs]
+        gt = torch._C._current_graph_task_id()
+        if gt != -1:
+            phase = chm.BWD
+            self.bwd_seen = True
+        else:
+            phase = chm.OPT if self.bwd_seen else chm.FWD
+        # a step is FWD* BWD* OPT*: a forward after a backward (interleaved micro-batches) is
+        # recorded in the later phase, so only tensors of the first forward are swap candidates
+        phase = max(phase, self.last_phase)
+        self.last_phase = phase
+        live = -1
+        if self.detailed:
+            live = torch.cuda.memory_allocated(self.dev) if not self.host_only else 0
+            for p, _, _, st in outs:
+                old = self.weak.pop(p, None)
+                if old is not None:
+                    torch.UntypedStorage._free_weak_ref(old)
+                self.weak[p] = st._weak_ref()
+        for p, _, _, _ in outs:
+            self.produced.add(p)
+        self.pending = (self._token(func), phase, [(p, n, d) for p, n, d, _ in ins],
+                        [(p, n, d) for p, n, d, _ in outs], live)
+
+    def _flush(self):
+        """send the pending op's record (with the frees since it ran) and carry out its actions"""
+        if self.pending is None:
+            return
+        tok, phase, ins, outs, live = self.pending
+        self.pending = None
+        freed = []
+        if self.detailed and self.weak:
+            dead = [p for p, r in self.weak.items() if torch.UntypedStorage._expired(r)]
+            for p in dead:
+                torch.UntypedStorage._free_weak_ref(self.weak.pop(p))
+            freed = dead
+        act = self.ctx.record_op(tok, phase, ins, outs, freed, live_bytes=live)
+        av = chm.actions_view(act) if self.policy is not None else None
+        if self.record_log:
+            self.log.append(dict(op=self.n_ops, token=tok, phase=phase, ins=[x[0] for x in ins],
+                                 outs=[x[0] for x in outs], actions=av))
+        self.n_ops += 1
+        if av is not None:
+            self._actions(av)
+
+    # ------------------------------------------------------------------ autograd boxes
+    def _pack(self, t):
+        if not isinstance(t, torch.Tensor) or t.device != self.dev or t.is_sparse:
+            return t
+        try:
+            st = t.untyped_storage()
+        except (RuntimeError, NotImplementedError):
+            return t
+        p = st.data_ptr()
+        if p not in self.produced or st.nbytes() < self.min_swap_bytes:
+            return t  # weights, inputs and tiny tensors stay as autograd saved them
+        h = self.holders.get(p)
+        if h is None or h.released:
+            h = self.holders[p] = _Holder(st, st.nbytes())
+        b = _Box(h, t)
+        h.boxes.add(b)
+        return b
+
+    def _unpack(self, b):
+        if not isinstance(b, _Box):
+            return b
+        if b.t is not None:
+            return b.t
+        self._internal = True
+        try:
+            return self._restore(b)
+        finally:
+            self._internal = False
+
+    def _restore(self, b):
+        h = b.holder
+        comp = None if self.host_only else torch.cuda.current_stream(self.dev)
+        if h.storage is None:  # needed before its swap-in was issued: demand swap-in (Q20)
+            if self.host_only:
+                raise RuntimeError("host-only runtime cannot restore a released tensor")
+            st = torch.empty(h.nbytes, dtype=torch.uint8, device=self.dev).untyped_storage()
+            bt = self.ctx.swap_in([(st.data_ptr(), h.host_off, h.nbytes)], comp, self.s_in)
+            self.ctx.batch_wait(bt, comp)
+            h.storage = st
+            h.in_issued = h.in_waited = True
+            self.stats["demand_swap_in"] += 1
+        elif h.in_issued and not h.in_waited:
+            self.ctx.item_wait(h.item, True, comp)
+            h.in_waited = True
+        t = torch.empty(0, dtype=b.dtype, device=self.dev).set_(h.storage, b.offset, b.size, b.stride)
+        b.t = t
+        return t
+
+    # ------------------------------------------------------------------ executor actions
+    def _actions(self, av):
+        comp = None if self.host_only else torch.cuda.current_stream(self.dev)
+        if av["swap_out"]:
+            for (d, off, nb), it in zip(av["swap_out"], av["swap_out_item"]):
+                self.item_holder[it] = (None, d, off, nb)
+            if not self.host_only:
+                self.ctx.issue_swap_out(comp, self.s_out)
+            self.stats["swap_out"] += len(av["swap_out"])
+        for it in av["release"]:
+            _, d, off, nb = self.item_holder[it]
+            h = self.holders.get(d)  # autograd has packed the op's saved tensors by now
+            if h is None or h.released:
+                self.stats["unheld"] += 1  # not saved for backward: nothing to release
+                continue
+            h.item, h.host_off = it, off
+            self.item_holder[it] = (weakref.ref(h), d, off, nb)
+            if not self.host_only:
+                self.ctx.item_wait(it, False, comp)  # event pair: reuse after the copy
+                h.storage = None
+                for b in list(h.boxes):
+                    b.t = None
+            h.released = True
+            self.stats["release"] += 1
+            self.stats["released_bytes"] += nb
+        if av["swap_in"]:
+            ptrs, scratch, keep = [], [], []
+            for (d, off, nb), it in zip(av["swap_in"], av["swap_in_item"]):
+                ref = self.item_holder[it][0]
+                h = ref() if ref is not None else None
+                if self.host_only:
+                    ptrs.append(0)
+                    continue
+                st = torch.empty(nb, dtype=torch.uint8, device=self.dev).untyped_storage()
+                ptrs.append(st.data_ptr())
+                if h is not None and h.released and h.storage is None:
+                    h.storage = st
+                    h.in_issued = True
+                else:  # nothing to restore into: land in a scratch block, freed after the copy
+                    scratch.append(it)
+                    keep.append(st)
+            if not self.host_only:
+                self.ctx.issue_swap_in(ptrs, comp, self.s_in)
+                for it in scratch:
+                    self.ctx.item_wait(it, True, comp)
+                del keep  # freed in compute-stream order, after the waits
+            self.stats["swap_in"] += len(av["swap_in"])
+        if not self.host_only:
+            for it in av["wait"]:  # before b_t (the unpack also waits): no block is reused early
+                self.ctx.item_wait(it, True, comp)
+                ref = self.item_holder.get(it, (None,))[0]
+                h = ref() if ref is not None else None
+                if h is not None:
+                    h.in_waited = True
+
+    # ------------------------------------------------------------------ planning
+    def _uninstall(self):
+        pt = self.policy[0]
+        self.ctx.policy_install(pt, np.zeros(max(pt.W, 1), np.uint64)[:pt.W])
+        self.policy = None
+
+    def _plan(self, t_iter):
+        t0 = time.perf_counter()
+        gf, gb = self.groups
+        pt = self.ctx.trace_build(self.hbm_budget, self.m0, self.bw, gf, gb, t_iter=t_iter, omega=self.omega)
+        plan = dict(n_ops=pt.N, K=pt.K, peak0=pt.peak0, budget=pt.budget, t_iter=t_iter)
+        if pt.K == 0 or pt.peak0 <= pt.budget:
+            plan["kind"] = "none"
+            self.policy = None
+            self.ctx.policy_install(pt, np.zeros(max(pt.W, 1), np.uint64)[:pt.W])
+        else:
+            keys = []
+            if not self.host_only and pt.K <= 4096:  # SEEDED base mask travels in kernel params
+                best = torch.empty(5, dtype=torch.int64, device=self.dev)
+                n = min(self.candidates, 1 << pt.K) if pt.K < 63 else self.candidates
+                kind = chm.EXHAUSTIVE if pt.K < 63 and (1 << pt.K) <= n else chm.SEEDED
+                self.ctx.eval_policies(pt, kind, 0, n, best=best, seed=self.seed, flip_thr=self.flip_thr)
+                k = best.cpu().numpy().view(chm.BEST_DTYPE)[0]
+                keys.append(("seeded" if kind == chm.SEEDED else "exhaustive", k, kind))
+            gen = []
+            if self.use_generator or self.host_only:
+                gen = [pt.generate_policy(cc, rr)[0] for cc in (0.0, 1.0, 2.0) for rr in (0.5, 1.0, 2.0)]
+                gen = [g for g in gen if len(g)]
+            if gen and not self.host_only:
+                off = np.zeros(len(gen) + 1, np.uint64)
+                off[1:] = np.cumsum([len(x) for x in gen])
+                gbest = torch.empty(5, dtype=torch.int64, device=self.dev)
+                self.ctx.eval_policies(pt, chm.EXPLICIT, 0, len(gen), best=gbest, item_offsets=off,
+                                       items=np.concatenate(gen))
+                keys.append(("generator", gbest.cpu().numpy().view(chm.BEST_DTYPE)[0], chm.EXPLICIT))
+            if keys:
+                name, k, kind = min(keys, key=lambda x: (int(x[1]["excess"]), float(x[1]["stall"]),
+                                                          int(x[1]["swapped_bytes"])))
+                plan.update(kind=name, excess=int(k["excess"]), stall=float(k["stall"]),
+                            swapped=int(k["swapped_bytes"]), peak=int(k["peak"]))
+                if kind == chm.EXPLICIT:
+                    items = gen[int(k["index"])]
+                    self._reserve_items(items, pt)
+                    self.ctx.policy_install_items(pt, items)
+                    plan["items"] = len(items)
+                    plan["tensors"] = [int(x) for x in items["t"]]
+                else:
+                    words = pt.candidate_mask(kind, int(k["index"]), seed=self.seed, flip_thr=self.flip_thr)
+                    self._reserve_words(words, pt)
+                    self.ctx.policy_install(pt, words)
+                    ks = [k for k in range(pt.K) if (int(words[k // 64]) >> (k % 64)) & 1]
+                    plan["items"] = len(ks)
+                    plan["tensors"] = [int(x) for x in pt.tables()["tensor"][ks]]
+            else:  # host-only: the generator's first plan, no device to score it
+                items = gen[0] if gen else np.zeros(0, chm.ITEM_DTYPE)
+                self.ctx.policy_install_items(pt, items)
+                plan.update(kind="generator-host", items=len(items), tensors=[int(x) for x in items["t"]])
+            self.policy = (pt, plan)
+        plan["plan_ms"] = (time.perf_counter() - t0) * 1e3
+        self.stats["plan_ms"] += plan["plan_ms"]
+        self.plans.append(plan)
+
+    def _reserve_words(self, words, pt):
+        if self.host_only:
+            return
+        tb = pt.tables()
+        need = 0
+        for k in range(pt.K):
+            if (int(words[k // 64]) >> (k % 64)) & 1:
+                need += (int(tb["nbytes"][k]) + 511) // 512 * 512
+        self.ctx.arena_reserve(max(need, 1 << 20))
+
+    def _reserve_items(self, items, pt):
+        if self.host_only:
+            return
+        tb = pt.tables()
+        rank_bytes = {int(t): int(n) for t, n in zip(tb["tensor"], tb["nbytes"])}
+        need = sum((rank_bytes.get(int(it["t"]), 0) + 511) // 512 * 512 for it in items)
+        self.ctx.arena_reserve(max(need, 1 << 20))
+
+    def _measure_bw(self) -> float:
+        """B of Eq. 3: one 256 MiB swap-out + swap-in through the swap kernel"""
+        nb = 256 << 20
+        self.ctx.arena_reserve(nb)
+        buf = torch.empty(nb, dtype=torch.uint8, device=self.dev)
+        comp = torch.cuda.current_stream(self.dev)
+        for _ in range(2):
+            t0 = time.perf_counter()
+            b = self.ctx.swap_out([(buf.data_ptr(), 0, nb)], comp, self.s_out)
+            self.ctx.batch_wait(b, comp)
+            b = self.ctx.swap_in([(buf.data_ptr(), 0, nb)], comp, self.s_in)
+            self.ctx.batch_wait(b, comp)
+            torch.cuda.synchronize(self.dev)
+            dt = time.perf_counter() - t0
+        del buf
+        return 2 * nb / dt
+
+    def close(self):
+        self.ctx.close()

@@ -1,0 +1,136 @@
+"""NEXT-2 on CPU: the PyTorch runtime (paper_2509_11076_b200/runtime.py) on a real eager training
+loop (workloads/tiny_gpt.py), host-only ctx (no copies).  Checks the stage machine over real
+steps, one plan per stable phase, App. A matching of every planned tensor in every
+later step, and matching under sequence drift -- an op inserted mid-forward shifts
+every later op index -- against a Capuchin-style fixed (op index, argument) matcher, which picks
+the wrong tensors."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from paper_2509_11076_b200 import chm  # noqa: E402
+from paper_2509_11076_b200.runtime import Runtime  # noqa: E402
+from workloads import tiny_gpt as G  # noqa: E402
+
+
+def _setup(n_batches=12, **algo1):
+    model = G.make(0)
+    opt = torch.optim.SGD(model.parameters(), lr=0.01)
+    data = G.batches(n_batches, 2, 16, 64)
+    rt = Runtime(None, hbm_budget=1, groups_fwd=4, groups_bwd=4, **algo1)
+    return model, opt, data, rt
+
+
+def _step(rt, model, opt, x, y, forwards=1):
+    with rt.step():
+        loss = sum(model(x, y) for _ in range(forwards))
+        loss.backward()
+        opt.step()
+        opt.zero_grad()
+
+
+def test_stages_plan_and_matching_every_step():
+    model, opt, data, rt = _setup()
+    stages, matched = [], []
+    for x, y in data:
+        _step(rt, model, opt, x, y)
+        stages.append(rt.stage)
+        matched.append(rt.ctx.exec_stats()["n_matched"])
+    # WarmUp until m = 2 stable comparisons, then GenPolicy (Detailed), then Stable after n = 5
+    assert stages[:2] == [chm.WARMUP, chm.WARMUP] and chm.GENPOLICY in stages and stages[-1] == chm.STABLE
+    assert len(rt.plans) == 1 and rt.plans[0]["items"] > 0
+    n_items = rt.plans[0]["items"]
+    first = stages.index(chm.GENPOLICY) + 1  # the Detailed step; its end installs the policy
+    per_step = np.diff([0] + matched)
+    assert all(v == 0 for v in per_step[:first + 1])
+    assert all(v == n_items for v in per_step[first + 1:]), per_step
+    st = rt.ctx.exec_stats()
+    assert st["n_stale"] == 0 and st["n_collisions"] == 0
+    assert rt.stats["unheld"] == 0  # every released tensor was one autograd saved
+    assert rt.stats["release"] == rt.stats["swap_out"] == rt.stats["swap_in"] == n_items * (len(data) - first - 1)
+
+
+def _identity(log):
+    """production rank -> (op, out slot); a_t and the argument position there (fixed-index key)"""
+    where, cur = [], {}
+    a, key = {}, {}
+    for e in log:
+        for j, p in enumerate(e["outs"]):
+            cur[p] = len(where)
+            where.append((e["op"], j))
+    cur = {}
+    for e in log:
+        for j, p in enumerate(e["ins"]):
+            r = cur.get(p)
+            if r is not None and e["phase"] == chm.FWD:
+                a[r] = e["op"]
+                key[r] = ("in", j)
+        for j, p in enumerate(e["outs"]):
+            r = sum(len(x["outs"]) for x in log[:e["op"]]) + j
+            cur[p] = r
+            if e["phase"] == chm.FWD:
+                a[r] = e["op"]
+                key[r] = ("out", j)
+    return where, a, key
+
+
+def test_matching_under_drift_vs_fixed_index_matcher():
+    # histogram cosine (cos_mode 1): an inserted op is a minor change, not a new sequence
+    # (positional cosine compares every later op with its shifted neighbour)
+    model, opt, data, rt = _setup(14, cos_mode=1)
+    rt.record_log = True
+    logs = []
+    for i, (x, y) in enumerate(data[:10]):
+        _step(rt, model, opt, x, y)
+        logs.append(rt.log)
+    assert rt.policy is not None
+    plan = rt.plans[0]
+    # the Detailed step is the one whose end planned: the last one before actions appear
+    det = max(i for i, lg in enumerate(logs) if all(e["actions"] is None for e in lg))
+    base_log = logs[det]
+    where, a_t, key = _identity(base_log)
+    ranks = plan["tensors"]
+    # one step with an op inserted before block 2 (a logging read of a weight)
+    model.drift_layer = 2
+    x, y = data[10]
+    m0 = rt.ctx.exec_stats()["n_matched"]
+    _step(rt, model, opt, x, y)
+    model.drift_layer = -1
+    drift = rt.log
+    assert rt.last_step["changed"] is False  # minor drift: Algo. 1 keeps the policy
+    tb = [e["token"] for e in base_log]
+    td = [e["token"] for e in drift]
+    ins_at = next(i for i in range(len(tb)) if tb[i] != td[i])
+    d = len(td) - len(tb)
+    assert d >= 1
+
+    def shift(i):
+        return i if i < ins_at else i + d
+    truth = sorted(drift[shift(where[r][0])]["outs"][where[r][1]] for r in ranks)
+    ours = sorted(p for e in drift if e["actions"] for (p, _, _) in e["actions"]["swap_out"])
+    assert rt.ctx.exec_stats()["n_matched"] - m0 == len(ranks)
+    assert ours == truth  # every planned tensor found, none confused with a neighbour
+    # Capuchin-style key (op index a_t, argument slot) recorded on the base step
+    fixed = []
+    for r in ranks:
+        e = drift[a_t[r]]
+        side, j = key[r]
+        lst = e["ins"] if side == "in" else e["outs"]
+        fixed.append(lst[j] if j < len(lst) else None)
+    wrong = sum(1 for f, t in zip(sorted(fixed, key=lambda v: -1 if v is None else v), truth) if f != t)
+    assert wrong > 0 and sorted(x for x in fixed if x is not None) != truth
+
+
+def test_sequence_change_uninstalls_and_replans():
+    model, opt, data, rt = _setup(22)
+    for x, y in data[:8]:
+        _step(rt, model, opt, x, y)
+    assert rt.policy is not None and len(rt.plans) == 1
+    x, y = data[8]
+    _step(rt, model, opt, x, y, forwards=2)  # e.g. two micro-batches: the op sequence doubles
+    assert rt.last_step["changed"] and rt.policy is None and rt.stage == chm.WARMUP
+    for x, y in data[9:]:
+        _step(rt, model, opt, x, y, forwards=2)
+    assert len(rt.plans) == 2 and rt.policy is not None
+    assert rt.plans[1]["n_ops"] > 1.9 * rt.plans[0]["n_ops"]
