@@ -105,16 +105,25 @@ class Runtime:
 
     hbm_budget: bytes the step may occupy (weights, optimizer state and activations); bw: host
     link bytes/s of Eq. 3 (default: measured once with the swap kernel); groups_fwd/groups_bwd:
-    logical layers per phase; candidates: SEEDED candidates per re-plan."""
+    logical layers per phase (P:283-288); candidates: SEEDED candidates per re-plan;
+    search_rounds: bound on the local search from the best SEEDED mask (0: off);
+    host_arena_bytes: pinned arena reserved up front (else grown to each policy at install)."""
 
     def __init__(self, device: Optional[int] = 0, *, hbm_budget: int, bw: Optional[float] = None,
                  groups_fwd: int = 8, groups_bwd: int = 8, omega: float = 1.0, candidates: int = 1 << 16,
                  seed: int = 1, flip_frac: float = 0.02, generator: bool = True, swap_ctas: int = 0,
-                 min_swap_bytes: int = 0, **algo1):
+                 min_swap_bytes: int = 0, search_rounds: int = 4096, host_arena_bytes: int = 0,
+                 swap_flags: int = chm.SWAP_AUTO, **algo1):
         self.host_only = device is None
         self.dev = torch.device("cpu") if self.host_only else torch.device("cuda", device)
         self.ctx = chm.Context(device=-1 if self.host_only else device, swap_ctas=swap_ctas,
-                               host_arena_bytes=0 if self.host_only else 1 << 20, **algo1)
+                               host_arena_bytes=0 if self.host_only else max(int(host_arena_bytes), 1 << 20),
+                               **algo1)
+        self.search_rounds = int(search_rounds)
+        # AUTO (default): tensors >= 4 MiB on the copy engines, which take no SMs from the step's
+        # compute (tools/stall_fidelity.py measured 10% shorter Llama-2 7B steps than with the
+        # kernel at 8 CTAs), smaller ones batched through the swap kernel
+        self.swap_flags = int(swap_flags)
         self.hbm_budget = int(hbm_budget)
         self.groups = (int(groups_fwd), int(groups_bwd))
         self.omega = omega
@@ -126,6 +135,8 @@ class Runtime:
         self._tok = {}
         self.stage = chm.WARMUP
         self.need_plan = True
+        self.force_plan = False
+        self.prev_t_iter = None
         self.record_log = False  # per-op log of the next steps (tests)
         self.log = []
         self.policy = None  # (trace, description)
@@ -155,9 +166,20 @@ class Runtime:
             self._in_step = False
         self._end()
 
+    def request_replan(self, hbm_budget: Optional[int] = None):
+        """record the next step in Detailed mode and re-plan at its end (e.g. a new budget),
+        whatever the stage; the installed policy keeps running meanwhile"""
+        if hbm_budget is not None:
+            self.hbm_budget = int(hbm_budget)
+        self.force_plan = True
+
     def _begin(self):
         self._in_step = True
-        self.detailed = self.stage == chm.GENPOLICY
+        # the ctx records every GenPolicy step in Detailed mode (P:250); the runtime pays for
+        # free polling and allocator reads only on the step it will plan from
+        self.detailed = (self.stage == chm.GENPOLICY and self.need_plan) or self.force_plan
+        if self.force_plan:
+            self.ctx.set_detailed(True)
         self.produced = set()  # storage addresses created by ops of this step
         self.holders = weakref.WeakValueDictionary()  # address -> _Holder (owned by autograd's boxes)
         self.pending = None    # (token, phase, ins, outs, live_bytes) of the last op
@@ -193,9 +215,16 @@ class Runtime:
             if self.policy is not None:
                 self._uninstall()
             self.need_plan = True
-        if stage_before == chm.GENPOLICY and self.detailed and self.need_plan and not d["changed"]:
-            self._plan(t_iter)  # once per stable phase, after its first Detailed iteration
+        if self.force_plan:
+            self.ctx.set_detailed(False)
+        if self.detailed and not d["changed"] and (self.force_plan or (stage_before == chm.GENPOLICY and self.need_plan)):
+            # T_iter of Eq. 1: the last Lightweight step without a policy (the Detailed one pays
+            # for free polling, a policy step for its stalls)
+            self._plan(self.prev_t_iter or t_iter)  # once per stable phase
             self.need_plan = False
+            self.force_plan = False
+        if not self.detailed and self.policy is None:
+            self.prev_t_iter = t_iter
 
     # ------------------------------------------------------------------ hook
     def _token(self, func) -> int:
@@ -309,7 +338,7 @@ class Runtime:
             if self.host_only:
                 raise RuntimeError("host-only runtime cannot restore a released tensor")
             st = torch.empty(h.nbytes, dtype=torch.uint8, device=self.dev).untyped_storage()
-            bt = self.ctx.swap_in([(st.data_ptr(), h.host_off, h.nbytes)], comp, self.s_in)
+            bt = self.ctx.swap_in([(st.data_ptr(), h.host_off, h.nbytes)], comp, self.s_in, self.swap_flags)
             self.ctx.batch_wait(bt, comp)
             h.storage = st
             h.in_issued = h.in_waited = True
@@ -328,7 +357,7 @@ class Runtime:
             for (d, off, nb), it in zip(av["swap_out"], av["swap_out_item"]):
                 self.item_holder[it] = (None, d, off, nb)
             if not self.host_only:
-                self.ctx.issue_swap_out(comp, self.s_out)
+                self.ctx.issue_swap_out(comp, self.s_out, self.swap_flags)
             self.stats["swap_out"] += len(av["swap_out"])
         for it in av["release"]:
             _, d, off, nb = self.item_holder[it]
@@ -363,7 +392,7 @@ class Runtime:
                     scratch.append(it)
                     keep.append(st)
             if not self.host_only:
-                self.ctx.issue_swap_in(ptrs, comp, self.s_in)
+                self.ctx.issue_swap_in(ptrs, comp, self.s_in, self.swap_flags)
                 for it in scratch:
                     self.ctx.item_wait(it, True, comp)
                 del keep  # freed in compute-stream order, after the waits
@@ -377,66 +406,110 @@ class Runtime:
                     h.in_waited = True
 
     # ------------------------------------------------------------------ planning
+    def uninstall(self):
+        """stop executing the installed policy (from the next step on)"""
+        if self.policy is not None:
+            self._uninstall()
+
     def _uninstall(self):
         pt = self.policy[0]
         self.ctx.policy_install(pt, np.zeros(max(pt.W, 1), np.uint64)[:pt.W])
         self.policy = None
 
+    @staticmethod
+    def _key(k):
+        return (int(k["excess"]), float(k["stall"]), int(k["swapped_bytes"]))
+
     def _plan(self, t_iter):
         t0 = time.perf_counter()
         gf, gb = self.groups
         pt = self.ctx.trace_build(self.hbm_budget, self.m0, self.bw, gf, gb, t_iter=t_iter, omega=self.omega)
-        plan = dict(n_ops=pt.N, K=pt.K, peak0=pt.peak0, budget=pt.budget, t_iter=t_iter)
+        plan = dict(n_ops=pt.N, K=pt.K, peak0=pt.peak0, budget=pt.budget, t_iter=t_iter,
+                    trace_ms=(time.perf_counter() - t0) * 1e3)
         if pt.K == 0 or pt.peak0 <= pt.budget:
             plan["kind"] = "none"
             self.policy = None
             self.ctx.policy_install(pt, np.zeros(max(pt.W, 1), np.uint64)[:pt.W])
+        elif self.host_only:  # the generator's first plan: no device to score it
+            gen = [g for g in (pt.generate_policy(cc, rr)[0] for cc in (0.0, 1.0, 2.0) for rr in (0.5, 1.0, 2.0))
+                   if len(g)]
+            items = gen[0] if gen else np.zeros(0, chm.ITEM_DTYPE)
+            self.ctx.policy_install_items(pt, items)
+            plan.update(kind="generator-host", items=len(items), tensors=[int(x) for x in items["t"]])
+            self.policy = (pt, plan)
         else:
             keys = []
-            if not self.host_only and pt.K <= 4096:  # SEEDED base mask travels in kernel params
+            t1 = time.perf_counter()
+            if pt.K <= 4096:  # SEEDED base mask travels in kernel params
                 best = torch.empty(5, dtype=torch.int64, device=self.dev)
                 n = min(self.candidates, 1 << pt.K) if pt.K < 63 else self.candidates
                 kind = chm.EXHAUSTIVE if pt.K < 63 and (1 << pt.K) <= n else chm.SEEDED
                 self.ctx.eval_policies(pt, kind, 0, n, best=best, seed=self.seed, flip_thr=self.flip_thr)
                 k = best.cpu().numpy().view(chm.BEST_DTYPE)[0]
-                keys.append(("seeded" if kind == chm.SEEDED else "exhaustive", k, kind))
+                words = pt.candidate_mask(kind, int(k["index"]), seed=self.seed, flip_thr=self.flip_thr)
+                keys.append(("seeded" if kind == chm.SEEDED else "exhaustive", k, words))
+            plan["eval_ms"] = (time.perf_counter() - t1) * 1e3
+            t1 = time.perf_counter()
             gen = []
-            if self.use_generator or self.host_only:
-                gen = [pt.generate_policy(cc, rr)[0] for cc in (0.0, 1.0, 2.0) for rr in (0.5, 1.0, 2.0)]
-                gen = [g for g in gen if len(g)]
-            if gen and not self.host_only:
+            if self.use_generator:
+                gen = [g for g in (pt.generate_policy(cc, rr)[0] for cc in (0.0, 1.0, 2.0) for rr in (0.5, 1.0, 2.0))
+                       if len(g)]
+            if gen:
                 off = np.zeros(len(gen) + 1, np.uint64)
                 off[1:] = np.cumsum([len(x) for x in gen])
                 gbest = torch.empty(5, dtype=torch.int64, device=self.dev)
                 self.ctx.eval_policies(pt, chm.EXPLICIT, 0, len(gen), best=gbest, item_offsets=off,
                                        items=np.concatenate(gen))
-                keys.append(("generator", gbest.cpu().numpy().view(chm.BEST_DTYPE)[0], chm.EXPLICIT))
-            if keys:
-                name, k, kind = min(keys, key=lambda x: (int(x[1]["excess"]), float(x[1]["stall"]),
-                                                          int(x[1]["swapped_bytes"])))
-                plan.update(kind=name, excess=int(k["excess"]), stall=float(k["stall"]),
-                            swapped=int(k["swapped_bytes"]), peak=int(k["peak"]))
-                if kind == chm.EXPLICIT:
-                    items = gen[int(k["index"])]
-                    self._reserve_items(items, pt)
-                    self.ctx.policy_install_items(pt, items)
-                    plan["items"] = len(items)
-                    plan["tensors"] = [int(x) for x in items["t"]]
-                else:
-                    words = pt.candidate_mask(kind, int(k["index"]), seed=self.seed, flip_thr=self.flip_thr)
-                    self._reserve_words(words, pt)
-                    self.ctx.policy_install(pt, words)
-                    ks = [k for k in range(pt.K) if (int(words[k // 64]) >> (k % 64)) & 1]
-                    plan["items"] = len(ks)
-                    plan["tensors"] = [int(x) for x in pt.tables()["tensor"][ks]]
-            else:  # host-only: the generator's first plan, no device to score it
-                items = gen[0] if gen else np.zeros(0, chm.ITEM_DTYPE)
-                self.ctx.policy_install_items(pt, items)
-                plan.update(kind="generator-host", items=len(items), tensors=[int(x) for x in items["t"]])
+                gk = gbest.cpu().numpy().view(chm.BEST_DTYPE)[0]
+                keys.append(("generator", gk, gen[int(gk["index"])]))
+            plan["generator_ms"] = (time.perf_counter() - t1) * 1e3
+            t1 = time.perf_counter()
+            if keys and keys[0][0] == "seeded" and self.search_rounds:
+                k, words, rounds = self._local_search(pt, keys[0][1], keys[0][2])
+                keys[0] = ("seeded+search", k, words)
+                plan["search_rounds"] = rounds
+            plan["search_ms"] = (time.perf_counter() - t1) * 1e3
+            name, k, sel = min(keys, key=lambda x: self._key(x[1]))
+            plan.update(kind=name, excess=int(k["excess"]), stall=float(k["stall"]),
+                        swapped=int(k["swapped_bytes"]), peak=int(k["peak"]))
+            t1 = time.perf_counter()
+            if name == "generator":
+                self._reserve_items(sel, pt)
+                self.ctx.policy_install_items(pt, sel)
+                plan.update(items=len(sel), tensors=[int(x) for x in sel["t"]])
+            else:
+                self._reserve_words(sel, pt)
+                self.ctx.policy_install(pt, sel)
+                ks = [q for q in range(pt.K) if (int(sel[q // 64]) >> (q % 64)) & 1]
+                plan.update(items=len(ks), tensors=[int(x) for x in pt.tables()["tensor"][ks]])
+            plan["install_ms"] = (time.perf_counter() - t1) * 1e3  # includes pinning arena growth
             self.policy = (pt, plan)
         plan["plan_ms"] = (time.perf_counter() - t0) * 1e3
         self.stats["plan_ms"] += plan["plan_ms"]
         self.plans.append(plan)
+
+    def _local_search(self, pt, key, words):
+        """steepest descent over single-bit flips of the mask: each round
+        replays all K neighbours at once (MASKS) and takes the best if it lowers the key
+        (excess, stall, swapped bytes) -- the evaluator's throughput turned into plan quality"""
+        K, W = pt.K, pt.W
+        idx = np.arange(K)
+        flip = np.zeros((K, W), np.uint64)
+        flip[idx, idx // 64] = np.left_shift(np.uint64(1), (idx % 64).astype(np.uint64))
+        masks_dev = torch.empty((K, W), dtype=torch.int64, device=self.dev)
+        best = torch.empty(5, dtype=torch.int64, device=self.dev)
+        cur = np.array(words, np.uint64)
+        rounds = 0
+        while rounds < self.search_rounds:
+            masks_dev.copy_(torch.from_numpy((cur[None, :] ^ flip).view(np.int64)))
+            self.ctx.eval_policies(pt, chm.MASKS, 0, K, best=best, masks=masks_dev)
+            nk = best.cpu().numpy().view(chm.BEST_DTYPE)[0]
+            if not self._key(nk) < self._key(key):
+                break
+            cur = cur ^ flip[int(nk["index"])]
+            key = nk
+            rounds += 1
+        return key, cur, rounds
 
     def _reserve_words(self, words, pt):
         if self.host_only:
@@ -457,16 +530,16 @@ class Runtime:
         self.ctx.arena_reserve(max(need, 1 << 20))
 
     def _measure_bw(self) -> float:
-        """B of Eq. 3: one 256 MiB swap-out + swap-in through the swap kernel"""
+        """B of Eq. 3: one 256 MiB swap-out + swap-in through the policy's copy path"""
         nb = 256 << 20
         self.ctx.arena_reserve(nb)
         buf = torch.empty(nb, dtype=torch.uint8, device=self.dev)
         comp = torch.cuda.current_stream(self.dev)
         for _ in range(2):
             t0 = time.perf_counter()
-            b = self.ctx.swap_out([(buf.data_ptr(), 0, nb)], comp, self.s_out)
+            b = self.ctx.swap_out([(buf.data_ptr(), 0, nb)], comp, self.s_out, self.swap_flags)
             self.ctx.batch_wait(b, comp)
-            b = self.ctx.swap_in([(buf.data_ptr(), 0, nb)], comp, self.s_in)
+            b = self.ctx.swap_in([(buf.data_ptr(), 0, nb)], comp, self.s_in, self.swap_flags)
             self.ctx.batch_wait(b, comp)
             torch.cuda.synchronize(self.dev)
             dt = time.perf_counter() - t0
