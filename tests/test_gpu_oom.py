@@ -22,134 +22,8 @@ from workloads import traces as W
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-from paper_2509_11076_b200 import chm  # noqa: E402
 from tests.test_gpu_executor_memory import _policy  # noqa: E402
-
-
-def _pattern(t, n, dev):
-    g = torch.Generator(device=dev).manual_seed(1000 + int(t))
-    return torch.randint(0, 256, (n,), dtype=torch.uint8, device=dev, generator=g)
-
-
-def run_capped(tr, cap, sel=None, arena_extra=1 << 30):
-    """one Detailed iteration under a cap of `cap` produced bytes; sel: swappable indices of an
-    installed policy (planned on an uncapped Detailed iteration first)"""
-    m = O.Model(tr)
-    sw = m.swappable()
-    dev = torch.device("cuda:0")
-    need = 0
-    if sel:
-        need = int(sum((int(tr.nbytes[sw["t"][k]]) + 511) // 512 * 512 for k in sel))
-    ctx = chm.Context(device=0, host_arena_bytes=need + arena_extra)
-    tok = [ctx.tokenize(nm) for nm in tr.op_names]
-    static_id = {t: (1 << 60) + t for t in range(tr.n_produced, tr.n_tensors)}
-    if sel:
-        ctx.set_detailed(True)
-        ids = np.array([(1 << 59) + int(p) for p in tr.ptr], np.uint64)  # planning pass: any ids
-        freed = set(int(t) for i in range(tr.n_ops) for t in tr.frees(i))
-        survivors = [t for t in range(tr.n_produced) if t not in freed]
-        for i in range(tr.n_ops):
-            fr = [ids[t] for t in tr.frees(i)] + ([ids[t] for t in survivors] if i == tr.n_ops - 1 else [])
-            # (survivors freed at the last op: F0 and the tables are unchanged, and no planning-pass
-            # id stays resident as a passive-swap candidate of the capped iteration)
-            ctx.record_op(tok[i], int(tr.phase[i]), [(ids[t], tr.nbytes[t], tr.dtype[t]) for t in tr.ins(i)],
-                          [(ids[t], tr.nbytes[t], tr.dtype[t]) for t in tr.outs(i)], fr)
-        ctx.detect_seq_change(tr.t_iter)
-        pt = ctx.trace_build(tr.budget, tr.static_bytes, tr.bw, tr.groups_fwd, tr.groups_bwd, t_iter=tr.t_iter)
-        words = np.zeros(max(pt.W, 1), np.uint64)
-        for k in sel:
-            words[k // 64] |= np.uint64(1 << (k % 64))
-        ctx.policy_install(pt, words[:pt.W])
-    ctx.set_detailed(True)
-    comp = torch.cuda.current_stream()
-    s_out, s_in, s_passive = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
-    storage, owner, handles, item_tensor = {}, {}, {}, {}
-    st = dict(live=0, peak=0, passive=0, restored=0, dropped=0, early=0, checked=0)
-
-    def hold(t, buf):
-        storage[t] = buf
-        owner[buf.data_ptr()] = t
-        st["live"] += int(tr.nbytes[t])
-
-    def drop(t):
-        buf = storage.pop(t)
-        owner.pop(buf.data_ptr())
-        st["live"] -= int(tr.nbytes[t])
-
-    def check(t):
-        assert torch.equal(storage[t], _pattern(t, int(tr.nbytes[t]), dev)), f"tensor {t} corrupted"
-        st["checked"] += 1
-
-    def alloc(t, nb, exclude):
-        """the allocator hook: Algo. 3 until the request fits under the cap"""
-        while st["live"] + nb > cap:
-            rel = ctx.oom_release(comp)  # (i)-(ii)
-            if rel:
-                for it in rel:
-                    drop(item_tensor[it])
-                st["early"] += len(rel)
-                continue
-            ex = [storage[u].data_ptr() for u in exclude if u in storage]
-            p = ctx.passive_swap(nb, ex, comp, s_passive)  # (iv)
-            u = owner[p["id"]]
-            assert p["nbytes"] == int(tr.nbytes[u])
-            handles[u] = p["handle"]
-            drop(u)
-            st["passive"] += 1
-        hold(t, torch.empty(nb, dtype=torch.uint8, device=dev))
-        return storage[t]
-
-    def ref(t):
-        return (storage[t].data_ptr() if t < tr.n_produced else static_id[t], int(tr.nbytes[t]), int(tr.dtype[t]))
-
-    measured = np.zeros(tr.n_ops, np.int64)
-    for i in range(tr.n_ops):
-        busy = [t for t in tr.ins(i) if t < tr.n_produced] + list(tr.outs(i))
-        for t in tr.ins(i):  # demand swap-in before the op reads it (reading Q20)
-            if t in handles:
-                buf = alloc(t, int(tr.nbytes[t]), busy)
-                ctx.passive_restore(handles.pop(t), buf.data_ptr(), comp, s_passive)
-                check(t)
-                st["restored"] += 1
-        for t in tr.outs(i):
-            alloc(t, int(tr.nbytes[t]), busy).copy_(_pattern(t, int(tr.nbytes[t]), dev))  # the op's compute
-        measured[i] = st["live"] + tr.static_bytes
-        st["peak"] = max(st["peak"], st["live"])
-        dead_out = [t for t in tr.frees(i) if t in handles]
-        act = ctx.record_op(tok[i], int(tr.phase[i]), [ref(t) for t in tr.ins(i)], [ref(t) for t in tr.outs(i)],
-                            [ref(t)[0] for t in tr.frees(i) if t not in handles], live_bytes=int(measured[i]))
-        av = chm.actions_view(act)
-        for t in dead_out:  # died while passively out
-            ctx.passive_restore(handles.pop(t), 0)
-            st["dropped"] += 1
-        for t in tr.frees(i):
-            if t in storage:
-                drop(t)
-        if av["swap_out"]:
-            for (d, off, nb), it in zip(av["swap_out"], av["swap_out_item"]):
-                item_tensor[it] = owner[d]
-            ctx.issue_swap_out(comp, s_out)
-        for it in av["release"]:  # custom recordStream (P:393)
-            ctx.item_wait(it, False, comp)
-            drop(item_tensor[it])
-        if av["swap_in"]:
-            ptrs = []
-            for (d, off, nb), it in zip(av["swap_in"], av["swap_in_item"]):
-                ptrs.append(alloc(item_tensor[it], int(nb), busy).data_ptr())
-            ctx.issue_swap_in(ptrs, comp, s_in)
-        for it in av["wait"]:
-            ctx.item_wait(it, True, comp)
-            check(item_tensor[it])
-    ctx.detect_seq_change(tr.t_iter)
-    torch.cuda.synchronize()
-    f0_log = ctx.trace_build(tr.budget, tr.static_bytes, tr.bw, tr.groups_fwd, tr.groups_bwd, t_iter=tr.t_iter,
-                             f0_source=1).tables()["f0"]
-    f0_ev = ctx.trace_build(tr.budget, tr.static_bytes, tr.bw, tr.groups_fwd, tr.groups_bwd,
-                            t_iter=tr.t_iter).tables()["f0"]
-    st["exec"] = ctx.exec_stats()
-    storage.clear()
-    ctx.close()
-    return m, measured, f0_log, f0_ev, st
+from tools.oom_driver import run_capped  # noqa: E402
 
 
 def _assert_reconstruction(m, f0_log, f0_ev):
@@ -165,7 +39,8 @@ def test_warmup_oom_passive_swaps(frac):
     tr = W.gpt2_xl(seq=512, batch=1)
     act_peak = int(O.Model(tr).f0().max() - tr.static_bytes)
     cap = int(act_peak * frac)
-    m, measured, f0_log, f0_ev, st = run_capped(tr, cap, arena_extra=act_peak)
+    m = O.Model(tr)
+    measured, f0_log, f0_ev, st = run_capped(tr, cap, arena_extra=act_peak)
     assert st["peak"] <= cap and st["passive"] > 0 and st["restored"] > 0
     assert st["checked"] == st["restored"]
     _assert_reconstruction(m, f0_log, f0_ev)
@@ -181,7 +56,8 @@ def test_policy_undershoot_releases_early_then_passive():
     fp = m0.replay(sw["t"][sel], sw["r"][sel], sw["s"][sel])["footprint"]
     act_peak = int(fp.max() - tr.static_bytes)
     cap = int(act_peak * 0.8)
-    m, measured, f0_log, f0_ev, st = run_capped(tr, cap, sel=sel, arena_extra=act_peak)
+    m = m0
+    measured, f0_log, f0_ev, st = run_capped(tr, cap, sel=sel, arena_extra=act_peak)
     assert st["peak"] <= cap
     assert st["early"] > 0, st
     assert st["exec"]["n_matched"] == len(sel)

@@ -1,7 +1,8 @@
 """NEXT-4 evidence: one GPT-2 XL (s=512, b=1) iteration under a cap on the produced bytes, Algo. 3
-handling every overflow (tests/test_gpu_oom.py's driver), for several caps; per cap: passive
-swaps, demand restores, early releases, bytes moved, wall time of the iteration and whether the
-Fig. 3 reconstruction equals the oracle F0.  Prints one JSON line.
+handling every overflow (tools/oom_driver.py), for several caps; per cap: passive swaps, demand
+restores, early releases, wall time of the iteration, and whether the Fig. 3 reconstruction
+(f0_source = 1: measured bytes + swap log) equals the F0 from the recorded events (f0_source =
+0).  (The oracle comparison of both: tests/test_gpu_oom.py.)  Prints one JSON line.
 
     python tools/oom_warmup.py
 """
@@ -14,39 +15,43 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import oracle as O  # noqa: E402  (reference F0 and the policy choice; not on the measured path)
-from tests.test_gpu_executor_memory import _policy  # noqa: E402
-from tests.test_gpu_oom import run_capped  # noqa: E402
+from paper_2509_11076_b200 import chm  # noqa: E402
+from tools.oom_driver import run_capped  # noqa: E402
 from workloads import traces as W  # noqa: E402
 
 
 def main():
     tr = W.gpt2_xl(seq=512, batch=1)
-    act_peak = int(O.Model(tr).f0().max() - tr.static_bytes)
+    h = chm.Context(device=-1)
+    h.set_detailed(True)
+    chm.record_iteration(h, tr)
+    h.detect_seq_change(tr.t_iter)
+    pt = h.trace_build(tr.budget, tr.static_bytes, tr.bw, tr.groups_fwd, tr.groups_bwd, t_iter=tr.t_iter)
+    act_peak = int(pt.peak0 - tr.static_bytes)
     out = dict(trace=tr.name, ops=tr.n_ops, no_swap_activation_peak=act_peak, runs=[])
     for frac in (1.0, 0.85, 0.7, 0.6, 0.5):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        m, measured, f0_log, f0_ev, st = run_capped(tr, int(act_peak * frac), arena_extra=act_peak)
+        measured, f0_log, f0_ev, st = run_capped(tr, int(act_peak * frac), arena_extra=act_peak)
         dt = time.perf_counter() - t0
         out["runs"].append(dict(mode="warmup", cap_frac=frac, wall_s=round(dt, 3), peak=st["peak"],
                                 passive=st["passive"], restored=st["restored"], dropped=st["dropped"],
-                                reconstruction_exact=bool(np.array_equal(f0_log, m.f0())),
-                                events_exact=bool(np.array_equal(f0_ev, m.f0()))))
-    m0 = O.Model(tr)
-    sel = _policy("C2b1", tr, m0)
-    sw = m0.swappable()
-    fp = m0.replay(sw["t"][sel], sw["r"][sel], sw["s"][sel])["footprint"]
-    pol_peak = int(fp.max() - tr.static_bytes)
+                                reconstruction_equals_events=bool(np.array_equal(f0_log, f0_ev))))
+    sd = W.SEEDED["C2"]
+    policy_peak = None
     for frac in (1.0, 0.9, 0.8):
+        # cap relative to the SEEDED best policy's own activation peak (first run: uncapped)
+        cap = 1 << 62 if policy_peak is None else int(policy_peak * frac)
         t0 = time.perf_counter()
-        m, measured, f0_log, f0_ev, st = run_capped(tr, int(pol_peak * frac), sel=sel, arena_extra=act_peak)
+        measured, f0_log, f0_ev, st = run_capped(tr, cap, seeded=(sd["seed"], sd["flip_thr"], 2000),
+                                                 arena_extra=act_peak)
         dt = time.perf_counter() - t0
+        if policy_peak is None:
+            policy_peak = st["peak"]
         out["runs"].append(dict(mode="policy", cap_frac_of_policy_peak=frac, wall_s=round(dt, 3), peak=st["peak"],
-                                early_released=st["early"], passive=st["passive"], restored=st["restored"],
-                                swapped_in_checked=st["checked"] - st["restored"],
-                                reconstruction_exact=bool(np.array_equal(f0_log, m.f0())),
-                                events_exact=bool(np.array_equal(f0_ev, m.f0()))))
+                                items=st["items"], early_released=st["early"], passive=st["passive"],
+                                restored=st["restored"], swapped_in_checked=st["checked"] - st["restored"],
+                                reconstruction_equals_events=bool(np.array_equal(f0_log, f0_ev))))
     print(json.dumps(out))
 
 

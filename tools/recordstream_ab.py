@@ -25,7 +25,6 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import oracle as O  # noqa: E402  (policy choice only; not on the measured path)
 from paper_2509_11076_b200 import chm  # noqa: E402
 from workloads import traces as W  # noqa: E402
 
@@ -110,18 +109,22 @@ def main():
     ap.add_argument("--policy-candidates", type=int, default=2000)
     args = ap.parse_args()
     tr = W.gpt2_xl(batch=args.batch)
-    m = O.Model(tr, t_iter=tr.n_ops * args.op_us * 1e-6)
+    # policy: the best of the SEEDED candidates, evaluated by the product on the GPU
+    t_iter = tr.n_ops * args.op_us * 1e-6
+    pc = chm.Context(device=0)
+    pc.set_detailed(True)
+    chm.record_iteration(pc, tr)
+    pc.detect_seq_change(tr.t_iter)
+    ptp = pc.trace_build(tr.budget, tr.static_bytes, tr.bw, tr.groups_fwd, tr.groups_bwd, t_iter=t_iter)
     sd = W.SEEDED["C2"]
-    best = m.eval(O.SEEDED, 0, args.policy_candidates, seed=sd["seed"], flip_thr=sd["flip_thr"], nthreads=16)["best"]
-    J = (m.K + 3) // 4
-    base = m.base_mask()
-    sw = m.swappable()
-    sel = {}
-    for k in range(m.K):
-        w = O.splitmix64(sd["seed"] ^ O.splitmix64((best.index * J + k // 4) % 2 ** 64))
-        bit = ((int(base[k // 64]) >> (k % 64)) & 1) ^ int(((w >> (16 * (k % 4))) & 0xFFFF) < (sd["flip_thr"] >> 48))
-        if bit:
-            sel[k] = int(sw["t"][k])
+    best = torch.empty(5, dtype=torch.int64, device="cuda:0")
+    pc.eval_policies(ptp, chm.SEEDED, 0, args.policy_candidates, best=best, seed=sd["seed"], flip_thr=sd["flip_thr"])
+    bk = best.cpu().numpy().view(chm.BEST_DTYPE)[0]
+    words = ptp.candidate_mask(chm.SEEDED, int(bk["index"]), seed=sd["seed"], flip_thr=sd["flip_thr"])
+    tens = ptp.tables()["tensor"]
+    sel = {k: int(tens[k]) for k in range(ptp.K) if (int(words[k // 64]) >> (k % 64)) & 1}
+    no_swap_peak, policy_peak = int(ptp.peak0 - tr.static_bytes), int(int(bk["peak"]) - tr.static_bytes)
+    pc.close()
     # cycles per microsecond of torch.cuda._sleep
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda._sleep(1000)
@@ -141,9 +144,7 @@ def main():
     res["naive_peak_extra_bytes"] = int(extra.max())
     res["config"] = dict(trace=tr.name, batch=args.batch, ops=tr.n_ops, swapped_items=len(sel), swapped_bytes=swapped,
                          op_us=args.op_us, t_iter_s=tr.n_ops * args.op_us * 1e-6,
-                         no_swap_peak_bytes=int(m.f0().max() - tr.static_bytes),
-                         policy_peak_bytes=int(m.eval(O.SEEDED, best.index, 1, seed=sd["seed"], flip_thr=sd["flip_thr"])["peak"][0]
-                                               - tr.static_bytes))
+                         no_swap_peak_bytes=no_swap_peak, policy_peak_bytes=policy_peak)
     print(json.dumps(res))
 
 
