@@ -38,7 +38,7 @@ typedef int32_t chm_status;
 enum {
   CHM_OK = 0,
   CHM_E_INVAL = -1,      /* invalid argument; *err_index names the offending item if given */
-  CHM_E_PARSE = -2,      /* reserved (trace files)                                           */
+  CHM_E_PARSE = -2,      /* malformed trace file (chm_trace_load); *err_offset = byte offset  */
   CHM_E_STATE = -3,      /* call not valid in the ctx's current state                        */
   CHM_E_NOMEM = -4,      /* host or device allocation failed                                  */
   CHM_E_CUDA = -5,       /* a CUDA runtime call failed; message has cudaGetErrorString        */
@@ -161,6 +161,22 @@ typedef struct {
  * uploaded to the ctx's device.  The trace is caller-owned: chm_trace_free. */
 chm_status chm_trace_build(chm_ctx *ctx, const chm_trace_params *params, chm_trace **out);
 void chm_trace_free(chm_trace *t);
+
+/* Detailed records as files (SURVEY §8(b) `chm_trace_load`): one JSON
+ * object per line, LF endings --
+ *   line 1  {"chm_trace":1,"t_iter_s":T,"tensors":[[nbytes,dtype],...]}
+ *   op      {"op":"aten::mm","tok":7,"phase":0,"in":[i,...],"out":[i,...],"free":[i,...],"live":B}
+ *   swap    {"swap":[from,to,nbytes]}        (Fig. 3 swap log, to = -1: still out at the end)
+ * Tensor ids index the header's table; a tensor no op outputs is live at iteration start.
+ * chm_trace_load parses `text` (len bytes, borrowed) and builds a trace exactly as
+ * chm_trace_build does from a recorded iteration (op names are tokenized through the ctx; "tok"
+ * is used only without a name).  Malformed input: CHM_E_PARSE, *err_offset = byte offset of
+ * the offending line or character, no trace.  chm_record_save writes the ctx's last Detailed
+ * iteration in this format into buf (cap bytes); *len = bytes needed (CHM_E_NOMEM if > cap, so a
+ * first call with cap = 0 sizes the buffer).  load(save(record)) rebuilds identical tables. */
+chm_status chm_trace_load(chm_ctx *ctx, const char *text, size_t len, const chm_trace_params *params,
+                          chm_trace **out, int64_t *err_offset);
+chm_status chm_record_save(chm_ctx *ctx, char *buf, size_t cap, size_t *len);
 
 typedef struct {
   uint32_t n_ops, n_tensors, n_swappable, n_layers, mask_words;

@@ -124,7 +124,7 @@ EXPORTS = [
     "chm_trace_get_info", "chm_trace_tables", "chm_eval_policies", "chm_eval_policies_ex", "chm_best_reduce", "chm_best_reduce_device", "chm_candidate_mask",
     "chm_policy_install", "chm_policy_install_items", "chm_generate_policy", "chm_exec_stats_get", "chm_host_arena", "chm_swap_out", "chm_swap_in",
     "chm_batch_wait", "chm_batch_query", "chm_batch_elapsed", "chm_arena_reserve", "chm_issue_swap_out", "chm_issue_swap_in", "chm_item_wait",
-    "chm_oom_release", "chm_passive_swap", "chm_passive_restore",
+    "chm_oom_release", "chm_passive_swap", "chm_passive_restore", "chm_trace_load", "chm_record_save",
 ]
 
 _lib = None
@@ -174,6 +174,8 @@ def load(path: str = LIB_PATH):
         "chm_issue_swap_in": (i32, [vp, vp, vp, vp, u32, P(u64)]),
         "chm_item_wait": (i32, [vp, u32, i32, vp]),
         "chm_oom_release": (i32, [vp, vp, vp, u32, P(u32)]),
+        "chm_trace_load": (i32, [vp, C.c_char_p, C.c_size_t, P(TraceParams), P(vp), P(i64)]),
+        "chm_record_save": (i32, [vp, vp, C.c_size_t, P(C.c_size_t)]),
         "chm_passive_swap": (i32, [vp, i64, vp, u32, vp, vp, P(Passive)]),
         "chm_passive_restore": (i32, [vp, u64, u64, vp, vp]),
     }
@@ -329,6 +331,31 @@ class Context:
         h = C.c_void_p()
         _check(load().chm_trace_build(self.h, C.byref(p), C.byref(h)))
         return Trace(self, h)
+
+    def trace_load(self, text: bytes, budget: int, static_bytes: int, bw: float, groups_fwd: int, groups_bwd: int,
+                   t_iter: float = 0.0, omega: float = 1.0, f0_source: int = 0) -> Trace:
+        """builds a trace from a Detailed-record file (chm_trace_load); ChmError.offset = byte
+        offset of a parse error"""
+        p = TraceParams(int(budget), int(static_bytes), float(t_iter), float(bw), int(groups_fwd), int(groups_bwd),
+                        float(omega), int(f0_source))
+        h = C.c_void_p()
+        off = C.c_int64(-1)
+        rc = load().chm_trace_load(self.h, text, len(text), C.byref(p), C.byref(h), C.byref(off))
+        if rc != CHM_OK:
+            err = ChmError(rc, (load().chm_last_error() or b"").decode())
+            err.offset = off.value
+            raise err
+        return Trace(self, h)
+
+    def record_save(self) -> bytes:
+        """the last Detailed iteration as a Detailed-record file (chm_record_save)"""
+        n = C.c_size_t()
+        rc = load().chm_record_save(self.h, None, 0, C.byref(n))
+        if rc not in (CHM_OK, CHM_E_NOMEM):
+            _check(rc)
+        buf = C.create_string_buffer(n.value)
+        _check(load().chm_record_save(self.h, buf, n.value, C.byref(n)))
+        return buf.raw[:n.value]
 
     # ------------------------------------------------------------ policy evaluation
     def eval_policies(self, trace: Trace, kind: int, first: int, count: int, *, best, seed: int = 0,

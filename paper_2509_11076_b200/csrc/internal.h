@@ -232,6 +232,9 @@ constexpr int kEventRing = 4096;
 constexpr int kMaxDescPerLaunch = 64;
 constexpr int kMaxSeededWords = 64;  // SEEDED base mask in kernel params: K <= 4096
 
+// trace.cpp: the trace build from a record (the ctx's last Detailed iteration or a loaded file)
+chm_status build_trace(chm_ctx *ctx, const IterRecord &R, const chm_trace_params *P, chm_trace **out);
+
 // executor.cpp: moves a released item's Detailed-record tensor index off its old address
 void stash_record(chm_ctx *ctx, PolicyItem &it);
 

@@ -15,8 +15,13 @@ enum { kFWD = 0, kBWD = 1, kOPT = 2 };
 extern "C" chm_status chm_trace_build(chm_ctx *ctx, const chm_trace_params *P, chm_trace **out) {
   if (!ctx || !P || !out) CHM_FAIL(CHM_E_INVAL, "chm_trace_build: NULL argument");
   *out = nullptr;
-  const IterRecord &R = ctx->last_detailed;
-  if (R.tokens.empty()) CHM_FAIL(CHM_E_STATE, "chm_trace_build: no Detailed-mode iteration recorded");
+  if (ctx->last_detailed.tokens.empty()) CHM_FAIL(CHM_E_STATE, "chm_trace_build: no Detailed-mode iteration recorded");
+  return build_trace(ctx, ctx->last_detailed, P, out);
+}
+
+// the build proper, from the ctx's last Detailed record or a loaded file (trace_io.cpp)
+chm_status chm::build_trace(chm_ctx *ctx, const IterRecord &R, const chm_trace_params *P, chm_trace **out) {
+  *out = nullptr;
   if (!(P->bw_bytes_per_s > 0.0)) CHM_FAIL(CHM_E_INVAL, "chm_trace_build: B must be > 0 (Eq. 3)");
   const double t_iter = P->t_iter_s > 0.0 ? P->t_iter_s : R.t_iter;
   if (!(t_iter >= 0.0)) CHM_FAIL(CHM_E_INVAL, "chm_trace_build: T_iter < 0");

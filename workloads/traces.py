@@ -83,6 +83,20 @@ class Trace:
         return self.free_idx[self.free_ptr[i]:self.free_ptr[i + 1]]
 
 
+def to_jsonl(trace: Trace) -> bytes:
+    """The trace as a Detailed-record file (the format `chm_trace_load` reads, include/chm.h):
+    header with the tensor table, then one line per op (format conversion only)."""
+    import json
+    lines = [json.dumps({"chm_trace": 1, "t_iter_s": float(trace.t_iter),
+                         "tensors": [[int(trace.nbytes[t]), int(trace.dtype[t])] for t in range(trace.n_tensors)]},
+                        separators=(",", ":"))]
+    for i in range(trace.n_ops):
+        lines.append(json.dumps({"op": trace.op_names[i], "phase": int(trace.phase[i]),
+                                 "in": [int(t) for t in trace.ins(i)], "out": [int(t) for t in trace.outs(i)],
+                                 "free": [int(t) for t in trace.frees(i)]}, separators=(",", ":")))
+    return ("\n".join(lines) + "\n").encode()
+
+
 class _Builder:
     """Records ops in dispatch order; frees are the eager refcount releases."""
 
