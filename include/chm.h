@@ -307,7 +307,8 @@ chm_status chm_exec_stats_get(chm_ctx *ctx, chm_exec_stats *s);
  *                      chm_record_op and not freed since; not bound to a policy item) whose size
  *                      is closest to `need`: the smallest one of at least `need` bytes, else the
  *                      largest; ties: the older.  `exclude` (n_exclude ids, e.g. the current op's
- *                      inputs) is skipped.  Copy goes to the arena above the installed policy's
+ *                      inputs) is skipped; `only` (n_only ids, nullable = no restriction) limits
+ *                      the choice to those ids (e.g. the tensors a framework can drop).  Copy goes to the arena above the installed policy's
  *                      slots (first fit); `compute` waits for it; *out names the tensor (`id`) and
  *                      a unique `handle`; the caller drops the block and retries.  CHM_E_NOMEM if
  *                      no tensor is eligible or the arena has no room.
@@ -331,7 +332,8 @@ typedef struct {
 chm_status chm_oom_release(chm_ctx *ctx, cudaStream_t compute, uint32_t *items, uint32_t cap,
                            uint32_t *n_items);
 chm_status chm_passive_swap(chm_ctx *ctx, int64_t need, const uint64_t *exclude, uint32_t n_exclude,
-                            cudaStream_t compute, cudaStream_t swap, chm_passive *out);
+                            const uint64_t *only, uint32_t n_only, cudaStream_t compute, cudaStream_t swap,
+                            chm_passive *out);
 chm_status chm_passive_restore(chm_ctx *ctx, uint64_t handle, uint64_t dev, cudaStream_t compute,
                                cudaStream_t swap);
 
@@ -339,7 +341,8 @@ chm_status chm_passive_restore(chm_ctx *ctx, uint64_t handle, uint64_t dev, cuda
 /* The ctx's pinned, device-mapped host arena (cudaHostAllocMapped|Portable). */
 chm_status chm_host_arena(chm_ctx *ctx, void **host_base, uint64_t *bytes);
 /* Grows the arena to at least `bytes` (e.g. to the installed policy's swapped bytes).  The old
- * arena is released: call only while no swap batch is in flight (contents are not kept). */
+ * arena is released: call only while no swap batch is in flight (contents are not kept);
+ * CHM_E_STATE while passive swaps hold data in it. */
 chm_status chm_arena_reserve(chm_ctx *ctx, uint64_t bytes);
 
 enum {

@@ -176,7 +176,7 @@ def load(path: str = LIB_PATH):
         "chm_oom_release": (i32, [vp, vp, vp, u32, P(u32)]),
         "chm_trace_load": (i32, [vp, C.c_char_p, C.c_size_t, P(TraceParams), P(vp), P(i64)]),
         "chm_record_save": (i32, [vp, vp, C.c_size_t, P(C.c_size_t)]),
-        "chm_passive_swap": (i32, [vp, i64, vp, u32, vp, vp, P(Passive)]),
+        "chm_passive_swap": (i32, [vp, i64, vp, u32, vp, u32, vp, vp, P(Passive)]),
         "chm_passive_restore": (i32, [vp, u64, u64, vp, vp]),
     }
     for name, (res, args) in sig.items():
@@ -447,13 +447,18 @@ class Context:
         _check(load().chm_oom_release(self.h, _stream(stream), buf, cap, C.byref(n)))
         return list(buf[:n.value])
 
-    def passive_swap(self, need: int, exclude=(), compute=None, swap=None) -> dict:
-        """(iv): swap out the resident tensor closest in size to `need`; the caller drops its
-        storage (the compute stream already waits for the copy)"""
+    def passive_swap(self, need: int, exclude=(), compute=None, swap=None, only=None) -> dict:
+        """(iv): swap out the resident tensor closest in size to `need` (among `only` if given);
+        the caller drops its storage (the compute stream already waits for the copy)"""
         ex = np.ascontiguousarray(list(exclude), np.uint64)
+        n_on = 0
+        on = None
+        if only is not None:
+            n_on = len(only)
+            on = np.ascontiguousarray(list(only) if n_on else [0], np.uint64)  # empty: nothing eligible
         out = Passive()
         _check(load().chm_passive_swap(self.h, int(need), _ptr(ex) if ex.size else None, int(ex.size),
-                                       _stream(compute), _stream(swap), C.byref(out)))
+                                       _ptr(on), n_on, _stream(compute), _stream(swap), C.byref(out)))
         return {k: getattr(out, k) for k, _ in Passive._fields_}
 
     def passive_restore(self, handle: int, dev: int, compute=None, swap=None):

@@ -71,8 +71,10 @@ static void passive_free_range(chm_ctx *ctx, uint64_t off, uint64_t bytes) {
 }
 
 extern "C" chm_status chm_passive_swap(chm_ctx *ctx, int64_t need, const uint64_t *exclude, uint32_t n_exclude,
-                                       cudaStream_t compute, cudaStream_t swap, chm_passive *out) {
-  if (!ctx || !out || (n_exclude && !exclude)) CHM_FAIL(CHM_E_INVAL, "chm_passive_swap: NULL argument");
+                                       const uint64_t *only, uint32_t n_only, cudaStream_t compute,
+                                       cudaStream_t swap, chm_passive *out) {
+  if (!ctx || !out || (n_exclude && !exclude) || (n_only && !only))
+    CHM_FAIL(CHM_E_INVAL, "chm_passive_swap: NULL argument");
   if (ctx->device < 0) CHM_FAIL(CHM_E_STATE, "chm_passive_swap: host-only ctx");
   // closest size to the request: the smallest resident tensor >= need, else the largest; ties
   // by age (older first)
@@ -84,6 +86,7 @@ extern "C" chm_status chm_passive_swap(chm_ctx *ctx, int64_t need, const uint64_
     const uint64_t id = kv.first;
     const int64_t sz = kv.second.nbytes;
     if (std::find(exclude, exclude + n_exclude, id) != exclude + n_exclude) continue;
+    if (only && std::find(only, only + n_only, id) == only + n_only) continue;
     auto lt = ctx->live.find(id);
     if (lt != ctx->live.end() && lt->second.item >= 0) continue;  // bound to a policy item
     const bool ab = sz >= need;

@@ -342,6 +342,9 @@ extern "C" chm_status chm_batch_elapsed(chm_ctx *ctx, uint64_t batch, float *ms)
 extern "C" chm_status chm_arena_reserve(chm_ctx *ctx, uint64_t bytes) {
   if (!ctx || ctx->device < 0) CHM_FAIL(CHM_E_INVAL, "chm_arena_reserve: NULL or host-only ctx");
   if (bytes <= ctx->arena_bytes) return CHM_OK;
+  if (!ctx->passive.empty())
+    CHM_FAIL(CHM_E_STATE, "chm_arena_reserve: %zu passive swaps hold arena data", ctx->passive.size());
+  ctx->passive_free.clear();  // re-derived from the new size at the next passive swap
   CHM_CUDA(cudaSetDevice(ctx->device));
   if (ctx->arena) {
     CHM_CUDA(cudaFreeHost(ctx->arena));

@@ -36,6 +36,7 @@ on CPU tensors (no copies): the CPU tests use it.
 from __future__ import annotations
 
 import contextlib
+import re
 import time
 import weakref
 from typing import Optional
@@ -58,7 +59,7 @@ def _dtype_code(dt) -> int:
 class _Holder:
     """one swapped (or swappable) storage: the device block while resident, its swap state"""
     __slots__ = ("storage", "nbytes", "item", "host_off", "released", "in_issued", "in_waited", "boxes",
-                 "__weakref__")
+                 "passive", "__weakref__")
 
     def __init__(self, storage, nbytes):
         self.storage = storage
@@ -68,6 +69,7 @@ class _Holder:
         self.released = False
         self.in_issued = False
         self.in_waited = False
+        self.passive = 0  # handle of a passive swap (Algo. 3 (iv)) holding the data
         self.boxes = weakref.WeakSet()
 
 
@@ -84,6 +86,14 @@ class _Box:
         self.offset = t.storage_offset()
 
 
+def _requested_bytes(e) -> int:
+    """the failed request's size from PyTorch's OOM message (1 MiB if it cannot be read)"""
+    m = re.search(r"Tried to allocate ([0-9.]+) (GiB|MiB|KiB|bytes)", str(e))
+    if not m:
+        return 1 << 20
+    return int(float(m.group(1)) * {"GiB": 1 << 30, "MiB": 1 << 20, "KiB": 1 << 10, "bytes": 1}[m.group(2)])
+
+
 class _Mode(TorchDispatchMode):
     def __init__(self, rt: "Runtime"):
         super().__init__()
@@ -95,7 +105,13 @@ class _Mode(TorchDispatchMode):
         if rt._internal:  # the runtime's own allocations / views (autograd unpack hook)
             return func(*args, **kwargs)
         rt._flush()
-        out = func(*args, **kwargs)
+        while True:
+            try:
+                out = func(*args, **kwargs)
+                break
+            except torch.OutOfMemoryError as e:  # Algo. 3: make room, then retry the op
+                if not rt._oom(_requested_bytes(e), tree_flatten((args, kwargs))[0]):
+                    raise
         rt._stage(func, args, kwargs, out)
         return out
 
@@ -113,13 +129,15 @@ class Runtime:
                  groups_fwd: int = 8, groups_bwd: int = 8, omega: float = 1.0, candidates: int = 1 << 16,
                  seed: int = 1, flip_frac: float = 0.02, generator: bool = True, swap_ctas: int = 0,
                  min_swap_bytes: int = 0, search_rounds: int = 4096, host_arena_bytes: int = 0,
-                 swap_flags: int = chm.SWAP_AUTO, **algo1):
+                 swap_flags: int = chm.SWAP_AUTO, oom_host_bytes: int = 0, **algo1):
         self.host_only = device is None
         self.dev = torch.device("cpu") if self.host_only else torch.device("cuda", device)
         self.ctx = chm.Context(device=-1 if self.host_only else device, swap_ctas=swap_ctas,
-                               host_arena_bytes=0 if self.host_only else max(int(host_arena_bytes), 1 << 20),
+                               host_arena_bytes=0 if self.host_only else
+                               max(int(host_arena_bytes) + int(oom_host_bytes), 1 << 20),
                                **algo1)
         self.search_rounds = int(search_rounds)
+        self.oom_host_bytes = int(oom_host_bytes)  # arena room for passive swaps (0: OOMs propagate)
         # AUTO (default): tensors >= 4 MiB on the copy engines, which take no SMs from the step's
         # compute (tools/stall_fidelity.py measured 10% shorter Llama-2 7B steps than with the
         # kernel at 8 CTAs), smaller ones batched through the swap kernel
@@ -142,13 +160,14 @@ class Runtime:
         self.policy = None  # (trace, description)
         self.plans = []
         self.stats = dict(steps=0, ops=0, swap_out=0, release=0, released_bytes=0, swap_in=0, demand_swap_in=0,
-                          unheld=0, plan_ms=0.0)
+                          unheld=0, plan_ms=0.0, oom=0, oom_released=0, passive=0, passive_bytes=0, passive_restored=0)
         if not self.host_only:
             self.s_out = torch.cuda.Stream(self.dev)
             self.s_in = torch.cuda.Stream(self.dev)
         self.bw = float(bw) if bw else (50e9 if self.host_only else self._measure_bw())
         self._in_step = False
         self._internal = False
+        self.passive_out = {}  # passive-swap handle -> weak holder
 
     # ------------------------------------------------------------------ step
     @contextlib.contextmanager
@@ -203,6 +222,11 @@ class Runtime:
         stage_before = self.stage
         d = self.ctx.detect_seq_change(t_iter)
         self.stage = d["stage"]
+        for hd, ref in list(self.passive_out.items()):  # died while passively out: drop the copy
+            h = ref()
+            if h is None or not h.boxes:
+                self.ctx.passive_restore(hd, 0)
+                del self.passive_out[hd]
         for ref in self.weak.values():
             torch.UntypedStorage._free_weak_ref(ref)
         self.weak = {}
@@ -334,10 +358,18 @@ class Runtime:
     def _restore(self, b):
         h = b.holder
         comp = None if self.host_only else torch.cuda.current_stream(self.dev)
-        if h.storage is None:  # needed before its swap-in was issued: demand swap-in (Q20)
+        if h.storage is None and h.passive:  # passively swapped on an OOM: bring it back
+            st = self._alloc(h.nbytes)
+            self.ctx.passive_restore(h.passive, st.data_ptr(), comp, self.s_in)
+            self.passive_out.pop(h.passive, None)
+            h.passive = 0
+            h.storage = st
+            h.in_issued = h.in_waited = True
+            self.stats["passive_restored"] += 1
+        elif h.storage is None:  # needed before its swap-in was issued: demand swap-in (Q20)
             if self.host_only:
                 raise RuntimeError("host-only runtime cannot restore a released tensor")
-            st = torch.empty(h.nbytes, dtype=torch.uint8, device=self.dev).untyped_storage()
+            st = self._alloc(h.nbytes)
             bt = self.ctx.swap_in([(st.data_ptr(), h.host_off, h.nbytes)], comp, self.s_in, self.swap_flags)
             self.ctx.batch_wait(bt, comp)
             h.storage = st
@@ -404,6 +436,68 @@ class Runtime:
                 h = ref() if ref is not None else None
                 if h is not None:
                     h.in_waited = True
+
+    # ------------------------------------------------------------------ OOM handling (Algo. 3)
+    def _alloc(self, nbytes: int):
+        """a device block for a restore; an OOM here goes through Algo. 3 as well"""
+        while True:
+            try:
+                return torch.empty(nbytes, dtype=torch.uint8, device=self.dev).untyped_storage()
+            except torch.OutOfMemoryError:
+                if not self._oom(nbytes, ()):
+                    raise
+
+    def _drop(self, h):
+        h.storage = None
+        for b in list(h.boxes):
+            b.t = None
+        h.released = True
+
+    def _oom(self, need: int, busy) -> bool:
+        """one round of Algo. 3: (i)-(ii) release every block whose swap-out is
+        issued and whose release point has not come; else (iv) passively swap the saved tensor
+        closest in size to the request.  False when nothing can be freed (the OOM propagates)."""
+        if self.host_only or not self._in_step:
+            return False
+        self.stats["oom"] += 1
+        comp = torch.cuda.current_stream(self.dev)
+        if self.policy is not None:
+            freed = 0
+            for it in self.ctx.oom_release(comp):
+                ent = self.item_holder.get(it)
+                h = self.holders.get(ent[1]) if ent is not None else None
+                if h is not None and not h.released:
+                    h.item, h.host_off = it, ent[2]
+                    self.item_holder[it] = (weakref.ref(h), ent[1], ent[2], ent[3])
+                    self._drop(h)
+                    freed += 1
+            self.stats["oom_released"] += freed
+            if freed:
+                return True
+        if not self.oom_host_bytes:
+            return False
+        busy_ptrs = set()
+        for x in busy:
+            if isinstance(x, torch.Tensor) and x.device == self.dev:
+                try:
+                    busy_ptrs.add(x.untyped_storage().data_ptr())
+                except (RuntimeError, NotImplementedError):
+                    pass
+        cand = [p for p, h in list(self.holders.items())
+                if h.storage is not None and not h.released and h.item < 0 and p not in busy_ptrs]
+        if not cand:
+            return False
+        try:
+            ps = self.ctx.passive_swap(need, (), comp, self.s_out, only=cand)
+        except chm.ChmError:
+            return False  # arena full or nothing eligible
+        h = self.holders.get(ps["id"])
+        h.passive = ps["handle"]
+        self.passive_out[ps["handle"]] = weakref.ref(h)
+        self._drop(h)
+        self.stats["passive"] += 1
+        self.stats["passive_bytes"] += ps["nbytes"]
+        return True
 
     # ------------------------------------------------------------------ planning
     def uninstall(self):
@@ -519,7 +613,7 @@ class Runtime:
         for k in range(pt.K):
             if (int(words[k // 64]) >> (k % 64)) & 1:
                 need += (int(tb["nbytes"][k]) + 511) // 512 * 512
-        self.ctx.arena_reserve(max(need, 1 << 20))
+        self.ctx.arena_reserve(max(need + self.oom_host_bytes, 1 << 20))
 
     def _reserve_items(self, items, pt):
         if self.host_only:
@@ -527,7 +621,7 @@ class Runtime:
         tb = pt.tables()
         rank_bytes = {int(t): int(n) for t, n in zip(tb["tensor"], tb["nbytes"])}
         need = sum((rank_bytes.get(int(it["t"]), 0) + 511) // 512 * 512 for it in items)
-        self.ctx.arena_reserve(max(need, 1 << 20))
+        self.ctx.arena_reserve(max(need + self.oom_host_bytes, 1 << 20))
 
     def _measure_bw(self) -> float:
         """B of Eq. 3: one 256 MiB swap-out + swap-in through the policy's copy path"""

@@ -1,0 +1,26 @@
+"""Algo. 3 in a real training loop (NEXT-4 through the NEXT-2 runtime): under a per-process
+memory cap below the model's no-swap peak, plain training runs out of memory; with the runtime
+(WarmUp stage, no policy yet) every OOM inside an op is handled by passive swaps of autograd-saved
+activations (chm_passive_swap restricted to them), restored by chm_passive_restore when backward
+unpacks them -- and training is bit-identical to the uncapped run.  Runs in a child process
+(tests/_oom_child.py) so the cap does not leak into other tests."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("frac", [0.6])
+def test_runtime_survives_a_memory_cap_with_passive_swaps(frac):
+    child = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_oom_child.py")
+    r = subprocess.run([sys.executable, child, str(frac)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out["plain_under_cap"] == "oom", out
+    assert out["losses_equal"] and out["params_equal"], out
+    st = out["stats"]
+    assert st["oom"] > 0 and st["passive"] > 0 and st["passive_restored"] == st["passive"], st
