@@ -205,6 +205,17 @@ def cpu_baseline(args, tr, best_swapped: int):
 
 
 # ----------------------------------------------------------------------------- this repo
+def _traffic(kernel: str, algorithmic_bytes: float):
+    """DRAM bytes per launch: the ncu-measured traffic / algorithmic ratio of `kernel`
+    (profiles/r01_ncu_traffic.json) times this run's algorithmic bytes per launch; None if absent"""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)[kernel]["ratio"]) * float(algorithmic_bytes)
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -355,7 +366,7 @@ def main():
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     # ---- warm-up + timed steps (device loop)
     step_ms, eval_ms, d2h_ms, h2d_ms = [], [], [], []
-    launches = 0
+    launches = launches_swap = 0
     for step in range(args.warmup):
         evaluate()
         execute(chm.SWAP_KERNEL)
@@ -373,6 +384,7 @@ def main():
             torch.cuda.synchronize()
             barrier()
             launches += n_l + 1 + (1 if P > 1 else 0)
+            launches_swap = n_l
             step_ms.append(ev[0].elapsed_time(ev[3]))
             eval_ms.append(ev[1].elapsed_time(ev[2]))
             d2h_ms.append(sum(ctx.batch_elapsed_ms(b) for b in outs))
@@ -495,7 +507,10 @@ def main():
         },
         "roofline": {
             "bound": "pcie", "kernel": "swap_copy_kernel (D2H + H2D)", "achieved": achieved_swap,
-            "peak": PCIE_GEN5_X16_GBPS, "unit": "GB/s", "frac": achieved_swap / PCIE_GEN5_X16_GBPS, "traffic": None,
+            "peak": PCIE_GEN5_X16_GBPS, "unit": "GB/s", "frac": achieved_swap / PCIE_GEN5_X16_GBPS,
+            "traffic": _traffic("swap_copy_kernel", 2 * bytes_swap / max(1, launches_swap)),
+            "traffic_source": "ncu dram bytes / algorithmic bytes (profiles/r01_ncu_traffic.json) x this run's "
+                              "algorithmic bytes per swap launch",
             "peak_source": "nominal PCIe Gen5 x16 per direction (no measured host-link peak in MEASURED_PEAKS.json; "
                            "the box's copy engines reach 57.3 D2H / 55.6 H2D GB/s, tools/probe_box.py)",
             "d2h_GBps": per_dir[0], "h2d_GBps": per_dir[1],
@@ -503,7 +518,8 @@ def main():
         "roofline_replay": {
             "bound": "hbm", "kernel": "replay_kernel<%s>" % ("true" if full else "false"),
             "achieved": fp_bytes / (t_eval * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
-            "frac": fp_bytes / (t_eval * 1e-3) / 1e9 / hbm_peak, "traffic": None,
+            "frac": fp_bytes / (t_eval * 1e-3) / 1e9 / hbm_peak,
+            "traffic": _traffic("replay_kernel_full", fp_bytes) if full else None,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst)",
             "algorithmic_bytes_per_launch": fp_bytes,
         },

@@ -37,7 +37,11 @@ def main(rep, out, title=""):
     if len(src) > 2:
         hdr = src[1]
         ix = {x: i for i, x in enumerate(hdr)}
-        data = src[2:]
+        data = []
+        for r in src[2:]:  # first kernel's rows only (a report with several launches repeats the header)
+            if len(r) != len(hdr) or r[ix["Warp Stall Sampling (All Samples)"]] == "Warp Stall Sampling (All Samples)":
+                break
+            data.append(r)
         tot = sum(float(r[ix["Warp Stall Sampling (All Samples)"]] or 0) for r in data)
         stalls = [x for x in hdr if x.startswith("stall_") and "Not Issued" not in x]
         agg = {x: sum(float(r[ix[x]] or 0) for r in data) for x in stalls}
