@@ -364,6 +364,7 @@ def main():
         return launches, outs, ins
 
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    spin_cycles = 1_000_000  # ~0.5 ms at 1.9 GHz
     # ---- warm-up + timed steps (device loop)
     step_ms, eval_ms, d2h_ms, h2d_ms = [], [], [], []
     launches = launches_swap = 0
@@ -375,6 +376,9 @@ def main():
         for step in range(args.steps):
             barrier()
             torch.cuda.synchronize()
+            # a short device-side wait first, so the events bracket the replay kernel itself and
+            # not the host's launch latency after an idle GPU
+            torch.cuda._sleep(spin_cycles)
             ev[0].record(comp)
             ev[1].record(comp)
             evaluate()
