@@ -287,6 +287,20 @@ chm_status chm_candidate_mask(const chm_trace *t, const chm_candidates *c, uint6
 chm_status chm_policy_install(chm_ctx *ctx, const chm_trace *t, const uint64_t *words);
 /* the same for an explicit item list (e.g. chm_generate_policy's output): releases after r,
  * swap-ins before s as given */
+/* The stall of one explicit item list (host, exact) under the stall models of reading Q11
+ * (SURVEY §8(f) NEXT-4), for comparison against measured stalls; out[3]:
+ *   out[0] R-stall -- what chm_eval_policies reports: pairwise sum over layers of
+ *          max(0, (out_l + in_l)/B - Bud_l), out_l = bytes released in layer lay(r),
+ *          in_l = bytes swapped in in layer lay(s);
+ *   out[1] per-direction budgets (full-duplex link): max(0, out_l/B - Bud_l) +
+ *          max(0, in_l/B - Bud_l) per layer, same pairwise order;
+ *   out[2] max-plus serial-stream timeline: ops take T_iter/N each; a swap-out enters the D2H
+ *          FIFO after op a_t, a swap-in the H2D FIFO before op s (not before its swap-out
+ *          ended); compute waits for the swap-out after op r (the release) and for the swap-in
+ *          before op b_t; the total wait.  Event order: before op i swap-ins (s = i) then waits
+ *          (b_t = i); after op i swap-outs (a_t = i) then releases (r = i); item order within
+ *          a kind.  Items are validated as for chm_policy_install_items. */
+chm_status chm_stall_models(const chm_trace *t, const chm_item *items, uint32_t n, double *out);
 chm_status chm_policy_install_items(chm_ctx *ctx, const chm_trace *t, const chm_item *items,
                                     uint32_t n);
 typedef struct {

@@ -79,6 +79,9 @@ def lib():
         L.orc_replay.restype = C.c_int64
         L.orc_stall.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
         L.orc_stall.restype = C.c_double
+        for fn in (L.orc_stall_dir, L.orc_stall_timeline):
+            fn.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
+            fn.restype = C.c_double
         L.orc_reconstruct.argtypes = [C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
                                       C.c_void_p, C.c_void_p]
         L.orc_eval.argtypes = [C.c_void_p, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
@@ -188,6 +191,16 @@ class Model:
     def stall(self, t, r, s) -> float:
         t, r, s = _arr(t, np.int32), _arr(r, np.int32), _arr(s, np.int32)
         return lib().orc_stall(self._h, len(t), _p(t), _p(r), _p(s))
+
+    def stall_dir(self, t, r, s) -> float:
+        """Q11 variant: per-direction layer budgets"""
+        t, r, s = _arr(t, np.int32), _arr(r, np.int32), _arr(s, np.int32)
+        return lib().orc_stall_dir(self._h, len(t), _p(t), _p(r), _p(s))
+
+    def stall_timeline(self, t, r, s) -> float:
+        """Q11 variant: max-plus serial-stream timeline"""
+        t, r, s = _arr(t, np.int32), _arr(r, np.int32), _arr(s, np.int32)
+        return lib().orc_stall_timeline(self._h, len(t), _p(t), _p(r), _p(s))
 
     def mask_items(self, mask_bits: Sequence[int]):
         """items {t, r, s} of the swappable tensors selected by bit list"""

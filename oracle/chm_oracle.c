@@ -296,6 +296,67 @@ double orc_stall(const orc_model *m, int32_t n_items, const int32_t *t, const in
   return st;
 }
 
+/* Q11 variant: per-direction budgets (the host link is full duplex) */
+double orc_stall_dir(const orc_model *m, int32_t n_items, const int32_t *t, const int32_t *r,
+                     const int32_t *s) {
+  int64_t *out = xcalloc((size_t)m->L + 1, sizeof(int64_t));
+  int64_t *in = xcalloc((size_t)m->L + 1, sizeof(int64_t));
+  for (int32_t k = 0; k < n_items; k++) {
+    out[m->lay_of_op[r[k]]] += m->S[t[k]];
+    in[m->lay_of_op[s[k]]] += m->S[t[k]];
+  }
+  int32_t P = 1;
+  while (P < m->L) P *= 2;
+  double *term = xcalloc((size_t)P, sizeof(double));
+  for (int32_t l = 0; l < m->L; l++) {
+    double xo = (double)out[l] / m->bw - m->bud[l];
+    double xi = (double)in[l] / m->bw - m->bud[l];
+    term[l] = (xo > 0.0 ? xo : 0.0) + (xi > 0.0 ? xi : 0.0);
+  }
+  double stall = pairwise_sum(term, 0, P);
+  free(term); free(in); free(out);
+  return stall;
+}
+
+/* Q11 variant: max-plus serial-stream timeline, walked op by op */
+double orc_stall_timeline(const orc_model *m, int32_t n_items, const int32_t *t, const int32_t *r,
+                          const int32_t *s) {
+  const double tau = m->N > 0 ? m->t_iter / (double)m->N : 0.0;
+  double now = 0.0, d2h_free = 0.0, h2d_free = 0.0, stall = 0.0;
+  double *out_end = xcalloc((size_t)n_items + 1, sizeof(double));
+  double *in_end = xcalloc((size_t)n_items + 1, sizeof(double));
+  for (int32_t i = 0; i < m->N; i++) {
+    /* before op i: swap-ins issued for s = i, then waits for b = i */
+    for (int32_t k = 0; k < n_items; k++) {
+      if (s[k] != i) continue;
+      double start = now;
+      if (h2d_free > start) start = h2d_free;
+      if (out_end[k] > start) start = out_end[k];
+      in_end[k] = start + (double)m->S[t[k]] / m->bw;
+      h2d_free = in_end[k];
+    }
+    for (int32_t k = 0; k < n_items; k++) {
+      if (m->b[t[k]] != i) continue;
+      if (in_end[k] > now) { stall += in_end[k] - now; now = in_end[k]; }
+    }
+    now += tau; /* op i */
+    /* after op i: swap-outs of a = i, then releases of r = i */
+    for (int32_t k = 0; k < n_items; k++) {
+      if (m->a[t[k]] != i) continue;
+      double start = now;
+      if (d2h_free > start) start = d2h_free;
+      out_end[k] = start + (double)m->S[t[k]] / m->bw;
+      d2h_free = out_end[k];
+    }
+    for (int32_t k = 0; k < n_items; k++) {
+      if (r[k] != i) continue;
+      if (out_end[k] > now) { stall += out_end[k] - now; now = out_end[k]; }
+    }
+  }
+  free(out_end); free(in_end);
+  return stall;
+}
+
 /* Fig. 3: actual usage = measured usage + bytes swapped out and not yet back */
 void orc_reconstruct(int32_t n_ops, const int64_t *measured, int32_t n_items, const int64_t *size,
                      const int32_t *r, const int32_t *s, int64_t *actual) {

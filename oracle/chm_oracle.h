@@ -63,6 +63,19 @@ int64_t orc_replay(const orc_model *m, int32_t n_items, const int32_t *t, const 
                    const int32_t *s, int64_t *footprint, int64_t *d2h, int64_t *h2d);
 double orc_stall(const orc_model *m, int32_t n_items, const int32_t *t, const int32_t *r,
                  const int32_t *s);
+/* Stall-model variants of reading Q11, same items:
+ *  orc_stall_dir: per-direction budgets -- each layer's swap-out and swap-in loads are charged
+ *    against Bud_l separately (a full-duplex link): pairwise sum over l of
+ *    max(0, out_l/B - Bud_l) + max(0, in_l/B - Bud_l), out_l at lay(r), in_l at lay(s).
+ *  orc_stall_timeline: max-plus serial-stream timeline -- ops take T_iter/N each; a swap-out
+ *    enters the D2H FIFO after op a_t, a swap-in the H2D FIFO before op s_t (not before its
+ *    swap-out ended); compute waits for the swap-out after op r_t (release) and for the swap-in
+ *    before op b_t.  Returns the total wait, events handled in op order (after op i: swap-outs,
+ *    releases; before op i+1: swap-ins, waits; item order within a kind). */
+double orc_stall_dir(const orc_model *m, int32_t n_items, const int32_t *t, const int32_t *r,
+                     const int32_t *s);
+double orc_stall_timeline(const orc_model *m, int32_t n_items, const int32_t *t, const int32_t *r,
+                          const int32_t *s);
 
 /* Fig. 3 reconstruction: measured[i] + bytes that are off device at op i */
 void orc_reconstruct(int32_t n_ops, const int64_t *measured, int32_t n_items,

@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libchm.so")
-SOURCES = ["core.cpp", "trace.cpp", "executor.cpp", "generator.cpp", "oom.cpp", "trace_io.cpp", "swap.cu", "replay.cu", "explicit.cu"]
+SOURCES = ["core.cpp", "trace.cpp", "executor.cpp", "generator.cpp", "oom.cpp", "trace_io.cpp", "stall.cpp", "swap.cu", "replay.cu", "explicit.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -125,6 +125,7 @@ EXPORTS = [
     "chm_policy_install", "chm_policy_install_items", "chm_generate_policy", "chm_exec_stats_get", "chm_host_arena", "chm_swap_out", "chm_swap_in",
     "chm_batch_wait", "chm_batch_query", "chm_batch_elapsed", "chm_arena_reserve", "chm_issue_swap_out", "chm_issue_swap_in", "chm_item_wait",
     "chm_oom_release", "chm_passive_swap", "chm_passive_restore", "chm_trace_load", "chm_record_save",
+    "chm_stall_models",
 ]
 
 _lib = None
@@ -176,6 +177,7 @@ def load(path: str = LIB_PATH):
         "chm_oom_release": (i32, [vp, vp, vp, u32, P(u32)]),
         "chm_trace_load": (i32, [vp, C.c_char_p, C.c_size_t, P(TraceParams), P(vp), P(i64)]),
         "chm_record_save": (i32, [vp, vp, C.c_size_t, P(C.c_size_t)]),
+        "chm_stall_models": (i32, [vp, vp, u32, vp]),
         "chm_passive_swap": (i32, [vp, i64, vp, u32, vp, u32, vp, vp, P(Passive)]),
         "chm_passive_restore": (i32, [vp, u64, u64, vp, vp]),
     }
@@ -243,6 +245,23 @@ class Trace:
         _check(load().chm_generate_policy(self.h, C.byref(GenParams(C_coef, rem_scale)), out.ctypes.data, cap,
                                           C.byref(n), C.byref(feas)))
         return out[:n.value], bool(feas.value)
+
+    def stall_models(self, items) -> np.ndarray:
+        """[R-stall, per-direction budgets, serial-stream timeline] of one item list (host)"""
+        its = np.ascontiguousarray(items, ITEM_DTYPE)
+        out = np.zeros(3, np.float64)
+        _check(load().chm_stall_models(self.h, _ptr(its) if its.size else None, int(its.size), _ptr(out)))
+        return out
+
+    def mask_items(self, words) -> np.ndarray:
+        """the item list {t, r, s} (solo timing) of a mask over the swappable set"""
+        tb = self.tables()
+        ks = [k for k in range(self.K) if (int(words[k // 64]) >> (k % 64)) & 1]
+        its = np.zeros(len(ks), ITEM_DTYPE)
+        its["t"] = tb["tensor"][ks]
+        its["r"] = tb["r"][ks]
+        its["s"] = tb["s"][ks]
+        return its
 
     def candidate_mask(self, kind: int, index: int, seed: int = 0, flip_thr: int = 0,
                        base: Optional[np.ndarray] = None) -> np.ndarray:

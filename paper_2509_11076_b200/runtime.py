@@ -158,6 +158,7 @@ class Runtime:
         self.record_log = False  # per-op log of the next steps (tests)
         self.log = []
         self.policy = None  # (trace, description)
+        self.policy_items = None  # installed item list {t, r, s}
         self.plans = []
         self.stats = dict(steps=0, ops=0, swap_out=0, release=0, released_bytes=0, swap_in=0, demand_swap_in=0,
                           unheld=0, plan_ms=0.0, oom=0, oom_released=0, passive=0, passive_bytes=0, passive_restored=0)
@@ -570,12 +571,12 @@ class Runtime:
             if name == "generator":
                 self._reserve_items(sel, pt)
                 self.ctx.policy_install_items(pt, sel)
-                plan.update(items=len(sel), tensors=[int(x) for x in sel["t"]])
+                self.policy_items = np.array(sel, chm.ITEM_DTYPE)
             else:
                 self._reserve_words(sel, pt)
                 self.ctx.policy_install(pt, sel)
-                ks = [q for q in range(pt.K) if (int(sel[q // 64]) >> (q % 64)) & 1]
-                plan.update(items=len(ks), tensors=[int(x) for x in pt.tables()["tensor"][ks]])
+                self.policy_items = pt.mask_items(sel)
+            plan.update(items=len(self.policy_items), tensors=[int(x) for x in self.policy_items["t"]])
             plan["install_ms"] = (time.perf_counter() - t1) * 1e3  # includes pinning arena growth
             self.policy = (pt, plan)
         plan["plan_ms"] = (time.perf_counter() - t0) * 1e3

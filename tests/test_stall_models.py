@@ -1,0 +1,125 @@
+"""Stall-model variants of reading Q11: per-direction layer budgets and the
+max-plus serial-stream timeline.  The oracle is pinned against closed forms derived by hand
+(one item: the copy time beyond its slack on each side; two items in one FIFO: their summed copy
+time beyond the shared slack), against invariants (per-direction <= one shared budget; a slower
+link never stalls less; an infinitely fast link never stalls), then the product's host
+evaluation (`chm_stall_models`) must equal the oracle bit for bit, and its R-stall entry must
+equal the replay kernels' model (the oracle's orc_stall)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2509_11076_b200 import chm
+from tests.helpers import make_trace
+from workloads import traces as W
+
+TAU = 1e-3  # op time T_iter / N of the hand traces
+
+
+def _hand(sizes, r=2, s=6):
+    """10 ops, 5 FWD + 5 BWD; every listed tensor is produced by op 0, used by op 1 (a = 1) and
+    op 8 (b = 8), freed at op 8; items released after r, swapped in before s"""
+    n = 10
+    T = len(sizes)
+    ins = [[] for _ in range(n)]
+    outs = [[] for _ in range(n)]
+    frees = [[] for _ in range(n)]
+    outs[0] = list(range(T))
+    ins[1] = list(range(T))
+    ins[8] = list(range(T))
+    frees[8] = list(range(T))
+    tr = make_trace([0] * 5 + [1] * 5, sizes, ins, outs, frees, 0, TAU * n, 1e9, 1 << 40, 5, 5)
+    m = O.Model(tr)
+    return tr, m, list(range(T)), [r] * T, [s] * T
+
+
+def test_timeline_single_item_closed_form():
+    # S / B = 2.5 tau: slack (r - a) tau = 1 tau on the way out, (b - s) tau = 2 tau on the way in
+    tr, m, t, r, s = _hand([int(2.5 * TAU * 1e9)])
+    exp = max(0.0, 2.5 * TAU - (2 - 1) * TAU) + max(0.0, 2.5 * TAU - (8 - 6) * TAU)
+    assert m.stall_timeline(t, r, s) == pytest.approx(exp, rel=1e-12)
+    # enough slack on both sides: no stall
+    tr, m, t, r, s = _hand([int(0.5 * TAU * 1e9)], r=3, s=6)
+    assert m.stall_timeline(t, r, s) == 0.0
+
+
+def test_timeline_fifo_two_items_closed_form():
+    # two 1.5 tau copies queue on each direction: (S1 + S2)/B beyond the shared slack
+    tr, m, t, r, s = _hand([int(1.5 * TAU * 1e9)] * 2)
+    exp = max(0.0, 3.0 * TAU - 1 * TAU) + max(0.0, 3.0 * TAU - 2 * TAU)
+    assert m.stall_timeline(t, r, s) == pytest.approx(exp, rel=1e-12)
+
+
+def _random_items(m, rng, n_max=None):
+    sw = m.swappable()
+    if m.K == 0:
+        return [], [], []
+    k = rng.choice(m.K, size=rng.integers(1, (n_max or m.K) + 1) if m.K > 1 else 1, replace=False)
+    return sw["t"][k], sw["r"][k], sw["s"][k]
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_invariants_on_random_traces(seed):
+    rng = np.random.default_rng(seed)
+    tr = W.random_trace(seed, bw=rng.uniform(2e8, 2e9), t_iter=rng.uniform(1e-4, 1e-2))
+    m = O.Model(tr)
+    t, r, s = _random_items(m, rng)
+    if len(t) == 0:
+        return
+    lay, dirs, tl = m.stall(t, r, s), m.stall_dir(t, r, s), m.stall_timeline(t, r, s)
+    assert 0.0 <= dirs <= lay + 1e-15  # two budgets per layer never stall more than one
+    assert tl >= 0.0
+    slow = O.Model(tr, bw=tr.bw / 2)
+    assert slow.stall(t, r, s) >= lay and slow.stall_dir(t, r, s) >= dirs
+    assert slow.stall_timeline(t, r, s) >= tl
+    fast = O.Model(tr, bw=1e30)
+    assert fast.stall(t, r, s) == fast.stall_dir(t, r, s) == fast.stall_timeline(t, r, s) == 0.0
+    # the timeline never waits longer than the copies themselves take
+    assert tl <= 2 * float(tr.nbytes[t].sum()) / tr.bw * (1 + 1e-12)
+
+
+def _product(tr):
+    ctx = chm.Context(device=-1)
+    ctx.set_detailed(True)
+    chm.record_iteration(ctx, tr)
+    ctx.detect_seq_change(tr.t_iter)
+    return ctx, ctx.trace_build(tr.budget, tr.static_bytes, tr.bw, tr.groups_fwd, tr.groups_bwd, t_iter=tr.t_iter,
+                                omega=tr.omega)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C5"])
+def test_product_equals_oracle_on_masks_and_generator_items(name):
+    tr = W.CONFIGS[name]()
+    m = O.Model(tr)
+    ctx, pt = _product(tr)
+    sw = m.swappable()
+    rng = np.random.default_rng(7)
+    for trial in range(6):
+        bits = rng.random(pt.K) < (0.1 + 0.15 * trial)
+        words = np.zeros(max(pt.W, 1), np.uint64)
+        for k in np.nonzero(bits)[0]:
+            words[k // 64] |= np.uint64(1 << int(k % 64))
+        got = pt.stall_models(pt.mask_items(words[:pt.W]))
+        t, r, s = sw["t"][bits], sw["r"][bits], sw["s"][bits]
+        exp = [m.stall(t, r, s), m.stall_dir(t, r, s), m.stall_timeline(t, r, s)]
+        assert got.tolist() == exp, (trial, got, exp)
+    for cc in (0.0, 1.0):
+        items, _ = pt.generate_policy(cc, 1.0)
+        if len(items) == 0:
+            continue
+        got = pt.stall_models(items)
+        p, f, a, b = m.tensor_table()
+        # production rank == trace tensor index for the synthetic traces
+        t, r, s = items["t"].astype(np.int32), items["r"], items["s"]
+        exp = [m.stall(t, r, s), m.stall_dir(t, r, s), m.stall_timeline(t, r, s)]
+        assert got.tolist() == exp
+
+
+def test_product_validates_items():
+    tr = W.tiny()
+    ctx, pt = _product(tr)
+    bad = np.zeros(1, chm.ITEM_DTYPE)
+    bad["t"] = 10 ** 6
+    with pytest.raises(chm.ChmError):
+        pt.stall_models(bad)
+    assert pt.stall_models(np.zeros(0, chm.ITEM_DTYPE)).tolist() == [0.0, 0.0, 0.0]

@@ -16,6 +16,7 @@ import os
 import sys
 import time
 
+import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -73,6 +74,7 @@ def main():
         rt.request_replan(m0 + int(frac * act_peak))
         one(rt)
         plan = rt.plans[-1]
+        models = rt.policy[0].stall_models(rt.policy_items) if rt.policy is not None else np.zeros(3)
         meas = [one(rt) for _ in range(args.steps)]
         t_pol = sorted(t for t, _ in meas)[len(meas) // 2]
         peak = max(p for _, p in meas) + m0
@@ -81,6 +83,8 @@ def main():
                          predicted_peak_gib=round(plan.get("peak", plan["peak0"]) / 2 ** 30, 3),
                          measured_peak_gib=round(peak / 2 ** 30, 3), excess_gib=round(plan.get("excess", 0) / 2 ** 30, 3),
                          predicted_stall_s=round(plan.get("stall", 0.0), 4), t_iter_s=round(plan["t_iter"], 4),
+                         stall_layer_s=round(float(models[0]), 4), stall_per_direction_s=round(float(models[1]), 4),
+                         stall_timeline_s=round(float(models[2]), 4),
                          step_s=round(t_pol, 4), measured_overhead_s=round(t_pol - t_np, 4), plan_ms=round(plan["plan_ms"], 1)))
     out = dict(flags=args.flags, swap_ctas=args.swap_ctas or 8, model="llama2-7b" if args.layers == 32 else f"llama2-7b-{args.layers}L", dtype="bf16", batch=args.batch,
                seq=args.seq, m0_gib=round(m0 / 2 ** 30, 3), no_swap_peak_gib=round((m0 + act_peak) / 2 ** 30, 3),
