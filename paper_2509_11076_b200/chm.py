@@ -47,6 +47,50 @@ class OpRecord(C.Structure):
                 ("freed", C.POINTER(C.c_uint64)), ("live_bytes", C.c_int64)]
 
 
+TENSOR_REF_DTYPE = np.dtype([("id", np.uint64), ("nbytes", np.int64), ("dtype", np.uint8)], align=True)
+
+
+class Recorder:
+    """chm_record_op with preallocated argument buffers: the per-op path of a framework hook
+    (one ctypes call, no per-op ctypes objects)."""
+
+    def __init__(self, ctx: "Context", cap: int = 64):
+        self.ctx = ctx
+        self._fn = load().chm_record_op
+        self.rec = OpRecord()
+        self.act = Actions()
+        self._rec_p = C.byref(self.rec)
+        self._act_p = C.byref(self.act)
+        self._alloc(cap)
+
+    def _alloc(self, cap: int):
+        self.cap = cap
+        self.ins = np.zeros(cap, TENSOR_REF_DTYPE)
+        self.outs = np.zeros(cap, TENSOR_REF_DTYPE)
+        self.freed = np.zeros(cap, np.uint64)
+        self.rec.in_ = C.cast(self.ins.ctypes.data, C.POINTER(TensorRef))
+        self.rec.out = C.cast(self.outs.ctypes.data, C.POINTER(TensorRef))
+        self.rec.freed = C.cast(self.freed.ctypes.data, C.POINTER(C.c_uint64))
+
+    def record(self, token: int, phase: int, ins=(), outs=(), freed=(), live_bytes: int = -1) -> "Actions":
+        """ins / outs: sequences of (id, nbytes, dtype) tuples"""
+        ni, no, nf = len(ins), len(outs), len(freed)
+        if max(ni, no, nf) > self.cap:
+            self._alloc(2 * max(ni, no, nf))
+        r = self.rec
+        if ni:
+            self.ins[:ni] = ins
+        if no:
+            self.outs[:no] = outs
+        if nf:
+            self.freed[:nf] = freed
+        r.token, r.phase, r.n_in, r.n_out, r.n_free, r.live_bytes = token, phase, ni, no, nf, live_bytes
+        rc = self._fn(self.ctx.h, self._rec_p, self._act_p)
+        if rc != CHM_OK:
+            _check(rc)
+        return self.act
+
+
 class SwapDesc(C.Structure):
     _fields_ = [("dev", C.c_uint64), ("host_off", C.c_uint64), ("nbytes", C.c_uint64)]
 

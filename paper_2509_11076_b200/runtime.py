@@ -44,7 +44,6 @@ from typing import Optional
 import numpy as np
 import torch
 from torch.utils._python_dispatch import TorchDispatchMode
-from torch.utils._pytree import tree_flatten
 
 from . import chm
 
@@ -86,6 +85,18 @@ class _Box:
         self.offset = t.storage_offset()
 
 
+def _collect(x, out):
+    """the tensors of an op's (nested) arguments or results, in order"""
+    if isinstance(x, torch.Tensor):
+        out.append(x)
+    elif isinstance(x, (list, tuple)):
+        for y in x:
+            _collect(y, out)
+    elif isinstance(x, dict):
+        for y in x.values():
+            _collect(y, out)
+
+
 def _requested_bytes(e) -> int:
     """the failed request's size from PyTorch's OOM message (1 MiB if it cannot be read)"""
     m = re.search(r"Tried to allocate ([0-9.]+) (GiB|MiB|KiB|bytes)", str(e))
@@ -110,7 +121,9 @@ class _Mode(TorchDispatchMode):
                 out = func(*args, **kwargs)
                 break
             except torch.OutOfMemoryError as e:  # Algo. 3: make room, then retry the op
-                if not rt._oom(_requested_bytes(e), tree_flatten((args, kwargs))[0]):
+                busy = []
+                _collect((args, kwargs), busy)
+                if not rt._oom(_requested_bytes(e), busy):
                     raise
         rt._stage(func, args, kwargs, out)
         return out
@@ -137,6 +150,9 @@ class Runtime:
                                max(int(host_arena_bytes) + int(oom_host_bytes), 1 << 20),
                                **algo1)
         self.search_rounds = int(search_rounds)
+        self._detect_bytes = bool(algo1.get("detect_bytes", 0))  # Q4 needs every op's outputs
+        self.rec = chm.Recorder(self.ctx)
+        self.light = False
         self.oom_host_bytes = int(oom_host_bytes)  # arena room for passive swaps (0: OOMs propagate)
         # AUTO (default): tensors >= 4 MiB on the copy engines, which take no SMs from the step's
         # compute (tools/stall_fidelity.py measured 10% shorter Llama-2 7B steps than with the
@@ -200,6 +216,9 @@ class Runtime:
         self.detailed = (self.stage == chm.GENPOLICY and self.need_plan) or self.force_plan
         if self.force_plan:
             self.ctx.set_detailed(True)
+        # nothing to execute, record or fall back on: tokens only, autograd saves as usual
+        self.light = (self.policy is None and not self.detailed and not self.oom_host_bytes
+                      and not self.record_log and not self._detect_bytes)
         self.produced = set()  # storage addresses created by ops of this step
         self.holders = weakref.WeakValueDictionary()  # address -> _Holder (owned by autograd's boxes)
         self.pending = None    # (token, phase, ins, outs, live_bytes) of the last op
@@ -278,11 +297,6 @@ class Runtime:
 
     def _stage(self, func, args, kwargs, out):
         """called after op dispatch: stash the op's record (sent when the next op arrives)"""
-        flat_in, _ = tree_flatten((args, kwargs))
-        flat_out, _ = tree_flatten(out)
-        ins = self._storages(flat_in)
-        in_ptrs = {p for p, _, _, _ in ins}
-        outs = [o for o in self._storages(flat_out) if o[0] not in in_ptrs]
         gt = torch._C._current_graph_task_id()
         if gt != -1:
             phase = chm.BWD
@@ -293,6 +307,16 @@ class Runtime:
         # recorded in the later phase, so only tensors of the first forward are swap candidates
         phase = max(phase, self.last_phase)
         self.last_phase = phase
+        if self.light:  # Lightweight mode, nothing installed: the token is the whole record
+            self.pending = (self._token(func), phase, (), (), -1)
+            return
+        flat_in, flat_out = [], []
+        _collect(args, flat_in)
+        _collect(kwargs, flat_in)
+        _collect(out, flat_out)
+        ins = self._storages(flat_in)
+        in_ptrs = {p for p, _, _, _ in ins}
+        outs = [o for o in self._storages(flat_out) if o[0] not in in_ptrs]
         live = -1
         if self.detailed:
             live = torch.cuda.memory_allocated(self.dev) if not self.host_only else 0
@@ -318,8 +342,11 @@ class Runtime:
             for p in dead:
                 torch.UntypedStorage._free_weak_ref(self.weak.pop(p))
             freed = dead
-        act = self.ctx.record_op(tok, phase, ins, outs, freed, live_bytes=live)
-        av = chm.actions_view(act) if self.policy is not None else None
+        act = self.rec.record(tok, phase, ins, outs, freed, live)
+        av = None
+        if self.policy is not None and (act.n_swap_out or act.n_release or act.n_swap_in or act.n_wait
+                                        or self.record_log):
+            av = chm.actions_view(act)
         if self.record_log:
             self.log.append(dict(op=self.n_ops, token=tok, phase=phase, ins=[x[0] for x in ins],
                                  outs=[x[0] for x in outs], actions=av))
@@ -329,7 +356,7 @@ class Runtime:
 
     # ------------------------------------------------------------------ autograd boxes
     def _pack(self, t):
-        if not isinstance(t, torch.Tensor) or t.device != self.dev or t.is_sparse:
+        if self.light or not isinstance(t, torch.Tensor) or t.device != self.dev or t.is_sparse:
             return t
         try:
             st = t.untyped_storage()
