@@ -180,6 +180,24 @@ def test_c2_bench_size_full_compare(ctx):
         assert np.array_equal(full["footprint"][c], one["footprint"][0])
 
 
+@pytest.mark.parametrize("name", ["C3", "C4a", "C4b", "C5"])
+def test_full_size_configs_all_keys_sampled_rows(ctx, name):
+    """BASELINE configs C3-C5 at full size: 10^5 SEEDED candidates (the bench's launch), every
+    key vs the oracle, footprint rows on a sample computed one by one"""
+    tr = W.CONFIGS[name]()
+    pt = product_trace(ctx, tr)
+    m = O.Model(tr)
+    sd = W.SEEDED[name[:2]]
+    n = 100_000
+    full = run_eval(ctx, pt, chm.SEEDED, 0, n, footprint=True, seed=sd["seed"], flip_thr=sd["flip_thr"])
+    ref = m.eval(O.SEEDED, 0, n, seed=sd["seed"], flip_thr=sd["flip_thr"], nthreads=16)
+    assert_same(dict(full, footprint=None), ref, tr.budget)
+    rng = np.random.default_rng(1)
+    for c in rng.choice(n, size=24, replace=False):
+        one = m.eval(O.SEEDED, int(c), 1, seed=sd["seed"], flip_thr=sd["flip_thr"], footprint=True)
+        assert np.array_equal(full["footprint"][c], one["footprint"][0])
+
+
 def test_candidate_mask_matches_oracle_decode(ctx):
     tr = W.tiny()
     pt = product_trace(ctx, tr)
