@@ -1,25 +1,27 @@
-// replay.cu -- policy evaluation (steps a4-a7): one candidate per CTA of a persistent grid.
+// replay.cu -- policy evaluation (steps a4-a7): one candidate per warp of a persistent grid.
 //
 // For candidate P (§5.4 simulator; readings SURVEY §8(c).2-.6) the event
 // replay gives F_P[i] = F0[i] - sum_{t in P} S_t [r_t < i < s_t].  With the solo timing of the
 // trace build every release r_t is the LAST op of layer lout_t ("completed within that
 // layer", reading Q6) and every swap-in s_t the FIRST op of layer lin_t (Q7), so the
-// offset is constant over each logical layer l:
+// offset is constant over each logical layer l (reading R-window):
 //   in_l  = sum_{t in P, lin_t = l} S_t,   out_l = sum_{t in P, lout_t = l} S_t
 //   D_l   = sum_{l' <= l} in_l' - sum_{l' < l} out_l'          (exact int64)
 //   F_P[i] = F0[i] + D_lay(i),   peak = max_l (max_{i in l} F0[i] + D_l)
-//   load_l = in_l + out_l,       stall = sum_l max(0, load_l / B - Bud_l), ascending l
-// -- the same integers as the event replay, in O(K + L) per candidate (+ O(N) to write the
-// footprint row in full mode).  Not a contraction: no tensor cores.  Full mode is bound by
-// the 8 B/op footprint write to HBM; search mode by the SEEDED hash decode (integer pipe).
+//   load_l = in_l + out_l,       stall = pairwise sum of max(0, load_l / B - Bud_l)  (R-stall)
+// -- the same integers as the event replay, in O(#flips + L) per candidate (+ O(N) to write the
+// footprint row in full mode).  Not a contraction: no tensor cores.  Full mode is bound by the
+// 8 B/op footprint write to HBM; search mode by the SEEDED hash decode and the layer scans.
 //
-// Per CTA: the trace image (layer maxima, budgets, sizes, lout/lin-sorted orders, F0, op->layer)
-// is staged once into shared memory by TMA bulk copies (cp.async.bulk + mbarrier).  Per
-// candidate: decode the mask (ballot), per-layer sums over the lout- and lin-sorted orders
-// (each thread a contiguous run, one shared atomic per run segment), warp 0 scans the L layer
-// offsets and forms peak / stall / key, then (full mode) all threads stream F0 + D_lay out with
-// 16 B streaming stores.  Stall terms are summed by one lane in ascending layer order with IEEE
-// div/sub/add intrinsics: bit-identical to the oracle's sequential loop.
+// Per CTA (512 threads, 2 per SM): the trace image (layer maxima, budgets, sizes, lout/lin, F0 in
+// int32 units or int64, op -> layer) is staged once into shared memory by TMA bulk copies
+// (cp.async.bulk + mbarrier), and the layer sums of a reference mask R (the SEEDED base) are
+// built once.  Per candidate (one warp, handed out by a global atomic counter): the items whose
+// bit differs from R add signed deltas to per-layer hi/lo 32-bit shared accumulators (exact),
+// warp scans over 32-layer chunks give D_l, the peak and the stall terms (xor-butterfly pairwise
+// tree with IEEE _rn intrinsics: bit-identical to the oracle), lane 0 writes peak / stall /
+// swapped and keeps the warp's best key; in full mode the warp streams F0 + D_lay out with 16 B
+// streaming stores.  Keys: warp -> CTA -> the last CTA to finish reduces (ticket).
 #include <algorithm>
 #include <climits>
 #include <cstring>
