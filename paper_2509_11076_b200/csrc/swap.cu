@@ -5,8 +5,9 @@
 // Kernel design (sm_100a, host-link bound, see DESIGN.md §"Swap kernel"): the descriptor list
 // travels in kernel parameter space (<= 64 descriptors + chunk prefix, ~2 KB); the bytes are cut
 // into 64 KiB chunks; each 512-thread CTA copies one chunk per grid-stride step with 8
-// independent 16 B loads per thread issued before the 8 stores (64 KiB in flight per CTA), so
-// a few dozen CTAs keep > 1 MB of PCIe reads in flight for swap-in.  Loads use the
+// independent 16 B loads per thread issued before the 8 stores (64 KiB in flight per CTA); the
+// default 8 CTAs (512 KiB in flight) already fill the host link and leave the other SMs to the
+// overlapped compute (tools/overlap.py, tools/stall_fidelity.py).  Loads use the
 // non-coherent path without L1 allocation; stores to HBM are streaming (.cs) so an overlapped
 // compute kernel keeps its L2.
 #include <algorithm>
