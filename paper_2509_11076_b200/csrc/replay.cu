@@ -68,6 +68,7 @@ struct EvalParams {
   long long *footprint;
   uint64_t ld;
   int row_pairs;  // 16 B stores per footprint row (ceil(N / 2))
+  int lay_per_lane;  // E: layers per lane, next power of two >= L over 32 (1 .. 8)
   Key *partial;
   unsigned int *ticket;
   unsigned long long *work;  // candidate counter for dynamic distribution
@@ -238,48 +239,62 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
       }
     }
     __syncwarp();
-    // layer l: in_l / out_l = R sums + deltas; CI / CO cumulative; D_l = CI(l) - CO(l) + out_l;
-    // term_l = max(0, (in_l + out_l) / B - Bud_l), pairwise tree (reading R-stall)
-    // D_l = D_R(l) + sum_{l' <= l} (din_l' - dout_{l'-1}) with D_R(l) = CIR(l) - COR(l) + OUTR(l):
-    // one warp scan per 32-layer chunk; load_l = in_l + out_l per layer
-    long long pk = LLONG_MIN, carry = 0, prev_dout = 0, swd = 0;
-    double cs[8];
-#pragma unroll
-    for (int j = 0; j < 8; j++) {
-      cs[j] = 0.0;
-      if (32 * j < L) {
-        const int l = lane + 32 * j;
-        long long din = 0, dout = 0;
-        if (l < L) {
-          din = split_sum(dI_hi[l], dI_lo[l]);
-          dout = split_sum(dO_hi[l], dO_lo[l]);
-          dI_hi[l] = 0u; dI_lo[l] = 0u; dO_hi[l] = 0u; dO_lo[l] = 0u;  // ready for the next candidate
-        }
-        const long long up = __shfl_up_sync(0xffffffffu, dout, 1);
-        long long e = din - (lane == 0 ? prev_dout : up);
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const long long y = __shfl_up_sync(0xffffffffu, e, o);
-          if (lane >= o) e += y;
-        }
-        double t = 0.0;
-        if (l < L) {
-          const long long d = s_DR[l] + carry + e;
-          if (kFull) s_D[l] = d;
-          pk = max(pk, mf0[l] + d);
-          const double x = __dsub_rn(__ddiv_rn(double(s_INR[l] + din + s_OUTR[l] + dout), p.tr.bw), bud[l]);
-          t = x > 0.0 ? x : 0.0;
-        }
-        swd += dout;
-        carry += __shfl_sync(0xffffffffu, e, 31);
-        prev_dout = __shfl_sync(0xffffffffu, dout, 31);
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) t = __dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, o));
-        cs[j] = t;
+    // layer l: in_l / out_l = R sums + deltas; D_l = CI(l) - CO(l) + out_l (CI / CO cumulative)
+    //   = D_R(l) + sum_{l' <= l} (din_l' - dout_{l'-1}),  D_R(l) = CIR(l) - COR(l) + OUTR(l);
+    // term_l = max(0, (in_l + out_l) / B - Bud_l), pairwise tree (reading R-stall).
+    // Blocked layers: lane owns E = lay_per_lane (1, 2, 4 or 8) consecutive layers E*lane + j;
+    // its partial sum, one warp scan of the lane totals, then D, peak and the terms per layer.
+    // The tree: 8 leaves per lane (zero past E), then the xor butterfly = the pairwise tree over
+    // 256 zero-padded leaves, whose value equals R-stall's tree over the next power of two >= L.
+    const int E = p.lay_per_lane, lb = E * lane;
+    long long tot = 0, lastd = 0;
+    for (int j = 0; j < E; j++) {
+      const int l = lb + j;
+      if (l < L) {
+        const long long din = split_sum(dI_hi[l], dI_lo[l]), dout = split_sum(dO_hi[l], dO_lo[l]);
+        tot += din - (j ? lastd : 0);
+        lastd = dout;
       }
     }
-    const double st = __dadd_rn(__dadd_rn(__dadd_rn(cs[0], cs[1]), __dadd_rn(cs[2], cs[3])),
-                                __dadd_rn(__dadd_rn(cs[4], cs[5]), __dadd_rn(cs[6], cs[7])));
+    const long long prev_last = __shfl_up_sync(0xffffffffu, lastd, 1);
+    tot -= lane ? prev_last : 0;
+    long long inc = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    long long run = inc - tot, pk = LLONG_MIN, swd = 0, prevd = lane ? prev_last : 0;
+    double ta = 0.0, tb = 0.0, tc = 0.0, td = 0.0;  // the lane's 8-leaf tree, folded as it grows
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      double tj = 0.0;
+      const int l = lb + j;
+      if (j < E && l < L) {
+        const long long din = split_sum(dI_hi[l], dI_lo[l]), dout = split_sum(dO_hi[l], dO_lo[l]);
+        dI_hi[l] = 0u; dI_lo[l] = 0u; dO_hi[l] = 0u; dO_lo[l] = 0u;  // ready for the next candidate
+        run += din - prevd;
+        prevd = dout;
+        const long long d = s_DR[l] + run;
+        if (kFull) s_D[l] = d;
+        pk = max(pk, mf0[l] + d);
+        const double x = __dsub_rn(__ddiv_rn(double(s_INR[l] + din + s_OUTR[l] + dout), p.tr.bw), bud[l]);
+        tj = x > 0.0 ? x : 0.0;
+        swd += dout;
+      }
+      // ((t0 + t1) + (t2 + t3)) + ((t4 + t5) + (t6 + t7))
+      if (j == 0) ta = tj;
+      else if (j == 1) ta = __dadd_rn(ta, tj);
+      else if (j == 2) tb = tj;
+      else if (j == 3) ta = __dadd_rn(ta, __dadd_rn(tb, tj));
+      else if (j == 4) tc = tj;
+      else if (j == 5) tc = __dadd_rn(tc, tj);
+      else if (j == 6) td = tj;
+      else ta = __dadd_rn(ta, __dadd_rn(tc, __dadd_rn(td, tj)));
+    }
+    double st = ta;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) st = __dadd_rn(st, __shfl_xor_sync(0xffffffffu, st, o));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       pk = max(pk, __shfl_xor_sync(0xffffffffu, pk, o));
@@ -433,6 +448,11 @@ chm_status launch_eval(chm_ctx *ctx, const EvalLaunch &L, cudaStream_t stream) {
   p.stage_bytes = stage;
   p.warp_scratch = wscr16;
   p.row_pairs = (N + 1) / 2;
+  {
+    int P2 = 32;
+    while (P2 < Ly) P2 *= 2;
+    p.lay_per_lane = P2 / 32;
+  }
   p.first = L.first;
   p.count = L.count;
   p.seed = L.seed;
