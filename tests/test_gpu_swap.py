@@ -58,6 +58,12 @@ def test_round_trip_sizes_and_alignments(ctx, flags):
     host = arena_view(ctx)
     for src, ho in zip(srcs, host_offs):
         assert np.array_equal(host[ho:ho + src.numel()], src.cpu().numpy())
+    # the whole written arena range against the oracle's swap definition (memcpy per descriptor)
+    exp = np.zeros(off, np.uint8)
+    exp[:] = host[:off]  # bytes between descriptors are not written by either side
+    src_host = [src.cpu().numpy() for src in srcs]
+    O.swap_execute([exp.ctypes.data + ho for ho in host_offs], [a.ctypes.data for a in src_host], sizes)
+    assert np.array_equal(host[:off], exp)
     dst = [torch.zeros(n + 32, dtype=torch.uint8, device="cuda") for n in sizes]
     in_descs = [(d[do:do + n].data_ptr(), ho, n) for d, n, do, ho in zip(dst, sizes, dev_offs, host_offs)]
     b_in = ctx.swap_in(in_descs, comp, s, flags)

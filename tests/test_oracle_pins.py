@@ -1,6 +1,5 @@
 """Pins of the CPU oracle against values fixed by the paper, hand derivations, brute force
 and invariants (not against itself).  -m "not gpu"."""
-import itertools
 import math
 
 import numpy as np

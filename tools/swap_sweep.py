@@ -1,7 +1,6 @@
 """Swap kernel sweep on one GPU: variant x CTAs, D2H and H2D GB/s for a 1 GiB batch of 64
 tensors (and a mixed-size batch), against per-tensor cudaMemcpyAsync on the copy engines.
 Byte-exactness of every variant is checked on the first run.  Writes gpurun_out/swap_sweep.json."""
-import ctypes
 import json
 import os
 import sys
