@@ -35,7 +35,9 @@ on CPU tensors (no copies): the CPU tests use it.
 """
 from __future__ import annotations
 
+import concurrent.futures
 import contextlib
+import os
 import re
 import time
 import weakref
@@ -95,6 +97,15 @@ def _collect(x, out):
     elif isinstance(x, dict):
         for y in x.values():
             _collect(y, out)
+
+
+def _generate_all(pt):
+    """Algo. 2's "best of n" grid (C x T_remaining scale, reading R-gen), one host thread per
+    variant (the generator only reads the trace; ctypes drops the GIL): non-empty item lists"""
+    grid = [(cc, rr) for cc in (0.0, 1.0, 2.0) for rr in (0.5, 1.0, 2.0)]
+    with concurrent.futures.ThreadPoolExecutor(max_workers=min(len(grid), os.cpu_count() or 1)) as ex:
+        lists = list(ex.map(lambda a: pt.generate_policy(*a)[0], grid))
+    return [g for g in lists if len(g)]
 
 
 def _requested_bytes(e) -> int:
@@ -553,8 +564,7 @@ class Runtime:
             self.policy = None
             self.ctx.policy_install(pt, np.zeros(max(pt.W, 1), np.uint64)[:pt.W])
         elif self.host_only:  # the generator's first plan: no device to score it
-            gen = [g for g in (pt.generate_policy(cc, rr)[0] for cc in (0.0, 1.0, 2.0) for rr in (0.5, 1.0, 2.0))
-                   if len(g)]
+            gen = _generate_all(pt)
             items = gen[0] if gen else np.zeros(0, chm.ITEM_DTYPE)
             self.ctx.policy_install_items(pt, items)
             plan.update(kind="generator-host", items=len(items), tensors=[int(x) for x in items["t"]])
@@ -574,8 +584,7 @@ class Runtime:
             t1 = time.perf_counter()
             gen = []
             if self.use_generator:
-                gen = [g for g in (pt.generate_policy(cc, rr)[0] for cc in (0.0, 1.0, 2.0) for rr in (0.5, 1.0, 2.0))
-                       if len(g)]
+                gen = _generate_all(pt)
             if gen:
                 off = np.zeros(len(gen) + 1, np.uint64)
                 off[1:] = np.cumsum([len(x) for x in gen])
