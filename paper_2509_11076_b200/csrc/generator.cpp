@@ -37,16 +37,32 @@ extern "C" chm_status chm_generate_policy(const chm_trace *tr, const chm_gen_par
   const int32_t N = tr->N, L = tr->L;
   const std::vector<int32_t> &lay = tr->lay_of_op;
   std::vector<int64_t> mre(N);
-  for (int32_t i = 0; i < N; i++) mre[i] = tr->F0[i] > tr->budget ? tr->F0[i] - tr->budget : 0;
+  int64_t n_pos = 0;  // MREs still > 0
+  for (int32_t i = 0; i < N; i++) {
+    mre[i] = tr->F0[i] > tr->budget ? tr->F0[i] - tr->budget : 0;
+    n_pos += mre[i] > 0;
+  }
+  // next_pos: first op >= i whose MRE is still > 0 (N: none); MREs only ever drop to 0, so a
+  // path-compressed "next" forest answers it in near-constant time
+  std::vector<int32_t> nxt(size_t(N) + 1);
+  for (int32_t i = 0; i <= N; i++) nxt[i] = (i < N && mre[i] <= 0) ? i + 1 : i;
+  auto next_pos = [&](int32_t i) {
+    int32_t r = i;
+    while (nxt[r] != r) r = nxt[r];
+    while (nxt[i] != r) { const int32_t t = nxt[i]; nxt[i] = r; i = t; }
+    return r;
+  };
   std::vector<double> rem(L);
   for (int32_t l = 0; l < L; l++) rem[l] = tr->bud[l] * gp->rem_scale;
-  auto mrl_empty = [&]() {
-    for (int64_t v : mre) if (v > 0) return false;
-    return true;
-  };
+  auto mrl_empty = [&]() { return n_pos == 0; };
   auto credit = [&](int32_t tid, int32_t sp) {  // the tensor is off device for ops (a_t, s_t)
-    for (int32_t i = tr->a[tid] + 1; i < sp; i++) mre[i] = std::max<int64_t>(0, mre[i] - tr->S_t[tid]);
+    for (int32_t i = tr->a[tid] + 1; i < sp; i++) {
+      if (mre[i] <= 0) continue;
+      mre[i] = std::max<int64_t>(0, mre[i] - tr->S_t[tid]);
+      if (mre[i] == 0) { n_pos--; nxt[i] = i + 1; }
+    }
   };
+  std::vector<int32_t> pos_prefix(size_t(N) + 1, 0);  // # MREs > 0 in ops [0, i), per round
   const int32_t n_prod = int32_t(tr->rank_to_tensor.size());
   std::vector<char> selected(n_prod, 0);
   struct Placed { int32_t rank, tid, s; uint32_t flags; };
@@ -56,11 +72,11 @@ extern "C" chm_status chm_generate_policy(const chm_trace *tr, const chm_gen_par
     std::vector<Cand> cl;
     int32_t max_n = 0;
     int64_t max_s = 0;
+    for (int32_t i = 0; i < N; i++) pos_prefix[i + 1] = pos_prefix[i] + (mre[i] > 0);
     for (int32_t rk = 0; rk < n_prod; rk++) {
       const int32_t tid = tr->rank_to_tensor[rk];
       if (selected[rk] || tr->a[tid] < 0 || tr->b[tid] < 0) continue;
-      int32_t cnt = 0;
-      for (int32_t i = tr->a[tid]; i < tr->b[tid]; i++) cnt += mre[i] > 0;
+      const int32_t cnt = tr->b[tid] > tr->a[tid] ? pos_prefix[tr->b[tid]] - pos_prefix[tr->a[tid]] : 0;
       if (!cnt) continue;
       cl.push_back({rk, tid, double(cnt)});
       max_n = std::max(max_n, cnt);
@@ -78,9 +94,8 @@ extern "C" chm_status chm_generate_policy(const chm_trace *tr, const chm_gen_par
     for (const Cand &c : cl) {
       const int32_t tid = c.tid;
       const double tswap = double(tr->S_t[tid]) / tr->bw;
-      int32_t first = -1;
-      for (int32_t i = tr->a[tid]; i < tr->b[tid]; i++) if (mre[i] > 0) { first = i; break; }
-      if (first < 0) continue;
+      const int32_t first = next_pos(tr->a[tid]);
+      if (first >= tr->b[tid]) continue;
       const int32_t lo = std::max(lay[first], lay[tr->a[tid]] + 1);
       int32_t found = -1;
       for (int32_t l = lay[tr->b[tid]] - 1; l >= lo; l--) if (rem[l] > tswap) { found = l; break; }
