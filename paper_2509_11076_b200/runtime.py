@@ -99,6 +99,35 @@ def _collect(x, out):
             _collect(y, out)
 
 
+def _key3(k):
+    return (int(k["excess"]), float(k["stall"]), int(k["swapped_bytes"]))
+
+
+def descend(ctx, pt, key, words, dev, max_rounds: int = 4096):
+    """steepest descent over single-bit flips of a mask (reading R-search): each round replays
+    all K neighbours at once (MASKS) and moves to the best one if it lowers the key (excess,
+    stall, swapped bytes) -- the evaluator's throughput turned into plan quality.  key: the
+    chm_best of `words`.  Returns (key, words, rounds)."""
+    K, W = pt.K, pt.W
+    idx = np.arange(K)
+    flip = np.zeros((K, W), np.uint64)
+    flip[idx, idx // 64] = np.left_shift(np.uint64(1), (idx % 64).astype(np.uint64))
+    masks_dev = torch.empty((K, W), dtype=torch.int64, device=dev)
+    best = torch.empty(5, dtype=torch.int64, device=dev)
+    cur = np.array(words, np.uint64)
+    rounds = 0
+    while rounds < max_rounds and K:
+        masks_dev.copy_(torch.from_numpy((cur[None, :] ^ flip).view(np.int64)))
+        ctx.eval_policies(pt, chm.MASKS, 0, K, best=best, masks=masks_dev)
+        nk = best.cpu().numpy().view(chm.BEST_DTYPE)[0]
+        if not _key3(nk) < _key3(key):
+            break
+        cur = cur ^ flip[int(nk["index"])]
+        key = nk
+        rounds += 1
+    return key, cur, rounds
+
+
 def _generate_all(pt):
     """Algo. 2's "best of n" grid (C x T_remaining scale, reading R-gen), one host thread per
     variant (the generator only reads the trace; ctypes drops the GIL): non-empty item lists"""
@@ -620,27 +649,7 @@ class Runtime:
         self.plans.append(plan)
 
     def _local_search(self, pt, key, words):
-        """steepest descent over single-bit flips of the mask: each round
-        replays all K neighbours at once (MASKS) and takes the best if it lowers the key
-        (excess, stall, swapped bytes) -- the evaluator's throughput turned into plan quality"""
-        K, W = pt.K, pt.W
-        idx = np.arange(K)
-        flip = np.zeros((K, W), np.uint64)
-        flip[idx, idx // 64] = np.left_shift(np.uint64(1), (idx % 64).astype(np.uint64))
-        masks_dev = torch.empty((K, W), dtype=torch.int64, device=self.dev)
-        best = torch.empty(5, dtype=torch.int64, device=self.dev)
-        cur = np.array(words, np.uint64)
-        rounds = 0
-        while rounds < self.search_rounds:
-            masks_dev.copy_(torch.from_numpy((cur[None, :] ^ flip).view(np.int64)))
-            self.ctx.eval_policies(pt, chm.MASKS, 0, K, best=best, masks=masks_dev)
-            nk = best.cpu().numpy().view(chm.BEST_DTYPE)[0]
-            if not self._key(nk) < self._key(key):
-                break
-            cur = cur ^ flip[int(nk["index"])]
-            key = nk
-            rounds += 1
-        return key, cur, rounds
+        return descend(self.ctx, pt, key, words, self.dev, self.search_rounds)
 
     def _reserve_words(self, words, pt):
         if self.host_only:

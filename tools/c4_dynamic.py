@@ -22,6 +22,7 @@ import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2509_11076_b200 import chm  # noqa: E402
+from paper_2509_11076_b200.runtime import descend  # noqa: E402
 from workloads import traces as W  # noqa: E402
 
 
@@ -88,6 +89,12 @@ def main():
                       generator_best=dict(excess_gib=int(gk["excess"]) / 2 ** 30, stall_s=float(gk["stall"]),
                                           swapped_gib=int(gk["swapped_bytes"]) / 2 ** 30))
             words = pt.candidate_mask(chm.SEEDED, int(bk["index"]), seed=sd["seed"], flip_thr=sd["flip_thr"])
+            t0 = time.perf_counter()
+            dk, words, rounds = descend(ctx, pt, bk, words, dev_t)  # the runtime's refinement
+            rp["descent_ms"] = (time.perf_counter() - t0) * 1e3
+            rp["replan_with_descent_ms"] = rp["replan_ms"] + rp["descent_ms"]
+            rp["descent_best"] = dict(rounds=rounds, excess_gib=int(dk["excess"]) / 2 ** 30, stall_s=float(dk["stall"]),
+                                      swapped_gib=int(dk["swapped_bytes"]) / 2 ** 30)
             policies[int(tr.meta["shape"]["seq"])] = (pt, words)
             replans.append(rp)
     out = dict(config=W.CONFIGS["C4a"]().meta["config"], detect_bytes=args.detect_bytes, cos_mode=args.cos_mode,
