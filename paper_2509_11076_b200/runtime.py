@@ -238,9 +238,34 @@ class Runtime:
             with torch.autograd.graph.saved_tensors_hooks(self._pack, self._unpack), mode:
                 yield self
                 self._flush()
-        finally:
+        except BaseException:
             self._in_step = False
+            self._abort()
+            raise
+        self._in_step = False
         self._end()
+
+    def _abort(self):
+        """a step that raised: close the partial iteration so the next step starts clean (its
+        sequence is short, so Algo. 1 sees a change and the policy is re-planned), drop the
+        step's boxes and any passive copies"""
+        self.pending = None
+        if not self.host_only:
+            torch.cuda.synchronize(self.dev)
+        for hd in list(self.passive_out):
+            self.ctx.passive_restore(hd, 0)
+        self.passive_out.clear()
+        for ref in self.weak.values():
+            torch.UntypedStorage._free_weak_ref(ref)
+        self.weak = {}
+        self.holders = weakref.WeakValueDictionary()
+        self.item_holder = {}
+        d = self.ctx.detect_seq_change(0.0)
+        self.stage = d["stage"]
+        if self.policy is not None:
+            self._uninstall()
+        self.need_plan = True
+        self.stats["aborted"] = self.stats.get("aborted", 0) + 1
 
     def request_replan(self, hbm_budget: Optional[int] = None):
         """record the next step in Detailed mode and re-plan at its end (e.g. a new budget),

@@ -134,3 +134,31 @@ def test_sequence_change_uninstalls_and_replans():
         _step(rt, model, opt, x, y, forwards=2)
     assert len(rt.plans) == 2 and rt.policy is not None
     assert rt.plans[1]["n_ops"] > 1.9 * rt.plans[0]["n_ops"]
+
+
+def test_interleaved_microbatches_and_a_failed_step():
+    """two (forward, backward) pairs per step: the second forward is recorded in the later phase
+    (FWD* BWD* OPT* is kept), the plan covers the first micro-batch and matches every step; a step
+    that raises closes its partial iteration, the policy is dropped and re-planned later"""
+    model, opt, data, rt = _setup(24)
+
+    def step2(x, y):
+        with rt.step():
+            model(x, y).backward()
+            model(x, y).backward()
+            opt.step()
+            opt.zero_grad()
+    for x, y in data[:8]:
+        step2(x, y)
+    assert rt.policy is not None and rt.plans[0]["items"] > 0
+    m0 = rt.ctx.exec_stats()["n_matched"]
+    step2(*data[8])
+    assert rt.ctx.exec_stats()["n_matched"] - m0 == rt.plans[0]["items"]
+    with pytest.raises(ValueError):
+        with rt.step():
+            model(*data[9]).backward()
+            raise ValueError("user error mid-step")
+    assert rt.policy is None and rt.stats["aborted"] == 1
+    for x, y in data[10:]:
+        step2(x, y)
+    assert len(rt.plans) == 2 and rt.policy is not None
