@@ -184,6 +184,7 @@ typedef struct {
   uint32_t argmax0;
   int64_t budget;
 } chm_trace_info;
+/* sizes of a built trace (N, T, K, L, W), its no-swap peak and first argmax, the budget */
 chm_status chm_trace_get_info(const chm_trace *t, chm_trace_info *info);
 /* Copies host-side tables out (each pointer nullable): f0[n_ops]; per swappable k:
  * tensor[k] (production-order tensor index), nbytes[k], r[k], s[k], lin[k], lout[k];
@@ -274,19 +275,6 @@ typedef struct {
 chm_status chm_generate_policy(const chm_trace *t, const chm_gen_params *p, chm_item *items,
                                uint32_t cap, uint32_t *n_items, int32_t *feasible);
 
-/* host: the swap set of global candidate `index` as mask words (mask_words u64) */
-chm_status chm_candidate_mask(const chm_trace *t, const chm_candidates *c, uint64_t index,
-                              uint64_t *words);
-
-/* ----------------------------------------------------------- policy install / trigger (a8) */
-/* Installs the swap set `words` of trace t as the active policy: every selected tensor gets
- * an item {App. A feature key after op a_t, release op r_t, swap-in op s_t, host offset in
- * the arena}.  Feature tables (top-32 one-hot, 8-bit index) come from the recorded
- * iteration's token frequencies (P:531-532).  Subsequent chm_record_op calls return the
- * policy's actions. */
-chm_status chm_policy_install(chm_ctx *ctx, const chm_trace *t, const uint64_t *words);
-/* the same for an explicit item list (e.g. chm_generate_policy's output): releases after r,
- * swap-ins before s as given */
 /* The stall of one explicit item list (host, exact) under the stall models of reading Q11
  * (SURVEY §8(f) NEXT-4), for comparison against measured stalls; out[3]:
  *   out[0] R-stall -- what chm_eval_policies reports: pairwise sum over layers of
@@ -301,12 +289,28 @@ chm_status chm_policy_install(chm_ctx *ctx, const chm_trace *t, const uint64_t *
  *          (b_t = i); after op i swap-outs (a_t = i) then releases (r = i); item order within
  *          a kind.  Items are validated as for chm_policy_install_items. */
 chm_status chm_stall_models(const chm_trace *t, const chm_item *items, uint32_t n, double *out);
+
+/* host: the swap set of global candidate `index` as mask words (mask_words u64) */
+chm_status chm_candidate_mask(const chm_trace *t, const chm_candidates *c, uint64_t index,
+                              uint64_t *words);
+
+/* ----------------------------------------------------------- policy install / trigger (a8) */
+/* Installs the swap set `words` of trace t as the active policy: every selected tensor gets
+ * an item {App. A feature key after op a_t, release op r_t, swap-in op s_t, host offset in
+ * the arena}.  Feature tables (top-32 one-hot, 8-bit index) come from the recorded
+ * iteration's token frequencies (P:531-532).  Subsequent chm_record_op calls return the
+ * policy's actions. */
+chm_status chm_policy_install(chm_ctx *ctx, const chm_trace *t, const uint64_t *words);
+/* the same for an explicit item list (e.g. chm_generate_policy's output): releases after r,
+ * swap-ins before s as given */
 chm_status chm_policy_install_items(chm_ctx *ctx, const chm_trace *t, const chm_item *items,
                                     uint32_t n);
 typedef struct {
   uint32_t n_items, n_matched, n_stale, n_collisions, n_demand_swap_in;
   uint64_t bytes_out, bytes_in;
 } chm_exec_stats;
+/* executor counters since the last install: items installed, matched swap-outs, items never
+ * matched in an iteration (stale), key collisions, demand swap-ins, bytes out / in */
 chm_status chm_exec_stats_get(chm_ctx *ctx, chm_exec_stats *s);
 
 /* ------------------------------------------------ WarmUp OOM handling (NEXT-4, Algo. 3) */
