@@ -1,0 +1,75 @@
+"""Property-based device parity (hypothesis): random traces, random candidate kinds and ranges,
+search and full mode -- the replay kernels against the oracle, every key and footprint row."""
+import numpy as np
+import pytest
+
+hypothesis = pytest.importorskip("hypothesis")
+from hypothesis import given, settings  # noqa: E402
+from hypothesis import strategies as st  # noqa: E402
+
+import oracle as O  # noqa: E402
+from workloads import traces as W  # noqa: E402
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2509_11076_b200 import chm  # noqa: E402
+from tests.test_gpu_parity import assert_same, product_trace, run_eval  # noqa: E402
+
+traces = st.builds(W.random_trace, seed=st.integers(0, 10 ** 6), n_layers=st.integers(1, 6),
+                   ops_per_layer=st.integers(1, 4), max_kib=st.sampled_from([1, 64, 4096]),
+                   bw=st.sampled_from([1e6, 1e8, 5e10]), t_iter=st.sampled_from([1e-5, 1e-3]))
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = chm.Context(device=0, host_arena_bytes=1 << 20)
+    yield c
+    c.close()
+
+
+@settings(max_examples=150, deadline=None)
+@given(tr=traces, kind=st.sampled_from(["exhaustive", "seeded", "masks", "explicit"]), first=st.integers(0, 5000),
+       count=st.integers(1, 700), full=st.booleans(), seed=st.integers(0, 2 ** 32), flip=st.floats(0.0, 0.9))
+def test_replay_matches_oracle(ctx, tr, kind, first, count, full, seed, flip):
+    pt = product_trace(ctx, tr)
+    m = O.Model(tr)
+    thr = int(flip * 2 ** 64) & ((1 << 64) - 1)
+    if kind == "exhaustive":
+        first = min(first, (1 << m.K) - 1)
+        count = min(count, (1 << m.K) - first)
+        res = run_eval(ctx, pt, chm.EXHAUSTIVE, first, count, footprint=full)
+        ref = m.eval(O.EXHAUSTIVE, first, count, footprint=full)
+    elif kind == "seeded":
+        res = run_eval(ctx, pt, chm.SEEDED, first, count, footprint=full, seed=seed, flip_thr=thr)
+        ref = m.eval(O.SEEDED, first, count, seed=seed, flip_thr=thr, footprint=full)
+    elif kind == "masks":
+        rng = np.random.default_rng(seed)
+        W_ = max(m.W, 1)
+        masks = rng.integers(0, 2 ** 63, size=(count, W_), dtype=np.int64).astype(np.uint64)
+        if m.K % 64:
+            masks[:, -1] &= np.uint64((1 << (m.K % 64)) - 1)
+        if m.K == 0:
+            masks[:] = 0
+        res = run_eval(ctx, pt, chm.MASKS, first, count, footprint=full,
+                       masks=torch.from_numpy(masks[:, :m.W].copy().view(np.int64)).cuda() if m.W else
+                       torch.zeros((count, 1), dtype=torch.int64, device="cuda"))
+        ref = m.eval(O.MASKS, first, count, words=masks[:, :m.W] if m.W else np.zeros((count, 1), np.uint64),
+                     footprint=full)
+    else:
+        rng = np.random.default_rng(seed)
+        sw = m.swappable()
+        lists = []
+        for _ in range(min(count, 40)):
+            k = rng.random(m.K) < 0.5
+            lists.append((sw["t"][k], sw["r"][k], sw["s"][k]))
+        off = np.zeros(len(lists) + 1, np.uint64)
+        off[1:] = np.cumsum([len(x[0]) for x in lists])
+        items = np.zeros(int(off[-1]), chm.ITEM_DTYPE)
+        if len(items):
+            items["t"] = np.concatenate([x[0] for x in lists])
+            items["r"] = np.concatenate([x[1] for x in lists])
+            items["s"] = np.concatenate([x[2] for x in lists])
+        res = run_eval(ctx, pt, chm.EXPLICIT, first, len(lists), footprint=full, item_offsets=off, items=items)
+        ref = O.eval_explicit(m, lists, first_index=first, footprint=full)
+    assert_same(res, ref, tr.budget)
