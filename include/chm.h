@@ -209,17 +209,21 @@ typedef enum {
                               t mod 4 of w = mix(seed ^ mix(c*J + t/4)), J = ceil(K/4),
                               mix = splitmix64 finaliser (reading R-seeded)     */
   CHM_CAND_MASKS = 2,      /* device masks [count][mask_words], little-endian u64 words  */
-  CHM_CAND_EXPLICIT = 3    /* host item lists: candidate c = items[item_offsets[c] ..
+  CHM_CAND_EXPLICIT = 3,   /* host item lists: candidate c = items[item_offsets[c] ..
                               item_offsets[c+1]); validated (CHM_E_INVAL + err_index = item):
                               t a produced activation, a_t <= r, r + 1 < s <= b_t, no
                               repeated t within a candidate                             */
+  CHM_CAND_FLIP1 = 4       /* the one-bit neighbourhood of base_mask: candidate g < K = base
+                              with bit g flipped, g = K: base itself (ids 0 .. K); the
+                              rounds of a local search (reading R-search)     */
 } chm_cand_kind;
 
 typedef struct {
   chm_cand_kind kind;
   uint64_t first_index, count; /* global candidate ids [first_index, first_index + count)  */
   uint64_t seed, flip_thr;     /* SEEDED                                                  */
-  const uint64_t *base_mask;   /* SEEDED, host, mask_words words; NULL: the trace's base  */
+  const uint64_t *base_mask;   /* SEEDED / FLIP1, host, mask_words words; NULL: the trace's
+                                  base                                                    */
   const uint64_t *masks;       /* MASKS, device [count][mask_words]                       */
   const uint64_t *item_offsets;/* EXPLICIT, host [count + 1]                              */
   const chm_item *items;       /* EXPLICIT, host                                          */

@@ -19,7 +19,7 @@ CHM_OK, CHM_E_INVAL, CHM_E_PARSE, CHM_E_STATE, CHM_E_NOMEM, CHM_E_CUDA, CHM_E_IN
     0, -1, -2, -3, -4, -5, -6, -7
 FWD, BWD, OPT = 0, 1, 2
 WARMUP, GENPOLICY, STABLE = 0, 1, 2
-EXHAUSTIVE, SEEDED, MASKS, EXPLICIT = 0, 1, 2, 3
+EXHAUSTIVE, SEEDED, MASKS, EXPLICIT, FLIP1 = 0, 1, 2, 3, 4
 SWAP_KERNEL, SWAP_CE, SWAP_AUTO = 0, 1, 2
 
 

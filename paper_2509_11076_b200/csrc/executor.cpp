@@ -38,6 +38,13 @@ extern "C" chm_status chm_candidate_mask(const chm_trace *t, const chm_candidate
       }
       return CHM_OK;
     }
+    case CHM_CAND_FLIP1: {
+      if (index > uint64_t(K)) CHM_FAIL(CHM_E_INVAL, "chm_candidate_mask: FLIP1 index %llu > K", (unsigned long long)index);
+      const uint64_t *base = c->base_mask ? c->base_mask : t->base.data();
+      std::copy(base, base + W, words);
+      if (index < uint64_t(K)) words[index / 64] ^= 1ull << (index % 64);
+      return CHM_OK;
+    }
     default:
       CHM_FAIL(CHM_E_INVAL, "chm_candidate_mask: MASKS candidates live on the device");
   }

@@ -170,8 +170,8 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
   for (int l = tid; l < 2 * L; l += blockDim.x) { r_hi[l] = 0u; r_lo[l] = 0u; }
   for (int l = lane; l < L; l += 32) { dI_hi[l] = 0u; dI_lo[l] = 0u; dO_hi[l] = 0u; dO_lo[l] = 0u; }
   __syncthreads();
-  const bool seeded = p.kind == CHM_CAND_SEEDED;
-  if (seeded) {  // R = base
+  const bool seeded = p.kind == CHM_CAND_SEEDED, flip1 = p.kind == CHM_CAND_FLIP1;
+  if (seeded || flip1) {  // R = base
     for (int k = tid; k < K; k += blockDim.x) {
       if (!((p.base[k >> 6] >> (k & 63)) & 1ull)) continue;
       acc_add(r_hi, r_lo, li_[k], S[k]);
@@ -229,6 +229,14 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
           acc_add(dI_hi, dI_lo, li_[k], v);
           acc_add(dO_hi, dO_lo, lo_[k], v);
         }
+      }
+    } else if (flip1) {  // one item differs from R: item g (none for g = K)
+      if (lane == 0 && g < uint64_t(K)) {
+        const int k = int(g);
+        const bool was = (p.base[k >> 6] >> (k & 63)) & 1ull;
+        const long long v = was ? -S[k] : S[k];
+        acc_add(dI_hi, dI_lo, li_[k], v);
+        acc_add(dO_hi, dO_lo, lo_[k], v);
       }
     } else {
       for (int k = lane; k < K; k += 32) {
@@ -507,6 +515,13 @@ extern "C" chm_status chm_eval_policies_ex(chm_ctx *ctx, const chm_trace *t, con
       else if (t->W) std::memcpy(L.base, t->base.data(), 8 * size_t(t->W));
       L.seed = c->seed;
       L.flip_thr = c->flip_thr;
+      break;
+    case CHM_CAND_FLIP1:
+      if (t->W > kMaxSeededWords) CHM_FAIL(CHM_E_INVAL, "FLIP1 candidates need K <= %d", 64 * kMaxSeededWords);
+      if (c->first_index + c->count > uint64_t(t->K) + 1)
+        CHM_FAIL(CHM_E_INVAL, "FLIP1 range exceeds K + 1 = %d candidates", t->K + 1);
+      if (c->base_mask) std::memcpy(L.base, c->base_mask, 8 * size_t(t->W));
+      else if (t->W) std::memcpy(L.base, t->base.data(), 8 * size_t(t->W));
       break;
     case CHM_CAND_MASKS:
       if (!c->masks && t->W) CHM_FAIL(CHM_E_INVAL, "MASKS candidates need a device mask array");

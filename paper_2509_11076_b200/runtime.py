@@ -105,24 +105,21 @@ def _key3(k):
 
 def descend(ctx, pt, key, words, dev, max_rounds: int = 4096):
     """steepest descent over single-bit flips of a mask (reading R-search): each round replays
-    all K neighbours at once (MASKS) and moves to the best one if it lowers the key (excess,
-    stall, swapped bytes) -- the evaluator's throughput turned into plan quality.  key: the
-    chm_best of `words`.  Returns (key, words, rounds)."""
-    K, W = pt.K, pt.W
-    idx = np.arange(K)
-    flip = np.zeros((K, W), np.uint64)
-    flip[idx, idx // 64] = np.left_shift(np.uint64(1), (idx % 64).astype(np.uint64))
-    masks_dev = torch.empty((K, W), dtype=torch.int64, device=dev)
+    the whole one-bit neighbourhood of the current mask in one FLIP1 launch (the mask travels in
+    kernel parameters) and moves to the best neighbour if it lowers the key (excess, stall,
+    swapped bytes) -- the evaluator's throughput turned into plan quality.  key: the chm_best of
+    `words`.  Returns (key, words, rounds)."""
+    K = pt.K
     best = torch.empty(5, dtype=torch.int64, device=dev)
     cur = np.array(words, np.uint64)
     rounds = 0
     while rounds < max_rounds and K:
-        masks_dev.copy_(torch.from_numpy((cur[None, :] ^ flip).view(np.int64)))
-        ctx.eval_policies(pt, chm.MASKS, 0, K, best=best, masks=masks_dev)
+        ctx.eval_policies(pt, chm.FLIP1, 0, K, best=best, base=cur)
         nk = best.cpu().numpy().view(chm.BEST_DTYPE)[0]
         if not _key3(nk) < _key3(key):
             break
-        cur = cur ^ flip[int(nk["index"])]
+        k = int(nk["index"])
+        cur[k // 64] ^= np.uint64(1 << (k % 64))
         key = nk
         rounds += 1
     return key, cur, rounds

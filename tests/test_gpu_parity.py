@@ -198,6 +198,30 @@ def test_full_size_configs_all_keys_sampled_rows(ctx, name):
         assert np.array_equal(full["footprint"][c], one["footprint"][0])
 
 
+@pytest.mark.parametrize("name", ["C1", "C2", "C5"])
+def test_flip1_neighbourhood_matches_oracle_masks(ctx, name):
+    """FLIP1 (the descent's candidates): candidate g = base with bit g flipped, g = K the base --
+    equal to the oracle's MASKS replay of those masks, every key and footprint row"""
+    tr = W.CONFIGS[name]()
+    pt = product_trace(ctx, tr)
+    m = O.Model(tr)
+    rng = np.random.default_rng(3)
+    base = np.zeros(m.W, np.uint64)
+    for k in np.nonzero(rng.random(m.K) < 0.4)[0]:
+        base[k // 64] |= np.uint64(1 << int(k % 64))
+    n = m.K + 1
+    res = run_eval(ctx, pt, chm.FLIP1, 0, n, footprint=True, base=base)
+    masks = np.repeat(base[None, :], n, axis=0)
+    for g in range(m.K):
+        masks[g, g // 64] ^= np.uint64(1 << (g % 64))
+    ref = m.eval(O.MASKS, 0, n, words=masks, footprint=True, nthreads=8)
+    assert_same(res, ref, tr.budget)
+    for g in (0, m.K // 2, m.K):
+        assert np.array_equal(pt.candidate_mask(chm.FLIP1, g, base=base), masks[g])
+    with pytest.raises(chm.ChmError):
+        run_eval(ctx, pt, chm.FLIP1, 1, n, base=base)  # past K + 1 candidates
+
+
 def test_candidate_mask_matches_oracle_decode(ctx):
     tr = W.tiny()
     pt = product_trace(ctx, tr)
