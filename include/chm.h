@@ -145,7 +145,9 @@ typedef struct {
   int64_t static_bytes;        /* M_0: bytes live at iteration start                    */
   double t_iter_s;             /* T_iter of Eq. 1; <= 0: the recorded iteration's time */
   double bw_bytes_per_s;       /* B of Eq. 3; must be > 0                   */
-  uint32_t groups_fwd, groups_bwd; /* logical layers per phase, >= 1        */
+  uint32_t groups_fwd, groups_bwd; /* logical layers per phase; 0: the phase's
+                                  layer count, its length over the token period that best
+                                  aligns the sequence with itself (stacked layers)        */
   double omega;                /* overlap factor on layer budgets, 1.0 default  */
   uint32_t f0_source;          /* 0: F0 from the recorded alloc/free events (+ static_bytes);
                                   1: Fig. 3 reconstruction: the recorded

@@ -12,6 +12,28 @@ using namespace chm;
 
 enum { kFWD = 0, kBWD = 1, kOPT = 2 };
 
+// Logical layers when the caller gives no group count: the paper groups each phase evenly and
+// finds the estimate reliable up to the model's layer count; a stacked model repeats
+// one layer's operators, so the count is the phase length over the period p that best aligns the
+// token sequence with itself shifted by p (the smallest p within 0.5% of the best match rate;
+// embedding / head ops at the ends only lower every rate a little).
+static int32_t auto_groups(const int32_t *tok, int32_t n) {
+  if (n < 4) return 1;
+  const int32_t pmax = std::min(n / 2, 4096);
+  std::vector<double> rate(size_t(pmax) + 1, 0.0);
+  double best = 0.0;
+  for (int32_t p = 1; p <= pmax; p++) {
+    int32_t m = 0;
+    for (int32_t i = 0; i + p < n; i++) m += tok[i] == tok[i + p];
+    rate[p] = double(m) / double(n - p);
+    best = std::max(best, rate[p]);
+  }
+  if (best < 0.5) return 1;  // no repeated structure
+  for (int32_t p = 1; p <= pmax; p++)
+    if (rate[p] >= best - 0.005) return std::max(1, n / p);
+  return 1;
+}
+
 extern "C" chm_status chm_trace_build(chm_ctx *ctx, const chm_trace_params *P, chm_trace **out) {
   if (!ctx || !P || !out) CHM_FAIL(CHM_E_INVAL, "chm_trace_build: NULL argument");
   *out = nullptr;
@@ -100,6 +122,9 @@ chm_status chm::build_trace(chm_ctx *ctx, const IterRecord &R, const chm_trace_p
   int32_t nph[3] = {0, 0, 0};
   for (int32_t i = 0; i < N; i++) nph[R.phase[i]]++;
   int32_t G[3] = {int32_t(P->groups_fwd), int32_t(P->groups_bwd), nph[kOPT] > 0 ? 1 : 0};
+  for (int ph = 0; ph < 2; ph++) {  // 0 groups: the phase's layer count, from its period
+    if (G[ph] == 0 && nph[ph] > 0) G[ph] = auto_groups(R.tokens.data() + (ph ? nph[0] : 0), nph[ph]);
+  }
   for (int ph = 0; ph < 2; ph++) {
     if (nph[ph] == 0) G[ph] = 0;
     else if (G[ph] < 1 || G[ph] > nph[ph]) {

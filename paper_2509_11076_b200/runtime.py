@@ -170,13 +170,14 @@ class Runtime:
     """Chameleon's runtime for one device (one process per GPU).
 
     hbm_budget: bytes the step may occupy (weights, optimizer state and activations); bw: host
-    link bytes/s of Eq. 3 (default: measured once with the swap kernel); groups_fwd/groups_bwd:
-    logical layers per phase (P:283-288); candidates: SEEDED candidates per re-plan;
+    link bytes/s of Eq. 3 (default: measured once through the policy's copy path);
+    groups_fwd/groups_bwd: logical layers per phase (0: the model's layer count,
+    detected from the recorded operator sequence); candidates: SEEDED candidates per re-plan;
     search_rounds: bound on the local search from the best SEEDED mask (0: off);
     host_arena_bytes: pinned arena reserved up front (else grown to each policy at install)."""
 
     def __init__(self, device: Optional[int] = 0, *, hbm_budget: int, bw: Optional[float] = None,
-                 groups_fwd: int = 8, groups_bwd: int = 8, omega: float = 1.0, candidates: int = 1 << 16,
+                 groups_fwd: int = 0, groups_bwd: int = 0, omega: float = 1.0, candidates: int = 1 << 16,
                  seed: int = 1, flip_frac: float = 0.02, generator: bool = True, swap_ctas: int = 0,
                  min_swap_bytes: int = 0, search_rounds: int = 4096, host_arena_bytes: int = 0,
                  swap_flags: int = chm.SWAP_AUTO, oom_host_bytes: int = 0, **algo1):

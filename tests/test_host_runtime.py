@@ -252,3 +252,37 @@ def test_c4_dynamic_schedule_detection():
         assert st[start + warm:start + warm + 6] == [1] * 6
         assert st[start + warm + 6] == 2
         del off
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4a", "C4b", "C5"])
+def test_auto_groups_find_the_layer_count(name):
+    """groups 0: each phase is split into its layer count, found from the token period (P:283-288
+    -- the grouping estimate holds up to the model's layer count); equals the configured groups
+    of the synthetic transformer traces, and the rest of the trace is the configured one's"""
+    tr = W.CONFIGS[name]()
+    ctx = host_ctx()
+    ctx.set_detailed(True)
+    chm.record_iteration(ctx, tr)
+    ctx.detect_seq_change(tr.t_iter)
+    auto = ctx.trace_build(tr.budget, tr.static_bytes, tr.bw, 0, 0, t_iter=tr.t_iter)
+    given = ctx.trace_build(tr.budget, tr.static_bytes, tr.bw, tr.groups_fwd, tr.groups_bwd, t_iter=tr.t_iter)
+    a, g = auto.tables(), given.tables()
+    for k in a:
+        assert np.array_equal(a[k], g[k]), k
+
+
+def test_auto_groups_on_a_real_model_sequence():
+    """the runtime's default (groups 0) on a 4-layer GPT: four FWD logical layers"""
+    torch = pytest.importorskip("torch")
+    from paper_2509_11076_b200.runtime import Runtime
+    from workloads import tiny_gpt as G
+    model = G.make(0, n_layer=4)
+    opt = torch.optim.SGD(model.parameters(), lr=0.01)
+    rt = Runtime(None, hbm_budget=1)
+    for x, y in G.batches(6, 2, 16, 64):
+        with rt.step():
+            model(x, y).backward()
+            opt.step()
+            opt.zero_grad()
+    assert rt.plans and rt.policy is not None
+    assert rt.policy[0].L == 4 + 4 + 1  # 4 FWD + 4 BWD logical layers + the optimizer's group
