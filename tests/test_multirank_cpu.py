@@ -50,7 +50,7 @@ def test_sharded_argmin_equals_global(world):
     import oracle as O
     from workloads import traces as W
     C = 3000
-    mgr = mp.Manager()
+    mgr = mp.get_context("spawn").Manager()
     out = mgr.dict()
     mp.spawn(_worker, args=(world, _free_port(), C, out), nprocs=world, join=True)
     tr = W.gpt2_xl()
@@ -96,7 +96,7 @@ def test_runtime_under_ddp_two_ranks():
     """one runtime per rank (host-only ctx) under DistributedDataParallel: the all-reduce inside
     backward does not disturb the profile -- each rank plans once and matches every planned
     tensor in every later step; the replicas stay identical"""
-    mgr = mp.Manager()
+    mgr = mp.get_context("spawn").Manager()
     out = mgr.dict()
     mp.spawn(_ddp_worker, args=(2, _free_port(), out), nprocs=2, join=True)
     for r in range(2):
