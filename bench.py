@@ -223,6 +223,7 @@ def _replan_c4(chm, dev, comp):
         chm._check(L.chm_record_op(ctx.h, ctypes.byref(r), ctypes.byref(act)))
     ctx.detect_seq_change(tr.t_iter)
     out["record_ms"] = (time.perf_counter() - t0) * 1e3
+    out["record_ns_per_op"] = out["record_ms"] * 1e6 / tr.n_ops  # host step a1 (+ a2 below)
     t0 = time.perf_counter()
     pt = ctx.trace_build(tr.budget, tr.static_bytes, tr.bw, tr.groups_fwd, tr.groups_bwd, t_iter=tr.t_iter)
     out["trace_build_ms"] = (time.perf_counter() - t0) * 1e3
@@ -336,9 +337,11 @@ def main():
     best_global = torch.empty(5, dtype=torch.int64, device=dev)
     comp = torch.cuda.current_stream(dev)
 
-    def evaluate():
+    def evaluate(ev_kernel=None):
         ctx.eval_policies(pt, chm.SEEDED, lo, cnt, best=best_local, seed=sd["seed"], flip_thr=sd["flip_thr"],
                           peak=peak, stall=stall, footprint=fp, ld=ld if full else 0, stream=comp)
+        if ev_kernel is not None:
+            ev_kernel.record(comp)  # replay kernel done; the rest is the argmin exchange
         if P > 1:
             dist.all_gather_into_tensor(gathered, best_local)
             ctx.best_reduce_device(gathered, P, best_global, comp)
@@ -422,7 +425,8 @@ def main():
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     spin_cycles = 1_000_000  # ~0.5 ms at 1.9 GHz
     # ---- warm-up + timed steps (device loop)
-    step_ms, eval_ms, d2h_ms, h2d_ms = [], [], [], []
+    step_ms, eval_ms, d2h_ms, h2d_ms, argmin_ms = [], [], [], [], []
+    ev_k = torch.cuda.Event(enable_timing=True)
     launches = launches_swap = 0
     for step in range(args.warmup):
         evaluate()
@@ -437,7 +441,7 @@ def main():
             torch.cuda._sleep(spin_cycles)
             ev[0].record(comp)
             ev[1].record(comp)
-            evaluate()
+            evaluate(ev_k)
             ev[2].record(comp)
             n_l, outs, ins = execute(chm.SWAP_KERNEL)
             ev[3].record(comp)
@@ -446,7 +450,8 @@ def main():
             launches += n_l + 1 + (1 if P > 1 else 0)
             launches_swap = n_l
             step_ms.append(ev[0].elapsed_time(ev[3]))
-            eval_ms.append(ev[1].elapsed_time(ev[2]))
+            eval_ms.append(ev[1].elapsed_time(ev_k))
+            argmin_ms.append(ev_k.elapsed_time(ev[2]))
             d2h_ms.append(sum(ctx.batch_elapsed_ms(b) for b in outs))
             h2d_ms.append(sum(ctx.batch_elapsed_ms(b) for b in ins))
     clocks = clk.summary()
@@ -530,6 +535,7 @@ def main():
     # ---- aggregate (max over ranks of time, sum of work)
     t_step = max_over_ranks(float(np.mean(step_ms)))
     t_eval = max_over_ranks(float(np.mean(eval_ms)))
+    t_argmin = max_over_ranks(float(np.mean(argmin_ms)))
     t_d2h = max_over_ranks(float(np.mean(d2h_ms)))
     t_h2d = max_over_ranks(float(np.mean(h2d_ms)))
     tot_bytes = sum_over_ranks(2.0 * bytes_swap)
@@ -538,6 +544,8 @@ def main():
     hbm_peak = measured_peaks().get("hbm_gbs", 6650.0)
     per_dir = [bytes_swap / (t_d2h * 1e-3) / 1e9 if t_d2h > 0 else 0.0,
                bytes_swap / (t_h2d * 1e-3) / 1e9 if t_h2d > 0 else 0.0]
+    ce_dir = ([bytes_swap / (np.mean(ce_d2h) * 1e-3) / 1e9, bytes_swap / (np.mean(ce_h2d) * 1e-3) / 1e9]
+              if ce_d2h and ce_h2d else None)
     achieved_swap = 2 * bytes_swap / ((t_d2h + t_h2d) * 1e-3) / 1e9
     e2e_t = max_over_ranks(float(np.mean(e2e_ms))) if e2e_ms else None
     if rank != 0:
@@ -578,6 +586,9 @@ def main():
             "peak_source": "nominal PCIe Gen5 x16 per direction (no measured host-link peak in MEASURED_PEAKS.json; "
                            "the box's copy engines reach 57.3 D2H / 55.6 H2D GB/s, tools/probe_box.py)",
             "d2h_GBps": per_dir[0], "h2d_GBps": per_dir[1],
+            "frac_of_copy_engines": ({"d2h": per_dir[0] / ce_dir[0], "h2d": per_dir[1] / ce_dir[1],
+                                      "what": "vs the same batches on the copy engines (best pinned large-block "
+                                              "cudaMemcpyAsync path), this run"} if ce_dir else None),
         },
         "roofline_replay": {
             "bound": "hbm", "kernel": "replay_kernel<%s>" % ("true" if full else "false"),
@@ -586,7 +597,9 @@ def main():
             "traffic": _traffic("replay_kernel_full", fp_bytes) if full else None,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst)",
             "algorithmic_bytes_per_launch": fp_bytes,
+            "frac_of_spec_8TBps": fp_bytes / (t_eval * 1e-3) / 1e9 / 8000.0,
         },
+        "argmin_exchange_us": t_argmin * 1e3 if P > 1 else None,
         "eval": {"candidates_per_s": C / (t_eval * 1e-3), "ms_per_launch": t_eval, "unit": "candidates/s"},
         "ce_baseline": {
             "what": "same batches, one cudaMemcpyAsync per tensor on the copy engines",
