@@ -305,7 +305,10 @@ chm_status chm_candidate_mask(const chm_trace *t, const chm_candidates *c, uint6
  * an item {App. A feature key after op a_t, release op r_t, swap-in op s_t, host offset in
  * the arena}.  Feature tables (top-32 one-hot, 8-bit index) come from the recorded
  * iteration's token frequencies.  Subsequent chm_record_op calls return the
- * policy's actions. */
+ * policy's actions.  When the policy's slots do not fit, a device ctx grows its arena to them
+ * plus the passive-swap room it kept above the previous policy (chm_arena_reserve; pinning
+ * takes time -- reserve ahead to keep it off the re-plan path); CHM_E_STATE while passive swaps
+ * are outstanding. */
 chm_status chm_policy_install(chm_ctx *ctx, const chm_trace *t, const uint64_t *words);
 /* the same for an explicit item list (e.g. chm_generate_policy's output): releases after r,
  * swap-ins before s as given */

@@ -100,14 +100,18 @@ struct InstallItem {
 static chm_status install_items(chm_ctx *ctx, const chm_trace *t, const std::vector<InstallItem> &sel) {
   uint64_t need = 0;
   for (const InstallItem &x : sel) need += (uint64_t(x.nbytes) + 511) & ~uint64_t(511);
-  if (ctx->device >= 0 && need > ctx->arena_bytes)  // a host-only ctx plans offsets only
-    CHM_FAIL(CHM_E_NOMEM, "chm_policy_install: policy needs %llu arena bytes, arena has %llu",
-             (unsigned long long)need, (unsigned long long)ctx->arena_bytes);
+  if (!ctx->passive.empty())
+    CHM_FAIL(CHM_E_STATE, "policy install: %zu passive swaps outstanding (restore them first)", ctx->passive.size());
+  if (ctx->device >= 0 && need > ctx->arena_bytes) {  // a host-only ctx plans offsets only
+    // grow to the policy's slots plus the passive-swap room kept above the previous policy
+    const uint64_t room = (ctx->policy_active && ctx->arena_bytes > ctx->passive_base)
+                              ? ctx->arena_bytes - ctx->passive_base : 0;
+    const chm_status st = chm_arena_reserve(ctx, need + room);
+    if (st != CHM_OK) return st;
+  }
   feature_tables(t->tokens, ctx->op_index, ctx->op_onehot);
   // feature key of every selected tensor right after op a_t (replay of the recorded uses)
   std::vector<int32_t> item_of_tensor(size_t(t->T), -1);
-  if (!ctx->passive.empty())
-    CHM_FAIL(CHM_E_STATE, "policy install: %zu passive swaps outstanding (restore them first)", ctx->passive.size());
   ctx->items.assign(sel.size(), PolicyItem());
   uint64_t off = 0;
   for (size_t j = 0; j < sel.size(); j++) {

@@ -173,14 +173,17 @@ class Runtime:
     link bytes/s of Eq. 3 (default: measured once through the policy's copy path);
     groups_fwd/groups_bwd: logical layers per phase (0: the model's layer count,
     detected from the recorded operator sequence); candidates: SEEDED candidates per re-plan;
-    search_rounds: bound on the local search from the best SEEDED mask (0: off);
+    search_rounds: bound on the local search from the best SEEDED mask (0: off); trials: distinct
+    plans (best simulated keys first) executed on consecutive real steps after a re-plan, the
+    fastest kept ("generates five different policies and selects the one with the best
+    runtime performance"; 1: keep the best key);
     host_arena_bytes: pinned arena reserved up front (else grown to each policy at install)."""
 
     def __init__(self, device: Optional[int] = 0, *, hbm_budget: int, bw: Optional[float] = None,
                  groups_fwd: int = 0, groups_bwd: int = 0, omega: float = 1.0, candidates: int = 1 << 16,
                  seed: int = 1, flip_frac: float = 0.02, generator: bool = True, swap_ctas: int = 0,
                  min_swap_bytes: int = 0, search_rounds: int = 4096, host_arena_bytes: int = 0,
-                 swap_flags: int = chm.SWAP_AUTO, oom_host_bytes: int = 0, **algo1):
+                 swap_flags: int = chm.SWAP_AUTO, oom_host_bytes: int = 0, trials: int = 5, **algo1):
         self.host_only = device is None
         self.dev = torch.device("cpu") if self.host_only else torch.device("cuda", device)
         self.ctx = chm.Context(device=-1 if self.host_only else device, swap_ctas=swap_ctas,
@@ -188,6 +191,9 @@ class Runtime:
                                max(int(host_arena_bytes) + int(oom_host_bytes), 1 << 20),
                                **algo1)
         self.search_rounds = int(search_rounds)
+        self.n_trials = int(trials)  # plans tried on real steps before one is kept (n = 5)
+        self.trials = None
+        self.trial_running = False
         self._detect_bytes = bool(algo1.get("detect_bytes", 0))  # Q4 needs every op's outputs
         self.rec = chm.Recorder(self.ctx)
         self.light = False
@@ -276,6 +282,7 @@ class Runtime:
         self._in_step = True
         # the ctx records every GenPolicy step in Detailed mode; the runtime pays for
         # free polling and allocator reads only on the step it will plan from
+        self.trial_running = self.trials is not None  # this step executes the current trial plan
         self.detailed = (self.stage == chm.GENPOLICY and self.need_plan) or self.force_plan
         if self.force_plan:
             self.ctx.set_detailed(True)
@@ -322,6 +329,9 @@ class Runtime:
             if self.policy is not None:
                 self._uninstall()
             self.need_plan = True
+            self.trials = None
+        elif self.trials is not None and self.trial_running:
+            self._trial_done(t_iter)
         if self.force_plan:
             self.ctx.set_detailed(False)
         if self.detailed and not d["changed"] and (self.force_plan or (stage_before == chm.GENPOLICY and self.need_plan)):
@@ -622,7 +632,7 @@ class Runtime:
             plan.update(kind="generator-host", items=len(items), tensors=[int(x) for x in items["t"]])
             self.policy = (pt, plan)
         else:
-            keys = []
+            cands = []  # (name, key, selection, is_item_list)
             t1 = time.perf_counter()
             if pt.K <= 4096:  # SEEDED base mask travels in kernel params
                 best = torch.empty(5, dtype=torch.int64, device=self.dev)
@@ -631,45 +641,109 @@ class Runtime:
                 self.ctx.eval_policies(pt, kind, 0, n, best=best, seed=self.seed, flip_thr=self.flip_thr)
                 k = best.cpu().numpy().view(chm.BEST_DTYPE)[0]
                 words = pt.candidate_mask(kind, int(k["index"]), seed=self.seed, flip_thr=self.flip_thr)
-                keys.append(("seeded" if kind == chm.SEEDED else "exhaustive", k, words))
+                cands.append(("seeded" if kind == chm.SEEDED else "exhaustive", k, words, False))
             plan["eval_ms"] = (time.perf_counter() - t1) * 1e3
             t1 = time.perf_counter()
-            gen = []
-            if self.use_generator:
-                gen = _generate_all(pt)
+            gen = _generate_all(pt) if self.use_generator else []
             if gen:
                 off = np.zeros(len(gen) + 1, np.uint64)
                 off[1:] = np.cumsum([len(x) for x in gen])
-                gbest = torch.empty(5, dtype=torch.int64, device=self.dev)
-                self.ctx.eval_policies(pt, chm.EXPLICIT, 0, len(gen), best=gbest, item_offsets=off,
-                                       items=np.concatenate(gen))
-                gk = gbest.cpu().numpy().view(chm.BEST_DTYPE)[0]
-                keys.append(("generator", gk, gen[int(gk["index"])]))
+                gkeys = torch.empty(5, dtype=torch.int64, device=self.dev)
+                gpk = torch.empty(len(gen), dtype=torch.int64, device=self.dev)
+                gst = torch.empty(len(gen), dtype=torch.float64, device=self.dev)
+                gsw = torch.empty(len(gen), dtype=torch.int64, device=self.dev)
+                self.ctx.eval_policies(pt, chm.EXPLICIT, 0, len(gen), best=gkeys, item_offsets=off,
+                                       items=np.concatenate(gen), peak=gpk, stall=gst, swapped=gsw)
+                pk, stl, swp = gpk.cpu().numpy(), gst.cpu().numpy(), gsw.cpu().numpy()
+                for j, g in enumerate(gen):  # every variant a key of its own (for the trials)
+                    kj = np.zeros(1, chm.BEST_DTYPE)[0]
+                    kj["excess"], kj["stall"], kj["swapped_bytes"] = max(0, int(pk[j]) - pt.budget), stl[j], swp[j]
+                    kj["index"], kj["peak"] = j, pk[j]
+                    cands.append((f"generator[{j}]", kj, g, True))
             plan["generator_ms"] = (time.perf_counter() - t1) * 1e3
             t1 = time.perf_counter()
-            if keys and keys[0][0] == "seeded" and self.search_rounds:
-                k, words, rounds = self._local_search(pt, keys[0][1], keys[0][2])
-                keys[0] = ("seeded+search", k, words)
+            if self.search_rounds and pt.K <= 4096:
+                starts = [c for c in cands if not c[3]][:1]
+                gen_c = sorted((c for c in cands if c[3]), key=lambda c: self._key(c[1]))[:1]
+                for c in gen_c:  # the generator's best as a mask (solo timing) to descend from
+                    starts.append((c[0] + "->mask", None, self._items_to_mask(pt, c[2]), False))
+                rounds = 0
+                for name, k0, w0, _ in starts:
+                    if k0 is None:
+                        kb = torch.empty(5, dtype=torch.int64, device=self.dev)
+                        self.ctx.eval_policies(pt, chm.FLIP1, pt.K, 1, best=kb, base=w0)  # the mask itself
+                        k0 = kb.cpu().numpy().view(chm.BEST_DTYPE)[0]
+                    k, w, r = self._local_search(pt, k0, w0)
+                    rounds += r
+                    cands.append((name + "+search", k, w, False))
                 plan["search_rounds"] = rounds
             plan["search_ms"] = (time.perf_counter() - t1) * 1e3
-            name, k, sel = min(keys, key=lambda x: self._key(x[1]))
-            plan.update(kind=name, excess=int(k["excess"]), stall=float(k["stall"]),
-                        swapped=int(k["swapped_bytes"]), peak=int(k["peak"]))
+            # distinct plans, best key first; the n best are tried on real steps
+            cands.sort(key=lambda c: self._key(c[1]))
+            # trial only plans as feasible as the best, and not ones whose host traffic (and pinned
+            # arena) dwarfs the best one's -- an unrefined start its own descent has improved on
+            b0 = cands[0][1]
+            cands = [c for c in cands if int(c[1]["excess"]) == int(b0["excess"])
+                     and int(c[1]["swapped_bytes"]) <= 1.5 * int(b0["swapped_bytes"]) + (64 << 20)]
+            uniq, seen = [], set()
+            for c in cands:
+                sig = (c[3], c[2].tobytes())
+                if sig not in seen:
+                    seen.add(sig)
+                    uniq.append(c)
+            uniq = uniq[:max(1, self.n_trials)]
             t1 = time.perf_counter()
-            if name == "generator":
-                self._reserve_items(sel, pt)
-                self.ctx.policy_install_items(pt, sel)
-                self.policy_items = np.array(sel, chm.ITEM_DTYPE)
-            else:
-                self._reserve_words(sel, pt)
-                self.ctx.policy_install(pt, sel)
-                self.policy_items = pt.mask_items(sel)
-            plan.update(items=len(self.policy_items), tensors=[int(x) for x in self.policy_items["t"]])
-            plan["install_ms"] = (time.perf_counter() - t1) * 1e3  # includes pinning arena growth
+            for c in uniq:  # the arena for the largest of them
+                (self._reserve_items if c[3] else self._reserve_words)(c[2], pt)
             self.policy = (pt, plan)
+            self._install_cand(pt, plan, uniq[0])
+            plan["install_ms"] = (time.perf_counter() - t1) * 1e3  # includes pinning arena growth
+            if len(uniq) > 1:
+                self.trials = dict(pt=pt, plan=plan, cands=uniq, times=[])
+                plan["trial_plans"] = [c[0] for c in uniq]
         plan["plan_ms"] = (time.perf_counter() - t0) * 1e3
         self.stats["plan_ms"] += plan["plan_ms"]
         self.plans.append(plan)
+
+    def _install_cand(self, pt, plan, cand):
+        name, k, sel, is_items = cand
+        if is_items:
+            self.ctx.policy_install_items(pt, sel)
+            self.policy_items = np.array(sel, chm.ITEM_DTYPE)
+        else:
+            self.ctx.policy_install(pt, sel)
+            self.policy_items = pt.mask_items(sel)
+        plan.update(kind=name, excess=int(k["excess"]), stall=float(k["stall"]), swapped=int(k["swapped_bytes"]),
+                    peak=int(k["peak"]), items=len(self.policy_items),
+                    tensors=[int(x) for x in self.policy_items["t"]])
+
+    def _items_to_mask(self, pt, items):
+        """the swappable-set mask of an item list's tensors (their solo timing)"""
+        tb = pt.tables()
+        k_of_rank = {int(t): k for k, t in enumerate(tb["tensor"])}
+        w = np.zeros(max(pt.W, 1), np.uint64)
+        for t in items["t"]:
+            k = k_of_rank.get(int(t))
+            if k is not None:
+                w[k // 64] |= np.uint64(1 << (k % 64))
+        return w[:pt.W]
+
+    def _trial_done(self, t_iter):
+        """"generates five different policies and selects the one with the best runtime
+        performance": the step that just ended ran trial len(times); try the next or keep the
+        fastest"""
+        tr = self.trials
+        tr["times"].append(t_iter)
+        plan = tr["plan"]
+        if len(tr["times"]) < len(tr["cands"]):
+            self._install_cand(tr["pt"], plan, tr["cands"][len(tr["times"])])
+            return
+        j = int(np.argmin(tr["times"]))
+        plan["trials"] = [dict(plan=c[0], step_s=round(t, 5), predicted_stall_s=float(c[1]["stall"]))
+                          for c, t in zip(tr["cands"], tr["times"])]
+        self._install_cand(tr["pt"], plan, tr["cands"][j])
+        plan["chosen"] = tr["cands"][j][0]
+        self.trials = None
 
     def _local_search(self, pt, key, words):
         return descend(self.ctx, pt, key, words, self.dev, self.search_rounds)

@@ -29,7 +29,7 @@ def main():
     ap.add_argument("--seq", type=int, default=4096)
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--budget-frac", type=float, default=0.6, help="budget = M0 + frac x no-swap activation peak")
-    ap.add_argument("--steps", type=int, default=9)
+    ap.add_argument("--steps", type=int, default=12)
     ap.add_argument("--plain-steps", type=int, default=2)
     ap.add_argument("--candidates", type=int, default=1 << 16)
     ap.add_argument("--search-rounds", type=int, default=4096)

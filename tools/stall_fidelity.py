@@ -64,7 +64,8 @@ def main():
     m0 = torch.cuda.memory_allocated()
     flags = dict(kernel=chm.SWAP_KERNEL, ce=chm.SWAP_CE, auto=chm.SWAP_AUTO)[args.flags]
     rt = Runtime(0, hbm_budget=m0 + act_peak, groups_fwd=args.layers, groups_bwd=args.layers,
-                 host_arena_bytes=int(args.arena_gib * 2 ** 30), swap_ctas=args.swap_ctas, swap_flags=flags)
+                 host_arena_bytes=int(args.arena_gib * 2 ** 30), swap_ctas=args.swap_ctas, swap_flags=flags,
+                 trials=1)  # one plan per budget: its predicted stall against its measured slowdown
     for _ in range(4):  # WarmUp -> GenPolicy; the first plan fits (no policy)
         one(rt)
     rows = []

@@ -68,7 +68,7 @@ def main():
     every["k"] = 0
     for row in list(out["rows"]):
         budget = int(row["peak_gib"] * gib)
-        rt = Runtime(0, hbm_budget=budget, groups_fwd=32, groups_bwd=32, host_arena_bytes=int(64 * gib))
+        rt = Runtime(0, hbm_budget=budget, groups_fwd=32, groups_bwd=32, host_arena_bytes=int(64 * gib), trials=1)
         for _ in range(4):  # WarmUp -> GenPolicy (plan)
             one(rt)
         t, p = med(rt)
