@@ -70,6 +70,10 @@ def test_runtime_swaps_are_bit_exact_and_lower_the_peak(reference):
     run = _train(rt)
     _check_exact(run, reference)
     assert len(rt.plans) == 1 and rt.plans[0]["items"] > 0, rt.plans
+    plan = rt.plans[0]
+    if len(plan.get("trial_plans", [])) > 1:  # the fastest measured trial is kept
+        times = [t["step_s"] for t in plan["trials"]]
+        assert plan["chosen"] == plan["trials"][times.index(min(times))]["plan"] == plan["kind"]
     st = rt.stats
     assert st["release"] > 0 and st["released_bytes"] > 0 and st["demand_swap_in"] == 0
     ex = rt.ctx.exec_stats()
