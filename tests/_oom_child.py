@@ -14,7 +14,7 @@ from workloads import tiny_gpt as G  # noqa: E402
 CFG = dict(vocab=512, d=256, n_layer=6, n_head=8, seq=256)
 
 
-def train(rt=None, steps=6):
+def train(rt=None, steps=10):
     dev = torch.device("cuda:0")
     model = G.make(0, dev, **CFG)
     opt = torch.optim.SGD(model.parameters(), lr=0.05)
@@ -40,13 +40,15 @@ def train(rt=None, steps=6):
 
 def main():
     frac = float(sys.argv[1])
+    budget_frac = float(sys.argv[2]) if len(sys.argv) > 2 else None  # plan a policy for this budget
     torch.cuda.reset_peak_memory_stats()
     base = torch.cuda.memory_allocated()
     ref_losses, ref_params = train()
     peak = torch.cuda.max_memory_allocated() - base
     torch.cuda.empty_cache()
     total = torch.cuda.get_device_properties(0).total_memory
-    rt = Runtime(0, hbm_budget=1 << 62, groups_fwd=6, groups_bwd=6, oom_host_bytes=1 << 30)
+    budget = (1 << 62) if budget_frac is None else torch.cuda.memory_allocated() + int(budget_frac * peak)
+    rt = Runtime(0, hbm_budget=budget, groups_fwd=6, groups_bwd=6, oom_host_bytes=1 << 30, trials=1)
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
     cap = torch.cuda.memory_reserved() + int(frac * peak)
@@ -62,7 +64,7 @@ def main():
     torch.cuda.empty_cache()
     losses, params = train(rt)
     out.update(losses_equal=losses == ref_losses, params_equal=bool(torch.equal(params, ref_params)),
-               stats=rt.stats, stages=rt.stage)
+               stats=rt.stats, stages=rt.stage, plans=[{k: v for k, v in p.items() if k != "tensors"} for p in rt.plans])
     print(json.dumps(out))
 
 

@@ -24,3 +24,17 @@ def test_runtime_survives_a_memory_cap_with_passive_swaps(frac):
     assert out["losses_equal"] and out["params_equal"], out
     st = out["stats"]
     assert st["oom"] > 0 and st["passive"] > 0 and st["passive_restored"] == st["passive"], st
+
+
+def test_runtime_policy_under_a_tighter_cap_releases_early():
+    """a policy planned for 80% of the activation peak, run under a 50% cap: OOMs inside ops go
+    through chm_oom_release first (marked blocks released early), then passive swaps; still
+    bit-identical training"""
+    child = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_oom_child.py")
+    r = subprocess.run([sys.executable, child, "0.5", "0.8"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out["losses_equal"] and out["params_equal"], out
+    st = out["stats"]
+    assert out["plans"] and out["plans"][0]["items"] > 0 and st["release"] > 0, out
+    assert st["oom"] > 0 and st["oom_released"] + st["passive"] > 0, st
