@@ -130,6 +130,14 @@ typedef struct {                 /* library-owned; valid until the next chm_reco
  * tensors, frees and live bytes.  If a policy is installed, App. A tensor
  * features are updated and the op's swap actions are returned in *actions (nullable). */
 chm_status chm_record_op(chm_ctx *ctx, const chm_op_record *op, chm_actions *actions);
+/* Lightweight mode in bulk: appends n operator tokens (and their phases) to the current
+ * iteration, as n chm_record_op calls without tensors would -- a hook can buffer an iteration's
+ * tokens and hand them over once.  An iteration started this way is recorded Lightweight (the
+ * ctx's Detailed request for it is dropped; the last Detailed record is kept).  CHM_E_STATE
+ * while a non-empty policy is installed (its actions need chm_record_op per op) or when the
+ * iteration already holds Detailed records; CHM_E_INVAL on a token < 1 or a phase out of
+ * FWD* BWD* OPT* order (the entries before the bad one are kept). */
+chm_status chm_record_tokens(chm_ctx *ctx, const int32_t *tokens, const uint8_t *phases, uint32_t n);
 /* force (1) or stop forcing (0) Detailed recording from the next chm_record_op on */
 chm_status chm_set_detailed(chm_ctx *ctx, int32_t detailed);
 

@@ -169,7 +169,7 @@ EXPORTS = [
     "chm_policy_install", "chm_policy_install_items", "chm_generate_policy", "chm_exec_stats_get", "chm_host_arena", "chm_swap_out", "chm_swap_in",
     "chm_batch_wait", "chm_batch_query", "chm_batch_elapsed", "chm_arena_reserve", "chm_issue_swap_out", "chm_issue_swap_in", "chm_item_wait",
     "chm_oom_release", "chm_passive_swap", "chm_passive_restore", "chm_trace_load", "chm_record_save",
-    "chm_stall_models",
+    "chm_stall_models", "chm_record_tokens",
 ]
 
 _lib = None
@@ -222,6 +222,7 @@ def load(path: str = LIB_PATH):
         "chm_trace_load": (i32, [vp, C.c_char_p, C.c_size_t, P(TraceParams), P(vp), P(i64)]),
         "chm_record_save": (i32, [vp, vp, C.c_size_t, P(C.c_size_t)]),
         "chm_stall_models": (i32, [vp, vp, u32, vp]),
+        "chm_record_tokens": (i32, [vp, vp, vp, u32]),
         "chm_passive_swap": (i32, [vp, i64, vp, u32, vp, u32, vp, vp, P(Passive)]),
         "chm_passive_restore": (i32, [vp, u64, u64, vp, vp]),
     }
@@ -380,6 +381,15 @@ class Context:
         rec = OpRecord(token, phase, ni, no, nf, a_in, a_out, a_fr, live_bytes)
         _check(load().chm_record_op(self.h, C.byref(rec), C.byref(self._actions)))
         return self._actions
+
+    def record_tokens(self, tokens, phases):
+        """Lightweight mode in bulk: an iteration's operator tokens and phases at once"""
+        t = np.ascontiguousarray(tokens, np.int32)
+        ph = np.ascontiguousarray(phases, np.uint8)
+        if t.size != ph.size:
+            raise ValueError("tokens and phases differ in length")
+        _check(load().chm_record_tokens(self.h, _ptr(t) if t.size else None, _ptr(ph) if ph.size else None,
+                                        int(t.size)))
 
     def detect_seq_change(self, t_iter: float):
         st, ch, ld, cs = C.c_int32(), C.c_int32(), C.c_double(), C.c_double()

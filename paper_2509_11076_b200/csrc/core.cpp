@@ -237,6 +237,24 @@ extern "C" chm_status chm_record_op(chm_ctx *ctx, const chm_op_record *op, chm_a
   return CHM_OK;
 }
 
+extern "C" chm_status chm_record_tokens(chm_ctx *ctx, const int32_t *tokens, const uint8_t *phases, uint32_t n) {
+  if (!ctx || (n && (!tokens || !phases))) CHM_FAIL(CHM_E_INVAL, "chm_record_tokens: NULL argument");
+  if (ctx->policy_active && !ctx->items.empty())
+    CHM_FAIL(CHM_E_STATE, "chm_record_tokens: a policy is installed (chm_record_op per op)");
+  IterRecord &R = ctx->cur;
+  if (R.detailed && !R.tokens.empty() && n)
+    CHM_FAIL(CHM_E_STATE, "chm_record_tokens: this iteration is being recorded in Detailed mode");
+  if (R.tokens.empty()) R.detailed = false;  // a bulk-recorded iteration is Lightweight
+  for (uint32_t j = 0; j < n; j++) {
+    if (tokens[j] < 1) CHM_FAIL(CHM_E_INVAL, "chm_record_tokens: token %d < 1 at %u", tokens[j], j);
+    if (phases[j] > CHM_OPT || (!R.phase.empty() && phases[j] < R.phase.back()))
+      CHM_FAIL(CHM_E_INVAL, "chm_record_tokens: bad or interleaved phase at %u", j);
+    R.tokens.push_back(tokens[j]);
+    R.phase.push_back(phases[j]);
+  }
+  return CHM_OK;
+}
+
 // Positional (cos_mode 0) or histogram (cos_mode 1) cosine similarity of two token
 // sequences: dot and squared norms are exact int64 sums, then one double divide + sqrt.
 static bool seq_compare(const std::vector<int32_t> &a, const std::vector<int32_t> &b,

@@ -150,6 +150,22 @@ class _Mode(TorchDispatchMode):
     def __torch_dispatch__(self, func, types, args=(), kwargs=None):
         kwargs = kwargs or {}
         rt = self.rt
+        if rt.light:  # Lightweight, nothing installed (no policy, no OOM handling): token + phase only
+            out = func(*args, **kwargs)
+            tok = rt._tok.get(func)
+            if tok is None:
+                tok = rt._token(func)
+            if torch._C._current_graph_task_id() != -1:
+                rt.bwd_seen = True
+                phase = chm.BWD
+            else:
+                phase = chm.OPT if rt.bwd_seen else chm.FWD
+            if phase < rt.last_phase:
+                phase = rt.last_phase
+            rt.last_phase = phase
+            rt.tok_buf.append(tok)
+            rt.ph_buf.append(phase)
+            return out
         if rt._internal:  # the runtime's own allocations / views (autograd unpack hook)
             return func(*args, **kwargs)
         rt._flush()
@@ -238,6 +254,9 @@ class Runtime:
             raise RuntimeError("Runtime.step is not reentrant")
         self._begin()
         mode = _Mode(self)
+        # the hooks stay on in every step: registered saved-tensor hooks change the operator
+        # sequence autograd dispatches (e.g. detaches), so steps with and without them would not
+        # compare as the same sequence in Algo. 1
         try:
             with torch.autograd.graph.saved_tensors_hooks(self._pack, self._unpack), mode:
                 yield self
@@ -254,6 +273,7 @@ class Runtime:
         sequence is short, so Algo. 1 sees a change and the policy is re-planned), drop the
         step's boxes and any passive copies"""
         self.pending = None
+        self.tok_buf, self.ph_buf = [], []
         if not self.host_only:
             torch.cuda.synchronize(self.dev)
         for hd in list(self.passive_out):
@@ -298,6 +318,7 @@ class Runtime:
         self.item_holder = {}  # policy item -> (weak holder, address, host offset, bytes)
         self.n_ops = 0
         self.log = []
+        self.tok_buf, self.ph_buf = [], []
         if not self.host_only:
             torch.cuda.synchronize(self.dev)
             self.m0 = torch.cuda.memory_allocated(self.dev)
@@ -306,6 +327,9 @@ class Runtime:
         self.t0 = time.perf_counter()
 
     def _end(self):
+        if self.tok_buf:
+            self.ctx.record_tokens(self.tok_buf, self.ph_buf)
+            self.n_ops += len(self.tok_buf)
         if not self.host_only:
             torch.cuda.synchronize(self.dev)
         t_iter = time.perf_counter() - self.t0
@@ -380,8 +404,9 @@ class Runtime:
         # recorded in the later phase, so only tensors of the first forward are swap candidates
         phase = max(phase, self.last_phase)
         self.last_phase = phase
-        if self.light:  # Lightweight mode, nothing installed: the token is the whole record
-            self.pending = (self._token(func), phase, (), (), -1)
+        if self.light:  # Lightweight mode, nothing installed: the token is the whole record,
+            self.tok_buf.append(self._token(func))  # handed over in bulk at the step's end
+            self.ph_buf.append(phase)
             return
         flat_in, flat_out = [], []
         _collect(args, flat_in)

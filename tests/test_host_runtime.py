@@ -286,3 +286,22 @@ def test_auto_groups_on_a_real_model_sequence():
             opt.zero_grad()
     assert rt.plans and rt.policy is not None
     assert rt.policy[0].L == 4 + 4 + 1  # 4 FWD + 4 BWD logical layers + the optimizer's group
+
+
+def test_record_tokens_equals_per_op_records():
+    """chm_record_tokens (bulk Lightweight mode) drives Algo. 1 exactly like chm_record_op per op"""
+    rng = np.random.default_rng(11)
+    base = rng.integers(1, 40, size=300).astype(np.int32)
+    phases = np.array([0] * 120 + [1] * 170 + [2] * 10, np.uint8)
+    a, b = host_ctx(), host_ctx()
+    for it in range(14):
+        seq = base if it < 8 else np.concatenate([base, base[:40]])  # a change at iteration 8
+        ph = phases if it < 8 else np.concatenate([phases[:120], np.zeros(40, np.uint8), phases[120:]])
+        for t, p in zip(seq, ph):
+            a.record_op(int(t), int(p))
+        b.record_tokens(seq, ph)
+        assert a.detect_seq_change(1e-3) == b.detect_seq_change(1e-3)
+    with pytest.raises(chm.ChmError):
+        b.record_tokens([1, 0], [0, 0])  # token 0
+    with pytest.raises(chm.ChmError):
+        b.record_tokens([1, 2], [1, 0])  # interleaved phases
