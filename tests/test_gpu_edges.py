@@ -102,3 +102,19 @@ def test_search_and_full_agree_on_many_candidates(ctx):
     b = run_eval(ctx, pt, chm.SEEDED, 0, 50000, footprint=True, seed=sd["seed"], flip_thr=sd["flip_thr"])
     assert np.array_equal(a["peak"], b["peak"]) and np.array_equal(a["stall"], b["stall"])
     assert np.array_equal(b["footprint"].max(axis=1), b["peak"])  # peak = max of the row
+
+
+@pytest.mark.parametrize("gf,gb", [(100, 100), (40, 20), (1, 1)])
+def test_layer_counts_across_lane_blockings(ctx, gf, gb):
+    """L from 3 to 201 logical layers: each lane of the replay warp owns E = P/32 layers
+    (P the next power of two >= L), E = 1 .. 8 -- keys and rows vs the oracle"""
+    import dataclasses
+    tr = W.random_trace(77, n_layers=50, ops_per_layer=3, bw=1e8, t_iter=1e-3)
+    tr = dataclasses.replace(tr, groups_fwd=gf, groups_bwd=gb)
+    pt = product_trace(ctx, tr)
+    m = O.Model(tr)
+    assert pt.L == m.L
+    for first, count in ((0, 3000), (12345, 777)):
+        res = run_eval(ctx, pt, chm.SEEDED, first, count, footprint=True, seed=9, flip_thr=int(0.1 * 2 ** 64))
+        ref = m.eval(O.SEEDED, first, count, seed=9, flip_thr=int(0.1 * 2 ** 64), footprint=True, nthreads=8)
+        assert_same(res, ref, tr.budget)
