@@ -63,6 +63,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--force-dist", action="store_true", help="NCCL argmin path even at N = 1 (one-rank group)")
     return ap.parse_args()
 
 
@@ -284,7 +285,15 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2509_11076_b200 import chm
-    if world > 1:
+    # collectives run whenever a process group is up: N > 1, or --force-dist at N = 1 (the NCCL
+    # argmin path exercised on one GPU: a one-rank all-gather)
+    use_dist = world > 1 or args.force_dist
+    if use_dist:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
@@ -292,18 +301,18 @@ def main():
     P = world
 
     def barrier():
-        if P > 1:
+        if use_dist:
             dist.barrier()
 
     def max_over_ranks(x: float) -> float:
-        if P == 1:
+        if not use_dist:
             return x
         t = torch.tensor([x], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(x: float) -> float:
-        if P == 1:
+        if not use_dist:
             return x
         t = torch.tensor([x], dtype=torch.float64, device=dev)
         dist.all_reduce(t)
@@ -342,7 +351,7 @@ def main():
                           peak=peak, stall=stall, footprint=fp, ld=ld if full else 0, stream=comp)
         if ev_kernel is not None:
             ev_kernel.record(comp)  # replay kernel done; the rest is the argmin exchange
-        if P > 1:
+        if use_dist:
             dist.all_gather_into_tensor(gathered, best_local)
             ctx.best_reduce_device(gathered, P, best_global, comp)
         else:
@@ -447,7 +456,7 @@ def main():
             ev[3].record(comp)
             torch.cuda.synchronize()
             barrier()
-            launches += n_l + 1 + (1 if P > 1 else 0)
+            launches += n_l + 1 + (1 if use_dist else 0)
             launches_swap = n_l
             step_ms.append(ev[0].elapsed_time(ev[3]))
             eval_ms.append(ev[1].elapsed_time(ev_k))
@@ -491,7 +500,7 @@ def main():
         pt2 = ctx.trace_build(tr.budget, tr.static_bytes, tr.bw, tr.groups_fwd, tr.groups_bwd, t_iter=tr.t_iter)
         ctx.eval_policies(pt2, chm.SEEDED, lo, cnt, best=best_local, seed=sd["seed"], flip_thr=sd["flip_thr"],
                           peak=peak, stall=stall, footprint=fp, ld=ld if full else 0, stream=comp)
-        if P > 1:
+        if use_dist:
             dist.all_gather_into_tensor(gathered, best_local)
             ctx.best_reduce_device(gathered, P, best_global, comp)
         else:
@@ -550,7 +559,7 @@ def main():
     e2e_t = max_over_ranks(float(np.mean(e2e_ms))) if e2e_ms else None
     if rank != 0:
         ctx.close()
-        if P > 1:
+        if use_dist:
             dist.destroy_process_group()
         return
     line = {
@@ -599,7 +608,7 @@ def main():
             "algorithmic_bytes_per_launch": fp_bytes,
             "frac_of_spec_8TBps": fp_bytes / (t_eval * 1e-3) / 1e9 / 8000.0,
         },
-        "argmin_exchange_us": t_argmin * 1e3 if P > 1 else None,
+        "argmin_exchange_us": t_argmin * 1e3 if use_dist else None,
         "eval": {"candidates_per_s": C / (t_eval * 1e-3), "ms_per_launch": t_eval, "unit": "candidates/s"},
         "ce_baseline": {
             "what": "same batches, one cudaMemcpyAsync per tensor on the copy engines",
@@ -628,7 +637,7 @@ def main():
         line["cpu_baseline"] = cpu_baseline(args, tr, bytes_swap)
     print(json.dumps(line), flush=True)
     ctx.close()
-    if P > 1:
+    if use_dist:
         dist.destroy_process_group()
 
 
