@@ -12,28 +12,32 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libchm.so")
+LIB_DEBUG = os.path.join(HERE, "libchm_debug.so")  # device-side bounds checks (CHM_DEBUG)
 SOURCES = ["core.cpp", "trace.cpp", "executor.cpp", "generator.cpp", "oom.cpp", "trace_io.cpp", "stall.cpp", "swap.cu", "replay.cu", "explicit.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, s) for s in SOURCES] + [os.path.join(CSRC, "internal.h"),
                                                        os.path.join(ROOT, "include", "chm.h"),
                                                        os.path.abspath(__file__)]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
-    objdir = os.path.join(HERE, "build")
+def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
+    """debug: libchm_debug.so with device-side bounds checks (CHM_DCHECK -> trap); load it with
+    CHM_LIB=<path> to run the tests against it"""
+    lib = LIB_DEBUG if debug else LIB
+    if not force and not _stale(lib):
+        return lib
+    objdir = os.path.join(HERE, "build_debug" if debug else "build")
     os.makedirs(objdir, exist_ok=True)
     common = ["-O3", "-std=c++17", "-lineinfo", "-I", os.path.join(ROOT, "include"),
-              "-Xcompiler", "-fPIC,-ffp-contract=off,-Wall", "--fmad=false"] + ARCH
+              "-Xcompiler", "-fPIC,-ffp-contract=off,-Wall", "--fmad=false"] + ARCH + (["-DCHM_DEBUG"] if debug else [])
     objs = []
     for src in SOURCES:
         obj = os.path.join(objdir, src + ".o")
@@ -46,12 +50,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
             print(" ".join(cmd), flush=True)
         subprocess.check_call(cmd)
         objs.append(obj)
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC] + ARCH + ["-shared", "-o", tmp] + objs +
                           ["-Xlinker", "-rpath,/usr/local/cuda/lib64", "-lcudart_static", "-lrt", "-lpthread", "-ldl"])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, debug="--debug" in sys.argv))

@@ -13,7 +13,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libchm.so")
+LIB_PATH = os.environ.get("CHM_LIB") or os.path.join(_HERE, "libchm.so")  # CHM_LIB: e.g. libchm_debug.so
 
 CHM_OK, CHM_E_INVAL, CHM_E_PARSE, CHM_E_STATE, CHM_E_NOMEM, CHM_E_CUDA, CHM_E_INFEASIBLE, CHM_E_NOKERNEL = \
     0, -1, -2, -3, -4, -5, -6, -7

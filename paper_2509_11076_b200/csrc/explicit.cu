@@ -63,6 +63,7 @@ __global__ void __launch_bounds__(256) replay_explicit_kernel(const __grid_const
   long long sw = 0;
   for (unsigned long long q = p.off[c] + tid; q < p.off[c + 1]; q += blockDim.x) {
     const chm_item it = p.items[q];
+    CHM_DCHECK(it.r >= 0 && it.r + 1 < it.s && it.s < p.N && (p.lay8[it.s] >> 3) < p.L && (p.lay8[it.r] >> 3) < p.L);
     const long long S = p.S_rank[it.t];
     atomicAdd(reinterpret_cast<unsigned long long *>(row + it.r + 1), (unsigned long long)(-S));
     atomicAdd(reinterpret_cast<unsigned long long *>(row + it.s), (unsigned long long)S);

@@ -10,6 +10,22 @@
 
 #include "../../include/chm.h"
 
+// device-side bounds checks of the debug build (build.py --debug): a failed check prints its
+// location and traps the kernel; compiled out otherwise
+#ifdef CHM_DEBUG
+#define CHM_DCHECK(c)                                                                  \
+  do {                                                                                 \
+    if (!(c)) {                                                                        \
+      printf("CHM_DCHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c);                \
+      __trap();                                                                        \
+    }                                                                                  \
+  } while (0)
+#else
+#define CHM_DCHECK(c) \
+  do {                \
+  } while (0)
+#endif
+
 namespace chm {
 
 // ---------------------------------------------------------------------------- errors

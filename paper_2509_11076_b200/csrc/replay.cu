@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
   uint64_t c0 = __shfl_sync(0xffffffffu, nxt, 0), c = c0;
   while (c < p.count) {
     if (lane == 0 && c == c0) nxt = atomicAdd(p.work, (unsigned long long)kGrab);
+    CHM_DCHECK(c < p.count);
     const uint64_t g = p.first + c;
     // decode: only the items whose bit differs from R add a signed delta to their layers
     if (seeded) {  // one hash word per 4 items (reading R-seeded); flips are ~flip_thr rare
@@ -224,6 +225,7 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
           f4 &= f4 - 1;
           const int k = 4 * q + e;
           if (k >= K) break;
+          CHM_DCHECK(li_[k] < L && lo_[k] < L);
           const bool was = (p.base[k >> 6] >> (k & 63)) & 1ull;
           const long long v = was ? -S[k] : S[k];
           acc_add(dI_hi, dI_lo, li_[k], v);
@@ -233,6 +235,7 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
     } else if (flip1) {  // one item differs from R: item g (none for g = K)
       if (lane == 0 && g < uint64_t(K)) {
         const int k = int(g);
+        CHM_DCHECK(li_[k] < L && lo_[k] < L);
         const bool was = (p.base[k >> 6] >> (k & 63)) & 1ull;
         const long long v = was ? -S[k] : S[k];
         acc_add(dI_hi, dI_lo, li_[k], v);
@@ -240,6 +243,7 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
       }
     } else {
       for (int k = lane; k < K; k += 32) {
+        CHM_DCHECK(li_[k] < L && lo_[k] < L);
         if (cand_bit(p, g, c, k)) {
           acc_add(dI_hi, dI_lo, li_[k], S[k]);
           acc_add(dO_hi, dO_lo, lo_[k], S[k]);
@@ -341,6 +345,7 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
           asm("ld.shared.v2.s64 {%0, %1}, [%2];" : "=l"(fx), "=l"(fy) : "r"(sF));
         }
         asm("ld.shared.u32 %0, [%1];" : "=r"(lz) : "r"(sL));
+        CHM_DCHECK((lz & 0xffffu) < 8u * unsigned(L) && (lz >> 16) < 8u * unsigned(L));
         asm("ld.shared.s64 %0, [%1];" : "=l"(d0) : "r"(sD + (lz & 0xffffu)));
         asm("ld.shared.s64 %0, [%1];" : "=l"(d1) : "r"(sD + (lz >> 16)));
         st_cs_v2(out, fx + d0, fy + d1);

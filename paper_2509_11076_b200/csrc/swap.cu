@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(kSwapThreads) swap_copy_kernel(const __grid_co
       if (p.chunk_begin[mid] <= c) lo = mid; else hi = mid;
     }
     const uint64_t off = (c - p.chunk_begin[lo]) << kChunkShift;
+    CHM_DCHECK(lo < p.n && c >= p.chunk_begin[lo] && off < p.bytes[lo]);
     const uint64_t len = min(kChunk, p.bytes[lo] - off);
     const char *s = reinterpret_cast<const char *>(p.src[lo]) + off;
     char *d = reinterpret_cast<char *>(p.dst[lo]) + off;
@@ -142,6 +143,7 @@ __global__ void __launch_bounds__(32) swap_bulk_kernel(const __grid_constant__ S
       if (p.chunk_begin[mid] <= c) lo = mid; else hi = mid;
     }
     const uint64_t off = (c - p.chunk_begin[lo]) * uint64_t(kBulkStage);
+    CHM_DCHECK(lo < p.n && off < p.bytes[lo]);
     len = unsigned(min(uint64_t(kBulkStage), p.bytes[lo] - off));
     src = reinterpret_cast<const char *>(p.src[lo]) + off;
     dst = reinterpret_cast<char *>(p.dst[lo]) + off;
