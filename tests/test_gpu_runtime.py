@@ -6,6 +6,8 @@ the Detailed step and every later step executes the policy with real swap kernel
 not change a single bit: losses and final parameters equal a plain run's exactly.  The policy must
 release bytes every step and lower the peak allocated memory.  With the swap-in actions dropped,
 every saved tensor comes back by demand swap-in (reading Q20) -- still bit-exact."""
+import contextlib
+
 import pytest
 
 torch = pytest.importorskip("torch")
@@ -19,7 +21,7 @@ BATCH = 16
 STEPS = 12
 
 
-def _train(rt=None, steps=STEPS):
+def _train(rt=None, steps=STEPS, amp=False):
     dev = torch.device("cuda:0")
     model = G.make(0, dev, **CFG)
     opt = torch.optim.SGD(model.parameters(), lr=0.05)
@@ -29,14 +31,17 @@ def _train(rt=None, steps=STEPS):
     for x, y in data:
         torch.cuda.reset_peak_memory_stats()
         base = torch.cuda.memory_allocated()
+        amp_ctx = torch.autocast("cuda", dtype=torch.bfloat16) if amp else contextlib.nullcontext()
         if rt is None:
-            loss = model(x, y)
+            with amp_ctx:
+                loss = model(x, y)
             loss.backward()
             opt.step()
             opt.zero_grad(set_to_none=True)
         else:
             with rt.step():
-                loss = model(x, y)
+                with amp_ctx:
+                    loss = model(x, y)
                 loss.backward()
                 opt.step()
                 opt.zero_grad(set_to_none=True)
@@ -97,4 +102,15 @@ def test_demand_swap_in_when_swap_ins_are_dropped(reference):
     run = _train(rt)
     _check_exact(run, reference)
     assert rt.stats["demand_swap_in"] > 0 and rt.stats["demand_swap_in"] == rt.stats["release"]
+    rt.close()
+
+
+def test_runtime_under_autocast_bf16():
+    """mixed precision (torch.autocast bf16): the cast ops are part of the profiled sequence and
+    the swapped activations are bf16 -- still bit-identical to the plain autocast run"""
+    ref = _train(amp=True)
+    rt = Runtime(0, hbm_budget=_budget(ref[2]), trials=1)
+    run = _train(rt, amp=True)
+    _check_exact(run, ref)
+    assert rt.plans and rt.stats["release"] > 0
     rt.close()

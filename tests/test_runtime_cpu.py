@@ -162,3 +162,31 @@ def test_interleaved_microbatches_and_a_failed_step():
     for x, y in data[10:]:
         step2(x, y)
     assert len(rt.plans) == 2 and rt.policy is not None
+
+
+def test_runtime_on_a_conv_net():
+    """not only transformers: a small CNN (conv / batch-norm / relu / pool / linear) profiles,
+    plans and matches every planned tensor each step"""
+    import torch.nn as nn
+    torch.manual_seed(0)
+    net = nn.Sequential(
+        nn.Conv2d(3, 16, 3, padding=1), nn.BatchNorm2d(16), nn.ReLU(),
+        nn.Conv2d(16, 16, 3, padding=1), nn.BatchNorm2d(16), nn.ReLU(), nn.MaxPool2d(2),
+        nn.Conv2d(16, 32, 3, padding=1), nn.BatchNorm2d(32), nn.ReLU(),
+        nn.Conv2d(32, 32, 3, padding=1), nn.BatchNorm2d(32), nn.ReLU(), nn.AdaptiveAvgPool2d(1),
+        nn.Flatten(), nn.Linear(32, 10))
+    opt = torch.optim.SGD(net.parameters(), lr=0.01, momentum=0.9)
+    rt = Runtime(None, hbm_budget=1)
+    g = torch.Generator().manual_seed(1)
+    matched = []
+    for _ in range(10):
+        x = torch.randn(4, 3, 32, 32, generator=g)
+        y = torch.randint(0, 10, (4,), generator=g)
+        with rt.step():
+            torch.nn.functional.cross_entropy(net(x), y).backward()
+            opt.step()
+            opt.zero_grad()
+        matched.append(rt.ctx.exec_stats()["n_matched"])
+    assert len(rt.plans) == 1 and rt.plans[0]["items"] > 0
+    per = np.diff([0] + matched)
+    assert per[-1] == rt.plans[0]["items"] and rt.ctx.exec_stats()["n_stale"] == 0
