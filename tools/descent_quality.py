@@ -1,3 +1,6 @@
+"""Plan quality of the descent (reading R-search) on traces small enough for EXHAUSTIVE: the
+best of 2,000 SEEDED candidates, its descent, and the exhaustive optimum, per trace (C1 and
+six random traces).  Prints one line per trace."""
 import numpy as np, torch, sys
 sys.path.insert(0, "/root/repo")
 from paper_2509_11076_b200 import chm

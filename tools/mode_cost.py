@@ -1,3 +1,5 @@
+"""Where the runtime hook's per-op cost goes on a host-bound model: step time without a hook,
+with an empty TorchDispatchMode, and under the runtime in Lightweight steps.  Prints one line."""
 import time, torch
 from torch.utils._python_dispatch import TorchDispatchMode
 import sys; sys.path.insert(0, "/root/repo")
