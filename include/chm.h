@@ -339,7 +339,8 @@ chm_status chm_exec_stats_get(chm_ctx *ctx, chm_exec_stats *s);
  *                      in *n_items; CHM_E_INVAL if more than cap) receives them; the caller drops
  *                      their device blocks and retries.  CHM_E_STATE on a host-only ctx.
  *   chm_passive_swap:  step (iv): swaps out the resident produced tensor (reported as an output of
- *                      chm_record_op and not freed since; not bound to a policy item) whose size
+ *                      chm_record_op in the current iteration and not freed since; not bound to
+ *                      a policy item) whose size
  *                      is closest to `need`: the smallest one of at least `need` bytes, else the
  *                      largest; ties: the older.  `exclude` (n_exclude ids, e.g. the current op's
  *                      inputs) is skipped; `only` (n_only ids, nullable = no restriction) limits

@@ -331,6 +331,7 @@ extern "C" chm_status chm_detect_seq_change(chm_ctx *ctx, double t_iter_s, chm_s
   }
   ctx->cur.clear();
   ctx->id_to_tensor.clear();
+  ctx->resident.clear();  // passive-swap candidates are this iteration's produced tensors
   for (auto &kv : ctx->passive) {  // still passively out: off the device from op 0 on
     ctx->cur.swaps.push_back({0, INT32_MAX, kv.second.nbytes, kv.second.id});
     kv.second.span = int32_t(ctx->cur.swaps.size()) - 1;
