@@ -114,3 +114,19 @@ def test_runtime_under_autocast_bf16():
     _check_exact(run, ref)
     assert rt.plans and rt.stats["release"] > 0
     rt.close()
+
+
+def test_soak_many_steps_bit_exact():
+    """200 steps under a policy (thousands of swap batches: the ctx's batch-event ring wraps)
+    end bit-identical to the plain run; host memory of the ctx stays bounded"""
+    import resource
+    steps = 200
+    ref = _train(steps=steps)
+    rt = Runtime(0, hbm_budget=_budget(ref[2]), trials=1)
+    rss0 = resource.getrusage(resource.RUSAGE_SELF).ru_maxrss
+    run = _train(rt, steps=steps)
+    _check_exact(run, ref)
+    batches = rt.stats["swap_out"] + rt.stats["swap_in"]
+    assert rt.stats["release"] > 0 and batches > 4096, rt.stats
+    assert resource.getrusage(resource.RUSAGE_SELF).ru_maxrss - rss0 < 512 * 1024  # KiB
+    rt.close()
