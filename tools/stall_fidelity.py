@@ -35,11 +35,20 @@ def main():
     ap.add_argument("--arena-gib", type=float, default=80.0)
     ap.add_argument("--swap-ctas", type=int, default=0, help="swap kernel CTAs (0: the library default, 8)")
     ap.add_argument("--flags", default="auto", choices=["kernel", "ce", "auto"])
+    ap.add_argument("--model", default="llama", choices=["llama", "gpt2xl"],
+                    help="gpt2xl: GPT-2 XL shape (48 layers, d 1600, 25 heads), fp32, attention written "
+                         "out (scores materialised), workloads/tiny_gpt.py; use --seq 1024 --batch 4")
     args = ap.parse_args()
-    cfg = dict(L.LLAMA2_7B, n_layer=args.layers)
-    model = L.make(cfg, max_seq=args.seq)
+    if args.model == "llama":
+        cfg = dict(L.LLAMA2_7B, n_layer=args.layers)
+        model = L.make(cfg, max_seq=args.seq)
+        x, y = L.batch(args.batch, args.seq, cfg["vocab"])
+    else:
+        from workloads import tiny_gpt as G
+        args.layers = 48
+        model = G.make(0, "cuda", vocab=50304, d=1600, n_layer=48, n_head=25, seq=args.seq)
+        x, y = G.batches(1, args.batch, args.seq, 50304, seed=1, device="cuda")[0]
     opt = torch.optim.SGD(model.parameters(), lr=1e-5)
-    x, y = L.batch(args.batch, args.seq, cfg["vocab"])
 
     def one(rt=None):
         torch.cuda.synchronize()
@@ -87,7 +96,9 @@ def main():
                          stall_layer_s=round(float(models[0]), 4), stall_per_direction_s=round(float(models[1]), 4),
                          stall_timeline_s=round(float(models[2]), 4),
                          step_s=round(t_pol, 4), measured_overhead_s=round(t_pol - t_np, 4), plan_ms=round(plan["plan_ms"], 1)))
-    out = dict(flags=args.flags, swap_ctas=args.swap_ctas or 8, model="llama2-7b" if args.layers == 32 else f"llama2-7b-{args.layers}L", dtype="bf16", batch=args.batch,
+    out = dict(flags=args.flags, swap_ctas=args.swap_ctas or 8,
+               model=("gpt2-xl-fp32" if args.model == "gpt2xl" else
+                      "llama2-7b" if args.layers == 32 else f"llama2-7b-{args.layers}L"), dtype="fp32" if args.model == "gpt2xl" else "bf16", batch=args.batch,
                seq=args.seq, m0_gib=round(m0 / 2 ** 30, 3), no_swap_peak_gib=round((m0 + act_peak) / 2 ** 30, 3),
                plain_step_s=round(t_plain, 4), bw_GBps=round(rt.bw / 1e9, 2), rows=rows, exec=rt.ctx.exec_stats(),
                demand_swap_in=rt.stats["demand_swap_in"])
