@@ -32,6 +32,7 @@ struct Cand {
 
 extern "C" chm_status chm_generate_policy(const chm_trace *tr, const chm_gen_params *gp, chm_item *items,
                                           uint32_t cap, uint32_t *n_items, int32_t *feasible) {
+  CHM_NVTX("chm_generate_policy");
   if (!tr || !gp || !n_items || (cap && !items)) CHM_FAIL(CHM_E_INVAL, "chm_generate_policy: NULL argument");
   if (!(gp->rem_scale >= 0.0)) CHM_FAIL(CHM_E_INVAL, "chm_generate_policy: rem_scale < 0");
   const int32_t N = tr->N, L = tr->L;

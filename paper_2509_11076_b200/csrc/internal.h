@@ -26,6 +26,15 @@
   } while (0)
 #endif
 
+// NVTX ranges around the ABI's heavier calls (visible to nsys / ncu --nvtx; a no-op without a
+// tool attached).  Header-only NVTX v3 from the CUDA toolkit.
+#include <nvtx3/nvToolsExt.h>
+struct ChmNvtxRange {
+  explicit ChmNvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~ChmNvtxRange() { nvtxRangePop(); }
+};
+#define CHM_NVTX(name) ChmNvtxRange chm_nvtx_range_(name)
+
 namespace chm {
 
 // ---------------------------------------------------------------------------- errors

@@ -497,6 +497,7 @@ extern "C" chm_status chm_eval_policies(chm_ctx *ctx, const chm_trace *t, const 
 
 extern "C" chm_status chm_eval_policies_ex(chm_ctx *ctx, const chm_trace *t, const chm_candidates *c,
                                            const chm_eval_out *o, cudaStream_t stream, int64_t *err_index) {
+  CHM_NVTX("chm_eval_policies");
   if (err_index) *err_index = -1;
   if (!ctx || !t || !c || !o) CHM_FAIL(CHM_E_INVAL, "chm_eval_policies: NULL argument");
   if (!o->best) CHM_FAIL(CHM_E_INVAL, "chm_eval_policies: out.best is required");

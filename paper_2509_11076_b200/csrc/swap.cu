@@ -262,6 +262,7 @@ static chm_status validate_batch(chm_ctx *ctx, const chm_swap_desc *d, uint32_t 
 static chm_status swap_batch(chm_ctx *ctx, const chm_swap_desc *d, uint32_t n, cudaStream_t compute,
                              cudaStream_t swap, uint32_t flags, uint64_t *batch, int64_t *err,
                              bool to_host) {
+  CHM_NVTX(to_host ? "chm_swap_out" : "chm_swap_in");
   if (!ctx) CHM_FAIL(CHM_E_INVAL, "swap: NULL ctx");
   if (ctx->device < 0) CHM_FAIL(CHM_E_STATE, "swap: host-only ctx");
   if (flags > CHM_SWAP_AUTO) CHM_FAIL(CHM_E_INVAL, "swap: unknown flags %u", flags);

@@ -35,6 +35,7 @@ static int32_t auto_groups(const int32_t *tok, int32_t n) {
 }
 
 extern "C" chm_status chm_trace_build(chm_ctx *ctx, const chm_trace_params *P, chm_trace **out) {
+  CHM_NVTX("chm_trace_build");
   if (!ctx || !P || !out) CHM_FAIL(CHM_E_INVAL, "chm_trace_build: NULL argument");
   *out = nullptr;
   if (ctx->last_detailed.tokens.empty()) CHM_FAIL(CHM_E_STATE, "chm_trace_build: no Detailed-mode iteration recorded");

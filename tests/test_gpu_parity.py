@@ -178,6 +178,9 @@ def test_c2_bench_size_full_compare(ctx):
     for c in rng.choice(n, size=64, replace=False):
         one = m.eval(O.SEEDED, int(c), 1, seed=sd["seed"], flip_thr=sd["flip_thr"], footprint=True)
         assert np.array_equal(full["footprint"][c], one["footprint"][0])
+    # and every footprint row of the launch (2.1 GB), element by element
+    ref_full = m.eval(O.SEEDED, 0, n, seed=sd["seed"], flip_thr=sd["flip_thr"], footprint=True, nthreads=16)
+    assert np.array_equal(full["footprint"], ref_full["footprint"])
 
 
 @pytest.mark.parametrize("name", ["C3", "C4a", "C4b", "C5"])

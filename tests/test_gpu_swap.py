@@ -217,3 +217,22 @@ def test_round_trip_kernel_variants(variant):
         torch.cuda.synchronize()
         assert all(torch.equal(a, b) for a, b in zip(dst, src))
     c.close()
+
+
+@pytest.mark.parametrize("flags", [chm.SWAP_KERNEL, chm.SWAP_CE])
+def test_config_sized_tensor_round_trip(flags):
+    """the largest activation of the configs (C3: [18, 4096, 11008] bf16 = 1.51 GiB), plus 7 bytes
+    so the tail is not a multiple of 16, out and back byte-exact; the arena holds the same bytes"""
+    n = 18 * 4096 * 11008 * 2 + 7
+    c = chm.Context(device=0, host_arena_bytes=n + 4096)
+    src = rand_bytes(n, 7)
+    comp, s = torch.cuda.current_stream(), torch.cuda.Stream()
+    c.batch_wait(c.swap_out([(src.data_ptr(), 0, n)], comp, s, flags), comp)
+    torch.cuda.synchronize()
+    host = arena_view(c)
+    assert np.array_equal(host[:n], src.cpu().numpy())
+    dst = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    c.batch_wait(c.swap_in([(dst.data_ptr(), 0, n)], comp, s, flags), comp)
+    torch.cuda.synchronize()
+    assert torch.equal(dst, src)
+    c.close()
