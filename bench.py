@@ -589,6 +589,7 @@ def main():
             "parallelism": f"dp{P}: per-rank swapping, candidates sharded, NCCL argmin all-gather",
             "l2": "inputs larger than L2 (swap set and footprint rows are GBs per step)",
             "swap_ctas": args.swap_ctas, "arena_pin_s": round(t_pin, 2),
+            "arena": ctx.arena_placement(),  # mode 2 = mmap + mbind(GPU's node) + THP + cudaHostRegister
         },
         "roofline": {
             "bound": "pcie", "kernel": "swap_copy_kernel (D2H + H2D)", "achieved": achieved_swap,

@@ -75,7 +75,16 @@ typedef struct {
   uint32_t swap_variant;      /* swap kernel: 0 16 B ld/st (default), 1 + L2::256B prefetch
                                  on loads, 2 TMA bulk copies staged through shared memory
                                  (16 B-aligned batches; others fall back to 0)              */
+  uint32_t arena_mode;        /* host arena allocation: CHM_ARENA_AUTO (0) = REGISTER;
+                                 CHM_ARENA_HOSTALLOC: cudaHostAlloc(Mapped|Portable), first
+                                 touch; CHM_ARENA_REGISTER: mmap + mbind to arena_numa + THP +
+                                 parallel pre-fault + cudaHostRegister(Mapped|Portable)      */
+  int32_t arena_numa;         /* REGISTER: -1 (default) the GPU's node (its PCIe device's
+                                 sysfs numa_node; no binding when that is -1), -2 no binding,
+                                 >= 0 bind to that node                                      */
+  uint32_t arena_threads;     /* REGISTER: pre-fault threads (0: min(cores, 32))             */
 } chm_config;
+enum { CHM_ARENA_AUTO = 0, CHM_ARENA_HOSTALLOC = 1, CHM_ARENA_REGISTER = 2 };
 
 /* fills the paper's defaults */
 void chm_config_default(chm_config *cfg);
@@ -374,8 +383,14 @@ chm_status chm_passive_restore(chm_ctx *ctx, uint64_t handle, uint64_t dev, cuda
                                cudaStream_t swap);
 
 /* ---------------------------------------------------------------- swap execution (a9-a11) */
-/* The ctx's pinned, device-mapped host arena (cudaHostAllocMapped|Portable). */
+/* The ctx's pinned, device-mapped host arena (chm_config.arena_mode); device pointer == host
+ * pointer (UVA). Swapped bytes land in host DRAM; placing them on the GPU's own
+ * NUMA node keeps the DMA off the inter-socket link on multi-socket 8-GPU hosts. */
 chm_status chm_host_arena(chm_ctx *ctx, void **host_base, uint64_t *bytes);
+/* Where the current arena lives: *numa_node (-1: not bound), *mode (CHM_ARENA_HOSTALLOC /
+ * CHM_ARENA_REGISTER, -1: no arena), *pin_seconds (wall time of its allocation + pinning). Any
+ * output may be NULL. */
+chm_status chm_arena_placement(const chm_ctx *ctx, int32_t *numa_node, int32_t *mode, double *pin_seconds);
 /* Grows the arena to at least `bytes` (e.g. to the installed policy's swapped bytes).  The old
  * arena is released: call only while no swap batch is in flight (contents are not kept);
  * CHM_E_STATE while passive swaps hold data in it. */

@@ -34,7 +34,10 @@ class Config(C.Structure):
                 ("cos_mode", C.c_uint32), ("detect_bytes", C.c_uint32), ("device", C.c_int32),
                 ("host_arena_bytes", C.c_uint64), ("swap_ctas", C.c_uint32), ("eval_ctas_per_sm", C.c_uint32),
                 ("match_window", C.c_uint32), ("time_batches", C.c_uint32),
-                ("ce_min_bytes", C.c_uint64), ("swap_variant", C.c_uint32)]
+                ("ce_min_bytes", C.c_uint64), ("swap_variant", C.c_uint32), ("arena_mode", C.c_uint32),
+                ("arena_numa", C.c_int32), ("arena_threads", C.c_uint32)]
+
+ARENA_AUTO, ARENA_HOSTALLOC, ARENA_REGISTER = 0, 1, 2
 
 
 class TensorRef(C.Structure):
@@ -169,7 +172,7 @@ EXPORTS = [
     "chm_policy_install", "chm_policy_install_items", "chm_generate_policy", "chm_exec_stats_get", "chm_host_arena", "chm_swap_out", "chm_swap_in",
     "chm_batch_wait", "chm_batch_query", "chm_batch_elapsed", "chm_arena_reserve", "chm_issue_swap_out", "chm_issue_swap_in", "chm_item_wait",
     "chm_oom_release", "chm_passive_swap", "chm_passive_restore", "chm_trace_load", "chm_record_save",
-    "chm_stall_models", "chm_record_tokens",
+    "chm_stall_models", "chm_record_tokens", "chm_arena_placement",
 ]
 
 _lib = None
@@ -187,6 +190,7 @@ def load(path: str = LIB_PATH):
     P = C.POINTER
     sig = {
         "chm_config_default": (None, [P(Config)]),
+        "chm_arena_placement": (i32, [vp, P(i32), P(i32), P(dbl)]),
         "chm_create": (i32, [P(Config), P(vp)]),
         "chm_destroy": (None, [vp]),
         "chm_last_error": (C.c_char_p, []),
@@ -332,7 +336,8 @@ class Context:
     """One chm_ctx per device / rank (single owner, not thread-safe)."""
 
     def __init__(self, device: int = 0, host_arena_bytes: int = 0, swap_ctas: int = 0, eval_ctas_per_sm: int = 0,
-                 time_batches: bool = False, swap_variant: int = 0, ce_min_bytes: int = 0, **algo1):
+                 time_batches: bool = False, swap_variant: int = 0, ce_min_bytes: int = 0,
+                 arena_mode: int = ARENA_AUTO, arena_numa: int = -1, arena_threads: int = 0, **algo1):
         L = load()
         cfg = Config()
         L.chm_config_default(C.byref(cfg))
@@ -343,6 +348,9 @@ class Context:
         cfg.time_batches = 1 if time_batches else 0
         cfg.swap_variant = swap_variant
         cfg.ce_min_bytes = ce_min_bytes
+        cfg.arena_mode = arena_mode
+        cfg.arena_numa = arena_numa
+        cfg.arena_threads = arena_threads
         for k, v in algo1.items():
             setattr(cfg, k, v)
         h = C.c_void_p()
@@ -486,6 +494,13 @@ class Context:
 
     def arena_reserve(self, nbytes: int):
         _check(load().chm_arena_reserve(self.h, int(nbytes)))
+
+    def arena_placement(self) -> dict:
+        """{"numa_node": bound node or -1, "mode": ARENA_HOSTALLOC / ARENA_REGISTER / -1,
+        "pin_s": seconds the last allocation + pinning took}"""
+        n, m, t = C.c_int32(), C.c_int32(), C.c_double()
+        _check(load().chm_arena_placement(self.h, C.byref(n), C.byref(m), C.byref(t)))
+        return {"numa_node": n.value, "mode": m.value, "pin_s": t.value}
 
     def batch_query(self, batch: int) -> bool:
         d = C.c_int32()

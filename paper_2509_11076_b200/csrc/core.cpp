@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <new>
+#include <string>
 
 #include "internal.h"
 
@@ -47,6 +48,9 @@ extern "C" void chm_config_default(chm_config *c) {
   c->time_batches = 0;
   c->swap_variant = 0;
   c->ce_min_bytes = 0;
+  c->arena_mode = CHM_ARENA_AUTO;
+  c->arena_numa = -1;
+  c->arena_threads = 0;
 }
 
 extern "C" chm_status chm_create(const chm_config *cfg, chm_ctx **out) {
@@ -56,6 +60,8 @@ extern "C" chm_status chm_create(const chm_config *cfg, chm_ctx **out) {
   if (cfg) c = *cfg; else chm_config_default(&c);
   if (c.len_tol <= 0 || c.cos_tol <= 0 || c.cos_tol > 1 || c.cos_mode > 1 || c.swap_variant > 2)
     CHM_FAIL(CHM_E_INVAL, "chm_create: invalid Algo. 1 thresholds / cos_mode");
+  if (c.arena_mode > CHM_ARENA_REGISTER || c.arena_numa < -2)
+    CHM_FAIL(CHM_E_INVAL, "chm_create: arena_mode %u / arena_numa %d", c.arena_mode, c.arena_numa);
   if (c.device < 0) {  // host-only ctx: profiler, detection, trace build, executor tables
     if (c.host_arena_bytes) CHM_FAIL(CHM_E_INVAL, "chm_create: a host-only ctx has no arena");
     chm_ctx *ctx = new (std::nothrow) chm_ctx();
@@ -79,6 +85,9 @@ extern "C" chm_status chm_create(const chm_config *cfg, chm_ctx **out) {
   ctx->cfg = c;
   ctx->device = c.device;
   ctx->num_sms = prop.multiProcessorCount;
+  ctx->arena_mode = c.arena_mode;
+  ctx->arena_numa = c.arena_numa;
+  ctx->arena_threads = c.arena_threads;
   ctx->events.resize(kEventRing, nullptr);
   ctx->fences.resize(kEventRing, nullptr);
   for (int i = 0; i < kEventRing; i++) {
@@ -99,21 +108,12 @@ extern "C" chm_status chm_create(const chm_config *cfg, chm_ctx **out) {
     }
   }
   if (c.host_arena_bytes) {
-    // pinned + device-mapped host arena (portable across contexts); this box has one NUMA
-    // node, so first-touch placement is NUMA-local by construction
-    cudaError_t e = cudaHostAlloc(&ctx->arena, c.host_arena_bytes,
-                                  cudaHostAllocMapped | cudaHostAllocPortable);
-    if (e != cudaSuccess) {
+    chm_status st = arena_alloc(ctx, c.host_arena_bytes);  // arena.cpp
+    if (st != CHM_OK) {
+      std::string msg = chm_last_error();
       chm_destroy(ctx);
-      CHM_FAIL(CHM_E_NOMEM, "chm_create: cudaHostAlloc(%llu) failed: %s",
-               (unsigned long long)c.host_arena_bytes, cudaGetErrorString(e));
+      CHM_FAIL(st, "chm_create: %s", msg.c_str());
     }
-    void *dptr = nullptr;
-    if (cudaHostGetDevicePointer(&dptr, ctx->arena, 0) != cudaSuccess || dptr != ctx->arena) {
-      chm_destroy(ctx);
-      CHM_FAIL(CHM_E_CUDA, "chm_create: mapped arena is not UVA-identical");
-    }
-    ctx->arena_bytes = c.host_arena_bytes;
   }
   *out = ctx;
   return CHM_OK;
@@ -127,7 +127,7 @@ extern "C" void chm_destroy(chm_ctx *ctx) {
   for (auto e : ctx->fences) if (e) cudaEventDestroy(e);
   for (auto e : ctx->t0) if (e) cudaEventDestroy(e);
   for (auto e : ctx->t1) if (e) cudaEventDestroy(e);
-  if (ctx->arena) cudaFreeHost(ctx->arena);
+  arena_free(ctx);
   if (ctx->eval_scratch) cudaFree(ctx->eval_scratch);
   delete ctx;
 }

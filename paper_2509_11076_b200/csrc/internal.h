@@ -237,7 +237,13 @@ struct chm_ctx {
   uint64_t passive_next = 1;  // next handle
   // swap
   void *arena = nullptr;
-  uint64_t arena_bytes = 0;
+  uint64_t arena_bytes = 0;      // usable bytes (as requested)
+  uint64_t arena_map_bytes = 0;  // REGISTER: mapped length (2 MiB multiple)
+  bool arena_registered = false;
+  uint32_t arena_mode = 0, arena_threads = 0;
+  int32_t arena_numa = -1;       // requested placement (chm_config.arena_numa)
+  int32_t arena_node = -1;       // actual binding
+  double arena_pin_s = 0;
   std::vector<cudaEvent_t> events;  // ring of batch-completion events
   std::vector<cudaEvent_t> fences;  // ring of compute->swap fence events
   std::vector<cudaEvent_t> t0, t1;  // timing events per batch slot (time_batches)
@@ -262,6 +268,11 @@ chm_status build_trace(chm_ctx *ctx, const IterRecord &R, const chm_trace_params
 
 // executor.cpp: moves a released item's Detailed-record tensor index off its old address
 void stash_record(chm_ctx *ctx, PolicyItem &it);
+
+// arena.cpp: pinned + mapped host arena (sets arena, arena_bytes; frees the mapping)
+int device_numa_node(int device);
+chm_status arena_alloc(chm_ctx *ctx, uint64_t bytes);
+void arena_free(chm_ctx *ctx);
 
 // launchers (swap.cu / replay.cu)
 chm_status launch_swap_copy(const chm_swap_desc *d, uint32_t n, char *arena, bool to_host,

@@ -350,17 +350,6 @@ extern "C" chm_status chm_arena_reserve(chm_ctx *ctx, uint64_t bytes) {
     CHM_FAIL(CHM_E_STATE, "chm_arena_reserve: %zu passive swaps hold arena data", ctx->passive.size());
   ctx->passive_free.clear();  // re-derived from the new size at the next passive swap
   CHM_CUDA(cudaSetDevice(ctx->device));
-  if (ctx->arena) {
-    CHM_CUDA(cudaFreeHost(ctx->arena));
-    ctx->arena = nullptr;
-    ctx->arena_bytes = 0;
-  }
-  cudaError_t e = cudaHostAlloc(&ctx->arena, bytes, cudaHostAllocMapped | cudaHostAllocPortable);
-  if (e != cudaSuccess) {
-    ctx->arena = nullptr;
-    CHM_FAIL(CHM_E_NOMEM, "chm_arena_reserve: cudaHostAlloc(%llu) failed: %s", (unsigned long long)bytes,
-             cudaGetErrorString(e));
-  }
-  ctx->arena_bytes = bytes;
-  return CHM_OK;
+  arena_free(ctx);  // arena.cpp
+  return arena_alloc(ctx, bytes);
 }

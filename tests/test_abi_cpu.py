@@ -65,3 +65,19 @@ def test_create_without_gpu_fails_loudly():
         pytest.skip("GPU present")
     with pytest.raises(chm.ChmError):
         chm.Context(device=0)
+
+
+def test_arena_config_validation():
+    """chm_config.arena_mode / arena_numa are validated before any device work (host-only ctx);
+    the defaults are AUTO and the GPU's own node (-1)"""
+    L = chm.load()
+    cfg = chm.Config()
+    L.chm_config_default(ctypes.byref(cfg))
+    assert (cfg.arena_mode, cfg.arena_numa, cfg.arena_threads) == (chm.ARENA_AUTO, -1, 0)
+    for mode, numa in ((3, -1), (chm.ARENA_REGISTER, -3)):
+        cfg.device, cfg.arena_mode, cfg.arena_numa = -1, mode, numa
+        h = ctypes.c_void_p()
+        assert L.chm_create(ctypes.byref(cfg), ctypes.byref(h)) == -1  # CHM_E_INVAL
+        assert b"arena" in L.chm_last_error()
+    ctx = chm.Context(device=-1)
+    assert ctx.arena_placement() == {"numa_node": -1, "mode": -1, "pin_s": 0.0}

@@ -236,3 +236,38 @@ def test_config_sized_tensor_round_trip(flags):
     torch.cuda.synchronize()
     assert torch.equal(dst, src)
     c.close()
+
+
+@pytest.mark.parametrize("mode,numa", [(chm.ARENA_HOSTALLOC, -1), (chm.ARENA_REGISTER, -1), (chm.ARENA_REGISTER, -2),
+                                       (chm.ARENA_REGISTER, 0)])
+def test_arena_modes_round_trip(mode, numa):
+    """both arena allocations (cudaHostAlloc; mmap + mbind + THP + pre-fault + cudaHostRegister) are
+    UVA-mapped and swap byte-exact on the kernel and copy-engine paths, also after a regrow;
+    placement reports the binding (node 0 is online on every host)"""
+    c = chm.Context(device=0, host_arena_bytes=(8 << 20) + 5, arena_mode=mode, arena_numa=numa, arena_threads=3)
+    pl = c.arena_placement()
+    assert pl["mode"] == mode and pl["pin_s"] > 0
+    if mode == chm.ARENA_REGISTER and numa == 0:
+        assert pl["numa_node"] == 0
+    if numa == -2 or mode == chm.ARENA_HOSTALLOC:
+        assert pl["numa_node"] == -1
+    comp, s = torch.cuda.current_stream(), torch.cuda.Stream()
+    for grow in (0, 40 << 20):
+        if grow:
+            c.arena_reserve(grow + 3)
+            assert c.host_arena()[1] == grow + 3 and c.arena_placement()["mode"] == mode
+        n_arena = c.host_arena()[1]
+        sizes = [1 << 20, (3 << 20) + 7, 4096]
+        src = [rand_bytes(n, 40 + j + grow) for j, n in enumerate(sizes)]
+        offs = [0, 1 << 20, n_arena - 4096]  # the last block ends at the arena's last byte
+        for flags in (chm.SWAP_KERNEL, chm.SWAP_CE):
+            descs = [(x.data_ptr(), o, x.numel()) for x, o in zip(src, offs)]
+            c.batch_wait(c.swap_out(descs, comp, s, flags), comp)
+            torch.cuda.synchronize()
+            host = arena_view(c)
+            assert all(np.array_equal(host[o:o + x.numel()], x.cpu().numpy()) for x, o in zip(src, offs))
+            dst = [torch.zeros_like(x) for x in src]
+            c.batch_wait(c.swap_in([(d.data_ptr(), o, d.numel()) for d, o in zip(dst, offs)], comp, s, flags), comp)
+            torch.cuda.synchronize()
+            assert all(torch.equal(a, b) for a, b in zip(dst, src))
+    c.close()
