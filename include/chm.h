@@ -77,11 +77,12 @@ typedef struct {
                                  (16 B-aligned batches; others fall back to 0)              */
   uint32_t arena_mode;        /* host arena allocation: CHM_ARENA_AUTO (0) = REGISTER;
                                  CHM_ARENA_HOSTALLOC: cudaHostAlloc(Mapped|Portable), first
-                                 touch; CHM_ARENA_REGISTER: mmap + mbind to arena_numa + THP +
-                                 parallel pre-fault + cudaHostRegister(Mapped|Portable)      */
+                                 touch; CHM_ARENA_REGISTER: mmap + MPOL_PREFERRED node
+                                 arena_numa + THP + MADV_DONTFORK + parallel pre-fault +
+                                 cudaHostRegister(Mapped|Portable)                           */
   int32_t arena_numa;         /* REGISTER: -1 (default) the GPU's node (its PCIe device's
                                  sysfs numa_node; no binding when that is -1), -2 no binding,
-                                 >= 0 bind to that node                                      */
+                                 >= 0 prefer that node (falls back to others when full)     */
   uint32_t arena_threads;     /* REGISTER: pre-fault threads (0: min(cores, 32))             */
 } chm_config;
 enum { CHM_ARENA_AUTO = 0, CHM_ARENA_HOSTALLOC = 1, CHM_ARENA_REGISTER = 2 };

@@ -4,7 +4,8 @@
 //   CHM_ARENA_HOSTALLOC: cudaHostAlloc(Mapped | Portable). The driver faults and pins 4 KiB pages
 //     on the calling thread, first-touch placement (r01: 94 GB in 41 s, 2.3 GB/s).
 //   CHM_ARENA_REGISTER: mmap anonymous memory, mbind it to the GPU's NUMA node (the node of its
-//     PCIe root, /sys/bus/pci/devices/<bus id>/numa_node) so DMA never crosses the socket link,
+//     PCIe root, /sys/bus/pci/devices/<bus id>/numa_node; preferred, not strict) so DMA does not
+//     cross the socket link,
 //     ask for transparent huge pages, pre-fault it with one thread per 1/T of the range (page
 //     zeroing runs in parallel), then cudaHostRegister(Mapped | Portable) pins the resident pages.
 // CHM_ARENA_AUTO picks REGISTER. Either way the device pointer must equal the host pointer
@@ -27,7 +28,9 @@ using namespace chm;
 
 namespace {
 
-constexpr int kMpolBind = 2;  // MPOL_BIND (linux/mempolicy.h); no libnuma dependency
+// MPOL_PREFERRED (linux/mempolicy.h; no libnuma dependency): the GPU's node first, other nodes
+// when it is full -- a strict MPOL_BIND would turn a full node into an OOM kill at pre-fault
+constexpr int kMpolPreferred = 1;
 
 int read_int_file(const char *path, int dflt) {
   FILE *f = std::fopen(path, "r");
@@ -92,10 +95,11 @@ chm_status arena_alloc(chm_ctx *ctx, uint64_t bytes) {
     void *p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
     if (p == MAP_FAILED) CHM_FAIL(CHM_E_NOMEM, "arena: mmap(%llu) failed: %s", (unsigned long long)len, strerror(errno));
     madvise(p, len, MADV_HUGEPAGE);  // best effort: THP may be disabled
+    madvise(p, len, MADV_DONTFORK);  // forked children (data-loader workers) never share the pinned pages
     if (node >= 0 && node < 1024) {
       unsigned long mask[1024 / (8 * sizeof(unsigned long))] = {0};
       mask[node / (8 * sizeof(unsigned long))] = 1ul << (node % (8 * sizeof(unsigned long)));
-      if (syscall(SYS_mbind, p, len, kMpolBind, mask, 1024ul, 0u) != 0) {
+      if (syscall(SYS_mbind, p, len, kMpolPreferred, mask, 1024ul, 0u) != 0) {
         int err = errno;
         munmap(p, len);
         CHM_FAIL(CHM_E_NOMEM, "arena: mbind to node %d failed: %s", node, strerror(err));
