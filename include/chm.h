@@ -268,7 +268,15 @@ typedef struct {
                               entries [n_ops, ld) of a row are unspecified)            */
   uint32_t ld;             /* leading dimension of footprint, >= n_ops, even            */
   chm_best *best;          /* device, 1 element (required)                              */
+  uint32_t stall_model;    /* CHM_STALL_LAYER (0, default): R-stall, the per-layer overflow;
+                              CHM_STALL_TIMELINE: the max-plus serial-stream timeline of
+                              chm_stall_models out[2] over the candidate's items in mask-bit
+                              order at their solo (r_t, s_t); `stall` and the argmin key then
+                              carry it.  Mask kinds only (EXPLICIT: CHM_E_INVAL).  Needs
+                              device scratch of ~8 B x (slots of the trace's event program) per
+                              resident thread, capped at 256 MiB (DESIGN.md §5 Timeline)    */
 } chm_eval_out;
+enum { CHM_STALL_LAYER = 0, CHM_STALL_TIMELINE = 1 };
 
 /* Evaluates candidates on `stream` (enqueue only).  For candidate P:
  *   F_P[i] = F0[i] - sum_{t in P} S_t [r_t < i < s_t]  (event replay of §8(c).2)

@@ -87,6 +87,9 @@ def lib():
         L.orc_eval.argtypes = [C.c_void_p, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
                                C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
                                C.c_void_p, C.POINTER(_Best)]
+        L.orc_eval_model.argtypes = [C.c_void_p, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
+                                     C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                     C.c_void_p, C.c_void_p, C.POINTER(_Best)]
         L.orc_splitmix64.argtypes = [C.c_uint64]
         L.orc_splitmix64.restype = C.c_uint64
         L.orc_key_less.argtypes = [C.POINTER(_Best), C.POINTER(_Best)]
@@ -210,16 +213,18 @@ class Model:
 
     def eval(self, kind: int, first: int, count: int, *, seed: int = 0, flip_thr: int = 0,
              words: Optional[np.ndarray] = None, budget: Optional[int] = None, nthreads: int = 1,
-             footprint: bool = False):
+             footprint: bool = False, stall_model: int = 0):
+        """stall_model 0: R-stall (§8(c).5); 1: the Q11 timeline (stall_timeline of each candidate's
+        items in mask-bit order) -- also the stall field of the argmin key"""
         peak = np.zeros(count, np.int64)
         stall = np.zeros(count, np.float64)
         swapped = np.zeros(count, np.int64)
         F = np.zeros((count, self.N), np.int64) if footprint else None
         w = _arr(words, np.uint64) if words is not None else None
         best = _Best()
-        rc = lib().orc_eval(self._h, kind, first, count, seed, flip_thr, _p(w),
-                            int(self.trace.budget if budget is None else budget), nthreads,
-                            _p(peak), _p(stall), _p(swapped), _p(F), C.byref(best))
+        rc = lib().orc_eval_model(self._h, kind, first, count, seed, flip_thr, _p(w),
+                                  int(self.trace.budget if budget is None else budget), nthreads, stall_model,
+                                  _p(peak), _p(stall), _p(swapped), _p(F), C.byref(best))
         if rc != 0:
             raise ValueError(lib().orc_error().decode())
         return dict(peak=peak, stall=stall, swapped=swapped, footprint=F, best=best)

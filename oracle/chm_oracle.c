@@ -394,6 +394,7 @@ typedef struct {
   int64_t budget;
   int64_t *peak, *swapped, *footprint;
   double *stall;
+  int stall_model;  /* 0: stall_items (R-stall, §8(c).5); 1: orc_stall_timeline (Q11 variant) */
   orc_best best;
   int have_best;
 } eval_job;
@@ -429,7 +430,7 @@ static void *eval_range(void *arg) {
       if (cand_bit(j, c, idx, k)) { t[n] = m->sw_t[k]; r[n] = m->sw_r[k]; s[n] = m->sw_s[k]; n++; }
     int64_t out_b;
     int64_t pk = replay_items(m, &w, n, t, r, s, j->footprint ? j->footprint + idx * (uint64_t)m->N : NULL, &out_b, NULL);
-    double st = stall_items(m, load, n, t, r, s);
+    double st = j->stall_model ? orc_stall_timeline(m, n, t, r, s) : stall_items(m, load, n, t, r, s);
     if (j->peak) j->peak[idx] = pk;
     if (j->stall) j->stall[idx] = st;
     if (j->swapped) j->swapped[idx] = out_b;
@@ -443,6 +444,15 @@ static void *eval_range(void *arg) {
 int orc_eval(const orc_model *m, int kind, uint64_t first, uint64_t count, uint64_t seed,
              uint64_t flip_thr, const uint64_t *words, int64_t budget, int nthreads,
              int64_t *peak, double *stall, int64_t *swapped, int64_t *footprint, orc_best *best) {
+  return orc_eval_model(m, kind, first, count, seed, flip_thr, words, budget, nthreads, 0, peak, stall,
+                        swapped, footprint, best);
+}
+
+/* orc_eval with the candidate's stall under stall_model 1 = the timeline (orc_stall_timeline of
+ * its items in mask-bit order): the stall and the key's second field change, nothing else */
+int orc_eval_model(const orc_model *m, int kind, uint64_t first, uint64_t count, uint64_t seed,
+                   uint64_t flip_thr, const uint64_t *words, int64_t budget, int nthreads, int stall_model,
+                   int64_t *peak, double *stall, int64_t *swapped, int64_t *footprint, orc_best *best) {
   if (kind == ORC_EXHAUSTIVE && m->K > 63) FAIL("EXHAUSTIVE needs K <= 63 (K = %d)", m->K);
   if (kind == ORC_MASKS && !words) FAIL("MASKS needs masks");
   if (nthreads < 1) nthreads = 1;
@@ -454,6 +464,7 @@ int orc_eval(const orc_model *m, int kind, uint64_t first, uint64_t count, uint6
     j->m = m; j->kind = kind; j->first = first; j->seed = seed; j->flip_thr = flip_thr;
     j->words = words; j->budget = budget; j->peak = peak; j->stall = stall; j->swapped = swapped;
     j->footprint = footprint;
+    j->stall_model = stall_model;
     j->lo = count * (uint64_t)i / (uint64_t)nthreads;
     j->hi = count * (uint64_t)(i + 1) / (uint64_t)nthreads;
     if (nthreads == 1) eval_range(j);

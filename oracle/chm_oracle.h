@@ -96,6 +96,9 @@ typedef struct {
 int orc_eval(const orc_model *m, int kind, uint64_t first, uint64_t count, uint64_t seed,
              uint64_t flip_thr, const uint64_t *words, int64_t budget, int nthreads,
              int64_t *peak, double *stall, int64_t *swapped, int64_t *footprint, orc_best *best);
+int orc_eval_model(const orc_model *m, int kind, uint64_t first, uint64_t count, uint64_t seed,
+                   uint64_t flip_thr, const uint64_t *words, int64_t budget, int nthreads, int stall_model,
+                   int64_t *peak, double *stall, int64_t *swapped, int64_t *footprint, orc_best *best);
 uint64_t orc_splitmix64(uint64_t z);
 int orc_key_less(const orc_best *x, const orc_best *y);
 

@@ -13,7 +13,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libchm.so")
 LIB_DEBUG = os.path.join(HERE, "libchm_debug.so")  # device-side bounds checks (CHM_DEBUG)
-SOURCES = ["core.cpp", "trace.cpp", "executor.cpp", "generator.cpp", "oom.cpp", "trace_io.cpp", "stall.cpp", "arena.cpp", "swap.cu", "replay.cu", "explicit.cu"]
+SOURCES = ["core.cpp", "trace.cpp", "executor.cpp", "generator.cpp", "oom.cpp", "trace_io.cpp", "stall.cpp", "arena.cpp", "swap.cu", "replay.cu", "timeline.cu", "explicit.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -22,7 +22,7 @@ def _stale(lib: str = LIB) -> bool:
     if not os.path.exists(lib):
         return True
     t = os.path.getmtime(lib)
-    deps = [os.path.join(CSRC, s) for s in SOURCES] + [os.path.join(CSRC, "internal.h"),
+    deps = [os.path.join(CSRC, s) for s in SOURCES] + [os.path.join(CSRC, "internal.h"), os.path.join(CSRC, "eval_common.cuh"),
                                                        os.path.join(ROOT, "include", "chm.h"),
                                                        os.path.abspath(__file__)]
     return any(os.path.getmtime(d) > t for d in deps)

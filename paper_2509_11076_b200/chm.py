@@ -151,7 +151,10 @@ BEST_DTYPE = np.dtype([("excess", np.int64), ("stall", np.float64), ("swapped_by
 
 class EvalOut(C.Structure):
     _fields_ = [("peak", C.c_void_p), ("stall", C.c_void_p), ("swapped", C.c_void_p), ("footprint", C.c_void_p),
-                ("ld", C.c_uint32), ("best", C.c_void_p)]
+                ("ld", C.c_uint32), ("best", C.c_void_p), ("stall_model", C.c_uint32)]
+
+
+STALL_LAYER, STALL_TIMELINE = 0, 1
 
 
 class ExecStats(C.Structure):
@@ -441,13 +444,14 @@ class Context:
     # ------------------------------------------------------------ policy evaluation
     def eval_policies(self, trace: Trace, kind: int, first: int, count: int, *, best, seed: int = 0,
                       flip_thr: int = 0, base: Optional[np.ndarray] = None, masks=None, peak=None, stall=None,
-                      swapped=None, footprint=None, ld: int = 0, stream=None, item_offsets=None, items=None):
+                      swapped=None, footprint=None, ld: int = 0, stream=None, item_offsets=None, items=None,
+                      stall_model: int = STALL_LAYER):
         b = np.ascontiguousarray(base, np.uint64) if base is not None else None
         off = np.ascontiguousarray(item_offsets, np.uint64) if item_offsets is not None else None
         its = np.ascontiguousarray(items, ITEM_DTYPE) if items is not None else None
         c = Candidates(kind, first, count, seed, flip_thr, _ptr(b), _ptr(masks), _ptr(off),
                        _ptr(its) if its is not None and its.size else None)
-        o = EvalOut(_ptr(peak), _ptr(stall), _ptr(swapped), _ptr(footprint), ld, _ptr(best))
+        o = EvalOut(_ptr(peak), _ptr(stall), _ptr(swapped), _ptr(footprint), ld, _ptr(best), stall_model)
         e = C.c_int64()
         rc = load().chm_eval_policies_ex(self.h, trace.h, C.byref(c), C.byref(o), _stream(stream), C.byref(e))
         if rc != CHM_OK:

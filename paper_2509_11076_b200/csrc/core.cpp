@@ -129,6 +129,8 @@ extern "C" void chm_destroy(chm_ctx *ctx) {
   for (auto e : ctx->t1) if (e) cudaEventDestroy(e);
   arena_free(ctx);
   if (ctx->eval_scratch) cudaFree(ctx->eval_scratch);
+  if (ctx->tl_scratch) cudaFree(ctx->tl_scratch);
+  if (ctx->tl_aux) cudaFree(ctx->tl_aux);
   delete ctx;
 }
 

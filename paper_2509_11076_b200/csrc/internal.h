@@ -185,6 +185,11 @@ struct chm_trace {
   // device copies
   void *dev_block = nullptr;
   chm::DevTrace dev;
+  // timeline event program (timeline.cu), built on first use by a CHM_STALL_TIMELINE eval
+  void *tl_dev = nullptr;          // device: events [tl_events] (8 B each), then cost [K] doubles
+  uint32_t tl_events = 0, tl_slots = 0;
+  size_t tl_cost_off = 0;
+  double tl_tau = 0.0;
 };
 
 struct chm_ctx {
@@ -252,6 +257,10 @@ struct chm_ctx {
   // eval scratch
   void *eval_scratch = nullptr;  // per-CTA partial keys + ticket / work counters
   size_t eval_scratch_bytes = 0;
+  void *tl_scratch = nullptr;  // timeline: per-thread slot values + internal peak / swapped / key
+  size_t tl_scratch_bytes = 0;
+  void *tl_aux = nullptr;      // timeline: peak / swapped the caller did not ask for + the replay's key
+  size_t tl_aux_bytes = 0;
   void *explicit_scratch = nullptr;  // EXPLICIT candidates: items + offsets + keys (device)
   size_t explicit_scratch_bytes = 0;
   size_t eval_attr_smem[3] = {0, 0, 0};  // cached kernel attribute / occupancy per variant
@@ -291,6 +300,10 @@ struct EvalLaunch {
   chm_best *best = nullptr;
 };
 chm_status launch_eval(chm_ctx *ctx, const EvalLaunch &L, cudaStream_t stream);
+// timeline.cu: the timeline stall of mask-kind candidates (after launch_eval wrote peak /
+// swapped); writes stall and the argmin key
+chm_status launch_timeline(chm_ctx *ctx, const chm_trace *t, const EvalLaunch &L, const int64_t *peak,
+                           const int64_t *swapped, cudaStream_t stream);
 // explicit.cu: generic replay of explicit item lists (arbitrary r, s)
 chm_status launch_eval_explicit(chm_ctx *ctx, const chm_trace *t, const chm_candidates *c,
                                 const chm_eval_out *o, cudaStream_t stream, int64_t *err_index);

@@ -26,33 +26,11 @@
 #include <climits>
 #include <cstring>
 
+#include "eval_common.cuh"
 #include "internal.h"
 
 namespace chm {
 namespace {
-
-struct Key {
-  long long excess;
-  double stall;
-  long long swapped;
-  unsigned long long index;
-  long long peak;
-};
-static_assert(sizeof(Key) == sizeof(chm_best), "key layout");
-
-__device__ __forceinline__ bool key_less(const Key &x, const Key &y) {
-  if (x.excess != y.excess) return x.excess < y.excess;
-  if (x.stall != y.stall) return x.stall < y.stall;
-  if (x.swapped != y.swapped) return x.swapped < y.swapped;
-  return x.index < y.index;
-}
-
-__device__ __forceinline__ uint64_t mix64(uint64_t z) {  // splitmix64 finaliser
-  z += 0x9E3779B97F4A7C15ull;
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-  return z ^ (z >> 31);
-}
 
 struct EvalParams {
   DevTrace tr;
@@ -504,6 +482,12 @@ extern "C" chm_status chm_eval_policies_ex(chm_ctx *ctx, const chm_trace *t, con
   if (c->count == 0) CHM_FAIL(CHM_E_INVAL, "chm_eval_policies: empty candidate range");
   if (ctx->device < 0 || !t->dev_block) CHM_FAIL(CHM_E_STATE, "chm_eval_policies: host-only ctx / trace");
   if (t->device != ctx->device) CHM_FAIL(CHM_E_INVAL, "chm_eval_policies: trace on another device");
+  if (o->stall_model > CHM_STALL_TIMELINE)
+    CHM_FAIL(CHM_E_INVAL, "chm_eval_policies: unknown stall model %u", o->stall_model);
+  const bool timeline = o->stall_model == CHM_STALL_TIMELINE;
+  if (timeline && c->kind == CHM_CAND_EXPLICIT)
+    CHM_FAIL(CHM_E_INVAL, "chm_eval_policies: the timeline stall model takes mask-kind candidates "
+             "(EXPLICIT lists: chm_stall_models)");
   EvalLaunch L;
   L.tr = t->dev;
   L.kind = int(c->kind);
@@ -554,7 +538,30 @@ extern "C" chm_status chm_eval_policies_ex(chm_ctx *ctx, const chm_trace *t, con
   L.ld = o->ld;
   L.best = o->best;
   CHM_CUDA(cudaSetDevice(ctx->device));
-  return launch_eval(ctx, L, stream);
+  if (!timeline) return launch_eval(ctx, L, stream);
+  // timeline: the replay gives peak / swapped (footprint rows as asked), then timeline.cu the
+  // stall of each candidate and the argmin key over (excess, timeline stall, swapped, index)
+  const size_t arr = (8 * size_t(c->count) + 255) & ~size_t(255);
+  const size_t aux = 256 + (o->peak ? 0 : arr) + (o->swapped ? 0 : arr);
+  if (ctx->tl_aux_bytes < aux) {
+    if (ctx->tl_aux) cudaFree(ctx->tl_aux);
+    ctx->tl_aux = nullptr;
+    ctx->tl_aux_bytes = 0;
+    CHM_CUDA(cudaMalloc(&ctx->tl_aux, aux));
+    ctx->tl_aux_bytes = aux;
+  }
+  char *ab = static_cast<char *>(ctx->tl_aux);
+  int64_t *peak = o->peak ? o->peak : reinterpret_cast<int64_t *>(ab + 256);
+  int64_t *swapped = o->swapped ? o->swapped : reinterpret_cast<int64_t *>(ab + 256 + (o->peak ? 0 : arr));
+  L.peak = peak;
+  L.swapped = swapped;
+  L.stall = nullptr;
+  L.best = reinterpret_cast<chm_best *>(ab);  // the R-stall key, not reported
+  const chm_status st = launch_eval(ctx, L, stream);
+  if (st != CHM_OK) return st;
+  L.stall = o->stall;
+  L.best = o->best;
+  return launch_timeline(ctx, t, L, peak, swapped, stream);
 }
 
 extern "C" chm_status chm_best_reduce_device(chm_ctx *ctx, const chm_best *keys, uint32_t n, chm_best *out,

@@ -1,0 +1,304 @@
+// timeline.cu -- the timeline stall model in the search (reading Q11's max-plus serial-stream
+// variant, chm_stall_models out[2]), one candidate per thread.
+//
+// The model ("NPU idle periods"): ops take tau = T_iter / N each; a swap-out
+// enters the D2H FIFO after op a_t, a swap-in the H2D FIFO before op s_t; compute waits for the
+// swap-out after op r_t (the release) and for the swap-in before op b_t; the stall is the total
+// wait.  For a mask-kind candidate every item sits at its solo (r_t, s_t), so the sequence of
+// events is the same for all candidates -- only which items are selected differs.  The host
+// sorts the 4K events of all swappable items once per trace into a program (op, then the
+// model's order within an op: swap-ins, waits, [op], swap-outs, releases; item order within a
+// kind), with the op ticks between events folded into each event.  Every thread walks the
+// program for its own candidate, skipping the items its mask does not select, with the same
+// floating-point operations in the same order as the host model (bit-identical to the oracle).
+//
+// A release needs the end time of its item's swap-out, computed many events earlier (a wait,
+// that of its swap-in).  Those values live in per-thread slots in global memory, [warp][slot]
+// [lane] so a warp's accesses are one coalesced 256 B line; the host colours the item intervals
+// [swap-out, release] and [swap-in, wait] over the program so that items whose intervals do not
+// overlap share a slot (C2: 470 slots for 936 items).  A swap-in never waits for its own
+// swap-out: the release at r_t < s_t already made `now` >= that end time, and `now` only grows,
+// so max(now, h2d, out_end) = max(now, h2d) exactly.
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <queue>
+#include <vector>
+
+#include "eval_common.cuh"
+#include "internal.h"
+
+namespace chm {
+namespace {
+
+enum : unsigned { TL_IN = 0, TL_WAIT = 1, TL_OUT = 2, TL_REL = 3, TL_NOP = 4 };
+constexpr int kTlThreads = 256;
+constexpr size_t kTlSlotCap = 256ull << 20;  // bytes of slot scratch at most (HBM is what swapping saves)
+
+// event: x = k | kind << 16, y = ticks | slot << 16 (8 B)
+struct TlParams {
+  const uint2 *ev;
+  const double *cost;
+  uint32_t n_ev, n_slots, ev_bytes, cost_bytes;
+  double tau;
+  int kind, K, W;
+  uint64_t first, count, seed, flip_thr;
+  uint64_t base[kMaxSeededWords];
+  const uint64_t *masks;
+  const long long *peak;
+  const long long *swapped;
+  double *stall;
+  long long budget;
+  double *slots;
+  Key *partial;
+  unsigned int *ticket;
+  Key *best;
+};
+
+__global__ void __launch_bounds__(kTlThreads) timeline_kernel(const __grid_constant__ TlParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ Key s_best[kTlThreads / 32];
+  __shared__ unsigned int s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, bd = blockDim.x;
+  uint2 *s_ev = reinterpret_cast<uint2 *>(smem);
+  double *s_cost = reinterpret_cast<double *>(smem + p.ev_bytes);
+  uint64_t *s_mask = reinterpret_cast<uint64_t *>(smem + p.ev_bytes + p.cost_bytes);
+  for (uint32_t i = tid; i < p.n_ev; i += bd) s_ev[i] = __ldg(p.ev + i);
+  for (int k = tid; k < p.K; k += bd) s_cost[k] = __ldg(p.cost + k);
+  __syncthreads();
+  const uint64_t G = uint64_t(gridDim.x) * bd, gl = uint64_t(blockIdx.x) * bd + tid;
+  double *slot0 = p.slots + (gl >> 5) * uint64_t(p.n_slots) * 32 + (gl & 31);
+  uint64_t *wm = s_mask + tid;  // word w of this thread's candidate at wm[w * bd]
+  Key best = key_none();
+  for (uint64_t c = gl; c < p.count; c += G) {
+    const uint64_t g = p.first + c;
+    if (p.kind == CHM_CAND_EXHAUSTIVE) {
+      wm[0] = g;
+    } else if (p.kind == CHM_CAND_MASKS) {
+      for (int w = 0; w < p.W; w++) wm[w * bd] = __ldg(p.masks + c * uint64_t(p.W) + w);
+    } else {  // SEEDED / FLIP1: the base, then the flips (reading R-seeded; FLIP1 one bit)
+      for (int w = 0; w < p.W; w++) wm[w * bd] = p.base[w];
+      if (p.kind == CHM_CAND_FLIP1) {
+        if (g < uint64_t(p.K)) wm[(g >> 6) * bd] ^= 1ull << (g & 63);
+      } else {
+        const uint64_t J = (uint64_t(p.K) + 3) >> 2;
+        const unsigned thr16 = unsigned(p.flip_thr >> 48);
+        for (uint64_t q = 0; q < J; q++) {
+          const uint64_t w = mix64(p.seed ^ mix64(g * J + q));
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            const uint64_t k = 4 * q + e;
+            if (k < uint64_t(p.K) && unsigned((w >> (16 * e)) & 0xffffull) < thr16)
+              wm[(k >> 6) * bd] ^= 1ull << (k & 63);
+          }
+        }
+      }
+    }
+    double now = 0.0, d2h = 0.0, h2d = 0.0, st = 0.0;
+    for (uint32_t e = 0; e < p.n_ev; e++) {
+      const uint2 x = s_ev[e];
+      const unsigned k = x.x & 0xffffu, kind = x.x >> 16, slot = x.y >> 16;
+      for (unsigned j = x.y & 0xffffu; j; j--) now = __dadd_rn(now, p.tau);  // ops between events
+      if (kind == TL_NOP || !((wm[(k >> 6) * bd] >> (k & 63)) & 1ull)) continue;
+      CHM_DCHECK(slot < p.n_slots && int(k) < p.K);
+      double *sl = slot0 + uint64_t(slot) * 32;
+      if (kind == TL_IN) {  // before op s: the H2D FIFO
+        const double v = __dadd_rn(h2d > now ? h2d : now, s_cost[k]);
+        h2d = v;
+        __stcg(sl, v);
+      } else if (kind == TL_OUT) {  // after op a: the D2H FIFO
+        const double v = __dadd_rn(d2h > now ? d2h : now, s_cost[k]);
+        d2h = v;
+        __stcg(sl, v);
+      } else {  // wait (before op b: swap-in done) / release (after op r: swap-out done)
+        const double v = __ldcg(sl);
+        if (v > now) {
+          st = __dadd_rn(st, __dsub_rn(v, now));
+          now = v;
+        }
+      }
+    }
+    const long long pk = p.peak[c], sw = p.swapped[c];
+    if (p.stall) p.stall[c] = st;
+    Key kk;
+    kk.excess = pk > p.budget ? pk - p.budget : 0;
+    kk.stall = st;
+    kk.swapped = sw;
+    kk.index = g;
+    kk.peak = pk;
+    if (key_less(kk, best)) best = kk;
+  }
+  // thread keys -> warp -> CTA -> the last CTA to finish reduces all CTA keys into *best
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const Key y = key_shfl_xor(best, o);
+    if (key_less(y, best)) best = y;
+  }
+  if (lane == 0) s_best[warp] = best;
+  __syncthreads();
+  if (tid == 0) {
+    Key b = s_best[0];
+    for (int w = 1; w < bd / 32; w++) if (key_less(s_best[w], b)) b = s_best[w];
+    p.partial[blockIdx.x] = b;
+    __threadfence();
+    const unsigned int t = atomicAdd(p.ticket, 1u);
+    s_last = (t == gridDim.x - 1) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (!s_last || warp != 0) return;
+  __threadfence();
+  Key b = key_none();
+  for (unsigned q = lane; q < gridDim.x; q += 32) {
+    Key k;
+    k.excess = __ldcg(&p.partial[q].excess);
+    k.stall = __ldcg(&p.partial[q].stall);
+    k.swapped = __ldcg(&p.partial[q].swapped);
+    k.index = __ldcg(&p.partial[q].index);
+    k.peak = __ldcg(&p.partial[q].peak);
+    if (key_less(k, b)) b = k;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const Key y = key_shfl_xor(b, o);
+    if (key_less(y, b)) b = y;
+  }
+  if (lane == 0) {
+    *p.best = b;
+    *p.ticket = 0u;
+  }
+}
+
+// the event program of a trace (host, once per trace): events sorted by (op, phase, item),
+// op ticks folded in, slot colouring of the item intervals
+chm_status build_program(const chm_trace *tc) {
+  chm_trace *t = const_cast<chm_trace *>(tc);  // the program is a cache of the immutable trace
+  if (t->tl_dev) return CHM_OK;
+  const int32_t K = t->K, N = t->N;
+  struct Ev { int32_t op; uint8_t ph; int32_t k; };
+  std::vector<Ev> ev;
+  ev.reserve(4 * size_t(K));
+  for (int32_t k = 0; k < K; k++) {
+    const int32_t tid = t->sw_tensor_idx[size_t(k)];
+    const int32_t a = t->a[size_t(tid)], b = t->b[size_t(tid)], r = t->sw_r[size_t(k)], s = t->sw_s[size_t(k)];
+    if (a < 0 || b < 0 || r < a || !(r + 1 < s) || s > b || b >= N)
+      CHM_FAIL(CHM_E_INVAL, "timeline: swappable %d (a %d, r %d, s %d, b %d) breaks a <= r < r + 1 < s <= b", k, a,
+               r, s, b);
+    ev.push_back({s, TL_IN, k});
+    ev.push_back({b, TL_WAIT, k});
+    ev.push_back({a, TL_OUT, k});
+    ev.push_back({r, TL_REL, k});
+  }
+  std::sort(ev.begin(), ev.end(), [](const Ev &x, const Ev &y) {
+    if (x.op != y.op) return x.op < y.op;
+    if (x.ph != y.ph) return x.ph < y.ph;
+    return x.k < y.k;
+  });
+  std::vector<uint32_t> slot_of(2 * size_t(K), 0);  // [k]: out slot, [K + k]: in slot
+  std::priority_queue<uint32_t, std::vector<uint32_t>, std::greater<uint32_t>> free_slots;
+  uint32_t n_slots = 0;
+  std::vector<uint2> prog;
+  prog.reserve(ev.size() + 8);
+  int64_t done = 0;  // ops executed before the current event
+  for (const Ev &e : ev) {
+    int64_t ticks = int64_t(e.op) + (e.ph >= TL_OUT ? 1 : 0) - done;
+    done += ticks;
+    while (ticks > 0xffff) {  // long gaps: tick-only events
+      prog.push_back(make_uint2(TL_NOP << 16, 0xffffu));
+      ticks -= 0xffff;
+    }
+    uint32_t slot;
+    const size_t key = (e.ph == TL_OUT || e.ph == TL_REL) ? size_t(e.k) : size_t(K) + size_t(e.k);
+    if (e.ph == TL_IN || e.ph == TL_OUT) {
+      if (free_slots.empty()) free_slots.push(n_slots++);
+      slot = free_slots.top();
+      free_slots.pop();
+      slot_of[key] = slot;
+    } else {
+      slot = slot_of[key];
+      free_slots.push(slot);
+    }
+    if (n_slots > 0xffffu) CHM_FAIL(CHM_E_INVAL, "timeline: more than 65535 concurrent items");
+    prog.push_back(make_uint2(uint32_t(e.k) | (uint32_t(e.ph) << 16), uint32_t(ticks) | (slot << 16)));
+  }
+  const size_t ev_bytes = (8 * prog.size() + 15) & ~size_t(15);
+  std::vector<double> cost(static_cast<size_t>(K));
+  for (int32_t k = 0; k < K; k++) cost[size_t(k)] = double(t->sw_S[size_t(k)]) / t->bw;  // Eq. 3, as the model
+  CHM_CUDA(cudaSetDevice(t->device));
+  void *d = nullptr;
+  CHM_CUDA(cudaMalloc(&d, ev_bytes + 8 * size_t(std::max(K, 1))));
+  cudaError_t e1 = cudaMemcpy(d, prog.data(), 8 * prog.size(), cudaMemcpyHostToDevice);
+  cudaError_t e2 = K ? cudaMemcpy(static_cast<char *>(d) + ev_bytes, cost.data(), 8 * size_t(K), cudaMemcpyHostToDevice)
+                     : cudaSuccess;
+  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    cudaFree(d);
+    CHM_FAIL(CHM_E_CUDA, "timeline: program upload failed");
+  }
+  t->tl_dev = d;
+  t->tl_events = uint32_t(prog.size());
+  t->tl_slots = std::max<uint32_t>(n_slots, 1);
+  t->tl_cost_off = ev_bytes;
+  t->tl_tau = N > 0 ? t->t_iter / double(N) : 0.0;
+  return CHM_OK;
+}
+
+}  // namespace
+
+chm_status launch_timeline(chm_ctx *ctx, const chm_trace *t, const EvalLaunch &L, const int64_t *peak,
+                           const int64_t *swapped, cudaStream_t stream) {
+  const chm_status st = build_program(t);
+  if (st != CHM_OK) return st;
+  const size_t ev_bytes = t->tl_cost_off, cost_bytes = (8 * size_t(t->K) + 15) & ~size_t(15);
+  const int W = std::max(t->W, 1);
+  const size_t smem = ev_bytes + cost_bytes + size_t(W) * kTlThreads * 8;
+  if (smem > 220 * 1024)
+    CHM_FAIL(CHM_E_INVAL, "timeline: event program + masks (%zu B) exceed shared memory", smem);
+  CHM_CUDA(cudaFuncSetAttribute(timeline_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  int per_sm = 0;
+  CHM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, timeline_kernel, kTlThreads, smem));
+  if (per_sm < 1) CHM_FAIL(CHM_E_INVAL, "timeline: kernel does not fit an SM");
+  const size_t per_thread = 8 * size_t(t->tl_slots);
+  const uint64_t cap_ctas = std::max<uint64_t>(1, kTlSlotCap / (per_thread * kTlThreads));
+  uint64_t grid64 = std::min<uint64_t>(uint64_t(ctx->num_sms) * per_sm, (L.count + kTlThreads - 1) / kTlThreads);
+  grid64 = std::max<uint64_t>(1, std::min(grid64, cap_ctas));
+  const int grid = int(grid64);
+  const size_t slot_bytes = size_t(grid) * kTlThreads * per_thread;
+  if (ctx->tl_scratch_bytes < slot_bytes) {
+    if (ctx->tl_scratch) cudaFree(ctx->tl_scratch);
+    ctx->tl_scratch = nullptr;
+    ctx->tl_scratch_bytes = 0;
+    CHM_CUDA(cudaMalloc(&ctx->tl_scratch, slot_bytes));
+    ctx->tl_scratch_bytes = slot_bytes;
+  }
+  const size_t need = size_t(grid) * sizeof(Key) + 256;  // partial keys + ticket (eval scratch)
+  if (ctx->eval_scratch_bytes < need) CHM_FAIL(CHM_E_STATE, "timeline: eval scratch too small");
+  TlParams p{};
+  p.ev = static_cast<const uint2 *>(t->tl_dev);
+  p.cost = reinterpret_cast<const double *>(static_cast<const char *>(t->tl_dev) + ev_bytes);
+  p.n_ev = t->tl_events;
+  p.n_slots = t->tl_slots;
+  p.ev_bytes = uint32_t(ev_bytes);
+  p.cost_bytes = uint32_t(cost_bytes);
+  p.tau = t->tl_tau;
+  p.kind = L.kind;
+  p.K = t->K;
+  p.W = t->W;
+  p.first = L.first;
+  p.count = L.count;
+  p.seed = L.seed;
+  p.flip_thr = L.flip_thr;
+  std::memcpy(p.base, L.base, sizeof p.base);
+  p.masks = L.masks;
+  p.peak = reinterpret_cast<const long long *>(peak);
+  p.swapped = reinterpret_cast<const long long *>(swapped);
+  p.stall = L.stall;
+  p.budget = t->budget;
+  p.slots = static_cast<double *>(ctx->tl_scratch);
+  p.ticket = reinterpret_cast<unsigned int *>(ctx->eval_scratch);
+  p.partial = reinterpret_cast<Key *>(static_cast<char *>(ctx->eval_scratch) + 256);
+  p.best = reinterpret_cast<Key *>(L.best);
+  timeline_kernel<<<grid, kTlThreads, smem, stream>>>(p);
+  CHM_CUDA(cudaGetLastError());
+  return CHM_OK;
+}
+
+}  // namespace chm

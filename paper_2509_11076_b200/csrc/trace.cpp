@@ -297,6 +297,10 @@ extern "C" void chm_trace_free(chm_trace *t) {
     cudaSetDevice(t->device);
     cudaFree(t->dev_block);
   }
+  if (t->tl_dev && t->device >= 0) {
+    cudaSetDevice(t->device);
+    cudaFree(t->tl_dev);
+  }
   delete t;
 }
 

@@ -1,0 +1,109 @@
+"""GPU parity of the timeline stall model in the search (chm_eval_out.stall_model =
+CHM_STALL_TIMELINE, csrc/timeline.cu) against the oracle's orc_eval_model(stall_model = 1), which
+scores each candidate's items with orc_stall_timeline (reading Q11's max-plus serial-stream
+variant, pinned in tests/test_stall_models.py).  Bar: peak, swapped, footprints and the argmin
+bit-exact; the stall within 1e-6 relative (asserted bit-identical: same IEEE operations in the
+same order on both sides)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from workloads import traces as W
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2509_11076_b200 import chm  # noqa: E402
+from tests.test_gpu_parity import assert_same, product_trace, run_eval  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = chm.Context(device=0)
+    yield c
+    c.close()
+
+
+def tl(ctx, pt, kind, first, count, **kw):
+    return run_eval(ctx, pt, kind, first, count, stall_model=chm.STALL_TIMELINE, **kw)
+
+
+def test_c1_exhaustive_all_subsets_prefix(ctx):
+    tr = W.tiny()
+    pt = product_trace(ctx, tr)
+    m = O.Model(tr)
+    n = 1 << 16
+    res = tl(ctx, pt, chm.EXHAUSTIVE, 0, n, footprint=True)
+    ref = m.eval(O.EXHAUSTIVE, 0, n, footprint=True, nthreads=8, stall_model=1)
+    assert_same(res, ref, tr.budget)
+    assert np.count_nonzero(ref["stall"]) > n // 10  # the model is exercised, not all zeros
+    # the layer model's outputs other than the stall are unchanged
+    lay = run_eval(ctx, pt, chm.EXHAUSTIVE, 0, n, footprint=True)
+    assert np.array_equal(lay["peak"], res["peak"]) and np.array_equal(lay["footprint"], res["footprint"])
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C5"])
+def test_seeded(ctx, name):
+    tr = W.CONFIGS[name]()
+    pt = product_trace(ctx, tr)
+    m = O.Model(tr)
+    sd = W.SEEDED[name[:2]]
+    res = tl(ctx, pt, chm.SEEDED, 29, 1200, seed=sd["seed"], flip_thr=sd["flip_thr"])
+    ref = m.eval(O.SEEDED, 29, 1200, seed=sd["seed"], flip_thr=sd["flip_thr"], nthreads=16, stall_model=1)
+    assert_same(res, ref, tr.budget)
+
+
+def test_masks_and_flip1_dense(ctx):
+    """random dense masks (many items in flight: the slot colouring under load) and FLIP1"""
+    tr = W.gpt2_xl()
+    pt = product_trace(ctx, tr)
+    m = O.Model(tr)
+    rng = np.random.default_rng(8)
+    for density in (0.1, 0.5, 0.95):
+        masks = np.zeros((300, m.W), np.uint64)
+        for i in range(300):
+            for k in np.nonzero(rng.random(m.K) < density)[0]:
+                masks[i, k // 64] |= np.uint64(1 << int(k % 64))
+        dmask = torch.from_numpy(masks.view(np.int64)).cuda()
+        res = tl(ctx, pt, chm.MASKS, 7, 300, masks=dmask)
+        ref = m.eval(O.MASKS, 7, 300, words=masks, nthreads=16, stall_model=1)
+        assert_same(res, ref, tr.budget)
+    base = masks[0]
+    n = m.K + 1
+    res = tl(ctx, pt, chm.FLIP1, 0, n, base=base)
+    fm = np.repeat(base[None, :], n, axis=0)
+    for g in range(m.K):
+        fm[g, g // 64] ^= np.uint64(1 << (g % 64))
+    ref = m.eval(O.MASKS, 0, n, words=fm, nthreads=16, stall_model=1)
+    assert_same(res, ref, tr.budget)
+
+
+def test_c2_bench_size_every_candidate(ctx):
+    """the bench's launch (10^5 SEEDED C2 candidates, full mode): every stall and the argmin"""
+    tr = W.gpt2_xl()
+    pt = product_trace(ctx, tr)
+    m = O.Model(tr)
+    sd = W.SEEDED["C2"]
+    n = 100_000
+    res = tl(ctx, pt, chm.SEEDED, 0, n, footprint=True, seed=sd["seed"], flip_thr=sd["flip_thr"])
+    ref = m.eval(O.SEEDED, 0, n, seed=sd["seed"], flip_thr=sd["flip_thr"], nthreads=16, stall_model=1)
+    res["footprint"] = None
+    assert_same(res, ref, tr.budget)
+
+
+def test_outputs_optional_and_errors(ctx):
+    """peak / swapped / stall may be omitted (internal scratch); EXPLICIT and unknown models fail"""
+    tr = W.tiny()
+    pt = product_trace(ctx, tr)
+    m = O.Model(tr)
+    best = torch.empty(5, dtype=torch.int64, device="cuda")
+    ctx.eval_policies(pt, chm.EXHAUSTIVE, 100, 5000, best=best, stall_model=chm.STALL_TIMELINE)
+    torch.cuda.synchronize()
+    b = best.cpu().numpy().view(chm.BEST_DTYPE)[0]
+    ref = m.eval(O.EXHAUSTIVE, 100, 5000, nthreads=8, stall_model=1)["best"]
+    assert (int(b["excess"]), float(b["stall"]), int(b["swapped_bytes"]), int(b["index"])) == ref.key()
+    with pytest.raises(chm.ChmError):
+        ctx.eval_policies(pt, chm.EXPLICIT, 0, 1, best=best, item_offsets=np.array([0, 0], np.uint64),
+                          items=np.zeros(0, chm.ITEM_DTYPE), stall_model=chm.STALL_TIMELINE)
+    with pytest.raises(chm.ChmError):
+        ctx.eval_policies(pt, chm.EXHAUSTIVE, 0, 4, best=best, stall_model=2)

@@ -123,3 +123,24 @@ def test_product_validates_items():
     with pytest.raises(chm.ChmError):
         pt.stall_models(bad)
     assert pt.stall_models(np.zeros(0, chm.ITEM_DTYPE)).tolist() == [0.0, 0.0, 0.0]
+
+
+def test_eval_model_timeline_is_stall_timeline_of_mask_items():
+    """orc_eval_model(stall_model = 1) scores each candidate with stall_timeline of its items in
+    mask-bit order; peak / swapped / footprint equal those of the R-stall evaluation; the key's
+    stall field follows the model"""
+    tr = W.tiny()
+    m = O.Model(tr)
+    n = 3000
+    a = m.eval(O.EXHAUSTIVE, 0, n, stall_model=1, footprint=True)
+    b = m.eval(O.EXHAUSTIVE, 0, n, footprint=True)
+    for c in (0, 1, 2, 17, 1234, n - 1):
+        t, r, s = m.mask_items([(c >> k) & 1 for k in range(m.K)])
+        assert a["stall"][c] == m.stall_timeline(t, r, s)
+    for key in ("peak", "swapped", "footprint"):
+        assert np.array_equal(a[key], b[key])
+    assert np.count_nonzero(a["stall"] != b["stall"]) > 0
+    i = int(a["best"].index)
+    exc = np.maximum(a["peak"] - tr.budget, 0)
+    order = np.lexsort((np.arange(n), a["swapped"], a["stall"], exc))
+    assert order[0] == i
