@@ -31,11 +31,14 @@
 namespace chm {
 namespace {
 
-enum : unsigned { TL_IN = 0, TL_WAIT = 1, TL_OUT = 2, TL_REL = 3, TL_NOP = 4 };
+enum : unsigned { TL_IN = 0, TL_WAIT = 1, TL_OUT = 2, TL_REL = 3 };  // NOP: item K (never selected)
 constexpr int kTlThreads = 256;
+constexpr int kTlGroup = 8;                   // events per group = prefetch distance
+constexpr unsigned kTlPrefetch = 1u << 17;    // event flag: its slot value is loaded a group ahead
 constexpr size_t kTlSlotCap = 256ull << 20;  // bytes of slot scratch at most (HBM is what swapping saves)
 
-// event: x = k | kind << 16, y = ticks | slot << 16 (8 B)
+// event (8 B): x = k (15 bits) | kind << 15 (2) | prefetch flag << 17 | ticks << 18 (14),
+//              y = slot | slot to load for the event one group ahead << 16 (0xffff: none)
 struct TlParams {
   const uint2 *ev;
   const double *cost;
@@ -62,24 +65,30 @@ __global__ void __launch_bounds__(kTlThreads) timeline_kernel(const __grid_const
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, bd = blockDim.x;
   uint2 *s_ev = reinterpret_cast<uint2 *>(smem);
   double *s_cost = reinterpret_cast<double *>(smem + p.ev_bytes);
-  uint64_t *s_mask = reinterpret_cast<uint64_t *>(smem + p.ev_bytes + p.cost_bytes);
+  unsigned *s_mask = reinterpret_cast<unsigned *>(smem + p.ev_bytes + p.cost_bytes);
   for (uint32_t i = tid; i < p.n_ev; i += bd) s_ev[i] = __ldg(p.ev + i);
   for (int k = tid; k < p.K; k += bd) s_cost[k] = __ldg(p.cost + k);
   __syncthreads();
   const uint64_t G = uint64_t(gridDim.x) * bd, gl = uint64_t(blockIdx.x) * bd + tid;
   double *slot0 = p.slots + (gl >> 5) * uint64_t(p.n_slots) * 32 + (gl & 31);
-  uint64_t *wm = s_mask + tid;  // word w of this thread's candidate at wm[w * bd]
+  unsigned *wm = s_mask + tid;  // 32-bit word w of this thread's candidate at wm[w * kTlThreads]
+  const int W32 = 2 * p.W;
   Key best = key_none();
   for (uint64_t c = gl; c < p.count; c += G) {
     const uint64_t g = p.first + c;
     if (p.kind == CHM_CAND_EXHAUSTIVE) {
-      wm[0] = g;
+      wm[0] = unsigned(g);
+      wm[kTlThreads] = unsigned(g >> 32);
     } else if (p.kind == CHM_CAND_MASKS) {
-      for (int w = 0; w < p.W; w++) wm[w * bd] = __ldg(p.masks + c * uint64_t(p.W) + w);
+      for (int w = 0; w < p.W; w++) {
+        const uint64_t x = __ldg(p.masks + c * uint64_t(p.W) + w);
+        wm[(2 * w) * kTlThreads] = unsigned(x);
+        wm[(2 * w + 1) * kTlThreads] = unsigned(x >> 32);
+      }
     } else {  // SEEDED / FLIP1: the base, then the flips (reading R-seeded; FLIP1 one bit)
-      for (int w = 0; w < p.W; w++) wm[w * bd] = p.base[w];
+      for (int w = 0; w < W32; w++) wm[w * kTlThreads] = unsigned(p.base[w >> 1] >> (32 * (w & 1)));
       if (p.kind == CHM_CAND_FLIP1) {
-        if (g < uint64_t(p.K)) wm[(g >> 6) * bd] ^= 1ull << (g & 63);
+        if (g < uint64_t(p.K)) wm[(g >> 5) * kTlThreads] ^= 1u << (g & 31);
       } else {
         const uint64_t J = (uint64_t(p.K) + 3) >> 2;
         const unsigned thr16 = unsigned(p.flip_thr >> 48);
@@ -87,36 +96,52 @@ __global__ void __launch_bounds__(kTlThreads) timeline_kernel(const __grid_const
           const uint64_t w = mix64(p.seed ^ mix64(g * J + q));
 #pragma unroll
           for (int e = 0; e < 4; e++) {
-            const uint64_t k = 4 * q + e;
-            if (k < uint64_t(p.K) && unsigned((w >> (16 * e)) & 0xffffull) < thr16)
-              wm[(k >> 6) * bd] ^= 1ull << (k & 63);
+            const unsigned k = unsigned(4 * q) + e;
+            if (k < unsigned(p.K) && unsigned((w >> (16 * e)) & 0xffffull) < thr16)
+              wm[(k >> 5) * kTlThreads] ^= 1u << (k & 31);
           }
         }
       }
     }
+    wm[(p.K >> 5) * kTlThreads] &= ~(1u << (p.K & 31));  // bit K: the never-selected item of NOPs
+    // the program in groups of kTlGroup events; each event carries the slot of the event one
+    // group ahead whose end time is already stored (the host checks), loaded here so that it
+    // has arrived when that event runs
     double now = 0.0, d2h = 0.0, h2d = 0.0, st = 0.0;
-    for (uint32_t e = 0; e < p.n_ev; e++) {
-      const uint2 x = s_ev[e];
-      const unsigned k = x.x & 0xffffu, kind = x.x >> 16, slot = x.y >> 16;
-      for (unsigned j = x.y & 0xffffu; j; j--) now = __dadd_rn(now, p.tau);  // ops between events
-      if (kind == TL_NOP || !((wm[(k >> 6) * bd] >> (k & 63)) & 1ull)) continue;
-      CHM_DCHECK(slot < p.n_slots && int(k) < p.K);
-      double *sl = slot0 + uint64_t(slot) * 32;
-      if (kind == TL_IN) {  // before op s: the H2D FIFO
-        const double v = __dadd_rn(h2d > now ? h2d : now, s_cost[k]);
-        h2d = v;
-        __stcg(sl, v);
-      } else if (kind == TL_OUT) {  // after op a: the D2H FIFO
-        const double v = __dadd_rn(d2h > now ? d2h : now, s_cost[k]);
-        d2h = v;
-        __stcg(sl, v);
-      } else {  // wait (before op b: swap-in done) / release (after op r: swap-out done)
-        const double v = __ldcg(sl);
-        if (v > now) {
-          st = __dadd_rn(st, __dsub_rn(v, now));
-          now = v;
+    double pf[kTlGroup];
+#pragma unroll
+    for (int j = 0; j < kTlGroup; j++) pf[j] = 0.0;
+    char *sbase = reinterpret_cast<char *>(slot0);
+    for (uint32_t e0 = 0; e0 < p.n_ev; e0 += kTlGroup) {
+      double nx[kTlGroup];
+#pragma unroll
+      for (int j = 0; j < kTlGroup; j++) {
+        const uint2 x = s_ev[e0 + j];  // n_ev is a multiple of kTlGroup (NOP padding)
+        const unsigned ps = x.y >> 16;
+        nx[j] = ps != 0xffffu ? __ldcg(reinterpret_cast<const double *>(sbase + (ps << 8))) : 0.0;
+        for (unsigned t = x.x >> 18; t; t--) now = __dadd_rn(now, p.tau);  // ops between events
+        const unsigned k = x.x & 0x7fffu, kind = (x.x >> 15) & 3u;
+        if (!((wm[(k >> 5) * kTlThreads] >> (k & 31)) & 1u)) continue;  // not selected (or a NOP)
+        CHM_DCHECK(int(k) < p.K && (x.y & 0xffffu) < p.n_slots);
+        double *sl = reinterpret_cast<double *>(sbase + ((x.y & 0xffffu) << 8));
+        if (kind == TL_IN) {  // before op s: the H2D FIFO
+          const double v = __dadd_rn(h2d > now ? h2d : now, s_cost[k]);
+          h2d = v;
+          __stcg(sl, v);
+        } else if (kind == TL_OUT) {  // after op a: the D2H FIFO
+          const double v = __dadd_rn(d2h > now ? d2h : now, s_cost[k]);
+          d2h = v;
+          __stcg(sl, v);
+        } else {  // wait (before op b: swap-in done) / release (after op r: swap-out done)
+          const double v = (x.x & kTlPrefetch) ? pf[j] : __ldcg(sl);
+          if (v > now) {
+            st = __dadd_rn(st, __dsub_rn(v, now));
+            now = v;
+          }
         }
       }
+#pragma unroll
+      for (int j = 0; j < kTlGroup; j++) pf[j] = nx[j];
     }
     const long long pk = p.peak[c], sw = p.swapped[c];
     if (p.stall) p.stall[c] = st;
@@ -194,32 +219,47 @@ chm_status build_program(const chm_trace *tc) {
     return x.k < y.k;
   });
   std::vector<uint32_t> slot_of(2 * size_t(K), 0);  // [k]: out slot, [K + k]: in slot
+  std::vector<size_t> store_at(2 * size_t(K), 0);   // program index of the item's swap-out / -in
   std::priority_queue<uint32_t, std::vector<uint32_t>, std::greater<uint32_t>> free_slots;
   uint32_t n_slots = 0;
   std::vector<uint2> prog;
   prog.reserve(ev.size() + 8);
   int64_t done = 0;  // ops executed before the current event
+  const uint32_t nop_k = uint32_t(K);  // mask bit K is cleared by the kernel: never selected
+  std::vector<uint32_t> pf_slot;       // per program event: its slot if prefetchable, else 0xffff
   for (const Ev &e : ev) {
     int64_t ticks = int64_t(e.op) + (e.ph >= TL_OUT ? 1 : 0) - done;
     done += ticks;
-    while (ticks > 0xffff) {  // long gaps: tick-only events
-      prog.push_back(make_uint2(TL_NOP << 16, 0xffffu));
-      ticks -= 0xffff;
+    while (ticks > 0x3fff) {  // long gaps: tick-only events
+      prog.push_back(make_uint2(nop_k | (0x3fffu << 18), 0u));
+      pf_slot.push_back(0xffffu);
+      ticks -= 0x3fff;
     }
-    uint32_t slot;
+    uint32_t slot, flag = 0;
     const size_t key = (e.ph == TL_OUT || e.ph == TL_REL) ? size_t(e.k) : size_t(K) + size_t(e.k);
+    const size_t idx = prog.size();
     if (e.ph == TL_IN || e.ph == TL_OUT) {
       if (free_slots.empty()) free_slots.push(n_slots++);
       slot = free_slots.top();
       free_slots.pop();
       slot_of[key] = slot;
+      store_at[key] = idx;
     } else {
       slot = slot_of[key];
       free_slots.push(slot);
+      // the kernel loads this value while it runs event idx - kTlGroup: the store must precede it
+      if (idx >= size_t(kTlGroup) && store_at[key] < idx - kTlGroup) flag = kTlPrefetch;
     }
-    if (n_slots > 0xffffu) CHM_FAIL(CHM_E_INVAL, "timeline: more than 65535 concurrent items");
-    prog.push_back(make_uint2(uint32_t(e.k) | (uint32_t(e.ph) << 16), uint32_t(ticks) | (slot << 16)));
+    if (n_slots >= 0xffffu) CHM_FAIL(CHM_E_INVAL, "timeline: more than 65534 concurrent items");
+    prog.push_back(make_uint2(uint32_t(e.k) | (uint32_t(e.ph) << 15) | flag | (uint32_t(ticks) << 18), slot));
+    pf_slot.push_back(flag ? slot : 0xffffu);
   }
+  while (prog.size() % kTlGroup) {  // whole groups
+    prog.push_back(make_uint2(nop_k, 0u));
+    pf_slot.push_back(0xffffu);
+  }
+  for (size_t i = 0; i + kTlGroup < prog.size(); i++) prog[i].y |= pf_slot[i + kTlGroup] << 16;
+  for (size_t i = prog.size() >= kTlGroup ? prog.size() - kTlGroup : 0; i < prog.size(); i++) prog[i].y |= 0xffffu << 16;
   const size_t ev_bytes = (8 * prog.size() + 15) & ~size_t(15);
   std::vector<double> cost(static_cast<size_t>(K));
   for (int32_t k = 0; k < K; k++) cost[size_t(k)] = double(t->sw_S[size_t(k)]) / t->bw;  // Eq. 3, as the model
@@ -248,8 +288,7 @@ chm_status launch_timeline(chm_ctx *ctx, const chm_trace *t, const EvalLaunch &L
   const chm_status st = build_program(t);
   if (st != CHM_OK) return st;
   const size_t ev_bytes = t->tl_cost_off, cost_bytes = (8 * size_t(t->K) + 15) & ~size_t(15);
-  const int W = std::max(t->W, 1);
-  const size_t smem = ev_bytes + cost_bytes + size_t(W) * kTlThreads * 8;
+  const size_t smem = ev_bytes + cost_bytes + size_t(2 * t->W + 1) * kTlThreads * 4;  // + bit K's word
   if (smem > 220 * 1024)
     CHM_FAIL(CHM_E_INVAL, "timeline: event program + masks (%zu B) exceed shared memory", smem);
   CHM_CUDA(cudaFuncSetAttribute(timeline_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));

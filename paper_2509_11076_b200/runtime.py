@@ -103,18 +103,18 @@ def _key3(k):
     return (int(k["excess"]), float(k["stall"]), int(k["swapped_bytes"]))
 
 
-def descend(ctx, pt, key, words, dev, max_rounds: int = 4096):
+def descend(ctx, pt, key, words, dev, max_rounds: int = 4096, stall_model: int = chm.STALL_LAYER):
     """steepest descent over single-bit flips of a mask (reading R-search): each round replays
     the whole one-bit neighbourhood of the current mask in one FLIP1 launch (the mask travels in
     kernel parameters) and moves to the best neighbour if it lowers the key (excess, stall,
     swapped bytes) -- the evaluator's throughput turned into plan quality.  key: the chm_best of
-    `words`.  Returns (key, words, rounds)."""
+    `words` (under the same stall model).  Returns (key, words, rounds)."""
     K = pt.K
     best = torch.empty(5, dtype=torch.int64, device=dev)
     cur = np.array(words, np.uint64)
     rounds = 0
     while rounds < max_rounds and K:
-        ctx.eval_policies(pt, chm.FLIP1, 0, K, best=best, base=cur)
+        ctx.eval_policies(pt, chm.FLIP1, 0, K, best=best, base=cur, stall_model=stall_model)
         nk = best.cpu().numpy().view(chm.BEST_DTYPE)[0]
         if not _key3(nk) < _key3(key):
             break
@@ -199,7 +199,8 @@ class Runtime:
                  groups_fwd: int = 0, groups_bwd: int = 0, omega: float = 1.0, candidates: int = 1 << 16,
                  seed: int = 1, flip_frac: float = 0.02, generator: bool = True, swap_ctas: int = 0,
                  min_swap_bytes: int = 0, search_rounds: int = 4096, host_arena_bytes: int = 0,
-                 swap_flags: int = chm.SWAP_AUTO, oom_host_bytes: int = 0, trials: int = 5, **algo1):
+                 swap_flags: int = chm.SWAP_AUTO, oom_host_bytes: int = 0, trials: int = 5,
+                 stall_model: int = chm.STALL_LAYER, **algo1):
         self.host_only = device is None
         self.dev = torch.device("cpu") if self.host_only else torch.device("cuda", device)
         self.ctx = chm.Context(device=-1 if self.host_only else device, swap_ctas=swap_ctas,
@@ -207,6 +208,9 @@ class Runtime:
                                max(int(host_arena_bytes) + int(oom_host_bytes), 1 << 20),
                                **algo1)
         self.search_rounds = int(search_rounds)
+        # the stall that ranks plans: R-stall (per-layer overflow) or the timeline (reading Q11,
+        # csrc/timeline.cu; explicit generator lists scored by chm_stall_models on the host)
+        self.stall_model = int(stall_model)
         self.n_trials = int(trials)  # plans tried on real steps before one is kept (n = 5)
         self.trials = None
         self.trial_running = False
@@ -663,7 +667,8 @@ class Runtime:
                 best = torch.empty(5, dtype=torch.int64, device=self.dev)
                 n = min(self.candidates, 1 << pt.K) if pt.K < 63 else self.candidates
                 kind = chm.EXHAUSTIVE if pt.K < 63 and (1 << pt.K) <= n else chm.SEEDED
-                self.ctx.eval_policies(pt, kind, 0, n, best=best, seed=self.seed, flip_thr=self.flip_thr)
+                self.ctx.eval_policies(pt, kind, 0, n, best=best, seed=self.seed, flip_thr=self.flip_thr,
+                                       stall_model=self.stall_model)
                 k = best.cpu().numpy().view(chm.BEST_DTYPE)[0]
                 words = pt.candidate_mask(kind, int(k["index"]), seed=self.seed, flip_thr=self.flip_thr)
                 cands.append(("seeded" if kind == chm.SEEDED else "exhaustive", k, words, False))
@@ -682,7 +687,8 @@ class Runtime:
                 pk, stl, swp = gpk.cpu().numpy(), gst.cpu().numpy(), gsw.cpu().numpy()
                 for j, g in enumerate(gen):  # every variant a key of its own (for the trials)
                     kj = np.zeros(1, chm.BEST_DTYPE)[0]
-                    kj["excess"], kj["stall"], kj["swapped_bytes"] = max(0, int(pk[j]) - pt.budget), stl[j], swp[j]
+                    st_j = pt.stall_models(g)[2] if self.stall_model == chm.STALL_TIMELINE else stl[j]
+                    kj["excess"], kj["stall"], kj["swapped_bytes"] = max(0, int(pk[j]) - pt.budget), st_j, swp[j]
                     kj["index"], kj["peak"] = j, pk[j]
                     cands.append((f"generator[{j}]", kj, g, True))
             plan["generator_ms"] = (time.perf_counter() - t1) * 1e3
@@ -696,7 +702,8 @@ class Runtime:
                 for name, k0, w0, _ in starts:
                     if k0 is None:
                         kb = torch.empty(5, dtype=torch.int64, device=self.dev)
-                        self.ctx.eval_policies(pt, chm.FLIP1, pt.K, 1, best=kb, base=w0)  # the mask itself
+                        self.ctx.eval_policies(pt, chm.FLIP1, pt.K, 1, best=kb, base=w0,  # the mask itself
+                                               stall_model=self.stall_model)
                         k0 = kb.cpu().numpy().view(chm.BEST_DTYPE)[0]
                     k, w, r = self._local_search(pt, k0, w0)
                     rounds += r
@@ -771,7 +778,7 @@ class Runtime:
         self.trials = None
 
     def _local_search(self, pt, key, words):
-        return descend(self.ctx, pt, key, words, self.dev, self.search_rounds)
+        return descend(self.ctx, pt, key, words, self.dev, self.search_rounds, self.stall_model)
 
     def _reserve_words(self, words, pt):
         if self.host_only:

@@ -130,3 +130,17 @@ def test_soak_many_steps_bit_exact():
     assert rt.stats["release"] > 0 and batches > 4096, rt.stats
     assert resource.getrusage(resource.RUSAGE_SELF).ru_maxrss - rss0 < 512 * 1024  # KiB
     rt.close()
+
+
+def test_runtime_ranks_plans_by_the_timeline(reference):
+    """stall_model = timeline: the runtime's search, descent and generator scoring rank plans by the
+    timeline stall; training stays bit-exact and the installed plan's reported stall is the host
+    timeline model (chm_stall_models out[2]) of its items"""
+    from paper_2509_11076_b200 import chm
+    rt = Runtime(0, hbm_budget=_budget(reference[2]), groups_fwd=6, groups_bwd=6, trials=1,
+                 stall_model=chm.STALL_TIMELINE)
+    run = _train(rt)
+    _check_exact(run, reference)
+    plan = rt.plans[0]
+    assert plan["items"] > 0
+    assert plan["stall"] == float(rt.policy[0].stall_models(rt.policy_items)[2])

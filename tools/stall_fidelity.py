@@ -38,6 +38,8 @@ def main():
     ap.add_argument("--model", default="llama", choices=["llama", "gpt2xl"],
                     help="gpt2xl: GPT-2 XL shape (48 layers, d 1600, 25 heads), fp32, attention written "
                          "out (scores materialised), workloads/tiny_gpt.py; use --seq 1024 --batch 4")
+    ap.add_argument("--stall-model", default="layer", choices=["layer", "timeline"],
+                    help="the stall that ranks the runtime's plans (R-stall or the timeline)")
     args = ap.parse_args()
     if args.model == "llama":
         cfg = dict(L.LLAMA2_7B, n_layer=args.layers)
@@ -74,7 +76,8 @@ def main():
     flags = dict(kernel=chm.SWAP_KERNEL, ce=chm.SWAP_CE, auto=chm.SWAP_AUTO)[args.flags]
     rt = Runtime(0, hbm_budget=m0 + act_peak, groups_fwd=args.layers, groups_bwd=args.layers,
                  host_arena_bytes=int(args.arena_gib * 2 ** 30), swap_ctas=args.swap_ctas, swap_flags=flags,
-                 trials=1)  # one plan per budget: its predicted stall against its measured slowdown
+                 trials=1,  # one plan per budget
+                 stall_model=chm.STALL_TIMELINE if args.stall_model == "timeline" else chm.STALL_LAYER)
     for _ in range(4):  # WarmUp -> GenPolicy; the first plan fits (no policy)
         one(rt)
     rows = []
@@ -96,7 +99,7 @@ def main():
                          stall_layer_s=round(float(models[0]), 4), stall_per_direction_s=round(float(models[1]), 4),
                          stall_timeline_s=round(float(models[2]), 4),
                          step_s=round(t_pol, 4), measured_overhead_s=round(t_pol - t_np, 4), plan_ms=round(plan["plan_ms"], 1)))
-    out = dict(flags=args.flags, swap_ctas=args.swap_ctas or 8,
+    out = dict(flags=args.flags, swap_ctas=args.swap_ctas or 8, stall_model=args.stall_model,
                model=("gpt2-xl-fp32" if args.model == "gpt2xl" else
                       "llama2-7b" if args.layers == 32 else f"llama2-7b-{args.layers}L"), dtype="fp32" if args.model == "gpt2xl" else "bf16", batch=args.batch,
                seq=args.seq, m0_gib=round(m0 / 2 ** 30, 3), no_swap_peak_gib=round((m0 + act_peak) / 2 ** 30, 3),
