@@ -193,14 +193,15 @@ class Runtime:
     plans (best simulated keys first) executed on consecutive real steps after a re-plan, the
     fastest kept ("generates five different policies and selects the one with the best
     runtime performance"; 1: keep the best key);
-    host_arena_bytes: pinned arena reserved up front (else grown to each policy at install)."""
+    host_arena_bytes: pinned arena reserved up front (else grown to each policy at install);
+    stall_model: the stall that ranks plans, chm.STALL_TIMELINE (default) or chm.STALL_LAYER."""
 
     def __init__(self, device: Optional[int] = 0, *, hbm_budget: int, bw: Optional[float] = None,
                  groups_fwd: int = 0, groups_bwd: int = 0, omega: float = 1.0, candidates: int = 1 << 16,
                  seed: int = 1, flip_frac: float = 0.02, generator: bool = True, swap_ctas: int = 0,
                  min_swap_bytes: int = 0, search_rounds: int = 4096, host_arena_bytes: int = 0,
                  swap_flags: int = chm.SWAP_AUTO, oom_host_bytes: int = 0, trials: int = 5,
-                 stall_model: int = chm.STALL_LAYER, **algo1):
+                 stall_model: int = chm.STALL_TIMELINE, **algo1):
         self.host_only = device is None
         self.dev = torch.device("cpu") if self.host_only else torch.device("cuda", device)
         self.ctx = chm.Context(device=-1 if self.host_only else device, swap_ctas=swap_ctas,
@@ -208,8 +209,9 @@ class Runtime:
                                max(int(host_arena_bytes) + int(oom_host_bytes), 1 << 20),
                                **algo1)
         self.search_rounds = int(search_rounds)
-        # the stall that ranks plans: R-stall (per-layer overflow) or the timeline (reading Q11,
-        # csrc/timeline.cu; explicit generator lists scored by chm_stall_models on the host)
+        # the stall that ranks plans: the timeline (default: reading Q11, csrc/timeline.cu; explicit
+        # generator lists scored by chm_stall_models on the host) or R-stall (per-layer overflow);
+        # timeline-ranked plans measured faster at mild budgets (DESIGN.md §5 Timeline)
         self.stall_model = int(stall_model)
         self.n_trials = int(trials)  # plans tried on real steps before one is kept (n = 5)
         self.trials = None
@@ -778,6 +780,9 @@ class Runtime:
         self.trials = None
 
     def _local_search(self, pt, key, words):
+        # the whole walk under the ranking model: a faster variant that first descended under
+        # R-stall and then under the timeline ended in worse plans (0.8 of the Llama-2 7B peak:
+        # 0.25 vs 0.17 s predicted, 1.08 vs 0.98 s measured steps)
         return descend(self.ctx, pt, key, words, self.dev, self.search_rounds, self.stall_model)
 
     def _reserve_words(self, words, pt):
