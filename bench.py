@@ -541,6 +541,25 @@ def main():
                  "gpu_eval_ms": ev[0].elapsed_time(ev[3]), "best_index": int(gb["index"]),
                  "best_peak": int(gb["peak"]), "best_excess": int(gb["excess"]), "best_stall_s": float(gb["stall"]),
                  "seeded_best_excess": int(bk["excess"]), "seeded_best_stall_s": float(bk["stall"])}
+    # ---- the same candidates ranked by the timeline stall (csrc/timeline.cu, reading Q11), the
+    # runtime's default ranking: device time of one launch (this rank's shard, search mode)
+    tl_ms = []
+    tl_best = torch.empty(5, dtype=torch.int64, device=dev)
+    for it in range(4):
+        torch.cuda.synchronize()
+        torch.cuda._sleep(spin_cycles)
+        ev[0].record(comp)
+        ctx.eval_policies(pt, chm.SEEDED, lo, cnt, best=tl_best, seed=sd["seed"], flip_thr=sd["flip_thr"],
+                          stall_model=chm.STALL_TIMELINE, stream=comp)
+        ev[3].record(comp)
+        torch.cuda.synchronize()
+        if it:
+            tl_ms.append(ev[0].elapsed_time(ev[3]))
+    tb_ = tl_best.cpu().numpy().view(chm.BEST_DTYPE)[0]
+    eval_timeline = {"ms_per_launch": float(np.mean(tl_ms)), "candidates_per_s": cnt / (np.mean(tl_ms) * 1e-3),
+                     "mode": "search (peak / swapped by the replay kernel, then the timeline kernel)",
+                     "best_index": int(tb_["index"]), "best_stall_s": float(tb_["stall"]),
+                     "layer_best_index": int(bk["index"])}
     # ---- re-plan latency on C4 (BASELINE configs[3]): the sequence switched to s = 8192; from the
     # Detailed iteration's records to an installed policy, through the public API (rank 0 work,
     # reported beside the line; not part of `value`)
@@ -615,6 +634,7 @@ def main():
         },
         "argmin_exchange_us": t_argmin * 1e3 if use_dist else None,
         "eval": {"candidates_per_s": C / (t_eval * 1e-3), "ms_per_launch": t_eval, "unit": "candidates/s"},
+        "eval_timeline": eval_timeline,
         "ce_baseline": {
             "what": "same batches, one cudaMemcpyAsync per tensor on the copy engines",
             "ms_per_step": float(np.mean(ce_ms)) if ce_ms else None,
