@@ -1,7 +1,8 @@
 """Write-pattern microbenchmark for the replay kernel's full mode (context only): 10^5 rows of
 2618 int64 (the C2 footprint rows, 2.09 GB) written (a) as one linear grid-stride stream,
 (b) one row per warp, rows handed out by an atomic counter (the replay kernel's pattern),
-(c) 16 consecutive rows per CTA written as one linear block by all 512 threads.
+(c) 16 consecutive rows per CTA written as one linear block by all 512 threads, (d) one row per
+warp composed in shared memory and written by TMA bulk stores (1 / 2 / 4 KiB, double-buffered).
 16 B streaming stores everywhere; 296 CTAs x 512 threads (2 per SM).  Prints GB/s."""
 import torch
 from torch.utils.cpp_extension import load_inline
@@ -40,12 +41,78 @@ __global__ void block_k(long long *out, int rows, int ld, unsigned long long *ct
     for (long long i = threadIdx.x; i < n2; i += blockDim.x) st2(b + 2 * i, c, i);
   }
 }
+// (d) row per warp, composed in a per-warp shared-memory chunk and written by TMA bulk stores
+// (cp.async.bulk.global.shared::cta), double-buffered: CH bytes per bulk store
+template <int CH>
+__global__ void rows_tma_k(long long *out, int rows, int ld, unsigned long long *ctr) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned char *buf = sm + warp * 2 * CH;
+  const unsigned sbuf = (unsigned)__cvta_generic_to_shared(buf);
+  int flip = 0;
+  while (true) {
+    unsigned long long c = 0;
+    if (lane == 0) c = atomicAdd(ctr, 1ull);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c >= (unsigned long long)rows) break;
+    long long *r = out + c * ld;
+    const long long row_bytes = (long long)ld * 8;
+    for (long long off = 0; off < row_bytes; off += CH) {
+      const int n = (int)min((long long)CH, row_bytes - off);
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      __syncwarp();
+      long long *sb = (long long *)(buf + flip * CH);
+      for (int q = lane; q < n / 16; q += 32) { sb[2 * q] = c; sb[2 * q + 1] = off / 16 + q; }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                     :: "l"((char *)r + off), "r"(sbuf + flip * CH), "r"(n) : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      flip ^= 1;
+    }
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+// (e) groups of G warps: G consecutive rows written as one linear block by the group's threads
+// (named barrier per group), i.e. 4736 / G concurrent write streams
+template <int G>
+__global__ void group_k(long long *out, int rows, int ld, unsigned long long *ctr) {
+  __shared__ unsigned long long c0[16];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, grp = warp / G, gt = threadIdx.x - grp * G * 32;
+  while (true) {
+    if (gt == 0) c0[grp] = atomicAdd(ctr, (unsigned long long)G);
+    asm volatile("bar.sync %0, %1;" :: "r"(grp + 1), "r"(G * 32) : "memory");
+    const unsigned long long c = c0[grp];
+    asm volatile("bar.sync %0, %1;" :: "r"(grp + 1), "r"(G * 32) : "memory");
+    if (c >= (unsigned long long)rows) break;
+    const long long nr = min((unsigned long long)G, rows - c);
+    long long *b = out + c * ld;
+    const long long n2 = nr * ld / 2;
+    for (long long i = gt; i < n2; i += G * 32) st2(b + 2 * i, c, i);
+  }
+  (void)lane;
+}
 void run(torch::Tensor out, int rows, int ld, torch::Tensor ctr, int mode) {
   auto *o = (long long *)out.data_ptr();
   auto *k = (unsigned long long *)ctr.data_ptr();
   if (mode == 0) linear_k<<<296, 512>>>(o, (long long)rows * ld / 2);
   else if (mode == 1) rows_k<<<296, 512>>>(o, rows, ld, k);
-  else block_k<<<296, 512>>>(o, rows, ld, k);
+  else if (mode == 2) block_k<<<296, 512>>>(o, rows, ld, k);
+  else if (mode == 3) {
+    cudaFuncSetAttribute(rows_tma_k<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 2 * 1024);
+    rows_tma_k<1024><<<296, 512, 16 * 2 * 1024>>>(o, rows, ld, k);
+  } else if (mode == 4) {
+    cudaFuncSetAttribute(rows_tma_k<2048>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 2 * 2048);
+    rows_tma_k<2048><<<296, 512, 16 * 2 * 2048>>>(o, rows, ld, k);
+  } else if (mode == 6) group_k<2><<<296, 512>>>(o, rows, ld, k);
+  else if (mode == 7) group_k<4><<<296, 512>>>(o, rows, ld, k);
+  else if (mode == 8) group_k<8><<<296, 512>>>(o, rows, ld, k);
+  else {
+    cudaFuncSetAttribute(rows_tma_k<4096>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 2 * 4096);
+    rows_tma_k<4096><<<296, 512, 16 * 2 * 4096>>>(o, rows, ld, k);
+  }
 }
 """
 mod = load_inline("write_pattern", cpp_sources="void run(torch::Tensor out, int rows, int ld, torch::Tensor ctr, int mode);",
@@ -55,7 +122,10 @@ rows, ld = 100_000, 2618
 out = torch.empty(rows * ld, dtype=torch.int64, device="cuda")
 ctr = torch.zeros(1, dtype=torch.int64, device="cuda")
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-for mode, name in ((0, "linear grid-stride"), (1, "row per warp (replay pattern)"), (2, "16 rows per CTA, linear")):
+for mode, name in ((0, "linear grid-stride"), (1, "row per warp (replay pattern)"), (2, "16 rows per CTA, linear"),
+                   (3, "row per warp, TMA bulk 1 KiB"), (4, "row per warp, TMA bulk 2 KiB"),
+                   (5, "row per warp, TMA bulk 4 KiB"), (6, "2-warp groups, 2 rows linear"),
+                   (7, "4-warp groups, 4 rows linear"), (8, "8-warp groups, 8 rows linear")):
     best = 1e9
     for it in range(8):
         ctr.zero_()
