@@ -1,4 +1,6 @@
-"""C3-style overlap: swaps on the swap stream while bf16 GEMMs run on the compute
+"""python tools/overlap.py [ctas,ctas,...]
+
+C3-style overlap: swaps on the swap stream while bf16 GEMMs run on the compute
 stream.  Reports GEMM TFLOP/s with no swap, with copy-engine swaps and with the swap kernel (its
 SM cost), and the swap GB/s under contention."""
 import json
@@ -21,7 +23,8 @@ def main():
     bufs = [torch.empty(nb, dtype=torch.uint8, device=dev) for _ in range(32)]  # 2 GiB
     descs = [(x.data_ptr(), j * nb, nb) for j, x in enumerate(bufs)]
     res = {}
-    for ctas in (8, 16, 32):
+    ctas_list = [int(x) for x in sys.argv[1].split(",")] if len(sys.argv) > 1 else [8, 16, 32]
+    for ctas in ctas_list:
         ctx = chm.Context(device=0, host_arena_bytes=2 << 30, swap_ctas=ctas, time_batches=True)
         comp, sw = torch.cuda.current_stream(), torch.cuda.Stream()
         for mode in ("none", "ce", "kernel"):
