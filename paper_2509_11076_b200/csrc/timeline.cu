@@ -21,6 +21,7 @@
 // so max(now, h2d, out_end) = max(now, h2d) exactly.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <queue>
 #include <vector>
@@ -37,12 +38,20 @@ constexpr int kTlGroup = 8;                   // events per group = prefetch dis
 constexpr unsigned kTlPrefetch = 1u << 17;    // event flag: its slot value is loaded a group ahead
 constexpr size_t kTlSlotCap = 256ull << 20;  // bytes of slot scratch at most (HBM is what swapping saves)
 
+template <bool kSm>
+__device__ __forceinline__ double ld_slot(const double *a) { return kSm ? *a : __ldcg(a); }
+template <bool kSm>
+__device__ __forceinline__ void st_slot(double *a, double v) {
+  if (kSm) *a = v;
+  else __stcg(a, v);
+}
+
 // event (8 B): x = k (15 bits) | kind << 15 (2) | prefetch flag << 17 | ticks << 18 (14),
 //              y = slot | slot to load for the event one group ahead << 16 (0xffff: none)
 struct TlParams {
   const uint2 *ev;
   const double *cost;
-  uint32_t n_ev, n_slots, ev_bytes, cost_bytes;
+  uint32_t n_ev, n_slots, ev_bytes, cost_bytes, slot_off;
   double tau;
   int kind, K, W;
   uint64_t first, count, seed, flip_thr;
@@ -58,9 +67,13 @@ struct TlParams {
   Key *best;
 };
 
-__global__ void __launch_bounds__(kTlThreads) timeline_kernel(const __grid_constant__ TlParams p) {
+// kT threads per CTA; kSm: the end-time slots live in shared memory (one warp per CTA, [slot]
+// [lane] after the masks) instead of global memory -- for launches too small to fill the GPU
+// (a descent round's FLIP1 neighbourhood), where one chain's latency is the launch's time
+template <int kT, bool kSm>
+__global__ void __launch_bounds__(kT) timeline_kernel(const __grid_constant__ TlParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ Key s_best[kTlThreads / 32];
+  __shared__ Key s_best[kT / 32];
   __shared__ unsigned int s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, bd = blockDim.x;
   uint2 *s_ev = reinterpret_cast<uint2 *>(smem);
@@ -70,25 +83,26 @@ __global__ void __launch_bounds__(kTlThreads) timeline_kernel(const __grid_const
   for (int k = tid; k < p.K; k += bd) s_cost[k] = __ldg(p.cost + k);
   __syncthreads();
   const uint64_t G = uint64_t(gridDim.x) * bd, gl = uint64_t(blockIdx.x) * bd + tid;
-  double *slot0 = p.slots + (gl >> 5) * uint64_t(p.n_slots) * 32 + (gl & 31);
-  unsigned *wm = s_mask + tid;  // 32-bit word w of this thread's candidate at wm[w * kTlThreads]
+  double *slot0 = kSm ? reinterpret_cast<double *>(smem + p.slot_off) + lane
+                      : p.slots + (gl >> 5) * uint64_t(p.n_slots) * 32 + (gl & 31);
+  unsigned *wm = s_mask + tid;  // 32-bit word w of this thread's candidate at wm[w * kT]
   const int W32 = 2 * p.W;
   Key best = key_none();
   for (uint64_t c = gl; c < p.count; c += G) {
     const uint64_t g = p.first + c;
     if (p.kind == CHM_CAND_EXHAUSTIVE) {
       wm[0] = unsigned(g);
-      wm[kTlThreads] = unsigned(g >> 32);
+      wm[kT] = unsigned(g >> 32);
     } else if (p.kind == CHM_CAND_MASKS) {
       for (int w = 0; w < p.W; w++) {
         const uint64_t x = __ldg(p.masks + c * uint64_t(p.W) + w);
-        wm[(2 * w) * kTlThreads] = unsigned(x);
-        wm[(2 * w + 1) * kTlThreads] = unsigned(x >> 32);
+        wm[(2 * w) * kT] = unsigned(x);
+        wm[(2 * w + 1) * kT] = unsigned(x >> 32);
       }
     } else {  // SEEDED / FLIP1: the base, then the flips (reading R-seeded; FLIP1 one bit)
-      for (int w = 0; w < W32; w++) wm[w * kTlThreads] = unsigned(p.base[w >> 1] >> (32 * (w & 1)));
+      for (int w = 0; w < W32; w++) wm[w * kT] = unsigned(p.base[w >> 1] >> (32 * (w & 1)));
       if (p.kind == CHM_CAND_FLIP1) {
-        if (g < uint64_t(p.K)) wm[(g >> 5) * kTlThreads] ^= 1u << (g & 31);
+        if (g < uint64_t(p.K)) wm[(g >> 5) * kT] ^= 1u << (g & 31);
       } else {
         const uint64_t J = (uint64_t(p.K) + 3) >> 2;
         const unsigned thr16 = unsigned(p.flip_thr >> 48);
@@ -98,12 +112,12 @@ __global__ void __launch_bounds__(kTlThreads) timeline_kernel(const __grid_const
           for (int e = 0; e < 4; e++) {
             const unsigned k = unsigned(4 * q) + e;
             if (k < unsigned(p.K) && unsigned((w >> (16 * e)) & 0xffffull) < thr16)
-              wm[(k >> 5) * kTlThreads] ^= 1u << (k & 31);
+              wm[(k >> 5) * kT] ^= 1u << (k & 31);
           }
         }
       }
     }
-    wm[(p.K >> 5) * kTlThreads] &= ~(1u << (p.K & 31));  // bit K: the never-selected item of NOPs
+    wm[(p.K >> 5) * kT] &= ~(1u << (p.K & 31));  // bit K: the never-selected item of NOPs
     // the program in groups of kTlGroup events; each event carries the slot of the event one
     // group ahead whose end time is already stored (the host checks), loaded here so that it
     // has arrived when that event runs
@@ -117,31 +131,35 @@ __global__ void __launch_bounds__(kTlThreads) timeline_kernel(const __grid_const
 #pragma unroll
       for (int j = 0; j < kTlGroup; j++) {
         const uint2 x = s_ev[e0 + j];  // n_ev is a multiple of kTlGroup (NOP padding)
-        const unsigned ps = x.y >> 16;
-        nx[j] = ps != 0xffffu ? __ldcg(reinterpret_cast<const double *>(sbase + (ps << 8))) : 0.0;
+        if (!kSm) {  // global slots: load one group ahead (shared-memory slots are close enough)
+          const unsigned ps = x.y >> 16;
+          nx[j] = ps != 0xffffu ? ld_slot<kSm>(reinterpret_cast<const double *>(sbase + (ps << 8))) : 0.0;
+        }
         for (unsigned t = x.x >> 18; t; t--) now = __dadd_rn(now, p.tau);  // ops between events
         const unsigned k = x.x & 0x7fffu, kind = (x.x >> 15) & 3u;
-        if (!((wm[(k >> 5) * kTlThreads] >> (k & 31)) & 1u)) continue;  // not selected (or a NOP)
+        if (!((wm[(k >> 5) * kT] >> (k & 31)) & 1u)) continue;  // not selected (or a NOP)
         CHM_DCHECK(int(k) < p.K && (x.y & 0xffffu) < p.n_slots);
         double *sl = reinterpret_cast<double *>(sbase + ((x.y & 0xffffu) << 8));
         if (kind == TL_IN) {  // before op s: the H2D FIFO
           const double v = __dadd_rn(h2d > now ? h2d : now, s_cost[k]);
           h2d = v;
-          __stcg(sl, v);
+          st_slot<kSm>(sl, v);
         } else if (kind == TL_OUT) {  // after op a: the D2H FIFO
           const double v = __dadd_rn(d2h > now ? d2h : now, s_cost[k]);
           d2h = v;
-          __stcg(sl, v);
+          st_slot<kSm>(sl, v);
         } else {  // wait (before op b: swap-in done) / release (after op r: swap-out done)
-          const double v = (x.x & kTlPrefetch) ? pf[j] : __ldcg(sl);
+          const double v = (!kSm && (x.x & kTlPrefetch)) ? pf[j] : ld_slot<kSm>(sl);
           if (v > now) {
             st = __dadd_rn(st, __dsub_rn(v, now));
             now = v;
           }
         }
       }
+      if (!kSm) {
 #pragma unroll
-      for (int j = 0; j < kTlGroup; j++) pf[j] = nx[j];
+        for (int j = 0; j < kTlGroup; j++) pf[j] = nx[j];
+      }
     }
     const long long pk = p.peak[c], sw = p.swapped[c];
     if (p.stall) p.stall[c] = st;
@@ -288,19 +306,38 @@ chm_status launch_timeline(chm_ctx *ctx, const chm_trace *t, const EvalLaunch &L
   const chm_status st = build_program(t);
   if (st != CHM_OK) return st;
   const size_t ev_bytes = t->tl_cost_off, cost_bytes = (8 * size_t(t->K) + 15) & ~size_t(15);
-  const size_t smem = ev_bytes + cost_bytes + size_t(2 * t->W + 1) * kTlThreads * 4;  // + bit K's word
+  const size_t mask_words = size_t(2 * t->W + 1);  // + bit K's word
+  const size_t per_thread = 8 * size_t(t->tl_slots);
+  // small launches (at most one wave of one-warp CTAs, e.g. a descent round's FLIP1
+  // neighbourhood): one warp per CTA with its slots in shared memory -- 23-25% less time per
+  // launch there (tools/timeline_paths.py); larger ones: 256-thread CTAs, slots in global memory
+  const size_t smem_sm = ev_bytes + cost_bytes + mask_words * 32 * 4 + 32 * per_thread;
+  bool use_sm = false;
+  int per_sm_sm = 0;
+  if (smem_sm <= 220 * 1024) {
+    CHM_CUDA(cudaFuncSetAttribute(timeline_kernel<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(smem_sm)));
+    CHM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_sm, timeline_kernel<32, true>, 32, smem_sm));
+    use_sm = per_sm_sm > 0 && L.count <= uint64_t(ctx->num_sms) * 32 * uint64_t(per_sm_sm);
+  }
+  if (const char *f = std::getenv("CHM_TL_SMEM"))  // measurement knob (tools/timeline_paths.py)
+    use_sm = f[0] == '1' && per_sm_sm > 0;
+  const int threads = use_sm ? 32 : kTlThreads;
+  const size_t smem = use_sm ? smem_sm : ev_bytes + cost_bytes + mask_words * kTlThreads * 4;
   if (smem > 220 * 1024)
     CHM_FAIL(CHM_E_INVAL, "timeline: event program + masks (%zu B) exceed shared memory", smem);
-  CHM_CUDA(cudaFuncSetAttribute(timeline_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  int per_sm = 0;
-  CHM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, timeline_kernel, kTlThreads, smem));
+  auto kern = use_sm ? timeline_kernel<32, true> : timeline_kernel<kTlThreads, false>;
+  int per_sm = per_sm_sm;
+  if (!use_sm) {
+    CHM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    CHM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+  }
   if (per_sm < 1) CHM_FAIL(CHM_E_INVAL, "timeline: kernel does not fit an SM");
-  const size_t per_thread = 8 * size_t(t->tl_slots);
-  const uint64_t cap_ctas = std::max<uint64_t>(1, kTlSlotCap / (per_thread * kTlThreads));
-  uint64_t grid64 = std::min<uint64_t>(uint64_t(ctx->num_sms) * per_sm, (L.count + kTlThreads - 1) / kTlThreads);
-  grid64 = std::max<uint64_t>(1, std::min(grid64, cap_ctas));
+  uint64_t grid64 = std::min<uint64_t>(uint64_t(ctx->num_sms) * per_sm, (L.count + threads - 1) / threads);
+  if (!use_sm) grid64 = std::min<uint64_t>(grid64, std::max<uint64_t>(1, kTlSlotCap / (per_thread * threads)));
+  grid64 = std::max<uint64_t>(1, grid64);
   const int grid = int(grid64);
-  const size_t slot_bytes = size_t(grid) * kTlThreads * per_thread;
+  const size_t slot_bytes = use_sm ? 0 : size_t(grid) * threads * per_thread;
   if (ctx->tl_scratch_bytes < slot_bytes) {
     if (ctx->tl_scratch) cudaFree(ctx->tl_scratch);
     ctx->tl_scratch = nullptr;
@@ -317,6 +354,7 @@ chm_status launch_timeline(chm_ctx *ctx, const chm_trace *t, const EvalLaunch &L
   p.n_slots = t->tl_slots;
   p.ev_bytes = uint32_t(ev_bytes);
   p.cost_bytes = uint32_t(cost_bytes);
+  p.slot_off = uint32_t(ev_bytes + cost_bytes + mask_words * 32 * 4);  // kSm: 16 B aligned
   p.tau = t->tl_tau;
   p.kind = L.kind;
   p.K = t->K;
@@ -335,7 +373,7 @@ chm_status launch_timeline(chm_ctx *ctx, const chm_trace *t, const EvalLaunch &L
   p.ticket = reinterpret_cast<unsigned int *>(ctx->eval_scratch);
   p.partial = reinterpret_cast<Key *>(static_cast<char *>(ctx->eval_scratch) + 256);
   p.best = reinterpret_cast<Key *>(L.best);
-  timeline_kernel<<<grid, kTlThreads, smem, stream>>>(p);
+  kern<<<grid, threads, smem, stream>>>(p);
   CHM_CUDA(cudaGetLastError());
   return CHM_OK;
 }

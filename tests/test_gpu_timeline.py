@@ -107,3 +107,17 @@ def test_outputs_optional_and_errors(ctx):
                           items=np.zeros(0, chm.ITEM_DTYPE), stall_model=chm.STALL_TIMELINE)
     with pytest.raises(chm.ChmError):
         ctx.eval_policies(pt, chm.EXHAUSTIVE, 0, 4, best=best, stall_model=2)
+
+
+@pytest.mark.parametrize("path", ["0", "1"])
+def test_both_slot_paths(ctx, path, monkeypatch):
+    """global-memory slots (256-thread CTAs) and shared-memory slots (one warp per CTA), forced
+    either way on the same launch, both bit-identical to the oracle"""
+    monkeypatch.setenv("CHM_TL_SMEM", path)
+    tr = W.CONFIGS["C5"]()
+    pt = product_trace(ctx, tr)
+    m = O.Model(tr)
+    sd = W.SEEDED["C5"]
+    res = tl(ctx, pt, chm.SEEDED, 5, 3000, seed=sd["seed"], flip_thr=sd["flip_thr"])
+    ref = m.eval(O.SEEDED, 5, 3000, seed=sd["seed"], flip_thr=sd["flip_thr"], nthreads=16, stall_model=1)
+    assert_same(res, ref, tr.budget)
