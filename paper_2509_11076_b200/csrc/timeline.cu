@@ -34,7 +34,7 @@ namespace {
 
 enum : unsigned { TL_IN = 0, TL_WAIT = 1, TL_OUT = 2, TL_REL = 3 };  // NOP: item K (never selected)
 constexpr int kTlThreads = 256;
-constexpr int kTlGroup = 8;                   // events per group = prefetch distance
+constexpr int kTlGroup = 4;                   // events per group = prefetch distance
 constexpr unsigned kTlPrefetch = 1u << 17;    // event flag: its slot value is loaded a group ahead
 constexpr size_t kTlSlotCap = 256ull << 20;  // bytes of slot scratch at most (HBM is what swapping saves)
 
@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(kT) timeline_kernel(const __grid_constant__ Tl
   double *s_cost = reinterpret_cast<double *>(smem + p.ev_bytes);
   unsigned *s_mask = reinterpret_cast<unsigned *>(smem + p.ev_bytes + p.cost_bytes);
   for (uint32_t i = tid; i < p.n_ev; i += bd) s_ev[i] = __ldg(p.ev + i);
-  for (int k = tid; k < p.K; k += bd) s_cost[k] = __ldg(p.cost + k);
+  for (int k = tid; k <= p.K; k += bd) s_cost[k] = __ldg(p.cost + k);  // [K] = 0: NOPs
   __syncthreads();
   const uint64_t G = uint64_t(gridDim.x) * bd, gl = uint64_t(blockIdx.x) * bd + tid;
   double *slot0 = kSm ? reinterpret_cast<double *>(smem + p.slot_off) + lane
@@ -127,25 +127,37 @@ __global__ void __launch_bounds__(kT) timeline_kernel(const __grid_constant__ Tl
     for (int j = 0; j < kTlGroup; j++) pf[j] = 0.0;
     char *sbase = reinterpret_cast<char *>(slot0);
     for (uint32_t e0 = 0; e0 < p.n_ev; e0 += kTlGroup) {
-      double nx[kTlGroup];
+      double nx[kTlGroup], cst[kTlGroup];
+      uint2 xs[kTlGroup];
+      bool sel[kTlGroup];
+      // the group's independent work first (event decode, selection, cost, prefetch), then the
+      // serial chain over `now` / the FIFOs
 #pragma unroll
       for (int j = 0; j < kTlGroup; j++) {
         const uint2 x = s_ev[e0 + j];  // n_ev is a multiple of kTlGroup (NOP padding)
+        xs[j] = x;
         if (!kSm) {  // global slots: load one group ahead (shared-memory slots are close enough)
           const unsigned ps = x.y >> 16;
           nx[j] = ps != 0xffffu ? ld_slot<kSm>(reinterpret_cast<const double *>(sbase + (ps << 8))) : 0.0;
         }
+        const unsigned k = x.x & 0x7fffu;
+        sel[j] = (wm[(k >> 5) * kT] >> (k & 31)) & 1u;  // not selected (or a NOP: item K)
+        cst[j] = s_cost[k];                              // cost[K] = 0 pads the NOPs
+      }
+#pragma unroll
+      for (int j = 0; j < kTlGroup; j++) {
+        const uint2 x = xs[j];
         for (unsigned t = x.x >> 18; t; t--) now = __dadd_rn(now, p.tau);  // ops between events
-        const unsigned k = x.x & 0x7fffu, kind = (x.x >> 15) & 3u;
-        if (!((wm[(k >> 5) * kT] >> (k & 31)) & 1u)) continue;  // not selected (or a NOP)
-        CHM_DCHECK(int(k) < p.K && (x.y & 0xffffu) < p.n_slots);
+        if (!sel[j]) continue;
+        const unsigned kind = (x.x >> 15) & 3u;
+        CHM_DCHECK(int(x.x & 0x7fffu) < p.K && (x.y & 0xffffu) < p.n_slots);
         double *sl = reinterpret_cast<double *>(sbase + ((x.y & 0xffffu) << 8));
         if (kind == TL_IN) {  // before op s: the H2D FIFO
-          const double v = __dadd_rn(h2d > now ? h2d : now, s_cost[k]);
+          const double v = __dadd_rn(h2d > now ? h2d : now, cst[j]);
           h2d = v;
           st_slot<kSm>(sl, v);
         } else if (kind == TL_OUT) {  // after op a: the D2H FIFO
-          const double v = __dadd_rn(d2h > now ? d2h : now, s_cost[k]);
+          const double v = __dadd_rn(d2h > now ? d2h : now, cst[j]);
           d2h = v;
           st_slot<kSm>(sl, v);
         } else {  // wait (before op b: swap-in done) / release (after op r: swap-out done)
@@ -265,8 +277,10 @@ chm_status build_program(const chm_trace *tc) {
     } else {
       slot = slot_of[key];
       free_slots.push(slot);
-      // the kernel loads this value while it runs event idx - kTlGroup: the store must precede it
-      if (idx >= size_t(kTlGroup) && store_at[key] < idx - kTlGroup) flag = kTlPrefetch;
+      // the kernel loads the values of group G at the start of group G - 1 (before any of its
+      // events run): the store must precede that group
+      const size_t grp = idx / kTlGroup;
+      if (grp >= 1 && store_at[key] < kTlGroup * (grp - 1)) flag = kTlPrefetch;
     }
     if (n_slots >= 0xffffu) CHM_FAIL(CHM_E_INVAL, "timeline: more than 65534 concurrent items");
     prog.push_back(make_uint2(uint32_t(e.k) | (uint32_t(e.ph) << 15) | flag | (uint32_t(ticks) << 18), slot));
@@ -279,14 +293,13 @@ chm_status build_program(const chm_trace *tc) {
   for (size_t i = 0; i + kTlGroup < prog.size(); i++) prog[i].y |= pf_slot[i + kTlGroup] << 16;
   for (size_t i = prog.size() >= kTlGroup ? prog.size() - kTlGroup : 0; i < prog.size(); i++) prog[i].y |= 0xffffu << 16;
   const size_t ev_bytes = (8 * prog.size() + 15) & ~size_t(15);
-  std::vector<double> cost(static_cast<size_t>(K));
+  std::vector<double> cost(static_cast<size_t>(K) + 1, 0.0);  // [K] = 0 for the NOP item
   for (int32_t k = 0; k < K; k++) cost[size_t(k)] = double(t->sw_S[size_t(k)]) / t->bw;  // Eq. 3, as the model
   CHM_CUDA(cudaSetDevice(t->device));
   void *d = nullptr;
-  CHM_CUDA(cudaMalloc(&d, ev_bytes + 8 * size_t(std::max(K, 1))));
+  CHM_CUDA(cudaMalloc(&d, ev_bytes + 8 * (size_t(K) + 1)));
   cudaError_t e1 = cudaMemcpy(d, prog.data(), 8 * prog.size(), cudaMemcpyHostToDevice);
-  cudaError_t e2 = K ? cudaMemcpy(static_cast<char *>(d) + ev_bytes, cost.data(), 8 * size_t(K), cudaMemcpyHostToDevice)
-                     : cudaSuccess;
+  cudaError_t e2 = cudaMemcpy(static_cast<char *>(d) + ev_bytes, cost.data(), 8 * (size_t(K) + 1), cudaMemcpyHostToDevice);
   if (e1 != cudaSuccess || e2 != cudaSuccess) {
     cudaFree(d);
     CHM_FAIL(CHM_E_CUDA, "timeline: program upload failed");
@@ -305,7 +318,7 @@ chm_status launch_timeline(chm_ctx *ctx, const chm_trace *t, const EvalLaunch &L
                            const int64_t *swapped, cudaStream_t stream) {
   const chm_status st = build_program(t);
   if (st != CHM_OK) return st;
-  const size_t ev_bytes = t->tl_cost_off, cost_bytes = (8 * size_t(t->K) + 15) & ~size_t(15);
+  const size_t ev_bytes = t->tl_cost_off, cost_bytes = (8 * (size_t(t->K) + 1) + 15) & ~size_t(15);
   const size_t mask_words = size_t(2 * t->W + 1);  // + bit K's word
   const size_t per_thread = 8 * size_t(t->tl_slots);
   // small launches (at most one wave of one-warp CTAs, e.g. a descent round's FLIP1
