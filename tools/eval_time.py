@@ -19,7 +19,7 @@ def main():
     full = "--search" not in sys.argv
     tr = W.CONFIGS[name]()
     sd = W.SEEDED[name]
-    ctx = chm.Context(device=0)
+    ctx = chm.Context(device=0, eval_ctas_per_sm=int(os.environ.get("EVAL_CTAS_PER_SM", "0")))
     ctx.set_detailed(True)
     chm.record_iteration(ctx, tr)
     ctx.detect_seq_change(tr.t_iter)
@@ -44,7 +44,7 @@ def main():
             ts.append(s.elapsed_time(e))
     byt = (8 * ld + 16) * n if full else 16 * n
     med = float(np.median(ts))
-    print(f"{os.environ.get('CHM_LIB', 'libchm.so')} {name} {'full' if full else 'search'}: median {med:.4f} ms "
+    print(f"ctas/SM {os.environ.get('EVAL_CTAS_PER_SM', 'auto')} {name} {'full' if full else 'search'}: median {med:.4f} ms "
           f"min {min(ts):.4f} ms  {byt / (med * 1e-3) / 1e9:.0f} GB/s")
 
 

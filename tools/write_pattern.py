@@ -94,6 +94,41 @@ __global__ void group_k(long long *out, int rows, int ld, unsigned long long *ct
   }
   (void)lane;
 }
+// (f) row per warp with 256-bit stores (st.global.cs.v4.s64, sm_100): 1 KiB per warp instruction
+__device__ __forceinline__ void st4(long long *d, long long a, long long b, long long c, long long e) {
+  asm volatile("st.global.cs.v4.s64 [%0], {%1, %2, %3, %4};" :: "l"(d), "l"(a), "l"(b), "l"(c), "l"(e));
+}
+__global__ void rows256_k(long long *out, int rows, int ld, unsigned long long *ctr) {
+  int lane = threadIdx.x & 31;
+  while (true) {
+    unsigned long long c = 0;
+    if (lane == 0) c = atomicAdd(ctr, 1ull);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c >= (unsigned long long)rows) break;
+    long long *r = out + c * ld;
+    const int h = (reinterpret_cast<unsigned long long>(r) & 31) ? 2 : 0;  // 16 B head to 32 B alignment
+    if (h && lane == 0) st2(r, c, c);
+    const int n4 = (ld - h) / 4;
+    for (int q = lane; q < n4; q += 32) st4(r + h + 4 * q, c, q, c, q);
+    for (int q = h + 4 * n4 + lane; q < ld; q += 32) r[q] = c;  // tail
+  }
+}
+// (g) row per warp, default write-back stores (no .cs) / L2 evict_last hint
+template <int kHint>
+__global__ void rows_wb_k(long long *out, int rows, int ld, unsigned long long *ctr) {
+  int lane = threadIdx.x & 31;
+  while (true) {
+    unsigned long long c = 0;
+    if (lane == 0) c = atomicAdd(ctr, 1ull);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c >= (unsigned long long)rows) break;
+    long long *r = out + c * ld;
+    for (int q = lane; q < ld / 2; q += 32) {
+      if (kHint == 0) asm volatile("st.global.v2.s64 [%0], {%1, %2};" :: "l"(r + 2 * q), "l"((long long)c), "l"((long long)q));
+      else asm volatile("st.global.L1::no_allocate.v2.s64 [%0], {%1, %2};" :: "l"(r + 2 * q), "l"((long long)c), "l"((long long)q));
+    }
+  }
+}
 void run(torch::Tensor out, int rows, int ld, torch::Tensor ctr, int mode) {
   auto *o = (long long *)out.data_ptr();
   auto *k = (unsigned long long *)ctr.data_ptr();
@@ -109,6 +144,9 @@ void run(torch::Tensor out, int rows, int ld, torch::Tensor ctr, int mode) {
   } else if (mode == 6) group_k<2><<<296, 512>>>(o, rows, ld, k);
   else if (mode == 7) group_k<4><<<296, 512>>>(o, rows, ld, k);
   else if (mode == 8) group_k<8><<<296, 512>>>(o, rows, ld, k);
+  else if (mode == 9) rows256_k<<<296, 512>>>(o, rows, ld, k);
+  else if (mode == 10) rows_wb_k<0><<<296, 512>>>(o, rows, ld, k);
+  else if (mode == 11) rows_wb_k<1><<<296, 512>>>(o, rows, ld, k);
   else {
     cudaFuncSetAttribute(rows_tma_k<4096>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 2 * 4096);
     rows_tma_k<4096><<<296, 512, 16 * 2 * 4096>>>(o, rows, ld, k);
@@ -125,7 +163,9 @@ s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True
 for mode, name in ((0, "linear grid-stride"), (1, "row per warp (replay pattern)"), (2, "16 rows per CTA, linear"),
                    (3, "row per warp, TMA bulk 1 KiB"), (4, "row per warp, TMA bulk 2 KiB"),
                    (5, "row per warp, TMA bulk 4 KiB"), (6, "2-warp groups, 2 rows linear"),
-                   (7, "4-warp groups, 4 rows linear"), (8, "8-warp groups, 8 rows linear")):
+                   (7, "4-warp groups, 4 rows linear"), (8, "8-warp groups, 8 rows linear"),
+                   (9, "row per warp, 256-bit stores"), (10, "row per warp, write-back stores"),
+                   (11, "row per warp, L1::no_allocate stores")):
     best = 1e9
     for it in range(8):
         ctr.zero_()
