@@ -33,7 +33,9 @@ namespace chm {
 namespace {
 
 enum : unsigned { TL_IN = 0, TL_WAIT = 1, TL_OUT = 2, TL_REL = 3 };  // NOP: item K (never selected)
-constexpr int kTlThreads = 256;
+constexpr int kTlThreads = 256;   // CTA size, one candidate per thread
+constexpr int kTlThreads2 = 128;  // CTA size, two candidates per thread
+constexpr int kTlCpt = 1;         // candidates per thread on the global-memory path
 constexpr int kTlGroup = 4;                   // events per group = prefetch distance
 constexpr unsigned kTlPrefetch = 1u << 17;    // event flag: its slot value is loaded a group ahead
 constexpr size_t kTlSlotCap = 256ull << 20;  // bytes of slot scratch at most (HBM is what swapping saves)
@@ -69,8 +71,9 @@ struct TlParams {
 
 // kT threads per CTA; kSm: the end-time slots live in shared memory (one warp per CTA, [slot]
 // [lane] after the masks) instead of global memory -- for launches too small to fill the GPU
-// (a descent round's FLIP1 neighbourhood), where one chain's latency is the launch's time
-template <int kT, bool kSm>
+// (a descent round's FLIP1 neighbourhood), where one chain's latency is the launch's time;
+// kC candidates per thread: their chains share the event decode and interleave (ILP)
+template <int kT, bool kSm, int kC>
 __global__ void __launch_bounds__(kT) timeline_kernel(const __grid_constant__ TlParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Key s_best[kT / 32];
@@ -83,105 +86,132 @@ __global__ void __launch_bounds__(kT) timeline_kernel(const __grid_constant__ Tl
   for (int k = tid; k <= p.K; k += bd) s_cost[k] = __ldg(p.cost + k);  // [K] = 0: NOPs
   __syncthreads();
   const uint64_t G = uint64_t(gridDim.x) * bd, gl = uint64_t(blockIdx.x) * bd + tid;
-  double *slot0 = kSm ? reinterpret_cast<double *>(smem + p.slot_off) + lane
-                      : p.slots + (gl >> 5) * uint64_t(p.n_slots) * 32 + (gl & 31);
-  unsigned *wm = s_mask + tid;  // 32-bit word w of this thread's candidate at wm[w * kT]
-  const int W32 = 2 * p.W;
-  Key best = key_none();
-  for (uint64_t c = gl; c < p.count; c += G) {
-    const uint64_t g = p.first + c;
-    if (p.kind == CHM_CAND_EXHAUSTIVE) {
-      wm[0] = unsigned(g);
-      wm[kT] = unsigned(g >> 32);
-    } else if (p.kind == CHM_CAND_MASKS) {
-      for (int w = 0; w < p.W; w++) {
-        const uint64_t x = __ldg(p.masks + c * uint64_t(p.W) + w);
-        wm[(2 * w) * kT] = unsigned(x);
-        wm[(2 * w + 1) * kT] = unsigned(x >> 32);
-      }
-    } else {  // SEEDED / FLIP1: the base, then the flips (reading R-seeded; FLIP1 one bit)
-      for (int w = 0; w < W32; w++) wm[w * kT] = unsigned(p.base[w >> 1] >> (32 * (w & 1)));
-      if (p.kind == CHM_CAND_FLIP1) {
-        if (g < uint64_t(p.K)) wm[(g >> 5) * kT] ^= 1u << (g & 31);
-      } else {
-        const uint64_t J = (uint64_t(p.K) + 3) >> 2;
-        const unsigned thr16 = unsigned(p.flip_thr >> 48);
-        for (uint64_t q = 0; q < J; q++) {
-          const uint64_t w = mix64(p.seed ^ mix64(g * J + q));
+  const int W32 = 2 * p.W, MW = W32 + 1;  // + bit K's word
+  char *sbase[kC];
+  unsigned *wm[kC];  // 32-bit word w of candidate ci of this thread at wm[ci][w * kT]
 #pragma unroll
-          for (int e = 0; e < 4; e++) {
-            const unsigned k = unsigned(4 * q) + e;
-            if (k < unsigned(p.K) && unsigned((w >> (16 * e)) & 0xffffull) < thr16)
-              wm[(k >> 5) * kT] ^= 1u << (k & 31);
+  for (int ci = 0; ci < kC; ci++) {
+    double *slot0 = kSm ? reinterpret_cast<double *>(smem + p.slot_off) + uint64_t(ci) * p.n_slots * 32 + lane
+                        : p.slots + ((gl >> 5) * kC + ci) * uint64_t(p.n_slots) * 32 + (gl & 31);
+    sbase[ci] = reinterpret_cast<char *>(slot0);
+    wm[ci] = s_mask + ci * MW * kT + tid;
+  }
+  Key best = key_none();
+  for (uint64_t q0 = gl; q0 * kC < p.count; q0 += G) {
+#pragma unroll
+    for (int ci = 0; ci < kC; ci++) {  // decode the masks (a candidate past the range: empty)
+      const uint64_t c = q0 * kC + ci, g = p.first + c;
+      unsigned *w_ = wm[ci];
+      if (c >= p.count) {
+        for (int w = 0; w < MW; w++) w_[w * kT] = 0u;
+        continue;
+      }
+      if (p.kind == CHM_CAND_EXHAUSTIVE) {
+        w_[0] = unsigned(g);
+        w_[kT] = unsigned(g >> 32);
+      } else if (p.kind == CHM_CAND_MASKS) {
+        for (int w = 0; w < p.W; w++) {
+          const uint64_t x = __ldg(p.masks + c * uint64_t(p.W) + w);
+          w_[(2 * w) * kT] = unsigned(x);
+          w_[(2 * w + 1) * kT] = unsigned(x >> 32);
+        }
+      } else {  // SEEDED / FLIP1: the base, then the flips (reading R-seeded; FLIP1 one bit)
+        for (int w = 0; w < W32; w++) w_[w * kT] = unsigned(p.base[w >> 1] >> (32 * (w & 1)));
+        if (p.kind == CHM_CAND_FLIP1) {
+          if (g < uint64_t(p.K)) w_[(g >> 5) * kT] ^= 1u << (g & 31);
+        } else {
+          const uint64_t J = (uint64_t(p.K) + 3) >> 2;
+          const unsigned thr16 = unsigned(p.flip_thr >> 48);
+          for (uint64_t q = 0; q < J; q++) {
+            const uint64_t w = mix64(p.seed ^ mix64(g * J + q));
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+              const unsigned k = unsigned(4 * q) + e;
+              if (k < unsigned(p.K) && unsigned((w >> (16 * e)) & 0xffffull) < thr16)
+                w_[(k >> 5) * kT] ^= 1u << (k & 31);
+            }
           }
         }
       }
+      w_[(p.K >> 5) * kT] &= ~(1u << (p.K & 31));  // bit K: the never-selected item of NOPs
     }
-    wm[(p.K >> 5) * kT] &= ~(1u << (p.K & 31));  // bit K: the never-selected item of NOPs
-    // the program in groups of kTlGroup events; each event carries the slot of the event one
-    // group ahead whose end time is already stored (the host checks), loaded here so that it
-    // has arrived when that event runs
-    double now = 0.0, d2h = 0.0, h2d = 0.0, st = 0.0;
-    double pf[kTlGroup];
+    double now[kC], d2h[kC], h2d[kC], st[kC], pf[kC][kTlGroup];
 #pragma unroll
-    for (int j = 0; j < kTlGroup; j++) pf[j] = 0.0;
-    char *sbase = reinterpret_cast<char *>(slot0);
+    for (int ci = 0; ci < kC; ci++) {
+      now[ci] = d2h[ci] = h2d[ci] = st[ci] = 0.0;
+#pragma unroll
+      for (int j = 0; j < kTlGroup; j++) pf[ci][j] = 0.0;
+    }
     for (uint32_t e0 = 0; e0 < p.n_ev; e0 += kTlGroup) {
-      double nx[kTlGroup], cst[kTlGroup];
+      double nx[kC][kTlGroup], cst[kTlGroup];
       uint2 xs[kTlGroup];
-      bool sel[kTlGroup];
+      bool sel[kC][kTlGroup];
       // the group's independent work first (event decode, selection, cost, prefetch), then the
-      // serial chain over `now` / the FIFOs
+      // serial chains over `now` / the FIFOs
 #pragma unroll
       for (int j = 0; j < kTlGroup; j++) {
         const uint2 x = s_ev[e0 + j];  // n_ev is a multiple of kTlGroup (NOP padding)
         xs[j] = x;
-        if (!kSm) {  // global slots: load one group ahead (shared-memory slots are close enough)
-          const unsigned ps = x.y >> 16;
-          nx[j] = ps != 0xffffu ? ld_slot<kSm>(reinterpret_cast<const double *>(sbase + (ps << 8))) : 0.0;
+        const unsigned k = x.x & 0x7fffu, ps = x.y >> 16;
+        cst[j] = s_cost[k];  // cost[K] = 0 pads the NOPs
+#pragma unroll
+        for (int ci = 0; ci < kC; ci++) {
+          if (!kSm)  // global slots: load one group ahead (shared-memory slots are close enough)
+            nx[ci][j] = ps != 0xffffu ? ld_slot<kSm>(reinterpret_cast<const double *>(sbase[ci] + (ps << 8))) : 0.0;
+          sel[ci][j] = (wm[ci][(k >> 5) * kT] >> (k & 31)) & 1u;  // not selected (or a NOP: item K)
         }
-        const unsigned k = x.x & 0x7fffu;
-        sel[j] = (wm[(k >> 5) * kT] >> (k & 31)) & 1u;  // not selected (or a NOP: item K)
-        cst[j] = s_cost[k];                              // cost[K] = 0 pads the NOPs
       }
 #pragma unroll
       for (int j = 0; j < kTlGroup; j++) {
         const uint2 x = xs[j];
-        for (unsigned t = x.x >> 18; t; t--) now = __dadd_rn(now, p.tau);  // ops between events
-        if (!sel[j]) continue;
-        const unsigned kind = (x.x >> 15) & 3u;
-        CHM_DCHECK(int(x.x & 0x7fffu) < p.K && (x.y & 0xffffu) < p.n_slots);
-        double *sl = reinterpret_cast<double *>(sbase + ((x.y & 0xffffu) << 8));
-        if (kind == TL_IN) {  // before op s: the H2D FIFO
-          const double v = __dadd_rn(h2d > now ? h2d : now, cst[j]);
-          h2d = v;
-          st_slot<kSm>(sl, v);
-        } else if (kind == TL_OUT) {  // after op a: the D2H FIFO
-          const double v = __dadd_rn(d2h > now ? d2h : now, cst[j]);
-          d2h = v;
-          st_slot<kSm>(sl, v);
-        } else {  // wait (before op b: swap-in done) / release (after op r: swap-out done)
-          const double v = (!kSm && (x.x & kTlPrefetch)) ? pf[j] : ld_slot<kSm>(sl);
-          if (v > now) {
-            st = __dadd_rn(st, __dsub_rn(v, now));
-            now = v;
+        const unsigned kind = (x.x >> 15) & 3u, so = (x.y & 0xffffu) << 8;
+        for (unsigned t = x.x >> 18; t; t--) {  // ops between events
+#pragma unroll
+          for (int ci = 0; ci < kC; ci++) now[ci] = __dadd_rn(now[ci], p.tau);
+        }
+        CHM_DCHECK((x.y & 0xffffu) < p.n_slots);
+#pragma unroll
+        for (int ci = 0; ci < kC; ci++) {
+          if (!sel[ci][j]) continue;
+          double *sl = reinterpret_cast<double *>(sbase[ci] + so);
+          if (kind == TL_IN) {  // before op s: the H2D FIFO
+            const double v = __dadd_rn(h2d[ci] > now[ci] ? h2d[ci] : now[ci], cst[j]);
+            h2d[ci] = v;
+            st_slot<kSm>(sl, v);
+          } else if (kind == TL_OUT) {  // after op a: the D2H FIFO
+            const double v = __dadd_rn(d2h[ci] > now[ci] ? d2h[ci] : now[ci], cst[j]);
+            d2h[ci] = v;
+            st_slot<kSm>(sl, v);
+          } else {  // wait (before op b: swap-in done) / release (after op r: swap-out done)
+            const double v = (!kSm && (x.x & kTlPrefetch)) ? pf[ci][j] : ld_slot<kSm>(sl);
+            if (v > now[ci]) {
+              st[ci] = __dadd_rn(st[ci], __dsub_rn(v, now[ci]));
+              now[ci] = v;
+            }
           }
         }
       }
       if (!kSm) {
 #pragma unroll
-        for (int j = 0; j < kTlGroup; j++) pf[j] = nx[j];
+        for (int ci = 0; ci < kC; ci++)
+#pragma unroll
+          for (int j = 0; j < kTlGroup; j++) pf[ci][j] = nx[ci][j];
       }
     }
-    const long long pk = p.peak[c], sw = p.swapped[c];
-    if (p.stall) p.stall[c] = st;
-    Key kk;
-    kk.excess = pk > p.budget ? pk - p.budget : 0;
-    kk.stall = st;
-    kk.swapped = sw;
-    kk.index = g;
-    kk.peak = pk;
-    if (key_less(kk, best)) best = kk;
+#pragma unroll
+    for (int ci = 0; ci < kC; ci++) {
+      const uint64_t c = q0 * kC + ci;
+      if (c >= p.count) continue;
+      const long long pk = p.peak[c], sw = p.swapped[c];
+      if (p.stall) p.stall[c] = st[ci];
+      Key kk;
+      kk.excess = pk > p.budget ? pk - p.budget : 0;
+      kk.stall = st[ci];
+      kk.swapped = sw;
+      kk.index = p.first + c;
+      kk.peak = pk;
+      if (key_less(kk, best)) best = kk;
+    }
   }
   // thread keys -> warp -> CTA -> the last CTA to finish reduces all CTA keys into *best
 #pragma unroll
@@ -328,29 +358,35 @@ chm_status launch_timeline(chm_ctx *ctx, const chm_trace *t, const EvalLaunch &L
   bool use_sm = false;
   int per_sm_sm = 0;
   if (smem_sm <= 220 * 1024) {
-    CHM_CUDA(cudaFuncSetAttribute(timeline_kernel<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CHM_CUDA(cudaFuncSetAttribute(timeline_kernel<32, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(smem_sm)));
-    CHM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_sm, timeline_kernel<32, true>, 32, smem_sm));
+    CHM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_sm, timeline_kernel<32, true, 1>, 32, smem_sm));
     use_sm = per_sm_sm > 0 && L.count <= uint64_t(ctx->num_sms) * 32 * uint64_t(per_sm_sm);
   }
   if (const char *f = std::getenv("CHM_TL_SMEM"))  // measurement knob (tools/timeline_paths.py)
     use_sm = f[0] == '1' && per_sm_sm > 0;
-  const int threads = use_sm ? 32 : kTlThreads;
-  const size_t smem = use_sm ? smem_sm : ev_bytes + cost_bytes + mask_words * kTlThreads * 4;
+  // global path: kC candidates per thread (CHM_TL_CPT, measurement knob; default below)
+  int cpt = kTlCpt;
+  if (const char *f = std::getenv("CHM_TL_CPT")) cpt = f[0] == '2' ? 2 : 1;
+  const int kc = use_sm ? 1 : cpt;
+  const int threads = use_sm ? 32 : (kc == 2 ? kTlThreads2 : kTlThreads);
+  const size_t smem = use_sm ? smem_sm : ev_bytes + cost_bytes + size_t(kc) * mask_words * threads * 4;
   if (smem > 220 * 1024)
     CHM_FAIL(CHM_E_INVAL, "timeline: event program + masks (%zu B) exceed shared memory", smem);
-  auto kern = use_sm ? timeline_kernel<32, true> : timeline_kernel<kTlThreads, false>;
+  auto kern = use_sm ? timeline_kernel<32, true, 1>
+                     : (kc == 2 ? timeline_kernel<kTlThreads2, false, 2> : timeline_kernel<kTlThreads, false, 1>);
   int per_sm = per_sm_sm;
   if (!use_sm) {
     CHM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     CHM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
   }
   if (per_sm < 1) CHM_FAIL(CHM_E_INVAL, "timeline: kernel does not fit an SM");
-  uint64_t grid64 = std::min<uint64_t>(uint64_t(ctx->num_sms) * per_sm, (L.count + threads - 1) / threads);
-  if (!use_sm) grid64 = std::min<uint64_t>(grid64, std::max<uint64_t>(1, kTlSlotCap / (per_thread * threads)));
+  const uint64_t units = (L.count + kc - 1) / kc;  // threads' worth of candidates
+  uint64_t grid64 = std::min<uint64_t>(uint64_t(ctx->num_sms) * per_sm, (units + threads - 1) / threads);
+  if (!use_sm) grid64 = std::min<uint64_t>(grid64, std::max<uint64_t>(1, kTlSlotCap / (per_thread * kc * threads)));
   grid64 = std::max<uint64_t>(1, grid64);
   const int grid = int(grid64);
-  const size_t slot_bytes = use_sm ? 0 : size_t(grid) * threads * per_thread;
+  const size_t slot_bytes = use_sm ? 0 : size_t(grid) * threads * per_thread * kc;
   if (ctx->tl_scratch_bytes < slot_bytes) {
     if (ctx->tl_scratch) cudaFree(ctx->tl_scratch);
     ctx->tl_scratch = nullptr;
@@ -367,7 +403,7 @@ chm_status launch_timeline(chm_ctx *ctx, const chm_trace *t, const EvalLaunch &L
   p.n_slots = t->tl_slots;
   p.ev_bytes = uint32_t(ev_bytes);
   p.cost_bytes = uint32_t(cost_bytes);
-  p.slot_off = uint32_t(ev_bytes + cost_bytes + mask_words * 32 * 4);  // kSm: 16 B aligned
+  p.slot_off = uint32_t(ev_bytes + cost_bytes + mask_words * 32 * 4);  // kSm (kC = 1): 16 B aligned
   p.tau = t->tl_tau;
   p.kind = L.kind;
   p.K = t->K;

@@ -109,15 +109,17 @@ def test_outputs_optional_and_errors(ctx):
         ctx.eval_policies(pt, chm.EXHAUSTIVE, 0, 4, best=best, stall_model=2)
 
 
-@pytest.mark.parametrize("path", ["0", "1"])
-def test_both_slot_paths(ctx, path, monkeypatch):
-    """global-memory slots (256-thread CTAs) and shared-memory slots (one warp per CTA), forced
-    either way on the same launch, both bit-identical to the oracle"""
+@pytest.mark.parametrize("path,cpt", [("0", "1"), ("0", "2"), ("1", "1")])
+def test_both_slot_paths(ctx, path, cpt, monkeypatch):
+    """global-memory slots (one or two candidates per thread) and shared-memory slots (one warp
+    per CTA), forced either way on the same launch (3001 candidates: a ragged last pair), all
+    bit-identical to the oracle"""
     monkeypatch.setenv("CHM_TL_SMEM", path)
+    monkeypatch.setenv("CHM_TL_CPT", cpt)
     tr = W.CONFIGS["C5"]()
     pt = product_trace(ctx, tr)
     m = O.Model(tr)
     sd = W.SEEDED["C5"]
-    res = tl(ctx, pt, chm.SEEDED, 5, 3000, seed=sd["seed"], flip_thr=sd["flip_thr"])
-    ref = m.eval(O.SEEDED, 5, 3000, seed=sd["seed"], flip_thr=sd["flip_thr"], nthreads=16, stall_model=1)
+    res = tl(ctx, pt, chm.SEEDED, 5, 3001, seed=sd["seed"], flip_thr=sd["flip_thr"])
+    ref = m.eval(O.SEEDED, 5, 3001, seed=sd["seed"], flip_thr=sd["flip_thr"], nthreads=16, stall_model=1)
     assert_same(res, ref, tr.budget)
