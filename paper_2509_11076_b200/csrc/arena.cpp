@@ -59,6 +59,18 @@ int online_nodes() {
   return hi + 1;
 }
 
+// MemAvailable from /proc/meminfo in bytes (0 when unreadable)
+uint64_t mem_available() {
+  FILE *f = std::fopen("/proc/meminfo", "r");
+  if (!f) return 0;
+  char line[256];
+  unsigned long long kb = 0;
+  while (std::fgets(line, sizeof line, f))
+    if (std::sscanf(line, "MemAvailable: %llu kB", &kb) == 1) break;
+  std::fclose(f);
+  return uint64_t(kb) * 1024;
+}
+
 }  // namespace
 
 namespace chm {
@@ -92,6 +104,12 @@ chm_status arena_alloc(chm_ctx *ctx, uint64_t bytes) {
   } else {
     const uint64_t huge = 2ull << 20;
     const uint64_t len = (bytes + huge - 1) / huge * huge;
+    // pre-faulting more than the host has would wake the OOM killer instead of failing here
+    // (cudaHostAlloc fails cleanly): refuse beyond 90% of MemAvailable
+    const uint64_t avail = mem_available();
+    if (avail && len > avail / 10 * 9)
+      CHM_FAIL(CHM_E_NOMEM, "arena: %llu B exceed 90%% of MemAvailable (%llu B)", (unsigned long long)len,
+               (unsigned long long)avail);
     void *p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
     if (p == MAP_FAILED) CHM_FAIL(CHM_E_NOMEM, "arena: mmap(%llu) failed: %s", (unsigned long long)len, strerror(errno));
     madvise(p, len, MADV_HUGEPAGE);  // best effort: THP may be disabled
