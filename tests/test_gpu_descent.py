@@ -33,3 +33,31 @@ def test_descent_reaches_the_exhaustive_optimum(seed):
     assert key(dk) <= key(sk)
     assert key(dk) == key(ex), (key(dk), key(ex), rounds)
     ctx.close()
+
+
+@pytest.mark.parametrize("seed", range(100, 103))
+@pytest.mark.parametrize("model", [chm.STALL_LAYER, chm.STALL_TIMELINE])
+def test_batched_descent_ends_in_a_single_flip_local_optimum(seed, model):
+    """descend(batch=8): each round moves to the best of the single best flip and the best 2..8
+    improving flips applied together; it ends where no single flip improves the key (the same
+    stopping rule as batch=1), never above its start"""
+    tr = W.random_trace(seed, n_layers=5, ops_per_layer=4, bw=3e7, t_iter=1e-3)
+    ctx = chm.Context(device=0)
+    ctx.set_detailed(True)
+    chm.record_iteration(ctx, tr)
+    ctx.detect_seq_change(tr.t_iter)
+    pt = ctx.trace_build(tr.budget, tr.static_bytes, tr.bw, tr.groups_fwd, tr.groups_bwd, t_iter=tr.t_iter)
+    best = torch.empty(5, dtype=torch.int64, device="cuda")
+    thr = int(0.02 * 2 ** 64)
+    ctx.eval_policies(pt, chm.SEEDED, 0, 2000, best=best, seed=1, flip_thr=thr, stall_model=model)
+    sk = best.cpu().numpy().view(chm.BEST_DTYPE)[0]
+    w = pt.candidate_mask(chm.SEEDED, int(sk["index"]), seed=1, flip_thr=thr)
+    dk, dw, rounds = descend(ctx, pt, sk, w, torch.device("cuda:0"), 4096, model, 8)
+    key = lambda k: (int(k["excess"]), float(k["stall"]), int(k["swapped_bytes"]))  # noqa: E731
+    assert key(dk) <= key(sk)
+    ctx.eval_policies(pt, chm.FLIP1, 0, pt.K + 1, best=best, base=dw, stall_model=model)
+    nb = best.cpu().numpy().view(chm.BEST_DTYPE)[0]
+    assert not key(nb) < key(dk)  # no improving single flip left
+    ctx.eval_policies(pt, chm.FLIP1, pt.K, 1, best=best, base=dw, stall_model=model)
+    assert key(best.cpu().numpy().view(chm.BEST_DTYPE)[0]) == key(dk)  # the reported key is the mask's
+    ctx.close()
