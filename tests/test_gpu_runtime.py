@@ -144,3 +144,46 @@ def test_runtime_ranks_plans_by_the_timeline(reference):
     plan = rt.plans[0]
     assert plan["items"] > 0
     assert plan["stall"] == float(rt.policy[0].stall_models(rt.policy_items)[2])
+
+
+def test_sequence_length_switch_replans_and_stays_exact():
+    """C4 (configs[3]) on a real model: the sequence length switches 128 -> 256 -> 128 mid-run.
+    The op sequence stays the same, so Algo. 1 needs reading Q4's byte signature (detect_bytes)
+    to see the switch; the runtime then re-plans for the new shape (the long phase exceeds the
+    budget without swapping), swaps under it, and trains bit-identically to a plain run."""
+    dev = torch.device("cuda:0")
+    cfg = dict(vocab=512, d=256, n_layer=6, n_head=8, seq=256)
+    sched = [128] * 8 + [256] * 10 + [128] * 8
+    data = [G.batches(1, BATCH, s, cfg["vocab"], seed=100 + i, device=dev)[0] for i, s in enumerate(sched)]
+
+    def run(rt):
+        model = G.make(0, dev, **cfg)
+        opt = torch.optim.SGD(model.parameters(), lr=0.05)
+        losses, peaks, changed = [], [], []
+        for x, y in data:
+            torch.cuda.synchronize()
+            torch.cuda.reset_peak_memory_stats()
+            base = torch.cuda.memory_allocated()
+            cm = rt.step() if rt is not None else contextlib.nullcontext()
+            with cm:
+                loss = model(x, y)
+                loss.backward()
+                opt.step()
+                opt.zero_grad(set_to_none=True)
+            torch.cuda.synchronize()
+            losses.append(loss.detach().clone())
+            peaks.append(torch.cuda.max_memory_allocated() - base)
+            changed.append(bool(rt.last_step["changed"]) if rt is not None else False)
+        return torch.stack(losses), [p.detach().clone() for p in model.parameters()], peaks, changed
+
+    ref_losses, ref_params, ref_peaks, _ = run(None)
+    long_peak = max(ref_peaks[8:18])
+    budget = torch.cuda.memory_allocated() + int(0.6 * long_peak) + (64 << 20)
+    rt = Runtime(0, hbm_budget=budget, groups_fwd=6, groups_bwd=6, detect_bytes=1, trials=1)
+    losses, params, peaks, changed = run(rt)
+    assert torch.equal(losses, ref_losses)
+    assert all(torch.equal(a, b) for a, b in zip(params, ref_params))
+    assert changed[8] and changed[18]  # both switches detected on their first step
+    long_plans = [p for p in rt.plans if p.get("items", 0) > 0]
+    assert long_plans, rt.plans
+    assert max(peaks[14:18]) < max(ref_peaks[14:18])  # the long phase runs its policy
