@@ -129,6 +129,21 @@ __global__ void rows_wb_k(long long *out, int rows, int ld, unsigned long long *
     }
   }
 }
+// (h) one warp writes R consecutive rows as one linear block (no inter-warp sync)
+template <int R>
+__global__ void warp_rows_k(long long *out, int rows, int ld, unsigned long long *ctr) {
+  int lane = threadIdx.x & 31;
+  while (true) {
+    unsigned long long c = 0;
+    if (lane == 0) c = atomicAdd(ctr, (unsigned long long)R);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c >= (unsigned long long)rows) break;
+    const long long nr = min((unsigned long long)R, rows - c);
+    long long *b = out + c * ld;
+    const long long n2 = nr * ld / 2;
+    for (long long i = lane; i < n2; i += 32) st2(b + 2 * i, c, i);
+  }
+}
 void run(torch::Tensor out, int rows, int ld, torch::Tensor ctr, int mode) {
   auto *o = (long long *)out.data_ptr();
   auto *k = (unsigned long long *)ctr.data_ptr();
@@ -145,6 +160,10 @@ void run(torch::Tensor out, int rows, int ld, torch::Tensor ctr, int mode) {
   else if (mode == 7) group_k<4><<<296, 512>>>(o, rows, ld, k);
   else if (mode == 8) group_k<8><<<296, 512>>>(o, rows, ld, k);
   else if (mode == 9) rows256_k<<<296, 512>>>(o, rows, ld, k);
+  else if (mode == 12) rows_k<<<296, 256>>>(o, rows, ld, k);
+  else if (mode == 14) warp_rows_k<2><<<296, 512>>>(o, rows, ld, k);
+  else if (mode == 15) warp_rows_k<4><<<296, 512>>>(o, rows, ld, k);
+  else if (mode == 13) rows_k<<<296, 128>>>(o, rows, ld, k);
   else if (mode == 10) rows_wb_k<0><<<296, 512>>>(o, rows, ld, k);
   else if (mode == 11) rows_wb_k<1><<<296, 512>>>(o, rows, ld, k);
   else {
@@ -156,24 +175,32 @@ void run(torch::Tensor out, int rows, int ld, torch::Tensor ctr, int mode) {
 mod = load_inline("write_pattern", cpp_sources="void run(torch::Tensor out, int rows, int ld, torch::Tensor ctr, int mode);",
                   cuda_sources=SRC, functions=["run"], extra_cuda_cflags=["-O3", "-gencode", "arch=compute_100a,code=sm_100a"],
                   verbose=False)
-rows, ld = 100_000, 2618
-out = torch.empty(rows * ld, dtype=torch.int64, device="cuda")
-ctr = torch.zeros(1, dtype=torch.int64, device="cuda")
+rows = 100_000
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-for mode, name in ((0, "linear grid-stride"), (1, "row per warp (replay pattern)"), (2, "16 rows per CTA, linear"),
-                   (3, "row per warp, TMA bulk 1 KiB"), (4, "row per warp, TMA bulk 2 KiB"),
-                   (5, "row per warp, TMA bulk 4 KiB"), (6, "2-warp groups, 2 rows linear"),
-                   (7, "4-warp groups, 4 rows linear"), (8, "8-warp groups, 8 rows linear"),
-                   (9, "row per warp, 256-bit stores"), (10, "row per warp, write-back stores"),
-                   (11, "row per warp, L1::no_allocate stores")):
-    best = 1e9
-    for it in range(8):
-        ctr.zero_()
-        torch.cuda._sleep(1_000_000)
-        s.record()
-        mod.run(out, rows, ld, ctr, mode)
-        e.record()
-        torch.cuda.synchronize()
-        if it >= 2:
-            best = min(best, s.elapsed_time(e))
-    print(f"{name:34s} {rows * ld * 8 / (best * 1e-3) / 1e9:8.1f} GB/s  {best:.3f} ms")
+ctr = torch.zeros(1, dtype=torch.int64, device="cuda")
+for ld in (2618, 2620):  # C2's row: 20,944 B (a 32 B sector split between rows) vs padded to 32 B
+    out = torch.empty(rows * ld, dtype=torch.int64, device="cuda")
+    print(f"-- ld = {ld} ({ld * 8} B rows, {'32 B-aligned' if ld % 4 == 0 else 'rows split 32 B sectors'})")
+    modes = ((0, "linear grid-stride"), (1, "row per warp (replay pattern)"), (2, "16 rows per CTA, linear"),
+             (3, "row per warp, TMA bulk 1 KiB"), (4, "row per warp, TMA bulk 2 KiB"),
+             (5, "row per warp, TMA bulk 4 KiB"), (6, "2-warp groups, 2 rows linear"),
+             (7, "4-warp groups, 4 rows linear"), (8, "8-warp groups, 8 rows linear"),
+             (9, "row per warp, 256-bit stores"), (10, "row per warp, write-back stores"),
+             (11, "row per warp, L1::no_allocate stores"), (12, "row per warp, 8 warps/CTA (2368 streams)"),
+             (13, "row per warp, 4 warps/CTA (1184 streams)"), (14, "one warp, 2 rows linear"),
+             (15, "one warp, 4 rows linear"))
+    if ld % 4 == 0:
+        modes = tuple(m for m in modes if m[0] in (0, 1, 2, 6, 14))
+    for mode, name in modes:
+        best = 1e9
+        for it in range(8):
+            ctr.zero_()
+            torch.cuda._sleep(1_000_000)
+            s.record()
+            mod.run(out, rows, ld, ctr, mode)
+            e.record()
+            torch.cuda.synchronize()
+            if it >= 2:
+                best = min(best, s.elapsed_time(e))
+        print(f"{name:42s} {rows * ld * 8 / (best * 1e-3) / 1e9:8.1f} GB/s  {best:.3f} ms")
+    del out
