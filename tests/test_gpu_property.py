@@ -73,3 +73,58 @@ def test_replay_matches_oracle(ctx, tr, kind, first, count, full, seed, flip):
         res = run_eval(ctx, pt, chm.EXPLICIT, first, len(lists), footprint=full, item_offsets=off, items=items)
         ref = O.eval_explicit(m, lists, first_index=first, footprint=full)
     assert_same(res, ref, tr.budget)
+
+
+@settings(max_examples=120, deadline=None)
+@given(tr=traces, kind=st.sampled_from(["exhaustive", "seeded", "masks", "flip1"]), first=st.integers(0, 5000),
+       count=st.integers(1, 700), seed=st.integers(0, 2 ** 32), flip=st.floats(0.0, 0.9),
+       path=st.sampled_from(["0", "1", "auto"]))
+def test_timeline_matches_oracle(ctx, tr, kind, first, count, seed, flip, path):
+    """the timeline stall model in the search (CHM_STALL_TIMELINE) on random traces and candidate
+    ranges, on either slot path, against the oracle's orc_eval_model(stall_model = 1)"""
+    import os
+    old = os.environ.pop("CHM_TL_SMEM", None)
+    if path != "auto":
+        os.environ["CHM_TL_SMEM"] = path
+    try:
+        pt = product_trace(ctx, tr)
+        m = O.Model(tr)
+        thr = int(flip * 2 ** 64) & ((1 << 64) - 1)
+        rng = np.random.default_rng(seed)
+        W_ = max(m.W, 1)
+        if kind == "exhaustive":
+            first = min(first, (1 << m.K) - 1)
+            count = min(count, (1 << m.K) - first)
+            res = run_eval(ctx, pt, chm.EXHAUSTIVE, first, count, stall_model=chm.STALL_TIMELINE)
+            ref = m.eval(O.EXHAUSTIVE, first, count, stall_model=1)
+        elif kind == "seeded":
+            res = run_eval(ctx, pt, chm.SEEDED, first, count, seed=seed, flip_thr=thr, stall_model=chm.STALL_TIMELINE)
+            ref = m.eval(O.SEEDED, first, count, seed=seed, flip_thr=thr, stall_model=1)
+        else:
+            if kind == "flip1":  # the one-bit neighbourhood of a random base, as MASKS for the oracle
+                base = rng.integers(0, 2 ** 63, size=W_, dtype=np.int64).astype(np.uint64)
+                if m.K % 64:
+                    base[-1] &= np.uint64((1 << (m.K % 64)) - 1)
+                if m.K == 0:
+                    base[:] = 0
+                first, count = 0, m.K + 1
+                masks = np.repeat(base[None, :], count, axis=0)
+                for g in range(m.K):
+                    masks[g, g // 64] ^= np.uint64(1 << (g % 64))
+                res = run_eval(ctx, pt, chm.FLIP1, 0, count, base=base[:m.W], stall_model=chm.STALL_TIMELINE)
+            else:
+                masks = rng.integers(0, 2 ** 63, size=(count, W_), dtype=np.int64).astype(np.uint64)
+                if m.K % 64:
+                    masks[:, -1] &= np.uint64((1 << (m.K % 64)) - 1)
+                if m.K == 0:
+                    masks[:] = 0
+                res = run_eval(ctx, pt, chm.MASKS, first, count, stall_model=chm.STALL_TIMELINE,
+                               masks=torch.from_numpy(masks[:, :m.W].copy().view(np.int64)).cuda() if m.W else
+                               torch.zeros((count, 1), dtype=torch.int64, device="cuda"))
+            ref = m.eval(O.MASKS, first, count, words=masks[:, :m.W] if m.W else np.zeros((count, 1), np.uint64),
+                         stall_model=1)
+        assert_same(res, ref, tr.budget)
+    finally:
+        os.environ.pop("CHM_TL_SMEM", None)
+        if old is not None:
+            os.environ["CHM_TL_SMEM"] = old
