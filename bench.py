@@ -261,6 +261,22 @@ def _replan_c4(chm, dev, comp):
                      "swapped_gib": int(dk["swapped_bytes"]) / gib},
                seeded_best={"excess_gib": int(bk["excess"]) / gib, "stall_s": float(bk["stall"])},
                generator_best={"excess_gib": int(gk["excess"]) / gib, "stall_s": float(gk["stall"])})
+    # the runtime's default ranking (the timeline stall, csrc/timeline.cu): the same eval and
+    # descent under it, single-flip and batched (search_batch = 16)
+    tl = {}
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ctx.eval_policies(pt, chm.SEEDED, 0, 100_000, best=best, seed=sd["seed"], flip_thr=sd["flip_thr"], stream=comp,
+                      stall_model=chm.STALL_TIMELINE)
+    tk = best.cpu().numpy().view(chm.BEST_DTYPE)[0]
+    tl["eval_1e5_ms"] = (time.perf_counter() - t0) * 1e3
+    w0 = pt.candidate_mask(chm.SEEDED, int(tk["index"]), seed=sd["seed"], flip_thr=sd["flip_thr"])
+    for b in (1, 16):
+        t0 = time.perf_counter()
+        k, _, r = descend(ctx, pt, tk, w0, dev, 4096, chm.STALL_TIMELINE, b)
+        tl[f"descent_batch{b}"] = {"ms": (time.perf_counter() - t0) * 1e3, "rounds": r,
+                                   "excess_gib": int(k["excess"]) / gib, "timeline_stall_s": float(k["stall"])}
+    out["timeline_ranking"] = tl
     ctx.close()
     return out
 
