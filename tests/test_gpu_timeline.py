@@ -78,12 +78,14 @@ def test_masks_and_flip1_dense(ctx):
     assert_same(res, ref, tr.budget)
 
 
-def test_c2_bench_size_every_candidate(ctx):
-    """the bench's launch (10^5 SEEDED C2 candidates, full mode): every stall and the argmin"""
-    tr = W.gpt2_xl()
+@pytest.mark.parametrize("name", ["C2", "C5"])
+def test_bench_size_every_candidate(ctx, name):
+    """the bench's launch size (10^5 SEEDED candidates, full mode) on C2 and on C5 (the per-rank
+    trace of the 8-GPU config): every stall and the argmin"""
+    tr = W.CONFIGS[name]()
     pt = product_trace(ctx, tr)
     m = O.Model(tr)
-    sd = W.SEEDED["C2"]
+    sd = W.SEEDED[name]
     n = 100_000
     res = tl(ctx, pt, chm.SEEDED, 0, n, footprint=True, seed=sd["seed"], flip_thr=sd["flip_thr"])
     ref = m.eval(O.SEEDED, 0, n, seed=sd["seed"], flip_thr=sd["flip_thr"], nthreads=16, stall_model=1)
