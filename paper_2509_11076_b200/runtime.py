@@ -765,8 +765,10 @@ class Runtime:
                     uniq.append(c)
             uniq = uniq[:max(1, self.n_trials)]
             t1 = time.perf_counter()
-            for c in uniq:  # the arena for the largest of them
-                (self._reserve_items if c[3] else self._reserve_words)(c[2], pt)
+            # the arena for the largest of them, pinned once (growing it per plan re-pins it)
+            if not self.host_only:
+                need = max((self._need_items if c[3] else self._need_words)(c[2], pt) for c in uniq)
+                self.ctx.arena_reserve(max(need + self.oom_host_bytes, 1 << 20))
             self.policy = (pt, plan)
             self._install_cand(pt, plan, uniq[0])
             plan["install_ms"] = (time.perf_counter() - t1) * 1e3  # includes pinning arena growth
@@ -823,23 +825,20 @@ class Runtime:
         # 0.25 vs 0.17 s predicted, 1.08 vs 0.98 s measured steps)
         return descend(self.ctx, pt, key, words, self.dev, self.search_rounds, self.stall_model, self.search_batch)
 
-    def _reserve_words(self, words, pt):
-        if self.host_only:
-            return
+    def _need_words(self, words, pt) -> int:
+        """arena bytes of a mask's items (512 B-rounded slots)"""
         tb = pt.tables()
         need = 0
         for k in range(pt.K):
             if (int(words[k // 64]) >> (k % 64)) & 1:
                 need += (int(tb["nbytes"][k]) + 511) // 512 * 512
-        self.ctx.arena_reserve(max(need + self.oom_host_bytes, 1 << 20))
+        return need
 
-    def _reserve_items(self, items, pt):
-        if self.host_only:
-            return
+    def _need_items(self, items, pt) -> int:
+        """arena bytes of an explicit item list (512 B-rounded slots)"""
         tb = pt.tables()
         rank_bytes = {int(t): int(n) for t, n in zip(tb["tensor"], tb["nbytes"])}
-        need = sum((rank_bytes.get(int(it["t"]), 0) + 511) // 512 * 512 for it in items)
-        self.ctx.arena_reserve(max(need + self.oom_host_bytes, 1 << 20))
+        return sum((rank_bytes.get(int(it["t"]), 0) + 511) // 512 * 512 for it in items)
 
     def _measure_bw(self) -> float:
         """B of Eq. 3: one 256 MiB swap-out + swap-in through the policy's copy path"""
