@@ -1,8 +1,10 @@
 """Stall-model variants of reading Q11: per-direction layer budgets and the
 max-plus serial-stream timeline.  The oracle is pinned against closed forms derived by hand
 (one item: the copy time beyond its slack on each side; two items in one FIFO: their summed copy
-time beyond the shared slack), against invariants (per-direction <= one shared budget; a slower
-link never stalls less; an infinitely fast link never stalls), then the product's host
+time beyond the shared slack), against the earliest-start schedule of the model's precedence DAG
+derived separately (absolute times, one final subtraction), against invariants (per-direction
+<= one shared budget; a slower link never stalls less; an infinitely fast link never stalls),
+then the product's host
 evaluation (`chm_stall_models`) must equal the oracle bit for bit, and its R-stall entry must
 equal the replay kernels' model (the oracle's orc_stall)."""
 import numpy as np
@@ -144,3 +146,50 @@ def test_eval_model_timeline_is_stall_timeline_of_mask_items():
     exc = np.maximum(a["peak"] - tr.budget, 0)
     order = np.lexsort((np.arange(n), a["swapped"], a["stall"], exc))
     assert order[0] == i
+
+
+def _dag_timeline(tr, m, t, r, s):
+    """The Q11 timeline derived independently as earliest start times of a precedence DAG (ops
+    of tau each in sequence; a FIFO per direction; the rules chm_stall_models documents), then
+    stall = (time the last op's releases are done) - N tau.  Absolute times and one final
+    subtraction, not the oracle's running `now` with stall increments."""
+    N = len(tr.phase)
+    tau = tr.t_iter / N
+    ranks = [int(x) for i in range(N) for x in tr.out_idx[tr.out_ptr[i]:tr.out_ptr[i + 1]]]
+    _, _, a, b = m.tensor_table()
+    items = list(range(len(t)))
+    S = [int(tr.nbytes[ranks[int(t[k])]]) for k in items]
+    dur = [S[k] / tr.bw for k in items]
+    out_end, in_end = {}, {}
+    pre = 0.0  # ready time before op i's swap-in / wait phase
+    d2h_free = h2d_free = 0.0
+    for i in range(N):
+        for k in items:  # swap-ins issued before op i, FIFO in item order
+            if s[k] == i:
+                st = max(pre, h2d_free, out_end.get(k, 0.0))
+                in_end[k] = st + dur[k]
+                h2d_free = in_end[k]
+        start = max([pre] + [in_end[k] for k in items if b[int(t[k])] == i])  # first-use waits
+        end = start + tau
+        for k in items:  # swap-outs issued after op i, FIFO in item order
+            if a[int(t[k])] == i:
+                st = max(end, d2h_free)
+                out_end[k] = st + dur[k]
+                d2h_free = out_end[k]
+        pre = max([end] + [out_end[k] for k in items if r[k] == i])  # releases after op i
+    return pre - N * tau
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_timeline_equals_the_precedence_dag(seed):
+    """pin: the oracle's timeline = the longest-path (earliest-start) schedule of the model's
+    precedence DAG on random traces and item sets, to rounding (the two sum in different orders)"""
+    rng = np.random.default_rng(100 + seed)
+    tr = W.random_trace(seed, bw=rng.uniform(2e7, 2e9), t_iter=rng.uniform(1e-4, 1e-2))
+    m = O.Model(tr)
+    t, r, s = _random_items(m, rng)
+    if len(t) == 0:
+        return
+    got = m.stall_timeline(t, r, s)
+    exp = _dag_timeline(tr, m, t, r, s)
+    assert got == pytest.approx(exp, rel=1e-9, abs=1e-12 * tr.t_iter)
