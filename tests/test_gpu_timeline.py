@@ -125,3 +125,31 @@ def test_both_slot_paths(ctx, path, cpt, monkeypatch):
     res = tl(ctx, pt, chm.SEEDED, 5, 3001, seed=sd["seed"], flip_thr=sd["flip_thr"])
     ref = m.eval(O.SEEDED, 5, 3001, seed=sd["seed"], flip_thr=sd["flip_thr"], nthreads=16, stall_model=1)
     assert_same(res, ref, tr.budget)
+
+
+def test_long_op_gaps_between_events():
+    """40,000 ops with the events of two activations far apart: gaps of more than 16,383 ops
+    between consecutive events take the program's tick-only NOP events"""
+    from tests.helpers import make_trace
+    n = 40_000
+    half = n // 2
+    ins = [[] for _ in range(n)]
+    outs = [[] for _ in range(n)]
+    frees = [[] for _ in range(n)]
+    outs[0] = [0, 1]
+    ins[1] = [0, 1]
+    outs[2] = [2]  # a transient that makes the forward peak sit after the activations' last use
+    frees[3] = [2]
+    ins[n - 2] = [0, 1]
+    frees[n - 2] = [0, 1]
+    tr = make_trace([0] * half + [1] * half, [64 << 20, 32 << 20, 16 << 20], ins, outs, frees, 0, 1.0, 1e7,
+                    (70 << 20), 4, 4)
+    ctx = chm.Context(device=0)
+    pt = product_trace(ctx, tr)
+    m = O.Model(tr)
+    assert pt.N == n and pt.K >= 1
+    res = tl(ctx, pt, chm.EXHAUSTIVE, 0, 1 << pt.K)
+    ref = m.eval(O.EXHAUSTIVE, 0, 1 << pt.K, stall_model=1)
+    assert_same(res, ref, tr.budget)
+    assert ref["stall"].max() > 0.0
+    ctx.close()
