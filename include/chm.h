@@ -274,7 +274,8 @@ typedef struct {
                               order at their solo (r_t, s_t); `stall` and the argmin key then
                               carry it.  Mask kinds only (EXPLICIT: CHM_E_INVAL).  Needs
                               device scratch of ~8 B x (slots of the trace's event program) per
-                              resident thread, capped at 256 MiB (DESIGN.md §5 Timeline)    */
+                              resident thread, capped at 512 MiB (DESIGN.md §5 Timeline);
+                              chm_release_scratch frees it                                 */
 } chm_eval_out;
 enum { CHM_STALL_LAYER = 0, CHM_STALL_TIMELINE = 1 };
 
@@ -287,6 +288,12 @@ chm_status chm_eval_policies(chm_ctx *ctx, const chm_trace *t, const chm_candida
 /* chm_eval_policies with the index of the offending EXPLICIT item on CHM_E_INVAL */
 chm_status chm_eval_policies_ex(chm_ctx *ctx, const chm_trace *t, const chm_candidates *c,
                                 const chm_eval_out *o, cudaStream_t stream, int64_t *err_index);
+/* Frees the device scratch the evaluation calls keep between launches (per-CTA keys, the
+ * timeline kernel's end-time slots -- up to 512 MiB at 10^5 candidates --, internal peak /
+ * swapped arrays, EXPLICIT item copies); the next chm_eval_policies allocates again.  Call it
+ * after a planning burst (the runtime does) so the HBM goes back to training; it synchronises
+ * the device (cudaFree), so not while an evaluation is in flight on another stream. */
+chm_status chm_release_scratch(chm_ctx *ctx);
 /* host: lexicographic min of n keys (e.g. after an all-gather across ranks) */
 chm_status chm_best_reduce(const chm_best *keys, uint32_t n, chm_best *out);
 /* device: the same min over n device keys into *out (device), enqueued on `stream` -- the

@@ -175,7 +175,7 @@ EXPORTS = [
     "chm_policy_install", "chm_policy_install_items", "chm_generate_policy", "chm_exec_stats_get", "chm_host_arena", "chm_swap_out", "chm_swap_in",
     "chm_batch_wait", "chm_batch_query", "chm_batch_elapsed", "chm_arena_reserve", "chm_issue_swap_out", "chm_issue_swap_in", "chm_item_wait",
     "chm_oom_release", "chm_passive_swap", "chm_passive_restore", "chm_trace_load", "chm_record_save",
-    "chm_stall_models", "chm_record_tokens", "chm_arena_placement",
+    "chm_stall_models", "chm_record_tokens", "chm_arena_placement", "chm_release_scratch",
 ]
 
 _lib = None
@@ -194,6 +194,7 @@ def load(path: str = LIB_PATH):
     sig = {
         "chm_config_default": (None, [P(Config)]),
         "chm_arena_placement": (i32, [vp, P(i32), P(i32), P(dbl)]),
+        "chm_release_scratch": (i32, [vp]),
         "chm_create": (i32, [P(Config), P(vp)]),
         "chm_destroy": (None, [vp]),
         "chm_last_error": (C.c_char_p, []),
@@ -498,6 +499,10 @@ class Context:
 
     def arena_reserve(self, nbytes: int):
         _check(load().chm_arena_reserve(self.h, int(nbytes)))
+
+    def release_scratch(self):
+        """frees the evaluation calls' device scratch (chm_release_scratch); synchronises"""
+        _check(load().chm_release_scratch(self.h))
 
     def arena_placement(self) -> dict:
         """{"numa_node": bound node or -1, "mode": ARENA_HOSTALLOC / ARENA_REGISTER / -1,

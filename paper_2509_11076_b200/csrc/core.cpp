@@ -14,6 +14,9 @@
 
 #include "internal.h"
 
+#include <map>
+#include <mutex>
+
 namespace chm {
 static thread_local char g_err[512];
 void set_error(const char *fmt, ...) {
@@ -362,3 +365,19 @@ extern "C" chm_status chm_best_reduce(const chm_best *keys, uint32_t n, chm_best
   *out = b;
   return CHM_OK;
 }
+
+namespace chm {
+cudaError_t ensure_dyn_smem(const void *f, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void *>, size_t> set;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t &cur = set[{dev, f}];
+  if (bytes <= cur) return cudaSuccess;
+  e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+  if (e == cudaSuccess) cur = bytes;
+  return e;
+}
+}  // namespace chm

@@ -226,7 +226,7 @@ chm_status launch_eval_explicit(chm_ctx *ctx, const chm_trace *t, const chm_cand
   p.ld = o->ld;
   const size_t smem = 8 * (size_t(t->N) + 2);
   if (smem > 200 * 1024) CHM_FAIL(CHM_E_INVAL, "EXPLICIT replay: N = %d too large for one CTA row", t->N);
-  CHM_CUDA(cudaFuncSetAttribute(replay_explicit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  CHM_CUDA(ensure_dyn_smem(reinterpret_cast<const void *>(replay_explicit_kernel), smem));
   replay_explicit_kernel<<<unsigned(c->count), 256, smem, stream>>>(p);
   CHM_CUDA(cudaGetLastError());
   xkey_reduce_kernel<<<1, 32, 0, stream>>>(p.keys, c->count, reinterpret_cast<XKey *>(o->best));

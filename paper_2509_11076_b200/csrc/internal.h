@@ -278,6 +278,12 @@ chm_status build_trace(chm_ctx *ctx, const IterRecord &R, const chm_trace_params
 // executor.cpp: moves a released item's Detailed-record tensor index off its old address
 void stash_record(chm_ctx *ctx, PolicyItem &it);
 
+// Raises kernel `f`'s dynamic shared-memory limit on the current device to at least `bytes`.
+// The attribute is process-wide per (device, kernel): it is only ever raised, so contexts whose
+// traces need different sizes can interleave launches (lowering it under another context's
+// launch made that launch fail with an invalid argument).
+cudaError_t ensure_dyn_smem(const void *f, size_t bytes);
+
 // arena.cpp: pinned + mapped host arena (sets arena, arena_bytes; frees the mapping)
 int device_numa_node(int device);
 chm_status arena_alloc(chm_ctx *ctx, uint64_t bytes);

@@ -411,10 +411,10 @@ chm_status launch_eval(chm_ctx *ctx, const EvalLaunch &L, cudaStream_t stream) {
   auto kern = fp ? (narrow ? replay_kernel<true, true> : replay_kernel<true, false>) : replay_kernel<false, false>;
   const int var = fp ? (narrow ? 2 : 1) : 0;
   int per_sm = 0;
+  CHM_CUDA(ensure_dyn_smem(reinterpret_cast<const void *>(kern), smem));
   if (ctx->eval_attr_smem[var] == smem) {
     per_sm = ctx->eval_per_sm[var];
   } else {
-    CHM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     CHM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
     ctx->eval_attr_smem[var] = smem;
     ctx->eval_per_sm[var] = per_sm;
@@ -571,5 +571,20 @@ extern "C" chm_status chm_best_reduce_device(chm_ctx *ctx, const chm_best *keys,
   CHM_CUDA(cudaSetDevice(ctx->device));
   best_reduce_kernel<<<1, 32, 0, stream>>>(reinterpret_cast<const Key *>(keys), n, reinterpret_cast<Key *>(out));
   CHM_CUDA(cudaGetLastError());
+  return CHM_OK;
+}
+
+extern "C" chm_status chm_release_scratch(chm_ctx *ctx) {
+  if (!ctx) CHM_FAIL(CHM_E_INVAL, "chm_release_scratch: NULL ctx");
+  if (ctx->device < 0) return CHM_OK;
+  CHM_CUDA(cudaSetDevice(ctx->device));
+  void **bufs[4] = {&ctx->eval_scratch, &ctx->tl_scratch, &ctx->tl_aux, &ctx->explicit_scratch};
+  size_t *sizes[4] = {&ctx->eval_scratch_bytes, &ctx->tl_scratch_bytes, &ctx->tl_aux_bytes,
+                      &ctx->explicit_scratch_bytes};
+  for (int i = 0; i < 4; i++) {
+    if (*bufs[i]) CHM_CUDA(cudaFree(*bufs[i]));  // implicit device synchronisation
+    *bufs[i] = nullptr;
+    *sizes[i] = 0;
+  }
   return CHM_OK;
 }

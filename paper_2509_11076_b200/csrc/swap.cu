@@ -203,12 +203,7 @@ chm_status launch_swap_copy(const chm_swap_desc *desc, uint32_t n, char *arena, 
     const int grid = int(std::min<uint64_t>(uint64_t(ctas), chunks));
     if (grid == 0) continue;
     if (bulk) {
-      static bool attr = false;
-      if (!attr) {
-        CHM_CUDA(cudaFuncSetAttribute(swap_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      kBulkStage * kBulkStages));
-        attr = true;
-      }
+      CHM_CUDA(ensure_dyn_smem(reinterpret_cast<const void *>(swap_bulk_kernel), size_t(kBulkStage) * kBulkStages));
       swap_bulk_kernel<<<grid, 32, kBulkStage * kBulkStages, stream>>>(p);
     } else if (variant == 1) {
       swap_copy_kernel<true><<<grid, kSwapThreads, 0, stream>>>(p);

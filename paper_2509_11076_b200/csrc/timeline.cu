@@ -38,7 +38,8 @@ constexpr int kTlThreads2 = 128;  // CTA size, two candidates per thread
 constexpr int kTlCpt = 1;         // candidates per thread on the global-memory path
 constexpr int kTlGroup = 4;                   // events per group = prefetch distance
 constexpr unsigned kTlPrefetch = 1u << 17;    // event flag: its slot value is loaded a group ahead
-constexpr size_t kTlSlotCap = 256ull << 20;  // bytes of slot scratch at most (HBM is what swapping saves)
+constexpr size_t kTlSlotCap = 512ull << 20;  // slot scratch at most (C2's 10^5 candidates in one wave: 376 MB;
+                                             // chm_release_scratch gives it back after planning)
 
 template <bool kSm>
 __device__ __forceinline__ double ld_slot(const double *a) { return kSm ? *a : __ldcg(a); }
@@ -358,8 +359,7 @@ chm_status launch_timeline(chm_ctx *ctx, const chm_trace *t, const EvalLaunch &L
   bool use_sm = false;
   int per_sm_sm = 0;
   if (smem_sm <= 220 * 1024) {
-    CHM_CUDA(cudaFuncSetAttribute(timeline_kernel<32, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(smem_sm)));
+    CHM_CUDA(ensure_dyn_smem(reinterpret_cast<const void *>(timeline_kernel<32, true, 1>), smem_sm));
     CHM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_sm, timeline_kernel<32, true, 1>, 32, smem_sm));
     use_sm = per_sm_sm > 0 && L.count <= uint64_t(ctx->num_sms) * 32 * uint64_t(per_sm_sm);
   }
@@ -377,13 +377,15 @@ chm_status launch_timeline(chm_ctx *ctx, const chm_trace *t, const EvalLaunch &L
                      : (kc == 2 ? timeline_kernel<kTlThreads2, false, 2> : timeline_kernel<kTlThreads, false, 1>);
   int per_sm = per_sm_sm;
   if (!use_sm) {
-    CHM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    CHM_CUDA(ensure_dyn_smem(reinterpret_cast<const void *>(kern), smem));
     CHM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
   }
   if (per_sm < 1) CHM_FAIL(CHM_E_INVAL, "timeline: kernel does not fit an SM");
   const uint64_t units = (L.count + kc - 1) / kc;  // threads' worth of candidates
   uint64_t grid64 = std::min<uint64_t>(uint64_t(ctx->num_sms) * per_sm, (units + threads - 1) / threads);
-  if (!use_sm) grid64 = std::min<uint64_t>(grid64, std::max<uint64_t>(1, kTlSlotCap / (per_thread * kc * threads)));
+  size_t cap = kTlSlotCap;
+  if (const char *f = std::getenv("CHM_TL_SCRATCH_MIB")) cap = size_t(std::max(1, std::atoi(f))) << 20;  // knob
+  if (!use_sm) grid64 = std::min<uint64_t>(grid64, std::max<uint64_t>(1, cap / (per_thread * kc * threads)));
   grid64 = std::max<uint64_t>(1, grid64);
   const int grid = int(grid64);
   const size_t slot_bytes = use_sm ? 0 : size_t(grid) * threads * per_thread * kc;

@@ -775,6 +775,8 @@ class Runtime:
             if len(uniq) > 1:
                 self.trials = dict(pt=pt, plan=plan, cands=uniq, times=[])
                 plan["trial_plans"] = [c[0] for c in uniq]
+        if not self.host_only:
+            self.ctx.release_scratch()  # the planner's device scratch goes back to training
         plan["plan_ms"] = (time.perf_counter() - t0) * 1e3
         self.stats["plan_ms"] += plan["plan_ms"]
         self.plans.append(plan)

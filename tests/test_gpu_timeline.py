@@ -153,3 +153,23 @@ def test_long_op_gaps_between_events():
     assert_same(res, ref, tr.budget)
     assert ref["stall"].max() > 0.0
     ctx.close()
+
+
+def test_release_scratch_between_launches(ctx):
+    """chm_release_scratch frees the evaluation scratch; the next launches (layer and timeline
+    models) allocate it again and give the same results"""
+    tr = W.CONFIGS["C5"]()
+    pt = product_trace(ctx, tr)
+    sd = W.SEEDED["C5"]
+    kw = dict(seed=sd["seed"], flip_thr=sd["flip_thr"])
+    a = tl(ctx, pt, chm.SEEDED, 0, 20_000, **kw)
+    b = run_eval(ctx, pt, chm.SEEDED, 0, 20_000, footprint=True, **kw)
+    for _ in range(2):
+        ctx.release_scratch()
+        a2 = tl(ctx, pt, chm.SEEDED, 0, 20_000, **kw)
+        ctx.release_scratch()
+        b2 = run_eval(ctx, pt, chm.SEEDED, 0, 20_000, footprint=True, **kw)
+        for x, y in ((a, a2), (b, b2)):
+            assert np.array_equal(x["stall"], y["stall"]) and np.array_equal(x["peak"], y["peak"])
+            assert x["best"].tobytes() == y["best"].tobytes()
+        assert np.array_equal(b["footprint"], b2["footprint"])
