@@ -39,6 +39,7 @@ import concurrent.futures
 import contextlib
 import os
 import re
+import threading
 import time
 import weakref
 from typing import Optional
@@ -229,14 +230,16 @@ class Runtime:
     runtime performance"; 1: keep the best key);
     host_arena_bytes: pinned arena reserved up front (else grown to each policy at install);
     stall_model: the stall that ranks plans, chm.STALL_TIMELINE (default) or chm.STALL_LAYER;
-    search_batch: flips tried together per descent round (1: single-flip steepest descent)."""
+    search_batch: flips tried together per descent round (1: single-flip steepest descent);
+    prepin: pin the host arena on a host thread during the Detailed step, sized 2 x (peak
+    allocated - budget), so the plan's install does not pin."""
 
     def __init__(self, device: Optional[int] = 0, *, hbm_budget: int, bw: Optional[float] = None,
                  groups_fwd: int = 0, groups_bwd: int = 0, omega: float = 1.0, candidates: int = 1 << 16,
                  seed: int = 1, flip_frac: float = 0.02, generator: bool = True, swap_ctas: int = 0,
                  min_swap_bytes: int = 0, search_rounds: int = 4096, host_arena_bytes: int = 0,
                  swap_flags: int = chm.SWAP_AUTO, oom_host_bytes: int = 0, trials: int = 5,
-                 stall_model: int = chm.STALL_TIMELINE, search_batch: int = 1, **algo1):
+                 stall_model: int = chm.STALL_TIMELINE, search_batch: int = 1, prepin: bool = True, **algo1):
         self.host_only = device is None
         self.dev = torch.device("cpu") if self.host_only else torch.device("cuda", device)
         self.ctx = chm.Context(device=-1 if self.host_only else device, swap_ctas=swap_ctas,
@@ -251,6 +254,10 @@ class Runtime:
         # flips per descent round (1: steepest single flip; > 1: also the best 2..n together --
         # 5-16x fewer rounds, plans within 0-3% of the single-flip ones, tools/descent_batch.py)
         self.search_batch = int(search_batch)
+        self.prepin = bool(prepin)
+        self._prepin_thread = None
+        self._peak_seen = 0  # max over finished steps of the allocator's peak (bytes)
+        self.prepin_log = []  # (bytes, seconds, error) of background arena reservations
         self.n_trials = int(trials)  # plans tried on real steps before one is kept (n = 5)
         self.trials = None
         self.trial_running = False
@@ -316,6 +323,7 @@ class Runtime:
         """a step that raised: close the partial iteration so the next step starts clean (its
         sequence is short, so Algo. 1 sees a change and the policy is re-planned), drop the
         step's boxes and any passive copies"""
+        self._join_prepin()
         self.pending = None
         self.tok_buf, self.ph_buf = [], []
         if not self.host_only:
@@ -350,6 +358,12 @@ class Runtime:
         self.detailed = (self.stage == chm.GENPOLICY and self.need_plan) or self.force_plan
         if self.force_plan:
             self.ctx.set_detailed(True)
+        if self.detailed:
+            # pin the plan's arena while this step records; not earlier: cudaHostRegister holds
+            # the driver and stalls the step's launches, and a WarmUp step's time is Eq. 1's
+            # T_iter (starting at the first step with a deficit made that step 4.5 s and the plan
+            # misjudge the layer budgets)
+            self._start_prepin()
         # nothing to execute, record or fall back on: tokens only, autograd saves as usual
         self.light = (self.policy is None and not self.detailed and not self.oom_host_bytes
                       and not self.record_log and not self._detect_bytes)
@@ -370,12 +384,49 @@ class Runtime:
             self.m0 = 0
         self.t0 = time.perf_counter()
 
+    def _start_prepin(self):
+        """the plan at the end of this Detailed step will need a pinned arena of at least the
+        bytes it swaps; the peak allocated so far minus the budget bounds them from below.
+        Reserve 2x that on a host thread while the step runs (the ctx's arena is idle: no
+        policy is installed and no passive swaps are enabled, so nothing else touches it)."""
+        if (not self.prepin or self.host_only or self.oom_host_bytes or self.policy is not None
+                or self._prepin_thread is not None):
+            return
+        deficit = max(self._peak_seen, torch.cuda.max_memory_allocated(self.dev)) - self.hbm_budget
+        if deficit <= 0:
+            return
+        try:
+            avail = next(int(ln.split()[1]) * 1024 for ln in open("/proc/meminfo") if ln.startswith("MemAvailable:"))
+        except (OSError, StopIteration, ValueError):
+            return
+        est = min(2 * deficit + (64 << 20), int(0.6 * avail))
+        if est <= self.ctx.host_arena()[1]:
+            return
+
+        def run():
+            t0 = time.perf_counter()
+            err = None
+            try:
+                self.ctx.arena_reserve(est)
+            except chm.ChmError as e:  # the plan's install reserves what it needs anyway
+                err = str(e)
+            self.prepin_log.append((est, time.perf_counter() - t0, err))
+
+        self._prepin_thread = threading.Thread(target=run, name="chm-prepin", daemon=True)
+        self._prepin_thread.start()
+
+    def _join_prepin(self):
+        if self._prepin_thread is not None:
+            self._prepin_thread.join()
+            self._prepin_thread = None
+
     def _end(self):
         if self.tok_buf:
             self.ctx.record_tokens(self.tok_buf, self.ph_buf)
             self.n_ops += len(self.tok_buf)
         if not self.host_only:
             torch.cuda.synchronize(self.dev)
+            self._peak_seen = max(self._peak_seen, torch.cuda.max_memory_allocated(self.dev))
         t_iter = time.perf_counter() - self.t0
         stage_before = self.stage
         d = self.ctx.detect_seq_change(t_iter)
@@ -685,6 +736,7 @@ class Runtime:
         return (int(k["excess"]), float(k["stall"]), int(k["swapped_bytes"]))
 
     def _plan(self, t_iter):
+        self._join_prepin()
         t0 = time.perf_counter()
         gf, gb = self.groups
         pt = self.ctx.trace_build(self.hbm_budget, self.m0, self.bw, gf, gb, t_iter=t_iter, omega=self.omega)
@@ -860,4 +912,5 @@ class Runtime:
         return 2 * nb / dt
 
     def close(self):
+        self._join_prepin()
         self.ctx.close()
