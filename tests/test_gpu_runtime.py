@@ -75,6 +75,10 @@ def test_runtime_swaps_are_bit_exact_and_lower_the_peak(reference):
     run = _train(rt)
     _check_exact(run, reference)
     assert len(rt.plans) == 1 and rt.plans[0]["items"] > 0, rt.plans
+    # the arena was pinned on the host thread during the Detailed step (2 x the deficit), large
+    # enough that the install did not grow it
+    assert rt.prepin_log and rt.prepin_log[0][2] is None, rt.prepin_log
+    assert rt.ctx.host_arena()[1] == rt.prepin_log[0][0]
     plan = rt.plans[0]
     if len(plan.get("trial_plans", [])) > 1:  # the fastest measured trial is kept
         times = [t["step_s"] for t in plan["trials"]]
