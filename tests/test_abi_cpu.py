@@ -81,3 +81,5 @@ def test_arena_config_validation():
         assert b"arena" in L.chm_last_error()
     ctx = chm.Context(device=-1)
     assert ctx.arena_placement() == {"numa_node": -1, "mode": -1, "pin_s": 0.0}
+    ctx.release_scratch()  # a host-only ctx holds no device scratch: a no-op
+    assert chm.load().chm_release_scratch(None) == -1  # CHM_E_INVAL
