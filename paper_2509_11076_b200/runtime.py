@@ -459,6 +459,8 @@ class Runtime:
             self._plan(self.prev_t_iter or t_iter)  # once per stable phase
             self.need_plan = False
             self.force_plan = False
+        if self.detailed:
+            self._join_prepin()  # the Detailed step's background pin never outlives it
         if not self.detailed and self.policy is None:
             self.prev_t_iter = t_iter
 
