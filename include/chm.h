@@ -212,6 +212,11 @@ chm_status chm_trace_get_info(const chm_trace *t, chm_trace_info *info);
 chm_status chm_trace_tables(const chm_trace *t, int64_t *f0, uint32_t *tensor, int64_t *nbytes,
                             int32_t *r, int32_t *s, int32_t *lin, int32_t *lout,
                             int32_t *lay_start, int32_t *lay_count, double *bud, uint64_t *base);
+/* 64-bit FNV-1a digest of everything an evaluation reads from the trace (N, K, L, W, budget, M_0,
+ * B, T_iter, F0, the layer table and Eq. 1 budgets, the swappable table, the default base), in a
+ * fixed field order.  Ranks that shard one candidate set (SURVEY §8(e), P:421 best-of-n) all-gather
+ * it and refuse to proceed on a mismatch.  Host-only; valid on a host-only ctx's trace. */
+chm_status chm_trace_digest(const chm_trace *t, uint64_t *digest);
 
 /* ------------------------------------------------------------- policy evaluation (a4-a7) */
 /* One swap item of an EXPLICIT candidate: tensor t = production-order index of a produced
@@ -281,7 +286,9 @@ enum { CHM_STALL_LAYER = 0, CHM_STALL_TIMELINE = 1 };
 
 /* Evaluates candidates on `stream` (enqueue only).  For candidate P:
  *   F_P[i] = F0[i] - sum_{t in P} S_t [r_t < i < s_t]  (event replay of §8(c).2)
- *   peak = max_i F_P[i]; stall = sum_l max(0, load_l / B - Bud_l) ascending in l (§8(c).5)
+ *   peak = max_i F_P[i]; stall = sum_l max(0, load_l / B - Bud_l) (§8(c).5 terms), summed as a
+ *   pairwise tree: terms indexed l = 0..L-1, zero-padded to the next power of two >= L, each
+ *   half summed recursively, IEEE double round-to-nearest (reading R-stall);
  * writes the per-candidate outputs and the argmin key of this batch into *best. */
 chm_status chm_eval_policies(chm_ctx *ctx, const chm_trace *t, const chm_candidates *c,
                              const chm_eval_out *o, cudaStream_t stream);

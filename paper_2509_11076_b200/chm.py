@@ -207,6 +207,7 @@ def load(path: str = LIB_PATH):
         "chm_trace_free": (None, [vp]),
         "chm_trace_get_info": (i32, [vp, P(TraceInfo)]),
         "chm_trace_tables": (i32, [vp] + [vp] * 11),
+        "chm_trace_digest": (i32, [vp, P(u64)]),
         "chm_eval_policies": (i32, [vp, vp, P(Candidates), P(EvalOut), vp]),
         "chm_eval_policies_ex": (i32, [vp, vp, P(Candidates), P(EvalOut), vp, P(i64)]),
         "chm_generate_policy": (i32, [vp, P(GenParams), vp, u32, P(u32), P(i32)]),
@@ -289,6 +290,12 @@ class Trace:
         _check(load().chm_trace_tables(self.h, *[out[k].ctypes.data for k in keys]))
         out["base"] = out["base"][:W]
         return out
+
+    def digest(self) -> int:
+        """64-bit digest of the evaluated tables (chm_trace_digest)"""
+        d = C.c_uint64()
+        _check(load().chm_trace_digest(self.h, C.byref(d)))
+        return d.value
 
     def generate_policy(self, C_coef: float = 1.0, rem_scale: float = 1.0):
         """Algo. 2 -> (items ITEM_DTYPE array, feasible)"""

@@ -335,3 +335,26 @@ extern "C" chm_status chm_trace_tables(const chm_trace *t, int64_t *f0, uint32_t
   if (base) std::copy(t->base.begin(), t->base.end(), base);
   return CHM_OK;
 }
+
+namespace {
+struct Fnv64 {  // FNV-1a over the bytes of each field, in a fixed order
+  uint64_t h = 0xcbf29ce484222325ull;
+  void bytes(const void *p, size_t n) {
+    const unsigned char *c = static_cast<const unsigned char *>(p);
+    for (size_t i = 0; i < n; i++) { h ^= c[i]; h *= 0x100000001b3ull; }
+  }
+  template <class T> void pod(const T &v) { bytes(&v, sizeof v); }
+  template <class T> void vec(const std::vector<T> &v) { pod(uint64_t(v.size())); bytes(v.data(), v.size() * sizeof(T)); }
+};
+}  // namespace
+
+extern "C" chm_status chm_trace_digest(const chm_trace *t, uint64_t *digest) {
+  if (!t || !digest) CHM_FAIL(CHM_E_INVAL, "chm_trace_digest: NULL argument");
+  Fnv64 f;
+  f.pod(t->N); f.pod(t->K); f.pod(t->L); f.pod(t->W);
+  f.pod(t->budget); f.pod(t->M0); f.pod(t->bw); f.pod(t->t_iter);
+  f.vec(t->F0); f.vec(t->lay_start); f.vec(t->lay_n); f.vec(t->bud);
+  f.vec(t->sw_S); f.vec(t->sw_r); f.vec(t->sw_s); f.vec(t->sw_lin); f.vec(t->sw_lout); f.vec(t->base);
+  *digest = f.h;
+  return CHM_OK;
+}

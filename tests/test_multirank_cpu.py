@@ -22,26 +22,44 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, C, out):
+def _worker(rank, world, port, C, out, budget_skew=0):
+    """bench.py's distributed evaluation steps with the product's helpers
+    (paper_2509_11076_b200.dist): trace built per rank through the ABI, digests all-gathered and
+    compared, contiguous shard, one key per rank all-gathered and reduced on the host
+    (chm_best_reduce, the gloo path of argmin_exchange)"""
     import sys
     sys.path.insert(0, ROOT)
     import oracle as O
     from paper_2509_11076_b200 import chm
+    from paper_2509_11076_b200 import dist as D
     from workloads import traces as W
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     tr = W.gpt2_xl()
     sd = W.SEEDED["C2"]
+    ctx = chm.Context(device=-1)
+    ctx.set_detailed(True)
+    chm.record_iteration(ctx, tr)
+    ctx.detect_seq_change(tr.t_iter)
+    pt = ctx.trace_build(tr.budget + (512 * rank if budget_skew else 0), tr.static_bytes, tr.bw, tr.groups_fwd,
+                         tr.groups_bwd, t_iter=tr.t_iter, omega=tr.omega)
+    try:
+        digest = D.check_same_trace(pt)
+    except RuntimeError as e:
+        out[rank] = ("mismatch", str(e))
+        dist.destroy_process_group()
+        return
+    lo, cnt = D.shard(C, world, rank)  # bench.py's shard rule
     m = O.Model(tr)
-    lo, hi = rank * C // world, (rank + 1) * C // world  # bench.py's shard rule
-    b = m.eval(O.SEEDED, lo, hi - lo, seed=sd["seed"], flip_thr=sd["flip_thr"], nthreads=2)["best"]
+    b = m.eval(O.SEEDED, lo, cnt, seed=sd["seed"], flip_thr=sd["flip_thr"], nthreads=2)["best"]
     key = np.array([(b.excess, b.stall, b.swapped, b.index, b.peak)], dtype=chm.BEST_DTYPE)
-    t = torch.from_numpy(key.view(np.int64).copy())
+    best_local = torch.from_numpy(key.view(np.int64).copy())
     gathered = torch.empty(world * 5, dtype=torch.int64)
-    dist.all_gather_into_tensor(gathered, t)
-    best = chm.best_reduce(gathered.numpy().view(chm.BEST_DTYPE))
-    out[rank] = (int(best.index), int(best.excess), float(best.stall), int(best.swapped_bytes))
+    best_global = torch.empty(5, dtype=torch.int64)
+    D.argmin_exchange(None, best_local, gathered, best_global, world)
+    g = best_global.numpy().view(chm.BEST_DTYPE)[0]
+    out[rank] = (int(g["index"]), int(g["excess"]), float(g["stall"]), int(g["swapped_bytes"]), digest)
     dist.destroy_process_group()
 
 
@@ -57,7 +75,29 @@ def test_sharded_argmin_equals_global(world):
     sd = W.SEEDED["C2"]
     ref = O.Model(tr).eval(O.SEEDED, 0, C, seed=sd["seed"], flip_thr=sd["flip_thr"], nthreads=4)["best"]
     for r in range(world):
-        assert out[r] == (ref.index, ref.excess, ref.stall, ref.swapped)
+        assert out[r][:4] == (ref.index, ref.excess, ref.stall, ref.swapped)
+    assert out[0][4] == out[1][4]
+
+
+def test_trace_mismatch_fails_loudly():
+    """ranks whose traces differ (here: the budget) must refuse to shard one candidate set"""
+    mgr = mp.get_context("spawn").Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(2, _free_port(), 100, out, 1), nprocs=2, join=True)
+    for r in range(2):
+        assert out[r][0] == "mismatch" and "digest differs" in out[r][1], out[r]
+
+
+def test_shard_rule_covers_every_candidate_once():
+    from paper_2509_11076_b200.dist import shard
+    for C in (0, 1, 7, 100_000, 10_000_001):
+        for P in (1, 2, 3, 4, 8):
+            parts = [shard(C, P, r) for r in range(P)]
+            assert parts[0][0] == 0 and sum(c for _, c in parts) == C
+            assert all(parts[r][0] + parts[r][1] == parts[r + 1][0] for r in range(P - 1))
+            assert max(c for _, c in parts) - min(c for _, c in parts) <= 1
+    with pytest.raises(ValueError):
+        shard(10, 2, 2)
 
 
 def _ddp_worker(rank, world, port, out):

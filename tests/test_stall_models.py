@@ -52,6 +52,47 @@ def test_timeline_fifo_two_items_closed_form():
     assert m.stall_timeline(t, r, s) == pytest.approx(exp, rel=1e-12)
 
 
+def _hand_items(sizes_tau, r, s):
+    """like _hand, but each item k has its own release op r[k] and swap-in op s[k]; sizes in
+    units of tau * B (so S/B = sizes_tau[k] * tau).  10 ops, one op per layer: Bud_l = tau."""
+    tr, m, t, _, _ = _hand([int(x * TAU * 1e9) for x in sizes_tau])
+    return tr, m, t, list(r), list(s)
+
+
+def test_stall_dir_one_item_two_layers_closed_form():
+    """orc_stall_dir (Q11 per-direction variant, P:333 / P:340): one item released after op 4
+    (out charged to layer 4) and swapped in before op 6 (in charged to layer 6),
+    S/B = 2.5 tau against Bud = tau in each layer:
+    stall = (2.5 - 1) tau [out, layer 4] + (2.5 - 1) tau [in, layer 6] = 3 tau (= R-stall here:
+    the two directions never share a layer)"""
+    tr, m, t, r, s = _hand_items([2.5], [4], [6])
+    assert m.stall_dir(t, r, s) == pytest.approx(3.0 * TAU, rel=1e-12)
+    assert m.stall(t, r, s) == pytest.approx(3.0 * TAU, rel=1e-12)
+    # under budget on both sides: nothing
+    tr, m, t, r, s = _hand_items([0.9], [4], [6])
+    assert m.stall_dir(t, r, s) == 0.0
+
+
+def test_stall_dir_opposite_directions_in_one_layer_closed_form():
+    """Three items (sizes in tau * B): A = 2.5 (r 4, s 6), B = 0.5 (r 2, s 4), C = 0.8 (r 3, s 6).
+    Layer 4 holds A's swap-out and B's swap-in; layer 6 the swap-ins of A and C.  By hand:
+      per direction: out l2 max(0, .5-1)=0, out l3 max(0, .8-1)=0, out l4 2.5-1=1.5,
+                     in l4 max(0, .5-1)=0, in l6 (2.5+.8)-1=2.3            -> 3.8 tau
+      R-stall (one budget per layer): l4 (2.5+.5)-1=2.0, l6 2.3, l2/l3 0  -> 4.3 tau
+    so R-stall - per-direction = 0.5 tau.  Plausible slips give other numbers: one budget of
+    2 Bud for both directions (l4 3-2=1, l6 3.3-2=1.3: 2.3 tau); swap-ins charged to lay(r)
+    (in l4 A 1.5, out l4 A 1.5: 3.0 tau); the max taken over the sum of both directions' terms
+    (l4 1.5-0.5=1.0: 3.3 tau)."""
+    tr, m, t, r, s = _hand_items([2.5, 0.5, 0.8], [4, 2, 3], [6, 4, 6])
+    d, lay = m.stall_dir(t, r, s), m.stall(t, r, s)
+    assert d == pytest.approx(3.8 * TAU, rel=1e-12)
+    assert lay == pytest.approx(4.3 * TAU, rel=1e-12)
+    assert lay - d == pytest.approx(0.5 * TAU, rel=1e-9)
+    # the item order does not matter (sums of integers per layer, then a fixed-order tree)
+    perm = [2, 0, 1]
+    assert m.stall_dir([t[k] for k in perm], [r[k] for k in perm], [s[k] for k in perm]) == d
+
+
 def _random_items(m, rng, n_max=None):
     sw = m.swappable()
     if m.K == 0:
