@@ -77,7 +77,7 @@ extern "C" chm_status chm_create(const chm_config *cfg, chm_ctx **out) {
   int ndev = 0;
   CHM_CUDA(cudaGetDeviceCount(&ndev));
   if (c.device >= ndev) CHM_FAIL(CHM_E_INVAL, "chm_create: device %d of %d", c.device, ndev);
-  CHM_CUDA(cudaSetDevice(c.device));
+  CHM_DEVICE_SCOPE(c.device);
   cudaDeviceProp prop;
   CHM_CUDA(cudaGetDeviceProperties(&prop, c.device));
   if (prop.major != 10 || prop.minor != 0)
@@ -125,7 +125,7 @@ extern "C" chm_status chm_create(const chm_config *cfg, chm_ctx **out) {
 extern "C" void chm_destroy(chm_ctx *ctx) {
   if (!ctx) return;
   if (ctx->device < 0) { delete ctx; return; }
-  cudaSetDevice(ctx->device);
+  DeviceGuard dg(ctx->device);
   for (auto e : ctx->events) if (e) cudaEventDestroy(e);
   for (auto e : ctx->fences) if (e) cudaEventDestroy(e);
   for (auto e : ctx->t0) if (e) cudaEventDestroy(e);

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <string>
 #include <unordered_map>
@@ -51,6 +52,27 @@ void set_error(const char *fmt, ...);
       CHM_FAIL(CHM_E_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
                __LINE__);                                                               \
   } while (0)
+
+// Makes `dev` current for the scope of one ABI call and gives the caller's device back on
+// return: libchm links its own CUDA runtime, but both runtimes share the driver's per-thread
+// current context, so a bare cudaSetDevice would silently move PyTorch's current device.
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t status = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) status = cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard &) = delete;
+  DeviceGuard &operator=(const DeviceGuard &) = delete;
+};
+#define CHM_DEVICE_SCOPE(dev)            \
+  ::chm::DeviceGuard chm_dev_guard_(dev); \
+  CHM_CUDA(chm_dev_guard_.status)
 
 // ---------------------------------------------------------------- detailed record
 struct TensorRec {
@@ -249,6 +271,7 @@ struct chm_ctx {
   int32_t arena_numa = -1;       // requested placement (chm_config.arena_numa)
   int32_t arena_node = -1;       // actual binding
   double arena_pin_s = 0;
+  std::atomic<int> arena_busy{0};  // 1 while chm_arena_reserve re-pins (swap calls: CHM_E_STATE)
   std::vector<cudaEvent_t> events;  // ring of batch-completion events
   std::vector<cudaEvent_t> fences;  // ring of compute->swap fence events
   std::vector<cudaEvent_t> t0, t1;  // timing events per batch slot (time_batches)

@@ -520,8 +520,10 @@ extern "C" chm_status chm_eval_policies_ex(chm_ctx *ctx, const chm_trace *t, con
     case CHM_CAND_EXPLICIT:
       if (o->footprint && (o->ld < uint32_t(t->N) || (o->ld & 1u)))
         CHM_FAIL(CHM_E_INVAL, "chm_eval_policies: footprint ld %u must be even and >= n_ops %d", o->ld, t->N);
-      CHM_CUDA(cudaSetDevice(ctx->device));
-      return launch_eval_explicit(ctx, t, c, o, stream, err_index);
+      {
+        CHM_DEVICE_SCOPE(ctx->device);
+        return launch_eval_explicit(ctx, t, c, o, stream, err_index);
+      }
     default:
       CHM_FAIL(CHM_E_INVAL, "chm_eval_policies: unknown candidate kind %d", int(c->kind));
   }
@@ -537,7 +539,7 @@ extern "C" chm_status chm_eval_policies_ex(chm_ctx *ctx, const chm_trace *t, con
   L.footprint = o->footprint;
   L.ld = o->ld;
   L.best = o->best;
-  CHM_CUDA(cudaSetDevice(ctx->device));
+  CHM_DEVICE_SCOPE(ctx->device);
   if (!timeline) return launch_eval(ctx, L, stream);
   // timeline: the replay gives peak / swapped (footprint rows as asked), then timeline.cu the
   // stall of each candidate and the argmin key over (excess, timeline stall, swapped, index)
@@ -568,7 +570,7 @@ extern "C" chm_status chm_best_reduce_device(chm_ctx *ctx, const chm_best *keys,
                                              cudaStream_t stream) {
   if (!ctx || !keys || !out || n == 0 || ctx->device < 0)
     CHM_FAIL(CHM_E_INVAL, "chm_best_reduce_device: bad argument");
-  CHM_CUDA(cudaSetDevice(ctx->device));
+  CHM_DEVICE_SCOPE(ctx->device);
   best_reduce_kernel<<<1, 32, 0, stream>>>(reinterpret_cast<const Key *>(keys), n, reinterpret_cast<Key *>(out));
   CHM_CUDA(cudaGetLastError());
   return CHM_OK;
@@ -577,7 +579,7 @@ extern "C" chm_status chm_best_reduce_device(chm_ctx *ctx, const chm_best *keys,
 extern "C" chm_status chm_release_scratch(chm_ctx *ctx) {
   if (!ctx) CHM_FAIL(CHM_E_INVAL, "chm_release_scratch: NULL ctx");
   if (ctx->device < 0) return CHM_OK;
-  CHM_CUDA(cudaSetDevice(ctx->device));
+  CHM_DEVICE_SCOPE(ctx->device);
   void **bufs[4] = {&ctx->eval_scratch, &ctx->tl_scratch, &ctx->tl_aux, &ctx->explicit_scratch};
   size_t *sizes[4] = {&ctx->eval_scratch_bytes, &ctx->tl_scratch_bytes, &ctx->tl_aux_bytes,
                       &ctx->explicit_scratch_bytes};

@@ -221,6 +221,7 @@ using namespace chm;
 
 extern "C" chm_status chm_host_arena(chm_ctx *ctx, void **host_base, uint64_t *bytes) {
   if (!ctx) CHM_FAIL(CHM_E_INVAL, "chm_host_arena: NULL ctx");
+  if (ctx->arena_busy.load()) CHM_FAIL(CHM_E_STATE, "chm_host_arena: the arena is being re-pinned");
   if (host_base) *host_base = ctx->arena;
   if (bytes) *bytes = ctx->arena_bytes;
   return CHM_OK;
@@ -229,6 +230,7 @@ extern "C" chm_status chm_host_arena(chm_ctx *ctx, void **host_base, uint64_t *b
 static chm_status validate_batch(chm_ctx *ctx, const chm_swap_desc *d, uint32_t n, int64_t *err) {
   if (err) *err = -1;
   if (n && !d) CHM_FAIL(CHM_E_INVAL, "swap: NULL descriptor list");
+  if (n && ctx->arena_busy.load()) CHM_FAIL(CHM_E_STATE, "swap: the host arena is being re-pinned (chm_arena_reserve)");
   if (n && !ctx->arena) CHM_FAIL(CHM_E_STATE, "swap: ctx has no host arena");
   for (uint32_t j = 0; j < n; j++) {
     if (d[j].nbytes == 0 || d[j].dev == 0 || d[j].host_off > ctx->arena_bytes ||
@@ -263,6 +265,7 @@ static chm_status swap_batch(chm_ctx *ctx, const chm_swap_desc *d, uint32_t n, c
   if (flags > CHM_SWAP_AUTO) CHM_FAIL(CHM_E_INVAL, "swap: unknown flags %u", flags);
   chm_status st = validate_batch(ctx, d, n, err);
   if (st != CHM_OK) return st;
+  CHM_DEVICE_SCOPE(ctx->device);
   const uint64_t b = ctx->next_batch++;
   const size_t slot = size_t(b % kEventRing);
   if (compute != swap) {  // swap stream starts after everything enqueued on compute so far
@@ -343,8 +346,21 @@ extern "C" chm_status chm_arena_reserve(chm_ctx *ctx, uint64_t bytes) {
   if (bytes <= ctx->arena_bytes) return CHM_OK;
   if (!ctx->passive.empty())
     CHM_FAIL(CHM_E_STATE, "chm_arena_reserve: %zu passive swaps hold arena data", ctx->passive.size());
+  int idle = 0;
+  if (!ctx->arena_busy.compare_exchange_strong(idle, 1))
+    CHM_FAIL(CHM_E_STATE, "chm_arena_reserve: another reserve is running on this ctx");
+  struct Busy { std::atomic<int> &b; ~Busy() { b.store(0); } } busy{ctx->arena_busy};
   ctx->passive_free.clear();  // re-derived from the new size at the next passive swap
-  CHM_CUDA(cudaSetDevice(ctx->device));
-  arena_free(ctx);  // arena.cpp
-  return arena_alloc(ctx, bytes);
+  CHM_DEVICE_SCOPE(ctx->device);
+  const uint64_t old = ctx->arena_bytes;
+  arena_free(ctx);  // arena.cpp; pinning old + new together would double the host footprint
+  const chm_status st = arena_alloc(ctx, bytes);
+  if (st != CHM_OK && old) {  // keep an arena of the old size: installed plans still fit it
+    const std::string msg = chm_last_error();
+    if (arena_alloc(ctx, old) != CHM_OK)
+      CHM_FAIL(st, "%s (and re-pinning the previous %llu B failed: %s)", msg.c_str(), (unsigned long long)old,
+               chm_last_error());
+    CHM_FAIL(st, "%s (the previous %llu B arena was re-pinned)", msg.c_str(), (unsigned long long)old);
+  }
+  return st;
 }

@@ -326,7 +326,7 @@ chm_status build_program(const chm_trace *tc) {
   const size_t ev_bytes = (8 * prog.size() + 15) & ~size_t(15);
   std::vector<double> cost(static_cast<size_t>(K) + 1, 0.0);  // [K] = 0 for the NOP item
   for (int32_t k = 0; k < K; k++) cost[size_t(k)] = double(t->sw_S[size_t(k)]) / t->bw;  // Eq. 3, as the model
-  CHM_CUDA(cudaSetDevice(t->device));
+  CHM_DEVICE_SCOPE(t->device);
   void *d = nullptr;
   CHM_CUDA(cudaMalloc(&d, ev_bytes + 8 * (size_t(K) + 1)));
   cudaError_t e1 = cudaMemcpy(d, prog.data(), 8 * prog.size(), cudaMemcpyHostToDevice);

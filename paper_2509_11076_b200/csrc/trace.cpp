@@ -278,7 +278,8 @@ chm_status chm::build_trace(chm_ctx *ctx, const IterRecord &R, const chm_trace_p
     *out = tr;
     return CHM_OK;
   }
-  cudaError_t e = cudaSetDevice(ctx->device);
+  DeviceGuard dg(ctx->device);
+  cudaError_t e = dg.status;
   if (e == cudaSuccess) e = cudaMalloc(&tr->dev_block, total);
   if (e == cudaSuccess) e = cudaMemcpy(tr->dev_block, host.data(), total, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
@@ -293,13 +294,10 @@ chm_status chm::build_trace(chm_ctx *ctx, const IterRecord &R, const chm_trace_p
 
 extern "C" void chm_trace_free(chm_trace *t) {
   if (!t) return;
-  if (t->dev_block && t->device >= 0) {
-    cudaSetDevice(t->device);
-    cudaFree(t->dev_block);
-  }
-  if (t->tl_dev && t->device >= 0) {
-    cudaSetDevice(t->device);
-    cudaFree(t->tl_dev);
+  if ((t->dev_block || t->tl_dev) && t->device >= 0) {
+    DeviceGuard dg(t->device);
+    if (t->dev_block) cudaFree(t->dev_block);
+    if (t->tl_dev) cudaFree(t->tl_dev);
   }
   delete t;
 }

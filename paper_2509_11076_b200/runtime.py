@@ -231,15 +231,18 @@ class Runtime:
     host_arena_bytes: pinned arena reserved up front (else grown to each policy at install);
     stall_model: the stall that ranks plans, chm.STALL_TIMELINE (default) or chm.STALL_LAYER;
     search_batch: flips tried together per descent round (1: single-flip steepest descent);
-    prepin: pin the host arena on a host thread during the Detailed step, sized 2 x (peak
-    allocated - budget), so the plan's install does not pin."""
+    prepin: pin the host arena on a host thread during the Detailed step, sized 1.25 x (peak
+    allocated - budget), so the plan's install does not pin;
+    host_pin_budget: most bytes this rank may pin for the arena (0: 0.6 x MemAvailable /
+    LOCAL_WORLD_SIZE, i.e. the node's pinnable RAM split between its ranks)."""
 
     def __init__(self, device: Optional[int] = 0, *, hbm_budget: int, bw: Optional[float] = None,
                  groups_fwd: int = 0, groups_bwd: int = 0, omega: float = 1.0, candidates: int = 1 << 16,
                  seed: int = 1, flip_frac: float = 0.02, generator: bool = True, swap_ctas: int = 0,
                  min_swap_bytes: int = 0, search_rounds: int = 4096, host_arena_bytes: int = 0,
                  swap_flags: int = chm.SWAP_AUTO, oom_host_bytes: int = 0, trials: int = 5,
-                 stall_model: int = chm.STALL_TIMELINE, search_batch: int = 1, prepin: bool = True, **algo1):
+                 stall_model: int = chm.STALL_TIMELINE, search_batch: int = 1, prepin: bool = True,
+                 host_pin_budget: int = 0, **algo1):
         self.host_only = device is None
         self.dev = torch.device("cpu") if self.host_only else torch.device("cuda", device)
         self.ctx = chm.Context(device=-1 if self.host_only else device, swap_ctas=swap_ctas,
@@ -255,6 +258,7 @@ class Runtime:
         # 5-16x fewer rounds, plans within 0-3% of the single-flip ones, tools/descent_batch.py)
         self.search_batch = int(search_batch)
         self.prepin = bool(prepin)
+        self.host_pin_budget = int(host_pin_budget)
         self._prepin_thread = None
         self._peak_seen = 0  # max over finished steps of the allocator's peak (bytes)
         self.prepin_log = []  # (bytes, seconds, error) of background arena reservations
@@ -395,11 +399,12 @@ class Runtime:
         deficit = max(self._peak_seen, torch.cuda.max_memory_allocated(self.dev)) - self.hbm_budget
         if deficit <= 0:
             return
-        try:
-            avail = next(int(ln.split()[1]) * 1024 for ln in open("/proc/meminfo") if ln.startswith("MemAvailable:"))
-        except (OSError, StopIteration, ValueError):
+        cap = self._pin_cap()
+        if cap <= 0:
             return
-        est = min(2 * deficit + (64 << 20), int(0.6 * avail))
+        # the deficit is a lower bound on the plan's swapped bytes; a quarter on top covers the
+        # usual plan without pinning (and keeping) twice what it needs
+        est = min(deficit + deficit // 4 + (64 << 20), cap)
         if est <= self.ctx.host_arena()[1]:
             return
 
@@ -414,6 +419,19 @@ class Runtime:
 
         self._prepin_thread = threading.Thread(target=run, name="chm-prepin", daemon=True)
         self._prepin_thread.start()
+
+    def _pin_cap(self) -> int:
+        """bytes this rank may pin: host_pin_budget, else 0.6 x MemAvailable split between the
+        node's ranks (every rank of a node pins during the same Detailed step and reads the same
+        MemAvailable)"""
+        if self.host_pin_budget:
+            return self.host_pin_budget
+        try:
+            avail = next(int(ln.split()[1]) * 1024 for ln in open("/proc/meminfo") if ln.startswith("MemAvailable:"))
+        except (OSError, StopIteration, ValueError):
+            return 0
+        local = max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
+        return int(0.6 * avail / local)
 
     def _join_prepin(self):
         if self._prepin_thread is not None:
@@ -456,8 +474,11 @@ class Runtime:
         if self.detailed and not d["changed"] and (self.force_plan or (stage_before == chm.GENPOLICY and self.need_plan)):
             # T_iter of Eq. 1: the last Lightweight step without a policy (the Detailed one pays
             # for free polling, a policy step for its stalls)
-            self._plan(self.prev_t_iter or t_iter)  # once per stable phase
-            self.need_plan = False
+            try:
+                self._plan(self.prev_t_iter or t_iter)  # once per stable phase
+            except Exception as e:  # noqa: BLE001 -- a failed plan must not fail every later step
+                self._plan_failed(e)
+            self.need_plan = False  # no policy until the next sequence change (or request_replan)
             self.force_plan = False
         if self.detailed:
             self._join_prepin()  # the Detailed step's background pin never outlives it
@@ -728,6 +749,25 @@ class Runtime:
         if self.policy is not None:
             self._uninstall()
 
+    def _plan_failed(self, e: Exception):
+        """planning raised (trace build bounds, arena NOMEM, ...): run without a policy and say
+        why in self.plans"""
+        self._join_prepin()
+        self.trials = None
+        if self.policy is not None:
+            try:
+                self._uninstall()
+            except chm.ChmError:
+                self.policy = None
+        self.policy_items = None
+        if not self.host_only:
+            try:
+                self.ctx.release_scratch()
+            except chm.ChmError:
+                pass
+        self.plans.append(dict(kind="error", error=f"{type(e).__name__}: {e}"))
+        self.stats["plan_errors"] = self.stats.get("plan_errors", 0) + 1
+
     def _uninstall(self):
         pt = self.policy[0]
         self.ctx.policy_install(pt, np.zeros(max(pt.W, 1), np.uint64)[:pt.W])
@@ -804,6 +844,8 @@ class Runtime:
                     cands.append((name + "+search", k, w, False))
                 plan["search_rounds"] = rounds
             plan["search_ms"] = (time.perf_counter() - t1) * 1e3
+            if not cands:  # K > 4096 and no generator lists: nothing to choose from
+                raise RuntimeError(f"no candidate plan (K = {pt.K}: SEEDED needs K <= 4096; generator off or empty)")
             # distinct plans, best key first; the n best are tried on real steps
             cands.sort(key=lambda c: self._key(c[1]))
             # trial only plans as feasible as the best, and not ones whose host traffic (and pinned
@@ -916,3 +958,11 @@ class Runtime:
     def close(self):
         self._join_prepin()
         self.ctx.close()
+
+    def __del__(self):
+        # a Runtime dropped without close(): the background pin writes ctx fields, so it must
+        # finish before chm_destroy runs
+        try:
+            self._join_prepin()
+        except Exception:  # noqa: BLE001
+            pass

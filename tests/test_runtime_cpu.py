@@ -190,3 +190,29 @@ def test_runtime_on_a_conv_net():
     assert len(rt.plans) == 1 and rt.plans[0]["items"] > 0
     per = np.diff([0] + matched)
     assert per[-1] == rt.plans[0]["items"] and rt.ctx.exec_stats()["n_stale"] == 0
+
+
+def test_planner_error_is_recorded_and_training_continues():
+    """a plan that raises (here: the trace build) must not escape rt.step() nor re-raise in every
+    later step: it is recorded in rt.plans, the runtime runs without a policy until the next
+    sequence change or request_replan"""
+    model, opt, data, rt = _setup()
+    real = rt.ctx.trace_build
+    calls = []
+
+    def broken(*a, **k):
+        calls.append(1)
+        raise chm.ChmError(chm.CHM_E_INVAL, "injected planner failure")
+
+    rt.ctx.trace_build = broken
+    for x, y in data:
+        _step(rt, model, opt, x, y)
+    assert len(calls) == 1  # planned once, failed once
+    assert rt.plans and rt.plans[-1]["kind"] == "error" and "injected" in rt.plans[-1]["error"]
+    assert rt.policy is None and rt.stats["plan_errors"] == 1 and rt.stats["release"] == 0
+    # a forced re-plan with a working trace build installs a policy again
+    rt.ctx.trace_build = real
+    rt.request_replan()
+    for x, y in G.batches(3, 2, 16, 64):
+        _step(rt, model, opt, x, y)
+    assert rt.plans[-1]["kind"] != "error" and rt.plans[-1]["items"] > 0
