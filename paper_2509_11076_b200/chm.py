@@ -171,7 +171,7 @@ class Passive(C.Structure):
 EXPORTS = [
     "chm_config_default", "chm_create", "chm_destroy", "chm_last_error", "chm_build_info", "chm_tokenize",
     "chm_record_op", "chm_set_detailed", "chm_detect_seq_change", "chm_trace_build", "chm_trace_free",
-    "chm_trace_get_info", "chm_trace_tables", "chm_eval_policies", "chm_eval_policies_ex", "chm_best_reduce", "chm_best_reduce_device", "chm_candidate_mask",
+    "chm_trace_get_info", "chm_trace_tables", "chm_trace_digest", "chm_eval_policies", "chm_eval_policies_ex", "chm_best_reduce", "chm_best_reduce_device", "chm_candidate_mask",
     "chm_policy_install", "chm_policy_install_items", "chm_generate_policy", "chm_exec_stats_get", "chm_host_arena", "chm_swap_out", "chm_swap_in",
     "chm_batch_wait", "chm_batch_query", "chm_batch_elapsed", "chm_arena_reserve", "chm_issue_swap_out", "chm_issue_swap_in", "chm_item_wait",
     "chm_oom_release", "chm_passive_swap", "chm_passive_restore", "chm_trace_load", "chm_record_save",
