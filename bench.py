@@ -1,21 +1,29 @@
 #!/usr/bin/env python
 """bench.py -- the Chameleon swap hot path on B200 (BASELINE.json metric and configs).
 
-One step = one pass of the whole hot path over the workload's iteration:
+One step = one pass of the whole hot path over one training iteration of the
+workload:
   policy evaluation: chm_eval_policies over this rank's shard of the 10^5 SEEDED candidates
   (full mode: every candidate's per-op footprint written), NCCL all-gather + device argmin of
-  the per-rank keys (N > 1); policy execution: the installed best policy replayed through the
-  profiler hook (chm_record_op per op: App. A matching + trigger tables), swap-outs after a_t,
-  stream-ordered releases at r_t, swap-ins before s_t and waits before b_t on real HBM buffers
-  and the pinned mapped host arena.
+  the per-rank keys (N > 1);
+  policy execution: the best policy replayed through the profiler hook (chm_record_op per op:
+  App. A matching + trigger tables), swap-outs after a_t, stream-ordered releases at r_t,
+  swap-ins before s_t and waits before b_t on real HBM buffers and the pinned mapped host
+  arena, while each op's compute runs on the compute stream (a bf16 GEMM calibrated to the
+  trace's per-op time T_iter / N: the swaps overlap compute as in P:389 / P:428).
 Inputs (activations, trace tables) are resident in HBM when the timed region starts.
 
-value = swap bytes moved by all ranks (D2H + H2D) / step time (device events, max over ranks);
-candidates/s of the evaluation is reported beside it.  `e2e` repeats the step through the public
-API from host-side records: Detailed recording, trace build + table upload, evaluation, best-key
-read-back, policy install, swap execution on the public API's default copy path (CHM_SWAP_AUTO,
-what the runtime uses: tensors >= 4 MiB on the copy engines, smaller ones in the kernel); `value`
-times the hand-written kernel path alone.
+Workload (default C3h): Llama-2 7B bf16, seq 4096, HBM budget = half the no-swap peak (2x
+oversubscription), batch 6 so the whole policy (~106 GB each way) fits the box's pinnable host
+RAM (C3 at b = 18 would need ~300 GB pinned).  C2 (GPT-2 1.5B) runs beside it as a
+block of its own at N = 1, as do C1's small-tensor swaps and the C4 re-plan.
+
+value = swap bytes moved per GPU (D2H + H2D) / step time (device events, max over ranks);
+`value_aggregate` = the sum over ranks / the same time.  Candidates/s of the evaluation, the
+swap GB/s per direction during overlap, GEMM TFLOP/s alone / with copy-engine swaps / with the
+kernel, and measured vs estimated stall are reported beside it.  `e2e` repeats the step through
+the public API from host records (Detailed recording, trace build + table upload, evaluation,
+best-key read-back, policy install, execution on the API's default copy path CHM_SWAP_AUTO).
 
     python bench.py [--gpus N --steps K --warmup W]        # this implementation
     python bench.py --impl reference ...                    # the CPU oracle (reference arm)
@@ -41,6 +49,7 @@ from workloads import traces as W  # noqa: E402
 METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
 PCIE_GEN5_X16_GBPS = 32 * 16 * 128 / 130 / 8  # 63.0 GB/s per direction (nominal)
 FAKE_ID_BASE = 1 << 60  # ids of tensors the policy does not swap (never dereferenced)
+GEMM_N = 8192  # stand-in compute: C[M, N] = A[M, N] @ B[N, N], bf16, M calibrated per trace
 
 
 def measured_peaks():
@@ -50,23 +59,43 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0, "_fallback": True}
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="chm", choices=["chm", "reference"])
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C3h", help="C3h (default), C2, C3, C5, ... (workloads/traces.py)")
+    ap.add_argument("--batch", type=int, default=6, help="C3h batch (sized to the box's host RAM)")
     ap.add_argument("--candidates", type=int, default=100_000)
     ap.add_argument("--search-mode", action="store_true", help="no footprint rows (peak/stall/argmin only)")
     ap.add_argument("--swap-ctas", type=int, default=8)
     ap.add_argument("--host-frac", type=float, default=0.6, help="max fraction of host RAM pinned per node")
+    ap.add_argument("--no-compute", action="store_true", help="no stand-in GEMMs (swap-only steps)")
+    ap.add_argument("--alone-steps", type=int, default=2, help="steps of compute alone (no swaps)")
     ap.add_argument("--ce-steps", type=int, default=1, help="steps of the copy-engine baseline")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--c2-steps", type=int, default=3, help="C2 block steps at N = 1 (0: skip)")
+    ap.add_argument("--c1-reps", type=int, default=1000, help="C1 small-tensor block repetitions (0: skip)")
+    ap.add_argument("--no-extras", action="store_true", help="skip generator / timeline / C4 re-plan blocks")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--force-dist", action="store_true", help="NCCL argmin path even at N = 1 (one-rank group)")
-    return ap.parse_args()
+    return ap.parse_args(argv)
+
+
+def workload(args):
+    if args.config == "C3h":
+        return W.llama2_7b_2x(args.batch)
+    return W.CONFIGS[args.config]()
+
+
+def workload_desc(args, tr):
+    d = {"workload": tr.meta["config"], "trace_name": tr.name}
+    if args.config == "C3h":
+        d["sizing"] = (f"batch {args.batch} (the SEEDED best policy fits 0.6 x the box's ~206 GB host RAM; b = 18 "
+                       f"would need ~300 GB pinned); HBM budget = half the no-swap peak (2x oversubscription)")
+    return d
 
 
 def mem_available():
@@ -74,6 +103,18 @@ def mem_available():
         if line.startswith("MemAvailable:"):
             return int(line.split()[1]) * 1024
     return 0
+
+
+def host_info():
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count() or 1, "cpu_model": model, "mem_available_bytes": mem_available()}
 
 
 class ClockSampler:
@@ -131,7 +172,7 @@ def run_reference(args, rank: int):
     if rank != 0:
         return
     import oracle as O
-    tr = W.CONFIGS[args.config]()
+    tr = workload(args)
     sd = W.SEEDED[args.config[:2]]
     m = O.Model(tr)
     cores = os.cpu_count() or 1
@@ -161,34 +202,40 @@ def run_reference(args, rank: int):
     value = 2 * n_b / t / 1e9
     sample = (f"per step 1/64 of the workload: {n_c} of {C} SEEDED candidates "
               f"({'search' if args.search_mode else 'full'} mode) + {n_b} of {bytes_pol} policy bytes "
-              f"swapped out and back (memcpy, the oracle's swap definition)")
+              f"swapped out and back (memcpy, the oracle's swap definition); no stand-in compute")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": tr.meta["config"], "candidates": C, "candidate_kind": "SEEDED"},
+            "config": dict(workload_desc(args, tr), candidates=C, candidate_kind="SEEDED"),
             "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": sample,
-                             "candidates_per_s": n_c / t},
+                             "candidates_per_s": n_c / t, **host_info()},
             "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 def cpu_baseline(args, tr, best_swapped: int):
-    """The oracle timed on this box's host cores (rank 0, N = 1): a bounded sample, extrapolated
-    to the full step (eval of C candidates + swap of the policy bytes out and in)."""
+    """The oracle timed on this box's host cores (rank 0): a bounded sample on all cores and on one
+    thread, extrapolated to the full step (eval of C candidates + swap of the policy bytes out and
+    in), plus C1's 2^24-subset brute force (SURVEY §8(d) "Oracle timed beside it")."""
     import oracle as O
     sd = W.SEEDED[args.config[:2]]
     m = O.Model(tr)
     cores = os.cpu_count() or 1
     budget_s = args.cpu_seconds
-    n = 2000
-    t0 = time.perf_counter()
-    m.eval(O.SEEDED, 0, n, seed=sd["seed"], flip_thr=sd["flip_thr"], nthreads=cores, footprint=not args.search_mode)
-    dt = time.perf_counter() - t0
-    n2 = int(min(args.candidates, max(n, n * (0.5 * budget_s) / max(dt, 1e-6))))
-    t0 = time.perf_counter()
-    m.eval(O.SEEDED, 0, n2, seed=sd["seed"], flip_thr=sd["flip_thr"], nthreads=cores, footprint=not args.search_mode)
-    t_eval = time.perf_counter() - t0
-    rate_c = n2 / t_eval
+    fpm = not args.search_mode
+
+    def rate(nthreads, share):
+        n = 500 * nthreads
+        t0 = time.perf_counter()
+        m.eval(O.SEEDED, 0, n, seed=sd["seed"], flip_thr=sd["flip_thr"], nthreads=nthreads, footprint=fpm)
+        dt = time.perf_counter() - t0
+        n2 = int(min(args.candidates, max(n, n * (share * budget_s) / max(dt, 1e-6))))
+        t0 = time.perf_counter()
+        m.eval(O.SEEDED, 0, n2, seed=sd["seed"], flip_thr=sd["flip_thr"], nthreads=nthreads, footprint=fpm)
+        return n2, n2 / (time.perf_counter() - t0)
+
+    n_all, rate_c = rate(cores, 0.4)
+    n_one, rate_1 = rate(1, 0.2)
     nb = 1 << 30
     src = np.ones(nb, np.uint8)
     dst = np.empty(nb, np.uint8)
@@ -198,15 +245,88 @@ def cpu_baseline(args, tr, best_swapped: int):
     for _ in range(reps):
         O.swap_execute([dst.ctypes.data], [src.ctypes.data], [nb])
     rate_b = reps * nb / (time.perf_counter() - t0)
+    # C1: all 2^K subsets (K = 24), search mode, all cores
+    c1 = O.Model(W.tiny())
+    t0 = time.perf_counter()
+    c1.eval(O.EXHAUSTIVE, 0, 1 << c1.K, nthreads=cores)
+    t_c1 = time.perf_counter() - t0
     t_step = args.candidates / rate_c + 2 * best_swapped / rate_b
     return {"value": 2 * best_swapped / t_step / 1e9, "unit": "GB/s", "cores": cores, "kind": "oracle",
-            "sample": (f"{n2} SEEDED candidates on {cores} threads ({rate_c:.0f} cand/s, "
-                       f"{'search' if args.search_mode else 'full'} mode) + 3 x 1 GiB memcpy swap "
-                       f"({rate_b / 1e9:.1f} GB/s), extrapolated to the full step"),
-            "candidates_per_s": rate_c}
+            "sample": (f"{n_all} SEEDED candidates on {cores} threads ({rate_c:.0f} cand/s) and {n_one} on 1 thread "
+                       f"({rate_1:.0f} cand/s), {'full' if fpm else 'search'} mode; 3 x 1 GiB memcpy swap "
+                       f"({rate_b / 1e9:.1f} GB/s); extrapolated to the full step (no stand-in compute)"),
+            "candidates_per_s": rate_c, "candidates_per_s_1thread": rate_1,
+            "c1_bruteforce": {"subsets": 1 << c1.K, "seconds": t_c1, "threads": cores},
+            **host_info()}
 
 
 # ----------------------------------------------------------------------------- this repo
+class Compute:
+    """Stand-in for the model's operators on the compute stream: one bf16 GEMM per traced op,
+    [M, 8192] x [8192, 8192], M calibrated so one GEMM takes the trace's per-op time T_iter / N
+    (the tau of Eq. 1's budgets and of the timeline stall model).  Each GEMM is bracketed by CUDA
+    events so its duration is measured alone and under the swaps."""
+
+    def __init__(self, dev, tau_s: float, n_ops: int):
+        import torch
+        self.torch = torch
+        n = GEMM_N
+        g = torch.Generator(device=dev).manual_seed(7)
+        self.B = torch.randn(n, n, dtype=torch.bfloat16, device=dev, generator=g)
+        self.A = torch.randn(2 * n, n, dtype=torch.bfloat16, device=dev, generator=g)
+        self.C = torch.empty(2 * n, n, dtype=torch.bfloat16, device=dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for _ in range(3):
+            torch.matmul(self.A[:n], self.B, out=self.C[:n])
+        torch.cuda.synchronize()
+        e0.record()
+        reps = 20
+        for _ in range(reps):
+            torch.matmul(self.A[:n], self.B, out=self.C[:n])
+        e1.record()
+        torch.cuda.synchronize()
+        rate = reps * 2.0 * n ** 3 / (e0.elapsed_time(e1) * 1e-3)
+        self.tau = tau_s
+        self.n_ops = n_ops
+        self._set_m(tau_s * rate / (2.0 * n * n))
+        self.rate_burst = rate
+        self.ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_ops)]
+
+    def _set_m(self, m: float):
+        n = GEMM_N
+        self.M = int(min(2 * n, max(128, round(m / 128) * 128)))
+        self.flops = 2.0 * self.M * n * n
+
+    def recalibrate(self, stream, passes: int = 2):
+        """a back-to-back GEMM iteration runs at the sustained (power-capped) rate, not the
+        burst rate of the first calibration: rescale M until one iteration of compute alone
+        takes N x tau (once or twice, whole iterations)"""
+        torch = self.torch
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        hist = []
+        for _ in range(passes):
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for i in range(self.n_ops):
+                torch.matmul(self.A[:self.M], self.B, out=self.C[:self.M])
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            hist.append({"M": self.M, "iteration_ms": ms})
+            self._set_m(self.M * (self.n_ops * self.tau * 1e3) / ms)
+        return hist
+
+    def op(self, i: int, stream):
+        e0, e1 = self.ev[i]
+        e0.record(stream)
+        self.torch.matmul(self.A[:self.M], self.B, out=self.C[:self.M])
+        e1.record(stream)
+
+    def gemm_ms(self) -> float:
+        """summed GEMM durations of the last iteration (call after a synchronize)"""
+        return float(sum(a.elapsed_time(b) for a, b in self.ev))
+
+
 def _replan_c4(chm, dev, comp):
     """C4 (Llama-2 13B, s = 8192 after a switch): record one Detailed iteration through
     chm_record_op, build the trace, evaluate 10^5 SEEDED candidates, run Algo. 2's grid (replayed
@@ -261,35 +381,191 @@ def _replan_c4(chm, dev, comp):
                      "swapped_gib": int(dk["swapped_bytes"]) / gib},
                seeded_best={"excess_gib": int(bk["excess"]) / gib, "stall_s": float(bk["stall"])},
                generator_best={"excess_gib": int(gk["excess"]) / gib, "stall_s": float(gk["stall"])})
-    # the runtime's default ranking (the timeline stall, csrc/timeline.cu): the same eval and
-    # descent under it, single-flip and batched (search_batch = 16)
-    tl = {}
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    ctx.eval_policies(pt, chm.SEEDED, 0, 100_000, best=best, seed=sd["seed"], flip_thr=sd["flip_thr"], stream=comp,
-                      stall_model=chm.STALL_TIMELINE)
-    tk = best.cpu().numpy().view(chm.BEST_DTYPE)[0]
-    tl["eval_1e5_ms"] = (time.perf_counter() - t0) * 1e3
-    w0 = pt.candidate_mask(chm.SEEDED, int(tk["index"]), seed=sd["seed"], flip_thr=sd["flip_thr"])
-    for b in (1, 16):
-        t0 = time.perf_counter()
-        k, _, r = descend(ctx, pt, tk, w0, dev, 4096, chm.STALL_TIMELINE, b)
-        tl[f"descent_batch{b}"] = {"ms": (time.perf_counter() - t0) * 1e3, "rounds": r,
-                                   "excess_gib": int(k["excess"]) / gib, "timeline_stall_s": float(k["stall"])}
-    out["timeline_ranking"] = tl
     ctx.close()
     return out
 
 
 def _traffic(kernel: str, algorithmic_bytes: float):
     """DRAM bytes per launch: the ncu-measured traffic / algorithmic ratio of `kernel`
-    (profiles/r01_ncu_traffic.json) times this run's algorithmic bytes per launch; None if absent"""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_ncu_traffic.json")
-    try:
-        with open(path) as f:
-            return float(json.load(f)[kernel]["ratio"]) * float(algorithmic_bytes)
-    except (OSError, KeyError, ValueError):
-        return None
+    (profiles/*_ncu_traffic.json, newest round first) times this run's algorithmic bytes per
+    launch; None if absent"""
+    for rnd in ("r02", "r01"):
+        path = os.path.join(ROOT, "profiles", f"{rnd}_ncu_traffic.json")
+        try:
+            with open(path) as f:
+                return float(json.load(f)[kernel]["ratio"]) * float(algorithmic_bytes)
+        except (OSError, KeyError, ValueError):
+            continue
+    return None
+
+
+class PolicyRun:
+    """The installed policy's execution through the profiler hook on real HBM buffers (setup
+    untimed): storage for every swapped tensor, pre-marshalled op records, the op loop."""
+
+    def __init__(self, chm, ctx, tr, pt, words, keep, dev, seed):
+        import torch
+        self.chm, self.ctx, self.tr = chm, ctx, tr
+        tb = pt.tables()
+        gen = torch.Generator(device=dev).manual_seed(seed)
+        self.storage = {}
+        ids = np.array([FAKE_ID_BASE + int(p) for p in tr.ptr], dtype=np.uint64)
+        for k in keep:
+            t = int(tb["tensor"][k])
+            buf = torch.empty(int(tr.nbytes[t]) // 8, dtype=torch.int64, device=dev)
+            buf.random_(generator=gen)
+            self.storage[t] = buf
+            ids[t] = buf.data_ptr()
+        self.item_dev = [self.storage[int(tb["tensor"][k])].data_ptr() for k in keep]  # swap-in destinations
+        self.real_ids = set(self.item_dev)
+        self.check_t = [int(tb["tensor"][k]) for k in keep[:: max(1, len(keep) // 8)]]
+        self.check_sum = {t: int(self.storage[t].sum().item()) for t in self.check_t}
+        tokens = [ctx.tokenize(nm) for nm in tr.op_names]
+        self.run = chm.PreparedIteration(tr, ids, tokens)
+        self.s_out = torch.cuda.Stream(dev)
+        self.s_in = torch.cuda.Stream(dev)
+        self.act = chm.Actions()
+        self.L = chm.load()
+        self.bytes_swap = sum(int(tb["nbytes"][k]) for k in keep)
+
+    def intact(self) -> bool:
+        return all(int(self.storage[t].sum().item()) == self.check_sum[t] for t in self.check_t)
+
+    def execute(self, comp, flags, compute=None, detailed=False):
+        """one iteration: per op, its compute (if any), then chm_record_op and the actions after
+        it.  flags None: compute alone (no hook, no swaps).  Returns (kernel launches, out
+        batches, in batches)."""
+        chm, ctx = self.chm, self.ctx
+        if detailed:
+            ctx.set_detailed(True)
+        launches = 0
+        outs, ins = [], []
+        h, act, L = ctx.h, self.act, self.L
+        for i, r in enumerate(self.run.recs):
+            if compute is not None:
+                compute.op(i, comp)
+            if flags is None:
+                continue
+            chm._check(L.chm_record_op(h, ctypes.byref(r), ctypes.byref(act)))
+            if act.n_swap_out:
+                n = act.n_swap_out
+                for j in range(n):
+                    if act.swap_out[j].dev not in self.real_ids:
+                        raise RuntimeError(f"executor matched a tensor outside the policy at op {i}")
+                outs.append(ctx.issue_swap_out(comp, self.s_out, flags))
+                launches += (n + 63) // 64 if flags == chm.SWAP_KERNEL else 0
+            for j in range(act.n_release):
+                ctx.item_wait(act.release_item[j], False, comp)
+            if act.n_swap_in:
+                n = act.n_swap_in
+                devs = [self.item_dev[act.swap_in_item[j]] for j in range(n)]
+                ins.append(ctx.issue_swap_in(devs, comp, self.s_in, flags))
+                launches += (n + 63) // 64 if flags == chm.SWAP_KERNEL else 0
+            for j in range(act.n_wait):
+                ctx.item_wait(act.wait_item[j], True, comp)
+        if flags is not None:
+            ctx.detect_seq_change(self.tr.t_iter)
+        if detailed:
+            ctx.set_detailed(False)
+        return launches, outs, ins
+
+    def close(self):
+        self.storage.clear()
+
+
+def _c1_block(chm, dev, reps):
+    """C1's execution measurement: the 24 activations of the tiny trace (4 KiB -
+    4 MiB) out and back in as one batch per direction, `reps` times: the swap kernel (one launch
+    per direction) vs one cudaMemcpyAsync per tensor (the copy engines)"""
+    import torch
+    tr = W.tiny()
+    h = chm.Context(device=-1)
+    h.set_detailed(True)
+    chm.record_iteration(h, tr)
+    h.detect_seq_change(tr.t_iter)
+    pt = h.trace_build(tr.budget, tr.static_bytes, tr.bw, tr.groups_fwd, tr.groups_bwd, t_iter=tr.t_iter)
+    sizes = [int(x) for x in pt.tables()["nbytes"]]
+    h.close()
+    total = sum(sizes)
+    ctx = chm.Context(device=dev.index, host_arena_bytes=total + 4096 * len(sizes))
+    g = torch.Generator(device=dev).manual_seed(1)
+    src = [torch.randint(0, 256, (n,), dtype=torch.uint8, device=dev, generator=g) for n in sizes]
+    dst = [torch.empty_like(x) for x in src]
+    offs = np.concatenate([[0], np.cumsum([(n + 511) // 512 * 512 for n in sizes])[:-1]]).astype(np.uint64)
+    d_out = [(x.data_ptr(), int(o), x.numel()) for x, o in zip(src, offs)]
+    d_in = [(x.data_ptr(), int(o), x.numel()) for x, o in zip(dst, offs)]
+    comp, s = torch.cuda.current_stream(dev), torch.cuda.Stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    res = {"tensors": len(sizes), "bytes": total, "min_bytes": min(sizes), "max_bytes": max(sizes), "reps": reps}
+    for name, flags in (("kernel", chm.SWAP_KERNEL), ("copy_engines", chm.SWAP_CE)):
+        for rep in range(reps + 20):
+            if rep == 20:
+                torch.cuda.synchronize()
+                e0.record(comp)
+            b = ctx.swap_out(d_out, comp, s, flags)
+            ctx.batch_wait(b, comp)
+            b = ctx.swap_in(d_in, comp, s, flags)
+            ctx.batch_wait(b, comp)
+        e1.record(comp)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        ok = all(torch.equal(a, c) for a, c in zip(src, dst))
+        for x in dst:
+            x.zero_()
+        res[name] = {"us_per_round_trip": ms * 1e3, "GBps": 2 * total / (ms * 1e-3) / 1e9, "byte_exact": ok,
+                     "calls_per_direction": 1 if flags == chm.SWAP_KERNEL else len(sizes)}
+    ctx.close()
+    res["kernel_speedup"] = res["copy_engines"]["us_per_round_trip"] / res["kernel"]["us_per_round_trip"]
+    return res
+
+
+def _swap_only_block(chm, args, dev, name, steps):
+    """A config's policy executed without compute (swap-bound steps), kernel and copy engines:
+    the r01 headline kept as a block (C2) beside the C3h line"""
+    import torch
+    tr = W.CONFIGS[name]()
+    sd = W.SEEDED[name[:2]]
+    ctx = chm.Context(device=dev.index, time_batches=True, swap_ctas=args.swap_ctas)
+    ctx.set_detailed(True)
+    chm.record_iteration(ctx, tr, [ctx.tokenize(nm) for nm in tr.op_names])
+    ctx.detect_seq_change(tr.t_iter)
+    ctx.set_detailed(False)
+    pt = ctx.trace_build(tr.budget, tr.static_bytes, tr.bw, tr.groups_fwd, tr.groups_bwd, t_iter=tr.t_iter)
+    best = torch.empty(5, dtype=torch.int64, device=dev)
+    ctx.eval_policies(pt, chm.SEEDED, 0, args.candidates, best=best, seed=sd["seed"], flip_thr=sd["flip_thr"])
+    bk = best.cpu().numpy().view(chm.BEST_DTYPE)[0]
+    words = pt.candidate_mask(chm.SEEDED, int(bk["index"]), seed=sd["seed"], flip_thr=sd["flip_thr"])
+    tb = pt.tables()
+    keep = [k for k in range(pt.K) if (int(words[k // 64]) >> (k % 64)) & 1]
+    need = sum((int(tb["nbytes"][k]) + 511) // 512 * 512 for k in keep)
+    if need > args.host_frac * mem_available():
+        ctx.close()
+        return {"workload": tr.meta["config"], "skipped": f"policy needs {need} B pinned, host RAM too small"}
+    ctx.arena_reserve(need)
+    ctx.policy_install(pt, words)
+    pr = PolicyRun(chm, ctx, tr, pt, words, keep, dev, 4321)
+    comp = torch.cuda.current_stream(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    res = {"workload": tr.meta["config"], "items": len(keep), "swap_bytes_per_direction": pr.bytes_swap}
+    for mode, flags, n in (("kernel", chm.SWAP_KERNEL, steps), ("copy_engines", chm.SWAP_CE, 1)):
+        pr.execute(comp, flags)  # warm-up
+        ms, d2h, h2d = [], [], []
+        for _ in range(n):
+            torch.cuda.synchronize()
+            ev0.record(comp)
+            _, outs, ins = pr.execute(comp, flags)
+            ev1.record(comp)
+            torch.cuda.synchronize()
+            ms.append(ev0.elapsed_time(ev1))
+            d2h.append(sum(ctx.batch_elapsed_ms(b) for b in outs))
+            h2d.append(sum(ctx.batch_elapsed_ms(b) for b in ins))
+        res[mode] = {"ms_per_step": float(np.mean(ms)), "GBps": 2 * pr.bytes_swap / (np.mean(ms) * 1e-3) / 1e9,
+                     "d2h_GBps": pr.bytes_swap / (np.mean(d2h) * 1e-3) / 1e9,
+                     "h2d_GBps": pr.bytes_swap / (np.mean(h2d) * 1e-3) / 1e9, "steps": n}
+    res["byte_exact_sample"] = pr.intact()
+    pr.close()
+    ctx.close()
+    return res
 
 
 def main():
@@ -303,6 +579,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2509_11076_b200 import chm
+    from paper_2509_11076_b200 import dist as D
     # collectives run whenever a process group is up: N > 1, or --force-dist at N = 1 (the NCCL
     # argmin path exercised on one GPU: a one-rank all-gather)
     use_dist = world > 1 or args.force_dist
@@ -312,11 +589,15 @@ def main():
             os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
             os.environ.setdefault("RANK", "0")
             os.environ.setdefault("WORLD_SIZE", "1")
+        else:  # communicator lines (nranks, rings / NVLS) visible in the log
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     P = world
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(P)))
 
     def barrier():
         if use_dist:
@@ -336,7 +617,7 @@ def main():
         dist.all_reduce(t)
         return float(t.item())
 
-    tr = W.CONFIGS[args.config]()
+    tr = workload(args)
     sd = W.SEEDED[args.config[:2]]
     ctx = chm.Context(device=local, time_batches=True, swap_ctas=args.swap_ctas)
     tokens = [ctx.tokenize(nm) for nm in tr.op_names]
@@ -351,9 +632,9 @@ def main():
     ctx.detect_seq_change(tr.t_iter)
     ctx.set_detailed(False)
     pt = ctx.trace_build(tr.budget, tr.static_bytes, tr.bw, tr.groups_fwd, tr.groups_bwd, t_iter=tr.t_iter)
+    digest = D.check_same_trace(pt, device=dev) if use_dist else pt.digest()  # ranks shard one trace
     C = args.candidates
-    lo, hi = rank * C // P, (rank + 1) * C // P
-    cnt = hi - lo
+    lo, cnt = D.shard(C, P, rank)
     full = not args.search_mode
     ld = (pt.N + 1) // 2 * 2
     peak = torch.empty(cnt, dtype=torch.int64, device=dev)
@@ -364,14 +645,13 @@ def main():
     best_global = torch.empty(5, dtype=torch.int64, device=dev)
     comp = torch.cuda.current_stream(dev)
 
-    def evaluate(ev_kernel=None):
-        ctx.eval_policies(pt, chm.SEEDED, lo, cnt, best=best_local, seed=sd["seed"], flip_thr=sd["flip_thr"],
+    def evaluate(ev_kernel=None, trace=pt):
+        ctx.eval_policies(trace, chm.SEEDED, lo, cnt, best=best_local, seed=sd["seed"], flip_thr=sd["flip_thr"],
                           peak=peak, stall=stall, footprint=fp, ld=ld if full else 0, stream=comp)
         if ev_kernel is not None:
             ev_kernel.record(comp)  # replay kernel done; the rest is the argmin exchange
         if use_dist:
-            dist.all_gather_into_tensor(gathered, best_local)
-            ctx.best_reduce_device(gathered, P, best_global, comp)
+            D.argmin_exchange(ctx, best_local, gathered, best_global, P, stream=comp)
         else:
             best_global.copy_(best_local)
 
@@ -383,7 +663,6 @@ def main():
     sel = [k for k in range(pt.K) if (int(words[k // 64]) >> (k % 64)) & 1]
     # host-RAM guard: the arena is pinned; with many ranks per node keep only a prefix of the
     # policy (mask-bit order) and say so in the JSON line
-    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(P)))
     budget_pin = int(args.host_frac * mem_available() / max(1, local_world))
     need, keep = 0, []
     for k in sel:
@@ -397,68 +676,26 @@ def main():
     for k in keep:
         words_exec[k // 64] |= np.uint64(1 << (k % 64))
     t0 = time.perf_counter()
-    ctx.arena_reserve(max(need, 1 << 20))
+    # concurrent cudaHostRegister calls of tens of GB serialise in the driver: two ranks at a time
+    D.staggered(local, local_world, lambda: ctx.arena_reserve(max(need, 1 << 20)), 2, barrier if use_dist else None)
     t_pin = time.perf_counter() - t0
     ctx.policy_install(pt, words_exec)
-    # real HBM storage for the swapped tensors; their data_ptr becomes the op records' ids
-    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
-    storage = {}
-    ids = sim_ids.copy()
-    for k in keep:
-        t = int(tb["tensor"][k])
-        buf = torch.empty(int(tr.nbytes[t]) // 8, dtype=torch.int64, device=dev)
-        buf.random_(generator=gen)
-        storage[t] = buf
-        ids[t] = buf.data_ptr()
-    item_dev = [storage[int(tb["tensor"][k])].data_ptr() for k in keep]  # swap-in destinations
-    real_ids = set(item_dev)
-    check_t = [int(tb["tensor"][k]) for k in keep[:: max(1, len(keep) // 8)]]
-    check_sum = {t: int(storage[t].sum().item()) for t in check_t}
-    run = chm.PreparedIteration(tr, ids, tokens)
-    s_out = torch.cuda.Stream(dev)
-    s_in = torch.cuda.Stream(dev)
-    bytes_swap = sum(int(tb["nbytes"][k]) for k in keep)
+    pr = PolicyRun(chm, ctx, tr, pt, words_exec, keep, dev, 1234 + rank)
+    bytes_swap = pr.bytes_swap
+    compute = None if args.no_compute else Compute(dev, tr.t_iter / pt.N, pt.N)
+    calib = compute.recalibrate(comp) if compute is not None else None
 
-    def execute(flags, detailed=False):
-        """one iteration of policy execution through the profiler hook; returns launches"""
-        if detailed:
-            ctx.set_detailed(True)
-        launches = 0
-        outs, ins = [], []
-        h = ctx.h
-        for r in run.recs:
-            chm._check(L.chm_record_op(h, ctypes.byref(r), ctypes.byref(act)))
-            if act.n_swap_out:
-                n = act.n_swap_out
-                for j in range(n):
-                    if act.swap_out[j].dev not in real_ids:
-                        raise RuntimeError(f"executor matched a tensor outside the policy at op {len(outs)}")
-                outs.append(ctx.issue_swap_out(comp, s_out, flags))
-                launches += (n + 63) // 64 if flags == chm.SWAP_KERNEL else 0
-            for j in range(act.n_release):
-                ctx.item_wait(act.release_item[j], False, comp)
-            if act.n_swap_in:
-                n = act.n_swap_in
-                devs = [item_dev[act.swap_in_item[j]] for j in range(n)]
-                ins.append(ctx.issue_swap_in(devs, comp, s_in, flags))
-                launches += (n + 63) // 64 if flags == chm.SWAP_KERNEL else 0
-            for j in range(act.n_wait):
-                ctx.item_wait(act.wait_item[j], True, comp)
-        ctx.detect_seq_change(tr.t_iter)
-        if detailed:
-            ctx.set_detailed(False)
-        return launches, outs, ins
-
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     spin_cycles = 1_000_000  # ~0.5 ms at 1.9 GHz
-    # ---- warm-up + timed steps (device loop)
-    step_ms, eval_ms, d2h_ms, h2d_ms, argmin_ms = [], [], [], [], []
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     ev_k = torch.cuda.Event(enable_timing=True)
+    # ---- warm-up + timed steps (device loop)
+    step_ms, eval_ms, exec_ms, d2h_ms, h2d_ms, argmin_ms, gemm_ms = [], [], [], [], [], [], []
     launches = launches_swap = 0
     for step in range(args.warmup):
         evaluate()
-        execute(chm.SWAP_KERNEL)
+        pr.execute(comp, chm.SWAP_KERNEL, compute)
     torch.cuda.synchronize()
+    barrier()
     with ClockSampler(local, enabled=not args.no_clocks) as clk:
         for step in range(args.steps):
             barrier()
@@ -470,7 +707,7 @@ def main():
             ev[1].record(comp)
             evaluate(ev_k)
             ev[2].record(comp)
-            n_l, outs, ins = execute(chm.SWAP_KERNEL)
+            n_l, outs, ins = pr.execute(comp, chm.SWAP_KERNEL, compute)
             ev[3].record(comp)
             torch.cuda.synchronize()
             barrier()
@@ -479,33 +716,38 @@ def main():
             step_ms.append(ev[0].elapsed_time(ev[3]))
             eval_ms.append(ev[1].elapsed_time(ev_k))
             argmin_ms.append(ev_k.elapsed_time(ev[2]))
+            exec_ms.append(ev[2].elapsed_time(ev[3]))
             d2h_ms.append(sum(ctx.batch_elapsed_ms(b) for b in outs))
             h2d_ms.append(sum(ctx.batch_elapsed_ms(b) for b in ins))
+            if compute is not None:
+                gemm_ms.append(compute.gemm_ms())
     clocks = clk.summary()
     st = ctx.exec_stats()
-    ok = all(int(storage[t].sum().item()) == check_sum[t] for t in check_t)
-    # ---- copy-engine baseline (per-tensor cudaMemcpyAsync on the same batches)
-    ce_ms, ce_d2h, ce_h2d = [], [], []
-    for step in range(args.ce_steps):
-        torch.cuda.synchronize()
-        ev[0].record(comp)
-        _, outs, ins = execute(chm.SWAP_CE)
-        ev[3].record(comp)
-        torch.cuda.synchronize()
-        ce_ms.append(ev[0].elapsed_time(ev[3]))
-        ce_d2h.append(sum(ctx.batch_elapsed_ms(b) for b in outs))
-        ce_h2d.append(sum(ctx.batch_elapsed_ms(b) for b in ins))
-    ok = ok and all(int(storage[t].sum().item()) == check_sum[t] for t in check_t)
-    # ---- AUTO engine selection (tensors >= 4 MiB on the copy engines, the rest in the kernel)
-    auto_ms = []
-    for step in range(args.ce_steps):
-        torch.cuda.synchronize()
-        ev[0].record(comp)
-        execute(chm.SWAP_AUTO)
-        ev[3].record(comp)
-        torch.cuda.synchronize()
-        auto_ms.append(ev[0].elapsed_time(ev[3]))
-    ok = ok and all(int(storage[t].sum().item()) == check_sum[t] for t in check_t)
+    ok = pr.intact()
+
+    def run_mode(flags, n):
+        """n untimed-by-the-headline steps of execution only: (exec ms, d2h ms, h2d ms, gemm ms)"""
+        res = ([], [], [], [])
+        for _ in range(n):
+            torch.cuda.synchronize()
+            ev[2].record(comp)
+            _, outs_, ins_ = pr.execute(comp, flags, compute)
+            ev[3].record(comp)
+            torch.cuda.synchronize()
+            res[0].append(ev[2].elapsed_time(ev[3]))
+            res[1].append(sum(ctx.batch_elapsed_ms(b) for b in outs_))
+            res[2].append(sum(ctx.batch_elapsed_ms(b) for b in ins_))
+            if compute is not None:
+                res[3].append(compute.gemm_ms())
+        return [float(np.mean(x)) if x else None for x in res]
+
+    # ---- compute alone (the same GEMM sequence, no hook, no swaps)
+    with ClockSampler(local, enabled=not args.no_clocks and compute is not None) as clk_alone:
+        alone = run_mode(None, args.alone_steps) if compute is not None else [None] * 4
+    # ---- copy-engine baseline (per-tensor cudaMemcpyAsync on the same batches, same compute)
+    with ClockSampler(local, enabled=not args.no_clocks) as clk_ce:
+        ce = run_mode(chm.SWAP_CE, args.ce_steps)
+    ok = ok and pr.intact()
     # ---- e2e: the GenPolicy loop through the public API from host records
     e2e_ms = []
     table_bytes = 8 * pt.N + 28 * pt.K + 8 * pt.L + 8 * pt.W
@@ -516,15 +758,9 @@ def main():
         ev[0].record(comp)
         # executes the policy (the public API's default copy path, AUTO: what Runtime uses) and
         # records the iteration
-        execute(chm.SWAP_AUTO, detailed=True)
+        pr.execute(comp, chm.SWAP_AUTO, compute, detailed=True)
         pt2 = ctx.trace_build(tr.budget, tr.static_bytes, tr.bw, tr.groups_fwd, tr.groups_bwd, t_iter=tr.t_iter)
-        ctx.eval_policies(pt2, chm.SEEDED, lo, cnt, best=best_local, seed=sd["seed"], flip_thr=sd["flip_thr"],
-                          peak=peak, stall=stall, footprint=fp, ld=ld if full else 0, stream=comp)
-        if use_dist:
-            dist.all_gather_into_tensor(gathered, best_local)
-            ctx.best_reduce_device(gathered, P, best_global, comp)
-        else:
-            best_global.copy_(best_local)
+        evaluate(trace=pt2)
         bk2 = best_global.cpu().numpy().view(chm.BEST_DTYPE)[0]  # the step's result, D2H
         w2 = pt2.candidate_mask(chm.SEEDED, int(bk2["index"]), seed=sd["seed"], flip_thr=sd["flip_thr"])
         assert truncated or np.array_equal(w2, words), "re-planned policy differs on an unchanged trace"
@@ -533,78 +769,105 @@ def main():
         torch.cuda.synchronize()
         e2e_ms.append(max(ev[0].elapsed_time(ev[3]), (time.perf_counter() - t0) * 1e3))
         pt2.free()
-    ok = ok and all(int(storage[t].sum().item()) == check_sum[t] for t in check_t)
+    ok = ok and pr.intact()
 
-    # ---- re-plan with the paper's generator (NEXT-1): Algo. 2 for a grid of (C, rem_scale) on the
-    # host, then the best of n by a GPU replay of the EXPLICIT item lists
-    t0 = time.perf_counter()
-    gen_lists = [pt.generate_policy(cc, rr)[0] for cc in (0.0, 0.5, 1.0, 2.0) for rr in (0.5, 1.0, 2.0)]
-    t_gen = time.perf_counter() - t0
-    off = np.zeros(len(gen_lists) + 1, np.uint64)
-    off[1:] = np.cumsum([len(x) for x in gen_lists])
-    g_items = np.concatenate(gen_lists)
-    g_peak = torch.empty(len(gen_lists), dtype=torch.int64, device=dev)
-    g_stall = torch.empty(len(gen_lists), dtype=torch.float64, device=dev)
-    g_best = torch.empty(5, dtype=torch.int64, device=dev)
-    torch.cuda.synchronize()
-    ev[0].record(comp)
-    ctx.eval_policies(pt, chm.EXPLICIT, 0, len(gen_lists), best=g_best, peak=g_peak, stall=g_stall,
-                      item_offsets=off, items=g_items, stream=comp)
-    ev[3].record(comp)
-    torch.cuda.synchronize()
-    gb = g_best.cpu().numpy().view(chm.BEST_DTYPE)[0]
-    generator = {"policies": len(gen_lists), "host_generate_ms": t_gen * 1e3,
-                 "gpu_eval_ms": ev[0].elapsed_time(ev[3]), "best_index": int(gb["index"]),
-                 "best_peak": int(gb["peak"]), "best_excess": int(gb["excess"]), "best_stall_s": float(gb["stall"]),
-                 "seeded_best_excess": int(bk["excess"]), "seeded_best_stall_s": float(bk["stall"])}
-    # ---- the same candidates ranked by the timeline stall (csrc/timeline.cu, reading Q11), the
-    # runtime's default ranking: device time of one launch (this rank's shard, search mode)
-    tl_ms = []
-    tl_best = torch.empty(5, dtype=torch.int64, device=dev)
-    for it in range(4):
+    # ---- the policy's estimated stall (the models chm_stall_models evaluates), at the trace's B
+    # and at the B this run's kernel measured, against the measured one: step with swaps minus
+    # the same step's compute alone
+    items = pt.mask_items(words_exec)
+    t_d2h = max_over_ranks(float(np.mean(d2h_ms)))
+    t_h2d = max_over_ranks(float(np.mean(h2d_ms)))
+    achieved_swap = 2 * bytes_swap / ((t_d2h + t_h2d) * 1e-3) / 1e9
+    est = {"B_trace_GBps": tr.bw / 1e9, "at_trace_B": dict(zip(("r_stall", "per_direction", "timeline"),
+                                                             pt.stall_models(items).tolist()))}
+    ptm = ctx.trace_build(tr.budget, tr.static_bytes, achieved_swap * 1e9, tr.groups_fwd, tr.groups_bwd,
+                          t_iter=tr.t_iter)
+    est["B_measured_GBps"] = achieved_swap  # the per-direction mean the kernel reached in the step
+    est["at_measured_B"] = dict(zip(("r_stall", "per_direction", "timeline"), ptm.stall_models(items).tolist()))
+    ptm.free()
+
+    # ---- rank-0 blocks beside the line: Algo. 2's grid, the timeline ranking, the C4 re-plan,
+    # C1's small tensors, C2 (N = 1: host RAM)
+    extras = {}
+    if rank == 0 and not args.no_extras:
+        t0 = time.perf_counter()
+        gen_lists = [pt.generate_policy(cc, rr)[0] for cc in (0.0, 0.5, 1.0, 2.0) for rr in (0.5, 1.0, 2.0)]
+        t_gen = time.perf_counter() - t0
+        off = np.zeros(len(gen_lists) + 1, np.uint64)
+        off[1:] = np.cumsum([len(x) for x in gen_lists])
+        g_best = torch.empty(5, dtype=torch.int64, device=dev)
         torch.cuda.synchronize()
-        torch.cuda._sleep(spin_cycles)
         ev[0].record(comp)
-        ctx.eval_policies(pt, chm.SEEDED, lo, cnt, best=tl_best, seed=sd["seed"], flip_thr=sd["flip_thr"],
-                          stall_model=chm.STALL_TIMELINE, stream=comp)
+        ctx.eval_policies(pt, chm.EXPLICIT, 0, len(gen_lists), best=g_best, item_offsets=off,
+                          items=np.concatenate(gen_lists), stream=comp)
         ev[3].record(comp)
         torch.cuda.synchronize()
-        if it:
-            tl_ms.append(ev[0].elapsed_time(ev[3]))
-    tb_ = tl_best.cpu().numpy().view(chm.BEST_DTYPE)[0]
-    eval_timeline = {"ms_per_launch": float(np.mean(tl_ms)), "candidates_per_s": cnt / (np.mean(tl_ms) * 1e-3),
-                     "mode": "search (peak / swapped by the replay kernel, then the timeline kernel)",
-                     "best_index": int(tb_["index"]), "best_stall_s": float(tb_["stall"]),
-                     "layer_best_index": int(bk["index"])}
-    # ---- re-plan latency on C4 (BASELINE configs[3]): the sequence switched to s = 8192; from the
-    # Detailed iteration's records to an installed policy, through the public API (rank 0 work,
-    # reported beside the line; not part of `value`)
-    replan = _replan_c4(chm, dev, comp) if rank == 0 else None
+        gb = g_best.cpu().numpy().view(chm.BEST_DTYPE)[0]
+        extras["generator"] = {"policies": len(gen_lists), "host_generate_ms": t_gen * 1e3,
+                               "gpu_eval_ms": ev[0].elapsed_time(ev[3]), "best_index": int(gb["index"]),
+                               "best_peak": int(gb["peak"]), "best_excess": int(gb["excess"]),
+                               "best_stall_s": float(gb["stall"]), "seeded_best_excess": int(bk["excess"]),
+                               "seeded_best_stall_s": float(bk["stall"])}
+        tl_ms = []
+        tl_best = torch.empty(5, dtype=torch.int64, device=dev)
+        for it in range(4):
+            torch.cuda.synchronize()
+            torch.cuda._sleep(spin_cycles)
+            ev[0].record(comp)
+            ctx.eval_policies(pt, chm.SEEDED, 0, C, best=tl_best, seed=sd["seed"], flip_thr=sd["flip_thr"],
+                              stall_model=chm.STALL_TIMELINE, stream=comp)
+            ev[3].record(comp)
+            torch.cuda.synchronize()
+            if it:
+                tl_ms.append(ev[0].elapsed_time(ev[3]))
+        tb_ = tl_best.cpu().numpy().view(chm.BEST_DTYPE)[0]
+        extras["eval_timeline"] = {"ms_per_launch": float(np.mean(tl_ms)), "candidates_per_s": C / (np.mean(tl_ms) * 1e-3),
+                                   "mode": "search (peak / swapped by the replay kernel, then the timeline kernel)",
+                                   "best_index": int(tb_["index"]), "best_stall_s": float(tb_["stall"]),
+                                   "layer_best_index": int(bk["index"])}
+        ctx.release_scratch()
+        extras["replan_c4"] = _replan_c4(chm, dev, comp)
+        if args.c1_reps:
+            extras["c1_small_swaps"] = _c1_block(chm, dev, args.c1_reps)
     # ---- aggregate (max over ranks of time, sum of work)
     t_step = max_over_ranks(float(np.mean(step_ms)))
     t_eval = max_over_ranks(float(np.mean(eval_ms)))
     t_argmin = max_over_ranks(float(np.mean(argmin_ms)))
-    t_d2h = max_over_ranks(float(np.mean(d2h_ms)))
-    t_h2d = max_over_ranks(float(np.mean(h2d_ms)))
+    t_exec = max_over_ranks(float(np.mean(exec_ms)))
     tot_bytes = sum_over_ranks(2.0 * bytes_swap)
-    value = tot_bytes / (t_step * 1e-3) / 1e9
+    e2e_t = max_over_ranks(float(np.mean(e2e_ms))) if e2e_ms else None
+    value = 2.0 * bytes_swap / (t_step * 1e-3) / 1e9  # per GPU (this rank's bytes, the slowest rank's time)
     fp_bytes = (8 * ld * cnt if full else 0) + 16 * cnt
     hbm_peak = measured_peaks().get("hbm_gbs", 6650.0)
     per_dir = [bytes_swap / (t_d2h * 1e-3) / 1e9 if t_d2h > 0 else 0.0,
                bytes_swap / (t_h2d * 1e-3) / 1e9 if t_h2d > 0 else 0.0]
-    ce_dir = ([bytes_swap / (np.mean(ce_d2h) * 1e-3) / 1e9, bytes_swap / (np.mean(ce_h2d) * 1e-3) / 1e9]
-              if ce_d2h and ce_h2d else None)
-    achieved_swap = 2 * bytes_swap / ((t_d2h + t_h2d) * 1e-3) / 1e9
-    e2e_t = max_over_ranks(float(np.mean(e2e_ms))) if e2e_ms else None
+    ce_dir = ([bytes_swap / (ce[1] * 1e-3) / 1e9, bytes_swap / (ce[2] * 1e-3) / 1e9] if ce[1] and ce[2] else None)
+    # release this run's HBM storage and pinned arena before the C2 block pins its own
+    pr.close()
+    arena_info = ctx.arena_placement()
+    ctx.close()
+    del fp, peak, stall
+    torch.cuda.empty_cache()
+    if rank == 0 and P == 1 and args.c2_steps and args.config != "C2":
+        extras["c2"] = _swap_only_block(chm, args, dev, "C2", args.c2_steps)
     if rank != 0:
-        ctx.close()
+        barrier()
         if use_dist:
             dist.destroy_process_group()
         return
+    gflop = compute.flops * pt.N / 1e9 if compute is not None else None
+
+    def tflops(ms):
+        return gflop / ms if (gflop and ms) else None  # GFLOP / ms = TFLOP/s
+
+    kernel_gemm_ms = float(np.mean(gemm_ms)) if gemm_ms else None
     line = {
         "metric": METRIC,
         "value": value,
         "unit": "GB/s",
+        "value_aggregate": tot_bytes / (t_step * 1e-3) / 1e9,
+        "value_what": "per GPU: this rank's swap bytes (D2H + H2D) / step time (max over ranks); value_aggregate: "
+                      "all ranks' bytes / the same time",
         "n_gpus": P,
         "steps": args.steps,
         "warmup": args.warmup,
@@ -615,29 +878,34 @@ def main():
         "dtype": "u8",
         "data": "synthetic",
         "config": {
-            "workload": tr.meta["config"],
-            "trace": {"ops": pt.N, "swappable": pt.K, "layers": pt.L, "peak0": pt.peak0, "budget": pt.budget},
+            **workload_desc(args, tr),
+            "trace": {"ops": pt.N, "swappable": pt.K, "layers": pt.L, "peak0": pt.peak0, "budget": pt.budget,
+                      "t_iter_s": tr.t_iter, "digest": f"{digest:016x}"},
             "candidates": C, "candidate_kind": "SEEDED", "candidates_per_rank": cnt,
             "eval_mode": "search" if args.search_mode else "full (per-op footprints written)",
             "policy": {"index": int(bk["index"]), "items": len(sel), "executed_items": len(keep),
                        "truncated_for_host_ram": truncated, "swap_bytes_per_direction": bytes_swap},
+            "compute": (None if compute is None else
+                        {"what": f"one bf16 GEMM [{compute.M}, {GEMM_N}] x [{GEMM_N}, {GEMM_N}] per op on the compute "
+                                 f"stream, calibrated to T_iter / N = {tr.t_iter / pt.N * 1e3:.3f} ms",
+                         "gflop_per_step": gflop}),
             "parallelism": f"dp{P}: per-rank swapping, candidates sharded, NCCL argmin all-gather",
             "l2": "inputs larger than L2 (swap set and footprint rows are GBs per step)",
-            "swap_ctas": args.swap_ctas, "arena_pin_s": round(t_pin, 2),
-            "arena": ctx.arena_placement(),  # mode 2 = mmap + mbind(GPU's node) + THP + cudaHostRegister
+            "swap_ctas": args.swap_ctas, "arena_pin_s": round(t_pin, 2), "arena": arena_info,
+            "host": host_info(),
         },
         "roofline": {
             "bound": "pcie", "kernel": "swap_copy_kernel (D2H + H2D)", "achieved": achieved_swap,
             "peak": PCIE_GEN5_X16_GBPS, "unit": "GB/s", "frac": achieved_swap / PCIE_GEN5_X16_GBPS,
             "traffic": _traffic("swap_copy_kernel", 2 * bytes_swap / max(1, launches_swap)),
-            "traffic_source": "ncu dram bytes / algorithmic bytes (profiles/r01_ncu_traffic.json) x this run's "
+            "traffic_source": "ncu dram bytes / algorithmic bytes (profiles/*_ncu_traffic.json) x this run's "
                               "algorithmic bytes per swap launch",
-            "peak_source": "nominal PCIe Gen5 x16 per direction (no measured host-link peak in MEASURED_PEAKS.json; "
-                           "the box's copy engines reach 57.3 D2H / 55.6 H2D GB/s, tools/probe_box.py)",
+            "peak_source": "nominal PCIe Gen5 x16 per direction (no measured host-link peak in MEASURED_PEAKS.json)",
             "d2h_GBps": per_dir[0], "h2d_GBps": per_dir[1],
+            "what": "swap-stream busy time of the kernel's batches during the overlapped step",
             "frac_of_copy_engines": ({"d2h": per_dir[0] / ce_dir[0], "h2d": per_dir[1] / ce_dir[1],
-                                      "what": "vs the same batches on the copy engines (best pinned large-block "
-                                              "cudaMemcpyAsync path), this run"} if ce_dir else None),
+                                      "what": "vs the same batches on the copy engines (one cudaMemcpyAsync per "
+                                              "tensor) under the same compute, this run"} if ce_dir else None),
         },
         "roofline_replay": {
             "bound": "hbm", "kernel": "replay_kernel<%s>" % ("true" if full else "false"),
@@ -650,22 +918,28 @@ def main():
         },
         "argmin_exchange_us": t_argmin * 1e3 if use_dist else None,
         "eval": {"candidates_per_s": C / (t_eval * 1e-3), "ms_per_launch": t_eval, "unit": "candidates/s"},
-        "eval_timeline": eval_timeline,
+        "overlap": {
+            "exec_ms": {"kernel": t_exec, "copy_engines": ce[0], "compute_alone": alone[0]},
+            "swap_GBps_during_overlap": {"kernel": {"d2h": per_dir[0], "h2d": per_dir[1]},
+                                         "copy_engines": ({"d2h": ce_dir[0], "h2d": ce_dir[1]} if ce_dir else None)},
+            "gemm_tflops": {"alone": tflops(alone[3]), "with_copy_engines": tflops(ce[3]),
+                            "with_kernel": tflops(kernel_gemm_ms),
+                            "what": "GEMM FLOPs / summed GEMM durations (CUDA events around each GEMM); compute "
+                                    "alone runs back to back and meets the power cap (see clocks), the swap steps "
+                                    "leave gaps at releases and waits"},
+            "clocks": {"kernel": clocks, "copy_engines": clk_ce.summary(), "compute_alone": clk_alone.summary()},
+            "compute_calibration": calib,
+            "stall_s": {"measured_kernel": (t_exec - alone[0]) * 1e-3 if alone[0] else None,
+                        "measured_copy_engines": (ce[0] - alone[0]) * 1e-3 if (alone[0] and ce[0]) else None,
+                        "estimated": est},
+        },
         "ce_baseline": {
-            "what": "same batches, one cudaMemcpyAsync per tensor on the copy engines",
-            "ms_per_step": float(np.mean(ce_ms)) if ce_ms else None,
-            "d2h_GBps": bytes_swap / (np.mean(ce_d2h) * 1e-3) / 1e9 if ce_d2h else None,
-            "h2d_GBps": bytes_swap / (np.mean(ce_h2d) * 1e-3) / 1e9 if ce_h2d else None,
-            "GBps": 2 * bytes_swap / (np.mean(ce_ms) * 1e-3) / 1e9 if ce_ms else None,
+            "what": "same batches and compute, one cudaMemcpyAsync per tensor on the copy engines",
+            "ms_per_step": ce[0], "d2h_GBps": ce_dir[0] if ce_dir else None, "h2d_GBps": ce_dir[1] if ce_dir else None,
+            "GBps": 2 * bytes_swap / (ce[0] * 1e-3) / 1e9 if ce[0] else None,
         },
-        "auto_mode": {
-            "what": "CHM_SWAP_AUTO: tensors >= 4 MiB on the copy engines, the rest in the kernel",
-            "ms_per_step": float(np.mean(auto_ms)) if auto_ms else None,
-            "GBps": 2 * bytes_swap / (np.mean(auto_ms) * 1e-3) / 1e9 if auto_ms else None,
-        },
-        "generator": generator,
-        "replan_c4": replan,
-        "e2e": {"value": tot_bytes / (e2e_t * 1e-3) / 1e9 if e2e_t else None, "unit": "GB/s",
+        **extras,
+        "e2e": {"value": 2.0 * bytes_swap / (e2e_t * 1e-3) / 1e9 if e2e_t else None, "unit": "GB/s",
                 "copy_path": "CHM_SWAP_AUTO (the runtime's default: >= 4 MiB on the copy engines, smaller in the kernel)",
                 "h2d_bytes_per_step": bytes_swap + table_bytes, "d2h_bytes_per_step": bytes_swap + 40,
                 "ms_per_step": e2e_t},
@@ -675,11 +949,10 @@ def main():
         "exec_stats": st,
         "clocks": clocks,
     }
-    if P == 1:
-        line["cpu_baseline"] = cpu_baseline(args, tr, bytes_swap)
+    line["cpu_baseline"] = cpu_baseline(args, tr, bytes_swap)
     print(json.dumps(line), flush=True)
-    ctx.close()
     if use_dist:
+        barrier()
         dist.destroy_process_group()
 
 

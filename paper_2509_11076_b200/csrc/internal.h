@@ -168,12 +168,15 @@ struct DevTrace {
   uint32_t o_S = 0;     // int64 [K]  swappable sizes (mask-bit order)
   uint32_t o_lo = 0;    // u16   [K]  lout (release layer) per swappable, mask-bit order
   uint32_t o_li = 0;    // u16   [K]  lin (swap-in layer) per swappable, mask-bit order
-  uint32_t o_f0 = 0;    // [N] no-swap footprint (full mode): int32 units of 2^f0_shift B if
-                        // f0_narrow, else int64
+  uint32_t o_f0 = 0;    // no-swap footprint (full mode): if f0_narrow int32 units of 2^f0_shift B,
+                        // N padded to 128 and lane-swizzled (block of 128 ops: lane l's ops 2l,
+                        // 2l+1, 64+2l, 65+2l adjacent); else int64 [N] in op order
   uint32_t o_f0w = 0;   // int64 [N] no-swap footprint, global only (not staged; EXPLICIT replay)
   int32_t f0_shift = 0;
   int32_t f0_narrow = 0;
   uint32_t o_lay = 0;   // u16   [N]  8 x logical layer of each op (byte offset into D, full mode)
+  uint32_t o_lay4 = 0;  // u8    [N padded to 128] logical layer of each op (L <= 256), lane-swizzled
+                        // like F0 (narrow only): one 32-bit load gives a lane's four ops' layers
   const uint64_t *base = nullptr;
   int32_t N = 0, K = 0, L = 0, W = 0;
   double bw = 1.0;

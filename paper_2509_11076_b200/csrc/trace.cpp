@@ -234,9 +234,21 @@ chm_status chm::build_trace(chm_ctx *ctx, const IterRecord &R, const chm_trace_p
   }
   D.f0_narrow = nonneg && (fmax >> g) < (int64_t(1) << 31) ? 1 : 0;
   D.f0_shift = g;
-  D.o_f0 = uint32_t(o); o += al((D.f0_narrow ? 4 : 8) * size_t(N));
-  D.o_lay = uint32_t(o); o += al(2 * size_t(N));
-  D.full_bytes = uint32_t(o);
+  // narrow: F0 and the ops' layers lane-swizzled for the row stream (see replay.cu): in each
+  // block of 128 ops, lane l's four ops 2l, 2l+1, 64+2l, 65+2l are stored together (one 16 B
+  // load of F0, one 32-bit load of the u8 layers); wide: F0 int64 and u16 8 x layer in op order
+  const size_t n128 = (size_t(N) + 127) / 128 * 128;
+  if (D.f0_narrow) {
+    D.o_f0 = uint32_t(o); o += al(4 * n128);
+    D.o_lay4 = uint32_t(o); o += al(n128);
+    D.full_bytes = uint32_t(o);
+    D.o_lay = uint32_t(o); o += al(2 * size_t(N));  // EXPLICIT replay only (global memory)
+  } else {
+    D.o_f0 = uint32_t(o); o += al(8 * size_t(N));
+    D.o_lay = uint32_t(o); o += al(2 * size_t(N));
+    D.o_lay4 = 0;
+    D.full_bytes = uint32_t(o);
+  }
   D.o_f0w = uint32_t(o); o += al(8 * size_t(N));
   const size_t o_base = al(o);
   const size_t total = o_base + al(8 * size_t(tr->W) + 8);
@@ -256,10 +268,16 @@ chm_status chm::build_trace(chm_ctx *ctx, const IterRecord &R, const chm_trace_p
     std::memcpy(h + D.o_lo, lo16.data(), 2 * size_t(tr->K));
     std::memcpy(h + D.o_li, li16.data(), 2 * size_t(tr->K));
   }
-  if (D.f0_narrow) {
-    std::vector<int32_t> f0u(N);
-    for (int32_t i = 0; i < N; i++) f0u[i] = int32_t(tr->F0[i] >> D.f0_shift);
-    std::memcpy(h + D.o_f0, f0u.data(), 4 * size_t(N));
+  if (D.f0_narrow) {  // swizzled position of op i: block i / 128, lane (i % 64) / 2, slot
+    std::vector<int32_t> f0u(n128, 0);
+    for (size_t i = 0; i < n128; i++) {
+      const size_t blk = i / 128, w = i % 128, lane = (w % 64) / 2, slot = (w / 64) * 2 + (w % 2);
+      const size_t at = blk * 128 + 4 * lane + slot;
+      const size_t src = std::min(i, size_t(N) - 1);  // padding: the last op's layer, F0 0
+      f0u[at] = i < size_t(N) ? int32_t(tr->F0[i] >> D.f0_shift) : 0;
+      h[D.o_lay4 + at] = uint8_t(tr->lay_of_op[src]);  // L <= 256 (checked above)
+    }
+    std::memcpy(h + D.o_f0, f0u.data(), 4 * n128);
   } else {
     std::memcpy(h + D.o_f0, tr->F0.data(), 8 * size_t(N));
   }

@@ -161,13 +161,15 @@ def test_seeded_custom_base_and_masks(ctx):
     assert_same(res, ref, tr.budget)
 
 
-def test_c2_bench_size_full_compare(ctx):
-    """C2 at the bench's full size (10^5 SEEDED candidates, the launch bench.py times), every
-    candidate's peak / stall / swapped and the argmin against the oracle; footprints on a sample."""
-    tr = W.gpt2_xl()
+@pytest.mark.parametrize("name", ["C2", "C3h"])
+def test_bench_size_full_compare(ctx, name):
+    """The launches bench.py times at full size (10^5 SEEDED candidates: C3h, the headline line's
+    workload, and C2, its block), every candidate's peak / stall / swapped and the argmin against
+    the oracle; footprints on a sample one by one, then every row element by element."""
+    tr = W.CONFIGS[name]()
     pt = product_trace(ctx, tr)
     m = O.Model(tr)
-    sd = W.SEEDED["C2"]
+    sd = W.SEEDED[name[:2]]
     n = 100_000
     res = run_eval(ctx, pt, chm.SEEDED, 0, n, seed=sd["seed"], flip_thr=sd["flip_thr"])
     ref = m.eval(O.SEEDED, 0, n, seed=sd["seed"], flip_thr=sd["flip_thr"], nthreads=16)
@@ -178,7 +180,7 @@ def test_c2_bench_size_full_compare(ctx):
     for c in rng.choice(n, size=64, replace=False):
         one = m.eval(O.SEEDED, int(c), 1, seed=sd["seed"], flip_thr=sd["flip_thr"], footprint=True)
         assert np.array_equal(full["footprint"][c], one["footprint"][0])
-    # and every footprint row of the launch (2.1 GB), element by element
+    # and every footprint row of the launch (C2 2.1 GB, C3h 1.26 GB), element by element
     ref_full = m.eval(O.SEEDED, 0, n, seed=sd["seed"], flip_thr=sd["flip_thr"], footprint=True, nthreads=16)
     assert np.array_equal(full["footprint"], ref_full["footprint"])
 

@@ -18,7 +18,7 @@ def main():
     name = next((a for a in sys.argv[1:] if not a.startswith("--")), "C2")
     full = "--search" not in sys.argv
     tr = W.CONFIGS[name]()
-    sd = W.SEEDED[name]
+    sd = W.SEEDED[name[:2]]
     ctx = chm.Context(device=0, eval_ctas_per_sm=int(os.environ.get("EVAL_CTAS_PER_SM", "0")))
     ctx.set_detailed(True)
     chm.record_iteration(ctx, tr)

@@ -433,6 +433,17 @@ def llama2_7b(seq: int = 4096, batch: int = 18, budget: Optional[int] = None) ->
                         "Llama-2 7B trace bf16 seq 4096, 2x HBM oversubscription, swap overlap with compute, 1 B200")
 
 
+def llama2_7b_2x(batch: int = 6) -> Trace:
+    """C3 sized to one box's host RAM: Llama-2 7B bf16, seq 4096, batch b, HBM budget
+    = half the no-swap peak estimate (static + every saved activation), i.e. 2x oversubscription of
+    the budget.  b = 6: peak0 141 GiB, budget 70 GiB, the SEEDED best swaps ~106 GB each way, which
+    fits the 0.6 x ~206 GB pinnable host RAM of the pool's single-socket B200 boxes (b = 18, the
+    2x-of-physical-HBM reading, would need ~300 GB pinned)."""
+    shp = ModelShape("llama", 32, 4096, 32, 11008, 32000, batch, 4096, 6.74e9, 4.0, 2048)
+    return _transformer(shp, f"C3-llama2-7b-b{batch}-2x", lambda m0, act: 0.5 * (m0 + act),
+                        "Llama-2 7B trace bf16 seq 4096, 2x HBM oversubscription, swap overlap with compute, 1 B200")
+
+
 def llama2_13b(seq: int) -> Trace:
     """C4: Llama-2 13B, b 1, seq 2048 or 8192, budget 80 GiB (A100-80GB class)."""
     shp = ModelShape("llama", 40, 5120, 40, 13824, 32000, 1, seq, 13.0e9, 4.0, 2048)
@@ -451,6 +462,7 @@ CONFIGS = {
     "C1": tiny,
     "C2": gpt2_xl,
     "C3": llama2_7b,
+    "C3h": llama2_7b_2x,
     "C4a": lambda: llama2_13b(2048),
     "C4b": lambda: llama2_13b(8192),
     "C5": llama2_7b_rank,
