@@ -22,6 +22,7 @@ namespace {
 
 constexpr int kSwapThreads = 512;
 constexpr int kUnroll = 8;
+constexpr int kMisUnroll = 4;  // misaligned views: words per thread per pass
 constexpr int kChunkShift = 16;  // 64 KiB = 512 threads x 8 x 16 B
 constexpr uint64_t kChunk = 1ull << kChunkShift;
 
@@ -60,6 +61,99 @@ __device__ __forceinline__ void st_plain(void *p, int4 v) {
                : "memory");
 }
 
+// dest word = bytes [r, r + 16) of the 32 bytes a || b (little endian), r = 4 q + sh / 8
+__device__ __forceinline__ int4 shift_combine(const int4 &a, const int4 &b, int q, unsigned sh) {
+  unsigned w0, w1, w2, w3, w4;
+  switch (q) {  // uniform over the chunk: no divergence
+    case 0: w0 = a.x; w1 = a.y; w2 = a.z; w3 = a.w; w4 = b.x; break;
+    case 1: w0 = a.y; w1 = a.z; w2 = a.w; w3 = b.x; w4 = b.y; break;
+    case 2: w0 = a.z; w1 = a.w; w2 = b.x; w3 = b.y; w4 = b.z; break;
+    default: w0 = a.w; w1 = b.x; w2 = b.y; w3 = b.z; w4 = b.w; break;
+  }
+  int4 v;
+  v.x = int(__funnelshift_r(w0, w1, sh));
+  v.y = int(__funnelshift_r(w1, w2, sh));
+  v.z = int(__funnelshift_r(w2, w3, sh));
+  v.w = int(__funnelshift_r(w3, w4, sh));
+  return v;
+}
+
+// One chunk [s, s + len) -> [d, d + len) where s or d is not 16 B aligned.  A head of
+// h < 144 bytes brings d to 16 B alignment (and the host side to 128 B); the body is written in aligned 16 B words, each built
+// from the two aligned 16 B source words it straddles (every source word is loaded once: a lane
+// takes its right neighbour's word by shuffle, the warp's last lane loads one extra) -- when s
+// and d share their misalignment the body is the plain vector copy; a tail of < 16 bytes ends
+// it.  An aligned 16 B word holding a byte of the source never crosses a page, so the loads
+// stay inside the source's pages.  Stores are 16 B transactions on the link, never single
+// bytes.
+__device__ __forceinline__ void copy_misaligned(const char *s, char *d, uint64_t len, bool to_host) {
+  // the head aligns the host side to 128 B (whole L2 lines, whole PCIe requests): swap-out,
+  // the destination; swap-in, the source's aligned words (then a few more bytes bring the
+  // device-side destination to 16 B, the source words stay 128 B-grouped)
+  const uintptr_t ua = reinterpret_cast<uintptr_t>(d), us = reinterpret_cast<uintptr_t>(s);
+  uint64_t h0;
+  if (to_host) {
+    h0 = (128u - (ua & 127u)) & 127u;
+  } else {
+    const uint64_t h1 = (128u - (us & 127u)) & 127u;
+    h0 = h1 + ((16u - ((ua + h1) & 15u)) & 15u);
+  }
+  const uint32_t h = uint32_t(h0 < len ? h0 : len);
+  if (threadIdx.x < h) d[threadIdx.x] = s[threadIdx.x];
+  const char *sb = s + h;
+  char *db = d + h;
+  const uint64_t body = len - h;
+  const uint32_t nvec = uint32_t(body >> 4);  // <= 4096 (64 KiB chunk)
+  const uint32_t r = uint32_t(reinterpret_cast<uintptr_t>(sb) & 15u);
+  const int lane = threadIdx.x & 31;
+  // kMisUnroll words per thread in flight per pass (zero-copy reads from host memory are
+  // latency-bound: 8 CTAs x 32 KiB in flight cover the link's bandwidth-delay product); words
+  // idx = pass + threadIdx.x + k * kSwapThreads
+  if (r == 0) {
+    for (uint32_t p0 = 0; p0 < nvec; p0 += kMisUnroll * kSwapThreads) {
+    int4 v[kMisUnroll];
+#pragma unroll
+    for (int k = 0; k < kMisUnroll; k++) {
+      const uint32_t idx = p0 + threadIdx.x + k * kSwapThreads;
+      if (idx < nvec) v[k] = ld_nc_na(sb + 16ull * idx);
+    }
+#pragma unroll
+    for (int k = 0; k < kMisUnroll; k++) {
+      const uint32_t idx = p0 + threadIdx.x + k * kSwapThreads;
+      if (idx < nvec) st_plain(db + 16ull * idx, v[k]);
+    }
+    }
+  } else {
+    const char *as = sb - r;  // aligned source words as[0 .. nvec] hold the body's bytes
+    const int q = int(r >> 2);
+    const unsigned sh = 8u * (r & 3u);
+    for (uint32_t p0 = 0; p0 < nvec; p0 += kMisUnroll * kSwapThreads) {
+    int4 a[kMisUnroll], e[kMisUnroll];  // e: the word after the warp's last one (lane 31 only)
+#pragma unroll
+    for (int k = 0; k < kMisUnroll; k++) {
+      const uint32_t idx = p0 + threadIdx.x + k * kSwapThreads;
+      a[k] = make_int4(0, 0, 0, 0);
+      e[k] = a[k];
+      if (idx <= nvec) a[k] = ld_nc_na(as + 16ull * idx);
+      if (lane == 31 && idx + 1 <= nvec) e[k] = ld_nc_na(as + 16ull * (idx + 1));
+    }
+#pragma unroll
+    for (int k = 0; k < kMisUnroll; k++) {
+      const uint32_t idx = p0 + threadIdx.x + k * kSwapThreads;
+      int4 b;
+      b.x = __shfl_down_sync(0xffffffffu, a[k].x, 1);
+      b.y = __shfl_down_sync(0xffffffffu, a[k].y, 1);
+      b.z = __shfl_down_sync(0xffffffffu, a[k].z, 1);
+      b.w = __shfl_down_sync(0xffffffffu, a[k].w, 1);
+      if (lane == 31) b = e[k];
+      if (idx < nvec) st_plain(db + 16ull * idx, shift_combine(a[k], b, q, sh));
+    }
+    }
+  }
+  const uint32_t tail = uint32_t(body & 15);
+  if (threadIdx.x < tail) db[16ull * nvec + threadIdx.x] = sb[16ull * nvec + threadIdx.x];
+}
+
 template <bool kPrefetch256>
 __global__ void __launch_bounds__(kSwapThreads) swap_copy_kernel(const __grid_constant__ SwapParams p) {
   for (uint64_t c = blockIdx.x; c < p.total_chunks; c += gridDim.x) {
@@ -91,8 +185,8 @@ __global__ void __launch_bounds__(kSwapThreads) swap_copy_kernel(const __grid_co
       }
       const uint32_t tail = uint32_t(len & 15);
       if (threadIdx.x < tail) d[16ull * nvec + threadIdx.x] = s[16ull * nvec + threadIdx.x];
-    } else {  // misaligned view: byte path
-      for (uint64_t b = threadIdx.x; b < len; b += kSwapThreads) d[b] = s[b];
+    } else {  // misaligned view: aligned 16 B stores fed by aligned 16 B loads (funnel shifts)
+      copy_misaligned(s, d, len, p.to_host != 0);
     }
   }
 }

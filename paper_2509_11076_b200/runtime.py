@@ -160,6 +160,60 @@ def descend(ctx, pt, key, words, dev, max_rounds: int = 4096, stall_model: int =
     return key, cur, rounds
 
 
+def items_to_mask(pt, items, tables=None):
+    """the swappable-set mask of an item list's tensors (their solo timing)"""
+    tb = tables if tables is not None else pt.tables()
+    k_of_rank = {int(t): k for k, t in enumerate(tb["tensor"])}
+    w = np.zeros(max(pt.W, 1), np.uint64)
+    for t in items["t"]:
+        k = k_of_rank.get(int(t))
+        if k is not None:
+            w[k // 64] |= np.uint64(1 << (k % 64))
+    return w[:pt.W]
+
+
+def seeded_multibase(ctx, pt, bases, count: int, seed: int, flip_thr: int, dev,
+                     stall_model: int = chm.STALL_LAYER):
+    """SEEDED candidates around several base masks (reading R-bases): `bases` is a list of
+    (name, mask); the count candidates are split into contiguous id ranges, range j flipping
+    around base j (candidate g of range j = base_j with the SEEDED flips of g), and every base is
+    also scored as it is (a FLIP1 launch at index K = the mask itself).  One base centred on the
+    no-swap peak's window wastes the search where that window is not the trouble (C4a fits with
+    nothing swapped); the empty mask and Algo. 2's plan anchor the search elsewhere.  Returns
+    (best key, its mask, name of its base, {base name: (best key, mask) around that base})."""
+    K, nb = pt.K, len(bases)
+    best = torch.empty(5, dtype=torch.int64, device=dev)
+    out, per = None, {}
+    for j, (name, w) in enumerate(bases):
+        w = np.ascontiguousarray(w, np.uint64)
+        ctx.eval_policies(pt, chm.FLIP1, K, 1, best=best, base=w, stall_model=stall_model)  # the base itself
+        kb = best.cpu().numpy().view(chm.BEST_DTYPE)[0].copy()
+        cands = [(kb, w.copy())]
+        lo, hi = j * count // nb, (j + 1) * count // nb
+        if hi > lo and K:
+            ctx.eval_policies(pt, chm.SEEDED, lo, hi - lo, best=best, seed=seed, flip_thr=flip_thr, base=w,
+                              stall_model=stall_model)
+            ks = best.cpu().numpy().view(chm.BEST_DTYPE)[0].copy()
+            cands.append((ks, pt.candidate_mask(chm.SEEDED, int(ks["index"]), seed=seed, flip_thr=flip_thr,
+                                                base=w)))
+        kj, wj = min(cands, key=lambda c: _key3(c[0]))
+        per[name] = (kj, wj)
+        if out is None or _key3(kj) < _key3(out[0]):
+            out = (kj, wj, name)
+    return out[0], out[1], out[2], per
+
+
+def default_bases(pt, gen_lists=None, gen_keys=None):
+    """R-bases: the empty mask, the trace's argmax-window base, and the mask of Algo. 2's best
+    item list (by its replayed key) when the generator ran"""
+    tb = pt.tables()
+    bases = [("empty", np.zeros(pt.W, np.uint64)), ("argmax-window", tb["base"][:pt.W].copy())]
+    if gen_lists:
+        j = min(range(len(gen_lists)), key=lambda i: _key3(gen_keys[i])) if gen_keys else 0
+        bases.append(("algo2", items_to_mask(pt, gen_lists[j], tb)))
+    return bases
+
+
 def _generate_all(pt):
     """Algo. 2's "best of n" grid (C x T_remaining scale, reading R-gen), one host thread per
     variant (the generator only reads the trace; ctypes drops the GIL): non-empty item lists"""
@@ -797,26 +851,16 @@ class Runtime:
         else:
             cands = []  # (name, key, selection, is_item_list)
             t1 = time.perf_counter()
-            if pt.K <= 4096:  # SEEDED base mask travels in kernel params
-                best = torch.empty(5, dtype=torch.int64, device=self.dev)
-                n = min(self.candidates, 1 << pt.K) if pt.K < 63 else self.candidates
-                kind = chm.EXHAUSTIVE if pt.K < 63 and (1 << pt.K) <= n else chm.SEEDED
-                self.ctx.eval_policies(pt, kind, 0, n, best=best, seed=self.seed, flip_thr=self.flip_thr,
-                                       stall_model=self.stall_model)
-                k = best.cpu().numpy().view(chm.BEST_DTYPE)[0]
-                words = pt.candidate_mask(kind, int(k["index"]), seed=self.seed, flip_thr=self.flip_thr)
-                cands.append(("seeded" if kind == chm.SEEDED else "exhaustive", k, words, False))
-            plan["eval_ms"] = (time.perf_counter() - t1) * 1e3
-            t1 = time.perf_counter()
             gen = _generate_all(pt) if self.use_generator else []
+            gkeys = []
             if gen:
                 off = np.zeros(len(gen) + 1, np.uint64)
                 off[1:] = np.cumsum([len(x) for x in gen])
-                gkeys = torch.empty(5, dtype=torch.int64, device=self.dev)
+                gbest = torch.empty(5, dtype=torch.int64, device=self.dev)
                 gpk = torch.empty(len(gen), dtype=torch.int64, device=self.dev)
                 gst = torch.empty(len(gen), dtype=torch.float64, device=self.dev)
                 gsw = torch.empty(len(gen), dtype=torch.int64, device=self.dev)
-                self.ctx.eval_policies(pt, chm.EXPLICIT, 0, len(gen), best=gkeys, item_offsets=off,
+                self.ctx.eval_policies(pt, chm.EXPLICIT, 0, len(gen), best=gbest, item_offsets=off,
                                        items=np.concatenate(gen), peak=gpk, stall=gst, swapped=gsw)
                 pk, stl, swp = gpk.cpu().numpy(), gst.cpu().numpy(), gsw.cpu().numpy()
                 for j, g in enumerate(gen):  # every variant a key of its own (for the trials)
@@ -825,13 +869,33 @@ class Runtime:
                     kj["excess"], kj["stall"], kj["swapped_bytes"] = max(0, int(pk[j]) - pt.budget), st_j, swp[j]
                     kj["index"], kj["peak"] = j, pk[j]
                     cands.append((f"generator[{j}]", kj, g, True))
+                    gkeys.append(kj)
             plan["generator_ms"] = (time.perf_counter() - t1) * 1e3
             t1 = time.perf_counter()
+            if pt.K <= 4096:  # SEEDED base masks travel in kernel params
+                if pt.K < 63 and (1 << pt.K) <= self.candidates:  # small: every subset
+                    best = torch.empty(5, dtype=torch.int64, device=self.dev)
+                    self.ctx.eval_policies(pt, chm.EXHAUSTIVE, 0, 1 << pt.K, best=best, stall_model=self.stall_model)
+                    k = best.cpu().numpy().view(chm.BEST_DTYPE)[0]
+                    cands.append(("exhaustive", k, pt.candidate_mask(chm.EXHAUSTIVE, int(k["index"])), False))
+                else:  # reading R-bases: around the empty mask, the argmax window and Algo. 2's plan
+                    k, words, bname, per = seeded_multibase(
+                        self.ctx, pt, default_bases(pt, gen, gkeys), self.candidates, self.seed, self.flip_thr,
+                        self.dev, self.stall_model)
+                    # every base's best is a start for the descent: the best start does not always
+                    # descend to the best plan (tools/multibase.py: C3h, C4b)
+                    for nm, (kx, wx) in sorted(per.items(), key=lambda kv: _key3(kv[1][0])):
+                        cands.append((f"seeded[{nm}]", kx, wx, False))
+                    plan["seeded_base"] = bname
+                    plan["seeded_per_base"] = {nm: dict(excess=int(x["excess"]), stall=float(x["stall"]),
+                                                        swapped=int(x["swapped_bytes"])) for nm, (x, _) in per.items()}
+            plan["eval_ms"] = (time.perf_counter() - t1) * 1e3
+            t1 = time.perf_counter()
             if self.search_rounds and pt.K <= 4096:
-                starts = [c for c in cands if not c[3]][:1]
+                starts = [c for c in cands if not c[3]]  # the exhaustive best, or each base's SEEDED best
                 gen_c = sorted((c for c in cands if c[3]), key=lambda c: self._key(c[1]))[:1]
                 for c in gen_c:  # the generator's best as a mask (solo timing) to descend from
-                    starts.append((c[0] + "->mask", None, self._items_to_mask(pt, c[2]), False))
+                    starts.append((c[0] + "->mask", None, items_to_mask(pt, c[2]), False))
                 rounds = 0
                 for name, k0, w0, _ in starts:
                     if k0 is None:
@@ -888,17 +952,6 @@ class Runtime:
         plan.update(kind=name, excess=int(k["excess"]), stall=float(k["stall"]), swapped=int(k["swapped_bytes"]),
                     peak=int(k["peak"]), items=len(self.policy_items),
                     tensors=[int(x) for x in self.policy_items["t"]])
-
-    def _items_to_mask(self, pt, items):
-        """the swappable-set mask of an item list's tensors (their solo timing)"""
-        tb = pt.tables()
-        k_of_rank = {int(t): k for k, t in enumerate(tb["tensor"])}
-        w = np.zeros(max(pt.W, 1), np.uint64)
-        for t in items["t"]:
-            k = k_of_rank.get(int(t))
-            if k is not None:
-                w[k // 64] |= np.uint64(1 << (k % 64))
-        return w[:pt.W]
 
     def _trial_done(self, t_iter):
         """"generates five different policies and selects the one with the best runtime

@@ -61,3 +61,32 @@ def test_batched_descent_ends_in_a_single_flip_local_optimum(seed, model):
     ctx.eval_policies(pt, chm.FLIP1, pt.K, 1, best=best, base=dw, stall_model=model)
     assert key(best.cpu().numpy().view(chm.BEST_DTYPE)[0]) == key(dk)  # the reported key is the mask's
     ctx.close()
+
+
+def test_multibase_seeded_finds_the_empty_plan_when_nothing_needs_swapping():
+    """C4a (Llama-2 13B at s = 2048) fits its 80 GiB budget with nothing swapped: the single-base
+    SEEDED search (centred on the no-swap peak's window) still swaps GBs; around several bases
+    (reading R-bases: the empty mask is one, scored as it is) the best key is the empty plan
+    (0, 0.0, 0).  The argmin is checked against the per-base keys it reports."""
+    import numpy as np
+
+    from paper_2509_11076_b200.runtime import default_bases, seeded_multibase
+    tr = W.CONFIGS["C4a"]()
+    sd = W.SEEDED["C4"]
+    ctx = chm.Context(device=0)
+    ctx.set_detailed(True)
+    chm.record_iteration(ctx, tr)
+    ctx.detect_seq_change(tr.t_iter)
+    pt = ctx.trace_build(tr.budget, tr.static_bytes, tr.bw, tr.groups_fwd, tr.groups_bwd, t_iter=tr.t_iter)
+    assert pt.peak0 <= pt.budget and pt.K > 0
+    dev = torch.device("cuda:0")
+    best = torch.empty(5, dtype=torch.int64, device=dev)
+    ctx.eval_policies(pt, chm.SEEDED, 0, 100_000, best=best, seed=sd["seed"], flip_thr=sd["flip_thr"])
+    single = best.cpu().numpy().view(chm.BEST_DTYPE)[0]
+    assert int(single["swapped_bytes"]) > 0  # r01's search never reaches the empty plan
+    k, w, name, per = seeded_multibase(ctx, pt, default_bases(pt), 100_000, sd["seed"], sd["flip_thr"], dev)
+    assert (int(k["excess"]), float(k["stall"]), int(k["swapped_bytes"])) == (0, 0.0, 0)
+    assert name == "empty" and not np.any(w)
+    key = lambda x: (int(x["excess"]), float(x["stall"]), int(x["swapped_bytes"]))  # noqa: E731
+    assert key(k) == min(key(x) for x, _ in per.values())
+    ctx.close()

@@ -113,6 +113,76 @@ def test_validation_errors(ctx):
         assert e.value.index == (1 if j == 3 else 0)
 
 
+@pytest.mark.parametrize("direction", ["out", "in"])
+def test_misalignment_matrix(ctx, direction):
+    """every (device, host) misalignment pair mod 16 through the kernel: same misalignment takes
+    the shifted vector body, different misalignment the funnel-shift body; sizes span a head, a
+    tail and more than one 64 KiB chunk.  Byte-exact against the oracle's swap definition."""
+    comp = torch.cuda.current_stream()
+    s = torch.cuda.Stream()
+    host = arena_view(ctx)
+    size_cycle = [1, 17, 4095, 65536 + 33, 3 * 65536 + 5, 200_003]
+    for dev_mis in range(16):
+        descs, srcs, dsts, off = [], [], [], 0
+        for host_mis in range(16):
+            n = size_cycle[(dev_mis + host_mis) % len(size_cycle)]
+            base = rand_bytes(n + 64, 1000 + 16 * dev_mis + host_mis)
+            ho = off + host_mis
+            off = (ho + n + 64 + 15) // 16 * 16
+            if direction == "out":
+                src = base[dev_mis:dev_mis + n]
+                descs.append((src.data_ptr(), ho, n))
+                srcs.append(src)
+            else:
+                host[ho:ho + n] = base[:n].cpu().numpy()
+                d = torch.zeros(n + 64, dtype=torch.uint8, device="cuda")
+                descs.append((d[dev_mis:dev_mis + n].data_ptr(), ho, n))
+                srcs.append(base[:n])
+                dsts.append((d, dev_mis, n))
+        if direction == "out":
+            ctx.batch_wait(ctx.swap_out(descs, comp, s, chm.SWAP_KERNEL), comp)
+            torch.cuda.synchronize()
+            exp = np.zeros(off, np.uint8)
+            exp[:] = host[:off]
+            src_host = [x.cpu().numpy() for x in srcs]
+            O.swap_execute([exp.ctypes.data + d[1] for d in descs], [a.ctypes.data for a in src_host],
+                           [d[2] for d in descs])
+            for (p_, ho, n), a in zip(descs, src_host):
+                assert np.array_equal(host[ho:ho + n], a), (dev_mis, ho % 16, n)
+            assert np.array_equal(host[:off], exp)
+        else:
+            ctx.batch_wait(ctx.swap_in(descs, comp, s, chm.SWAP_KERNEL), comp)
+            torch.cuda.synchronize()
+            for (d, do, n), src in zip(dsts, srcs):
+                assert torch.equal(d[do:do + n], src), (dev_mis, n)
+                assert int(d[:do].sum()) == 0 and int(d[do + n:].sum()) == 0
+
+
+@pytest.mark.parametrize("sabotage", [False, True])
+def test_swap_in_hazard(ctx, sabotage):
+    """The wait before b_t (a swapped-in tensor must be on the device before its first
+    backward use): the compute stream reads the destination right after the swap-in is issued.
+    With the wait it reads the swapped-in bytes; sabotage (no wait) must be caught reading stale
+    ones on a 256 MiB block."""
+    n = 256 << 20
+    src = rand_bytes(n, 91)
+    comp = torch.cuda.current_stream()
+    s = torch.cuda.Stream()
+    ctx.batch_wait(ctx.swap_out([(src.data_ptr(), 0, n)], comp, s), comp)
+    dst = torch.full((n,), 0x5A, dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+    b = ctx.swap_in([(dst.data_ptr(), 0, n)], comp, s)
+    if not sabotage:
+        ctx.batch_wait(b, comp)  # the executor's wait before b_t
+    seen = dst.clone()  # the first use, on the compute stream
+    torch.cuda.synchronize()
+    fresh = torch.equal(seen, src)
+    if sabotage:
+        assert not fresh and int((seen == 0x5A).sum()) > 0, "sabotage run read fresh bytes: test is not sensitive"
+    else:
+        assert fresh
+
+
 @pytest.mark.parametrize("sabotage", [False, True])
 def test_release_hazard(ctx, sabotage):
     """Custom recordStream: after the stream-ordered release the compute stream reuses the
