@@ -57,5 +57,34 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False) -> st
     return lib
 
 
+HOOK_DIR = os.path.join(HERE, "build_hook")
+HOOK_SRC = os.path.join(CSRC, "hook.cpp")
+HOOK_NAME = "chm_hook"
+
+
+def hook_path() -> str:
+    return os.path.join(HOOK_DIR, HOOK_NAME + ".so")
+
+
+def build_hook(force: bool = False, verbose: bool = False) -> str:
+    """the profiler hook at operator dispatch (csrc/hook.cpp): a PyTorch C++ extension, built
+    in-tree (build_hook/chm_hook.so) with torch's own compiler flags; it calls libchm through the
+    addresses of its C entry points, so it does not link it"""
+    so = hook_path()
+    deps = [HOOK_SRC, os.path.join(ROOT, "include", "chm.h"), os.path.abspath(__file__)]
+    if not force and os.path.exists(so) and all(os.path.getmtime(d) <= os.path.getmtime(so) for d in deps):
+        return so
+    os.makedirs(HOOK_DIR, exist_ok=True)
+    from torch.utils import cpp_extension
+    cpp_extension.load(name=HOOK_NAME, sources=[HOOK_SRC], build_directory=HOOK_DIR,
+                       extra_include_paths=[os.path.join(ROOT, "include"), "/usr/local/cuda/include"],
+                       extra_cflags=["-O3", "-std=c++17"], extra_ldflags=["-lc10_cuda"], with_cuda=False,
+                       is_python_module=True, verbose=verbose)
+    os.utime(so)
+    return so
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, debug="--debug" in sys.argv))
+    if "--no-hook" not in sys.argv:
+        print(build_hook(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -35,8 +35,10 @@ on CPU tensors (no copies): the CPU tests use it.
 """
 from __future__ import annotations
 
+import collections
 import concurrent.futures
 import contextlib
+import ctypes
 import os
 import re
 import threading
@@ -58,6 +60,25 @@ def _dtype_code(dt) -> int:
     return _DTYPE_CODE.get(dt, 15)
 
 
+_HOOK = None
+
+
+def native_hook():
+    """the C++ profiler hook at operator dispatch (csrc/hook.cpp, a PyTorch extension built
+    in-tree by build.py; built here on first use if missing)"""
+    global _HOOK
+    if _HOOK is None:
+        import importlib.util
+
+        from . import build as _b
+        path = _b.build_hook()
+        spec = importlib.util.spec_from_file_location(_b.HOOK_NAME, path)
+        mod = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(mod)
+        _HOOK = mod
+    return _HOOK
+
+
 class _Holder:
     """one swapped (or swappable) storage: the device block while resident, its swap state"""
     __slots__ = ("storage", "nbytes", "item", "host_off", "released", "in_issued", "in_waited", "boxes",
@@ -72,20 +93,35 @@ class _Holder:
         self.in_issued = False
         self.in_waited = False
         self.passive = 0  # handle of a passive swap (Algo. 3 (iv)) holding the data
-        self.boxes = weakref.WeakSet()
+        self.boxes = []   # weak references to the boxes over this storage (autograd owns them)
+
+    def live_boxes(self):
+        return [b for b in (r() for r in self.boxes) if b is not None]
+
+    def drop_views(self):
+        """the device block goes away: every box keeps its view description, drops the tensor"""
+        for b in self.live_boxes():
+            b.drop()
 
 
 class _Box:
-    """what autograd saves instead of an activation: a view description over a holder"""
+    """what autograd saves instead of an activation: the tensor while its block is resident; a
+    view description over the holder once the block is released (taken then, not at pack time:
+    most saved tensors are never released)"""
     __slots__ = ("holder", "t", "dtype", "size", "stride", "offset", "__weakref__")
 
     def __init__(self, holder, t):
         self.holder = holder
         self.t = t
-        self.dtype = t.dtype
-        self.size = tuple(t.size())
-        self.stride = tuple(t.stride())
-        self.offset = t.storage_offset()
+
+    def drop(self):
+        t = self.t
+        if t is not None:
+            self.dtype = t.dtype
+            self.size = tuple(t.size())
+            self.stride = tuple(t.stride())
+            self.offset = t.storage_offset()
+            self.t = None
 
 
 def _collect(x, out):
@@ -288,7 +324,17 @@ class Runtime:
     prepin: pin the host arena on a host thread during the Detailed step, sized 1.25 x (peak
     allocated - budget), so the plan's install does not pin;
     host_pin_budget: most bytes this rank may pin for the arena (0: 0.6 x MemAvailable /
-    LOCAL_WORLD_SIZE, i.e. the node's pinnable RAM split between its ranks)."""
+    LOCAL_WORLD_SIZE, i.e. the node's pinnable RAM split between its ranks);
+    native_hook: the profiler hook in C++ at operator dispatch (csrc/hook.cpp) instead of the
+    Python TorchDispatchMode.  None (default): C++ unless OOM handling is on (oom_host_bytes > 0).
+    The two see different op granularities -- C++ the ops the program calls, above autograd;
+    Python the ops below it -- so one runtime keeps one of them for its lifetime.  Algo. 3
+    keeps the Python hook: it retries the failing op at the lowest level, and every tensor a
+    composite op creates inside (e.g. matmul's contiguous copies) is a recorded, passively
+    swappable tensor there, while above autograd those stay invisible to the executor and a
+    retry re-runs the whole composite (measured: under a 60% cap the C++ hook runs out of
+    passive candidates against allocator fragmentation, tools/debug_oom.py).  record_log needs
+    the Python hook."""
 
     def __init__(self, device: Optional[int] = 0, *, hbm_budget: int, bw: Optional[float] = None,
                  groups_fwd: int = 0, groups_bwd: int = 0, omega: float = 1.0, candidates: int = 1 << 16,
@@ -296,7 +342,7 @@ class Runtime:
                  min_swap_bytes: int = 0, search_rounds: int = 4096, host_arena_bytes: int = 0,
                  swap_flags: int = chm.SWAP_AUTO, oom_host_bytes: int = 0, trials: int = 5,
                  stall_model: int = chm.STALL_TIMELINE, search_batch: int = 1, prepin: bool = True,
-                 host_pin_budget: int = 0, **algo1):
+                 host_pin_budget: int = 0, native_hook: Optional[bool] = None, **algo1):
         self.host_only = device is None
         self.dev = torch.device("cpu") if self.host_only else torch.device("cuda", device)
         self.ctx = chm.Context(device=-1 if self.host_only else device, swap_ctas=swap_ctas,
@@ -354,6 +400,25 @@ class Runtime:
         self._in_step = False
         self._internal = False
         self.passive_out = {}  # passive-swap handle -> weak holder
+        self.oom_log = collections.deque(maxlen=256)  # Algo. 3 decisions, latest last
+        self.host_timing = False  # C++ hook: measure the runtime's own host time per step
+        self.host_cost = None
+        self._hook_py_s = 0.0
+        if native_hook is None:
+            native_hook = not self.oom_host_bytes
+        self._nh = globals()["native_hook"]() if native_hook else None
+
+    def _attach_hook(self):
+        """hands this runtime's ctx and callbacks to the C++ hook for one step"""
+        L = chm.load()
+        addr = lambda f: ctypes.cast(f, ctypes.c_void_p).value  # noqa: E731
+        dev = not self.host_only
+        self._nh.attach(self.ctx.h.value, addr(L.chm_record_op), addr(L.chm_tokenize), addr(L.chm_record_tokens),
+                        addr(L.chm_last_error), int(self.dev.index) if dev else -1,
+                        self._native_actions, self._native_oom,
+                        addr(L.chm_issue_swap_out), addr(L.chm_issue_swap_in), addr(L.chm_item_wait),
+                        self.s_out.cuda_stream if dev else 0, self.s_in.cuda_stream if dev else 0,
+                        self.swap_flags, self._native_release, self._native_swap_in)
 
     # ------------------------------------------------------------------ step
     @contextlib.contextmanager
@@ -362,14 +427,42 @@ class Runtime:
         if self._in_step:
             raise RuntimeError("Runtime.step is not reentrant")
         self._begin()
-        mode = _Mode(self)
         # the hooks stay on in every step: registered saved-tensor hooks change the operator
         # sequence autograd dispatches (e.g. detaches), so steps with and without them would not
         # compare as the same sequence in Algo. 1
         try:
-            with torch.autograd.graph.saved_tensors_hooks(self._pack, self._unpack), mode:
-                yield self
-                self._flush()
+            if self._nh is not None:
+                nh = self._nh
+                self._attach_hook()
+                try:
+                    nh.set_timing(self.host_timing)
+                    self._hook_py_s = 0.0
+                    nh.begin_step(self.light, self.detailed, self.policy is not None, bool(self.oom_host_bytes))
+                    # above autograd the op sequence is the same with and without saved-tensor hooks,
+                    # so they are on only where boxes are needed: a policy to execute, or OOM
+                    # handling that may passively swap saved tensors
+                    boxes = self.policy is not None or bool(self.oom_host_bytes)
+                    with (torch.autograd.graph.saved_tensors_hooks(self._pack, self._unpack) if boxes
+                          else contextlib.nullcontext()):
+                        nh.enable(True)
+                        try:
+                            yield self
+                        finally:
+                            nh.enable(False)
+                    self.n_ops, n_act, n_retry, n_out, n_in = nh.end_step()
+                    self.stats["swap_out"] += n_out
+                    self.stats["swap_in"] += n_in
+                    if self.host_timing:  # the runtime's own host time in this step (tools/stable_cost.py)
+                        self_ns, cb_ns = nh.timing()
+                        self.host_cost = dict(hook_self_s=self_ns * 1e-9, actions_s=cb_ns * 1e-9,
+                                              pack_unpack_s=self._hook_py_s, ops=self.n_ops,
+                                              total_s=self_ns * 1e-9 + self._hook_py_s)
+                finally:
+                    nh.detach()
+            else:
+                with torch.autograd.graph.saved_tensors_hooks(self._pack, self._unpack), _Mode(self):
+                    yield self
+                    self._flush()
         except BaseException:
             self._in_step = False
             self._abort()
@@ -384,6 +477,8 @@ class Runtime:
         self._join_prepin()
         self.pending = None
         self.tok_buf, self.ph_buf = [], []
+        if self._nh is not None:
+            self._nh.abort_step()
         if not self.host_only:
             torch.cuda.synchronize(self.dev)
         for hd in list(self.passive_out):
@@ -423,6 +518,8 @@ class Runtime:
             # misjudge the layer budgets)
             self._start_prepin()
         # nothing to execute, record or fall back on: tokens only, autograd saves as usual
+        if self.record_log and self._nh is not None:
+            raise ValueError("record_log needs the Python hook: Runtime(..., native_hook=False)")
         self.light = (self.policy is None and not self.detailed and not self.oom_host_bytes
                       and not self.record_log and not self._detect_bytes)
         self.produced = set()  # storage addresses created by ops of this step
@@ -505,7 +602,7 @@ class Runtime:
         self.stage = d["stage"]
         for hd, ref in list(self.passive_out.items()):  # died while passively out: drop the copy
             h = ref()
-            if h is None or not h.boxes:
+            if h is None or not h.live_boxes():
                 self.ctx.passive_restore(hd, 0)
                 del self.passive_out[hd]
         for ref in self.weak.values():
@@ -626,6 +723,14 @@ class Runtime:
 
     # ------------------------------------------------------------------ autograd boxes
     def _pack(self, t):
+        if self.host_timing:
+            t0 = time.perf_counter()
+            r = self._pack_impl(t)
+            self._hook_py_s += time.perf_counter() - t0
+            return r
+        return self._pack_impl(t)
+
+    def _pack_impl(self, t):
         if self.light or not isinstance(t, torch.Tensor) or t.device != self.dev or t.is_sparse:
             return t
         try:
@@ -633,25 +738,41 @@ class Runtime:
         except (RuntimeError, NotImplementedError):
             return t
         p = st.data_ptr()
-        if p not in self.produced or st.nbytes() < self.min_swap_bytes:
+        # C++ hook (above autograd): this pack runs inside the op, before its outputs are
+        # recorded -- anything not read before the step created it is the step's own
+        produced = not self._nh.is_static(p) if self._nh is not None else p in self.produced
+        if not produced or st.nbytes() < self.min_swap_bytes:
             return t  # weights, inputs and tiny tensors stay as autograd saved them
         h = self.holders.get(p)
         if h is None or h.released:
             h = self.holders[p] = _Holder(st, st.nbytes())
         b = _Box(h, t)
-        h.boxes.add(b)
+        h.boxes.append(weakref.ref(b))
         return b
 
     def _unpack(self, b):
+        if self.host_timing:
+            t0 = time.perf_counter()
+            r = self._unpack_impl(b)
+            self._hook_py_s += time.perf_counter() - t0
+            return r
+        return self._unpack_impl(b)
+
+    def _unpack_impl(self, b):
         if not isinstance(b, _Box):
             return b
         if b.t is not None:
             return b.t
         self._internal = True
+        nh = self._nh if self._nh is not None and self._nh.enabled() else None
+        if nh is not None:  # the restore's own allocations are not ops of the program
+            nh.enable(False)
         try:
             return self._restore(b)
         finally:
             self._internal = False
+            if nh is not None:
+                nh.enable(True)
 
     def _restore(self, b):
         h = b.holder
@@ -680,6 +801,50 @@ class Runtime:
         b.t = t
         return t
 
+    # ------------------------------------------------------------------ native hook callbacks
+    def _native_actions(self, act_addr: int):
+        """csrc/hook.cpp: the executor returned actions for the op just recorded"""
+        self._actions(chm.actions_view(chm.Actions.from_address(act_addr)))
+
+    def _native_release(self, items):
+        """csrc/hook.cpp, after op r_t: stream-ordered releases (the hook issued the swap-outs);
+        items: (item, device address, host offset, bytes)"""
+        comp = torch.cuda.current_stream(self.dev).cuda_stream
+        wait = chm.load().chm_item_wait
+        st = self.stats
+        for it, d, off, nb in items:
+            h = self.holders.get(d)  # autograd has packed the op's saved tensors by now
+            if h is None or h.released:
+                st["unheld"] += 1  # not saved for backward: nothing to release
+                continue
+            h.item, h.host_off = it, off
+            self.item_holder[it] = (weakref.ref(h), d, off, nb)
+            chm._check(wait(self.ctx.h, it, 0, comp))  # event pair: reuse after the copy (P:393)
+            h.storage = None
+            h.drop_views()
+            h.released = True
+            st["release"] += 1
+            st["released_bytes"] += nb
+
+    def _native_swap_in(self, pairs):
+        """csrc/hook.cpp, before op s_t: the hook allocated a block per item and issued the
+        swap-in; each block goes to its box's holder, or (nothing to restore into) is kept
+        until the compute stream waited for its copy"""
+        comp = None
+        for it, blk in pairs:
+            ref = self.item_holder.get(it, (None,))[0]
+            h = ref() if ref is not None else None
+            if h is not None and h.released and h.storage is None:
+                h.storage = blk.untyped_storage()
+                h.in_issued = True
+            else:  # scratch: freed in compute-stream order after the wait
+                comp = comp or torch.cuda.current_stream(self.dev).cuda_stream
+                chm._check(chm.load().chm_item_wait(self.ctx.h, it, 1, comp))
+
+    def _native_oom(self, msg: str, busy_ptrs) -> bool:
+        """csrc/hook.cpp: an op ran out of device memory; make room (Algo. 3), then it retries"""
+        return self._oom(_requested_bytes(msg), (), busy_ptrs=set(busy_ptrs))
+
     # ------------------------------------------------------------------ executor actions
     def _actions(self, av):
         comp = None if self.host_only else torch.cuda.current_stream(self.dev)
@@ -700,8 +865,7 @@ class Runtime:
             if not self.host_only:
                 self.ctx.item_wait(it, False, comp)  # event pair: reuse after the copy
                 h.storage = None
-                for b in list(h.boxes):
-                    b.t = None
+                h.drop_views()
             h.released = True
             self.stats["release"] += 1
             self.stats["released_bytes"] += nb
@@ -747,17 +911,18 @@ class Runtime:
 
     def _drop(self, h):
         h.storage = None
-        for b in list(h.boxes):
-            b.t = None
+        h.drop_views()
         h.released = True
 
-    def _oom(self, need: int, busy) -> bool:
+    def _oom(self, need: int, busy, busy_ptrs=None) -> bool:
         """one round of Algo. 3: (i)-(ii) release every block whose swap-out is
         issued and whose release point has not come; else (iv) passively swap the saved tensor
         closest in size to the request.  False when nothing can be freed (the OOM propagates)."""
         if self.host_only or not self._in_step:
+            self.oom_log.append(("refused", "not in a step"))
             return False
         self.stats["oom"] += 1
+        self.oom_log.append(("oom", need, torch.cuda.memory_allocated(self.dev), self.stats["steps"], self.n_ops))
         comp = torch.cuda.current_stream(self.dev)
         if self.policy is not None:
             freed = 0
@@ -771,10 +936,12 @@ class Runtime:
                     freed += 1
             self.stats["oom_released"] += freed
             if freed:
+                self.oom_log.append(("released", freed))
                 return True
         if not self.oom_host_bytes:
+            self.oom_log.append(("refused", "no passive room (oom_host_bytes = 0)"))
             return False
-        busy_ptrs = set()
+        busy_ptrs = set(busy_ptrs or ())
         for x in busy:
             if isinstance(x, torch.Tensor) and x.device == self.dev:
                 try:
@@ -783,18 +950,27 @@ class Runtime:
                     pass
         cand = [p for p, h in list(self.holders.items())
                 if h.storage is not None and not h.released and h.item < 0 and p not in busy_ptrs]
+        if self._nh is not None:  # C++ hook: storages a completed op created (not an op's internals)
+            cand = [p for p in cand if self._nh.produced_live(p)]
         if not cand:
+            self.oom_log.append(("refused", f"no saved tensor to swap ({len(self.holders)} holders)",
+                                 sorted((h.nbytes for h in self.holders.values()), reverse=True)[:8]))
             return False
         try:
             ps = self.ctx.passive_swap(need, (), comp, self.s_out, only=cand)
-        except chm.ChmError:
-            return False  # arena full or nothing eligible
+        except chm.ChmError as e:  # arena full or nothing eligible
+            self.oom_log.append(("refused", f"passive swap: {e}",
+                                 sorted((self.holders[p].nbytes for p in cand), reverse=True)[:8], len(cand)))
+            return False
         h = self.holders.get(ps["id"])
         h.passive = ps["handle"]
         self.passive_out[ps["handle"]] = weakref.ref(h)
+        a0 = torch.cuda.memory_allocated(self.dev)
         self._drop(h)
+        self.oom_log.append(("freed", a0 - torch.cuda.memory_allocated(self.dev)))
         self.stats["passive"] += 1
         self.stats["passive_bytes"] += ps["nbytes"]
+        self.oom_log.append(("passive", ps["nbytes"]))
         return True
 
     # ------------------------------------------------------------------ planning
@@ -1010,6 +1186,9 @@ class Runtime:
 
     def close(self):
         self._join_prepin()
+        if self._nh is not None and self.ctx.h:
+            self._nh.forget(self.ctx.h.value)
+        self._nh = None
         self.ctx.close()
 
     def __del__(self):

@@ -62,7 +62,11 @@ def main():
     import gc
     gc.collect()
     torch.cuda.empty_cache()
-    losses, params = train(rt)
+    try:
+        losses, params = train(rt)
+    except torch.OutOfMemoryError as e:
+        print(json.dumps(dict(out, error=str(e)[:300], oom_log=list(rt.oom_log), stats=rt.stats)))
+        raise
     out.update(losses_equal=losses == ref_losses, params_equal=bool(torch.equal(params, ref_params)),
                stats=rt.stats, stages=rt.stage, plans=[{k: v for k, v in p.items() if k != "tensors"} for p in rt.plans])
     print(json.dumps(out))

@@ -84,7 +84,7 @@ def test_runtime_swaps_are_bit_exact_and_lower_the_peak(reference):
         times = [t["step_s"] for t in plan["trials"]]
         assert plan["chosen"] == plan["trials"][times.index(min(times))]["plan"] == plan["kind"]
     st = rt.stats
-    assert st["release"] > 0 and st["released_bytes"] > 0 and st["demand_swap_in"] == 0
+    assert st["release"] > 0 and st["released_bytes"] > 0 and st["demand_swap_in"] == 0, st
     ex = rt.ctx.exec_stats()
     assert ex["n_stale"] == 0 and ex["bytes_out"] == ex["bytes_in"] > 0
     # steps after the plan run below the plain run's peak
@@ -93,19 +93,30 @@ def test_runtime_swaps_are_bit_exact_and_lower_the_peak(reference):
     rt.close()
 
 
-def test_demand_swap_in_when_swap_ins_are_dropped(reference):
-    rt = Runtime(0, hbm_budget=_budget(reference[2]), groups_fwd=6, groups_bwd=6)
-    orig = rt._actions
+@pytest.mark.parametrize("native", [True, False])
+def test_demand_swap_in_when_swap_ins_are_dropped(reference, native):
+    rt = Runtime(0, hbm_budget=_budget(reference[2]), groups_fwd=6, groups_bwd=6, native_hook=native)
+    if native:  # the C++ hook issues the swap-ins; none of the blocks reaches its box
+        import paper_2509_11076_b200.chm as chm_
 
-    def no_swap_in(av):
-        if av["swap_in"]:  # the executor's swap-ins never happen: drift of the worst kind
-            av = dict(av, swap_in=[], swap_in_item=[], wait=[])
-            rt._dropped = getattr(rt, "_dropped", 0) + 1
-        orig(av)
-    rt._actions = no_swap_in
+        def lost(pairs):
+            comp = torch.cuda.current_stream().cuda_stream
+            for it, _ in pairs:  # copy lands in a scratch block that is dropped after it
+                chm_._check(chm_.load().chm_item_wait(rt.ctx.h, it, 1, comp))
+        rt._native_swap_in = lost
+        rt._nh.detach()  # re-attached per step with the patched callback
+    else:
+        orig = rt._actions
+
+        def no_swap_in(av):
+            if av["swap_in"]:  # the executor's swap-ins never happen: drift of the worst kind
+                av = dict(av, swap_in=[], swap_in_item=[], wait=[])
+                rt._dropped = getattr(rt, "_dropped", 0) + 1
+            orig(av)
+        rt._actions = no_swap_in
     run = _train(rt)
     _check_exact(run, reference)
-    assert rt.stats["demand_swap_in"] > 0 and rt.stats["demand_swap_in"] == rt.stats["release"]
+    assert rt.stats["demand_swap_in"] > 0 and rt.stats["demand_swap_in"] == rt.stats["release"], rt.stats
     rt.close()
 
 
