@@ -1067,7 +1067,8 @@ class Runtime:
                                                         swapped=int(x["swapped_bytes"])) for nm, (x, _) in per.items()}
             plan["eval_ms"] = (time.perf_counter() - t1) * 1e3
             t1 = time.perf_counter()
-            if self.search_rounds and pt.K <= 4096:
+            floor = any(self._key(c[1]) == (0, 0.0, 0) for c in cands)  # the empty plan fits: nothing to gain
+            if self.search_rounds and pt.K <= 4096 and not floor:
                 starts = [c for c in cands if not c[3]]  # the exhaustive best, or each base's SEEDED best
                 gen_c = sorted((c for c in cands if c[3]), key=lambda c: self._key(c[1]))[:1]
                 for c in gen_c:  # the generator's best as a mask (solo timing) to descend from
