@@ -175,8 +175,9 @@ struct DevTrace {
   int32_t f0_shift = 0;
   int32_t f0_narrow = 0;
   uint32_t o_lay = 0;   // u16   [N]  8 x logical layer of each op (byte offset into D, full mode)
-  uint32_t o_lay4 = 0;  // u8    [N padded to 128] logical layer of each op (L <= 256), lane-swizzled
-                        // like F0 (narrow only): one 32-bit load gives a lane's four ops' layers
+  uint32_t o_lay4 = 0;  // u16   [N padded to 128] 8 x logical layer of each op (its byte offset
+                        // into a D row), lane-swizzled like F0 (narrow only): one 8 B load gives
+                        // a lane's four ops' offsets
   const uint64_t *base = nullptr;
   int32_t N = 0, K = 0, L = 0, W = 0;
   double bw = 1.0;
@@ -289,8 +290,8 @@ struct chm_ctx {
   size_t tl_aux_bytes = 0;
   void *explicit_scratch = nullptr;  // EXPLICIT candidates: items + offsets + keys (device)
   size_t explicit_scratch_bytes = 0;
-  size_t eval_attr_smem[3] = {0, 0, 0};  // cached kernel attribute / occupancy per variant
-  int eval_per_sm[3] = {0, 0, 0};
+  size_t eval_attr_smem[12] = {};  // cached kernel attribute / occupancy per variant (mode x E)
+  int eval_per_sm[12] = {};
 };
 
 namespace chm {

@@ -47,6 +47,7 @@ struct EvalParams {
   uint64_t ld;
   int row_pairs;  // 16 B stores per footprint row (ceil(N / 2))
   int lay_per_lane;  // E: layers per lane, next power of two >= L over 32 (1 .. 8)
+  uint32_t item_table;  // bytes of the per-item delta / layer table in shared memory
   Key *partial;
   unsigned int *ticket;
   unsigned long long *work;  // candidate counter for dynamic distribution
@@ -98,7 +99,13 @@ __device__ __forceinline__ void stage_image(unsigned char *dst, const unsigned c
   }
 }
 
-constexpr int kEvalThreads = 512;  // 16 warps per CTA, one candidate per warp
+#ifndef CHM_EVAL_THREADS
+#define CHM_EVAL_THREADS 512
+#endif
+#ifndef CHM_EVAL_MINB
+#define CHM_EVAL_MINB 2
+#endif
+constexpr int kEvalThreads = CHM_EVAL_THREADS;  // 16 warps per CTA, one candidate per warp
 constexpr int kChunk = 32;         // consecutive candidates per CTA-level grab
 
 // the warp's next candidate (all lanes get it): lane 0 takes the shared lock, opens a new chunk
@@ -138,8 +145,22 @@ __device__ __forceinline__ void acc_add(unsigned *hi, unsigned *lo, int l, long 
   atomicAdd(lo + l, neg ? 0u - w : w);
 }
 
-template <bool kFull, bool kNarrow>
-__global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_constant__ EvalParams p) {
+// kE: layers per lane (1, 2, 4, 8 = the next power of two >= L over 32), a template parameter so
+// the per-layer passes have compile-time trip counts and keep the layer deltas in registers
+// a flipped item: its precomputed signed split delta into the per-layer accumulators of the
+// warp's candidate (swap-in layer lin, release layer lout)
+__device__ __forceinline__ void flip_item(const uint2 *dv, const unsigned *lay2, int k, unsigned *dI_hi,
+                                          unsigned *dI_lo, unsigned *dO_hi, unsigned *dO_lo) {
+  const uint2 v = dv[k];
+  const unsigned lz = lay2[k], li = lz & 0xffffu, lo = lz >> 16;
+  atomicAdd(dI_hi + li, v.x);
+  atomicAdd(dI_lo + li, v.y);
+  atomicAdd(dO_hi + lo, v.x);
+  atomicAdd(dO_lo + lo, v.y);
+}
+
+template <bool kFull, bool kNarrow, int kE>
+__global__ void __launch_bounds__(kEvalThreads, CHM_EVAL_MINB) replay_kernel(const __grid_constant__ EvalParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ __align__(8) uint64_t s_mbar;
   __shared__ Key s_best[kEvalThreads / 32];
@@ -161,8 +182,12 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
   long long *s_SWR = s_DR + L;    // [L] (entry 0: total bytes of R)
   unsigned *r_hi = reinterpret_cast<unsigned *>(s_SWR + L);  // [2L] R accumulators (in, out)
   unsigned *r_lo = r_hi + 2 * L;                             // [2L]
+  // per item k: its delta against R (-S if R has it, +S else) split as acc_add splits it, and
+  // its layers lin | lout << 16 -- a flip is one 8 B + one 4 B shared load and four atomics
+  uint2 *s_dv = reinterpret_cast<uint2 *>(r_lo + 2 * L);     // [K]
+  unsigned *s_lay2 = reinterpret_cast<unsigned *>(s_dv + K);  // [K]
   // per-warp scratch: D[L] (int64) and the candidate's signed deltas vs R, split hi/lo 32-bit
-  unsigned char *wscr = reinterpret_cast<unsigned char *>(r_lo + 2 * L) + size_t(warp) * p.warp_scratch;
+  unsigned char *wscr = reinterpret_cast<unsigned char *>(s_dv) + p.item_table + size_t(warp) * p.warp_scratch;
   long long *s_D = reinterpret_cast<long long *>(wscr);
   unsigned *dI_hi = reinterpret_cast<unsigned *>(s_D + L);
   unsigned *dI_lo = dI_hi + L;
@@ -177,12 +202,17 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
   for (int l = lane; l < L; l += 32) { dI_hi[l] = 0u; dI_lo[l] = 0u; dO_hi[l] = 0u; dO_lo[l] = 0u; }
   __syncthreads();
   const bool seeded = p.kind == CHM_CAND_SEEDED, flip1 = p.kind == CHM_CAND_FLIP1;
-  if (seeded || flip1) {  // R = base
-    for (int k = tid; k < K; k += blockDim.x) {
-      if (!((p.base[k >> 6] >> (k & 63)) & 1ull)) continue;
+  for (int k = tid; k < K; k += blockDim.x) {
+    const bool in_r = (seeded || flip1) && ((p.base[k >> 6] >> (k & 63)) & 1ull);  // R = base
+    if (in_r) {
       acc_add(r_hi, r_lo, li_[k], S[k]);
       acc_add(r_hi + L, r_lo + L, lo_[k], S[k]);
     }
+    const long long v = in_r ? -S[k] : S[k];
+    const unsigned long long a = (unsigned long long)(v < 0 ? -v : v);
+    const unsigned h = unsigned(a >> 16), w = unsigned(a & 0xffffull);
+    s_dv[k] = make_uint2(v < 0 ? 0u - h : h, v < 0 ? 0u - w : w);
+    s_lay2[k] = unsigned(li_[k]) | (unsigned(lo_[k]) << 16);
   }
   __syncthreads();
   if (warp == 0) {  // cumulative R sums over layers
@@ -205,8 +235,13 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
   }
   __syncthreads();
 
-  Key best;
-  best.excess = LLONG_MAX; best.stall = 0.0; best.swapped = LLONG_MAX; best.index = ~0ull; best.peak = 0;
+  // the warp's best key lives in shared memory (lane 0 updates it once per candidate): ten
+  // fewer registers in every thread of the loop
+  if (lane == 0) {
+    Key b0;
+    b0.excess = LLONG_MAX; b0.stall = 0.0; b0.swapped = LLONG_MAX; b0.index = ~0ull; b0.peak = 0;
+    s_best[warp] = b0;
+  }
   // dynamic distribution in two levels: the CTA takes chunks of kChunk consecutive candidates
   // from a global counter, its warps take single candidates from the CTA's chunk under a
   // shared-memory lock (warps the scheduler favours do more, none idles at the end).  A CTA's
@@ -232,30 +267,14 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
           f4 &= f4 - 1;
           const int k = 4 * q + e;
           if (k >= K) break;
-          CHM_DCHECK(li_[k] < L && lo_[k] < L);
-          const bool was = (p.base[k >> 6] >> (k & 63)) & 1ull;
-          const long long v = was ? -S[k] : S[k];
-          acc_add(dI_hi, dI_lo, li_[k], v);
-          acc_add(dO_hi, dO_lo, lo_[k], v);
+          flip_item(s_dv, s_lay2, k, dI_hi, dI_lo, dO_hi, dO_lo);
         }
       }
     } else if (flip1) {  // one item differs from R: item g (none for g = K)
-      if (lane == 0 && g < uint64_t(K)) {
-        const int k = int(g);
-        CHM_DCHECK(li_[k] < L && lo_[k] < L);
-        const bool was = (p.base[k >> 6] >> (k & 63)) & 1ull;
-        const long long v = was ? -S[k] : S[k];
-        acc_add(dI_hi, dI_lo, li_[k], v);
-        acc_add(dO_hi, dO_lo, lo_[k], v);
-      }
+      if (lane == 0 && g < uint64_t(K)) flip_item(s_dv, s_lay2, int(g), dI_hi, dI_lo, dO_hi, dO_lo);
     } else {
-      for (int k = lane; k < K; k += 32) {
-        CHM_DCHECK(li_[k] < L && lo_[k] < L);
-        if (cand_bit(p, g, c, k)) {
-          acc_add(dI_hi, dI_lo, li_[k], S[k]);
-          acc_add(dO_hi, dO_lo, lo_[k], S[k]);
-        }
-      }
+      for (int k = lane; k < K; k += 32)  // R is empty: the table holds +S
+        if (cand_bit(p, g, c, k)) flip_item(s_dv, s_lay2, k, dI_hi, dI_lo, dO_hi, dO_lo);
     }
     __syncwarp();
     // layer l: in_l / out_l = R sums + deltas; D_l = CI(l) - CO(l) + out_l (CI / CO cumulative)
@@ -265,14 +284,28 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
     // its partial sum, one warp scan of the lane totals, then D, peak and the terms per layer.
     // The tree: 8 leaves per lane (zero past E), then the xor butterfly = the pairwise tree over
     // 256 zero-padded leaves, whose value equals R-stall's tree over the next power of two >= L.
-    const int E = p.lay_per_lane, lb = E * lane;
+    const int lb = kE * lane;
+    // this candidate's deltas of the lane's layers, kept in registers between the two passes
+    // (kE <= 4; at kE = 8 the second pass reads them again: 32 more registers would spill)
+    constexpr bool kKeep = kE <= 4;
+    constexpr int kR = kKeep ? kE : 1;
+    long long din[kR], dout[kR];
     long long tot = 0, lastd = 0;
-    for (int j = 0; j < E; j++) {
+#pragma unroll
+    for (int j = 0; j < kE; j++) {
       const int l = lb + j;
       if (l < L) {
-        const long long din = split_sum(dI_hi[l], dI_lo[l]), dout = split_sum(dO_hi[l], dO_lo[l]);
-        tot += din - (j ? lastd : 0);
-        lastd = dout;
+        const long long a = split_sum(dI_hi[l], dI_lo[l]), b = split_sum(dO_hi[l], dO_lo[l]);
+        if (kKeep) {
+          din[j % kR] = a;
+          dout[j % kR] = b;
+          dI_hi[l] = 0u; dI_lo[l] = 0u; dO_hi[l] = 0u; dO_lo[l] = 0u;  // ready for the next candidate
+        }
+        tot += a - (j ? lastd : 0);
+        lastd = b;
+      } else if (kKeep) {
+        din[j % kR] = 0;
+        dout[j % kR] = 0;
       }
     }
     const long long prev_last = __shfl_up_sync(0xffffffffu, lastd, 1);
@@ -284,33 +317,38 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
       if (lane >= o) inc += y;
     }
     long long run = inc - tot, pk = LLONG_MIN, swd = 0, prevd = lane ? prev_last : 0;
-    double ta = 0.0, tb = 0.0, tc = 0.0, td = 0.0;  // the lane's 8-leaf tree, folded as it grows
+    double t[kE];  // the lane's leaves of the pairwise tree
 #pragma unroll
-    for (int j = 0; j < 8; j++) {
-      double tj = 0.0;
+    for (int j = 0; j < kE; j++) {
+      t[j] = 0.0;
       const int l = lb + j;
-      if (j < E && l < L) {
-        const long long din = split_sum(dI_hi[l], dI_lo[l]), dout = split_sum(dO_hi[l], dO_lo[l]);
-        dI_hi[l] = 0u; dI_lo[l] = 0u; dO_hi[l] = 0u; dO_lo[l] = 0u;  // ready for the next candidate
-        run += din - prevd;
-        prevd = dout;
+      if (l < L) {
+        long long a, b;
+        if (kKeep) {
+          a = din[j % kR];
+          b = dout[j % kR];
+        } else {
+          a = split_sum(dI_hi[l], dI_lo[l]);
+          b = split_sum(dO_hi[l], dO_lo[l]);
+          dI_hi[l] = 0u; dI_lo[l] = 0u; dO_hi[l] = 0u; dO_lo[l] = 0u;  // ready for the next candidate
+        }
+        run += a - prevd;
+        prevd = b;
         const long long d = s_DR[l] + run;
         if (kFull) s_D[l] = d;
         pk = max(pk, mf0[l] + d);
-        const double x = __dsub_rn(__ddiv_rn(double(s_INR[l] + din + s_OUTR[l] + dout), p.tr.bw), bud[l]);
-        tj = x > 0.0 ? x : 0.0;
-        swd += dout;
+        const double x = __dsub_rn(__ddiv_rn(double(s_INR[l] + a + s_OUTR[l] + b), p.tr.bw), bud[l]);
+        t[j] = x > 0.0 ? x : 0.0;
+        swd += b;
       }
-      // ((t0 + t1) + (t2 + t3)) + ((t4 + t5) + (t6 + t7))
-      if (j == 0) ta = tj;
-      else if (j == 1) ta = __dadd_rn(ta, tj);
-      else if (j == 2) tb = tj;
-      else if (j == 3) ta = __dadd_rn(ta, __dadd_rn(tb, tj));
-      else if (j == 4) tc = tj;
-      else if (j == 5) tc = __dadd_rn(tc, tj);
-      else if (j == 6) td = tj;
-      else ta = __dadd_rn(ta, __dadd_rn(tc, __dadd_rn(td, tj)));
     }
+    // the lane's kE leaves pairwise -- (t0 + t1) + (t2 + t3) ... -- equal to the 8-leaf tree with
+    // zero leaves past kE (terms are >= +0, and x + 0 == x); then the xor butterfly over lanes
+#pragma unroll
+    for (int w = 1; w < kE; w <<= 1)
+#pragma unroll
+      for (int j = 0; j + w < kE; j += 2 * w) t[j] = __dadd_rn(t[j], t[j + w]);
+    const double ta = t[0];
     double st = ta;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) st = __dadd_rn(st, __shfl_xor_sync(0xffffffffu, st, o));
@@ -330,42 +368,46 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
       k.swapped = swp;
       k.index = g;
       k.peak = pk;
-      if (key_less(k, best)) best = k;
+      if (key_less(k, s_best[warp])) s_best[warp] = k;
     }
     if (kFull && kNarrow) {
       __syncwarp();  // s_D visible to the warp
       // F_P[i] = F0[i] + D[lay(i)] over blocks of 128 ops: lane l writes ops (2l, 2l+1) and
       // (64+2l, 65+2l), so each of the warp's two 16 B streaming stores covers 512 contiguous
       // bytes.  Per lane and block: one 16 B shared load of the four ops' F0 (int32 units,
-      // swizzled by the trace build), one 32-bit load of their layers (u8), D of each pair's
-      // layer (a second load only when a pair straddles a layer boundary).  32-bit shared
-      // addresses.
+      // swizzled by the trace build), one 8 B load of their D offsets (u16), D of each pair's
+      // layer (a second load only when a pair straddles a layer boundary); no store guards but
+      // in the ragged last block.  32-bit shared addresses.
       const int nb = (p.tr.N + 127) >> 7, np = p.row_pairs, unit = 1 << p.tr.f0_shift;
+      const int nbf = np >> 6;  // blocks whose 64 pairs all lie in the row: no store guards
       const unsigned sD = static_cast<unsigned>(__cvta_generic_to_shared(s_D));
       unsigned sF = static_cast<unsigned>(__cvta_generic_to_shared(f0)) + 16u * lane;
-      unsigned sL = static_cast<unsigned>(__cvta_generic_to_shared(img + p.tr.o_lay4)) + 4u * lane;
+      unsigned sL = static_cast<unsigned>(__cvta_generic_to_shared(img + p.tr.o_lay4)) + 8u * lane;
       long long *out = p.footprint + c * p.ld + 2 * lane;
-      int pr = lane;  // pair index of the first store
+      // per block: the four ops' F0 (16 B) and D offsets (8 B: u16 8 x layer each), D of each
+      // pair (a second load only where a pair straddles a layer boundary), two 16 B stores;
+      // the loop runs over whole blocks and one more iteration for the ragged last block
       for (int b = 0; b < nb; b++) {
         int f0x, f0y, f0z, f0w;
-        unsigned lz;
+        unsigned oa, ob;
         asm("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(f0x), "=r"(f0y), "=r"(f0z), "=r"(f0w) : "r"(sF));
-        asm("ld.shared.u32 %0, [%1];" : "=r"(lz) : "r"(sL));
-        const unsigned b0 = lz & 0xffu, b1 = (lz >> 8) & 0xffu, b2 = (lz >> 16) & 0xffu, b3 = lz >> 24;
-        CHM_DCHECK(b0 < unsigned(L) && b1 < unsigned(L) && b2 < unsigned(L) && b3 < unsigned(L));
-        long long d0, d2;
-        asm("ld.shared.s64 %0, [%1];" : "=l"(d0) : "r"(sD + 8u * b0));
-        asm("ld.shared.s64 %0, [%1];" : "=l"(d2) : "r"(sD + 8u * b2));
-        long long d1 = d0, d3 = d2;
-        if (b1 != b0) asm("ld.shared.s64 %0, [%1];" : "=l"(d1) : "r"(sD + 8u * b1));
-        if (b3 != b2) asm("ld.shared.s64 %0, [%1];" : "=l"(d3) : "r"(sD + 8u * b3));
+        asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(oa), "=r"(ob) : "r"(sL));
+        const unsigned a0 = oa & 0xffffu, a1 = oa >> 16, b0 = ob & 0xffffu, b1 = ob >> 16;
+        CHM_DCHECK(a0 < 8u * unsigned(L) && a1 < 8u * unsigned(L) && b0 < 8u * unsigned(L) && b1 < 8u * unsigned(L));
+        long long d0, d1, d2, d3;
+        asm("ld.shared.s64 %0, [%1];" : "=l"(d0) : "r"(sD + a0));
+        asm("ld.shared.s64 %0, [%1];" : "=l"(d2) : "r"(sD + b0));
+        d1 = d0;
+        d3 = d2;
+        if (a1 != a0) asm("ld.shared.s64 %0, [%1];" : "=l"(d1) : "r"(sD + a1));
+        if (b1 != b0) asm("ld.shared.s64 %0, [%1];" : "=l"(d3) : "r"(sD + b1));
+        const int pr = 64 * b + lane;
         // IMAD.WIDE, exact: |F0| < 2^31 units
-        if (pr < np) st_cs_v2(out, (long long)f0x * unit + d0, (long long)f0y * unit + d1);
-        if (pr + 32 < np) st_cs_v2(out + 64, (long long)f0z * unit + d2, (long long)f0w * unit + d3);
+        if (b < nbf || pr < np) st_cs_v2(out, (long long)f0x * unit + d0, (long long)f0y * unit + d1);
+        if (b < nbf || pr + 32 < np) st_cs_v2(out + 64, (long long)f0z * unit + d2, (long long)f0w * unit + d3);
         sF += 512u;
-        sL += 128u;
+        sL += 256u;
         out += 128;
-        pr += 64;
       }
     } else if (kFull) {
       __syncwarp();  // s_D visible to the warp
@@ -400,7 +442,6 @@ __global__ void __launch_bounds__(kEvalThreads, 2) replay_kernel(const __grid_co
     c = next_candidate(p.work, p.count, lane, &s_lock, &s_cbase, &s_left);
   }
   // warp keys -> CTA key -> the last CTA to finish reduces all CTA keys into *best
-  if (lane == 0) s_best[warp] = best;
   __syncthreads();
   __shared__ unsigned int s_last;
   if (tid == 0) {
@@ -467,13 +508,25 @@ chm_status launch_eval(chm_ctx *ctx, const EvalLaunch &L, cudaStream_t stream) {
   const bool fp = L.footprint != nullptr;
   const uint32_t stage = fp ? L.tr.full_bytes : L.tr.search_bytes;
   const uint32_t wscr16 = uint32_t((8 * size_t(Ly) + 16 * size_t(Ly) + 15) & ~size_t(15));
-  const size_t cta_tab = (32 * size_t(Ly) + 16 * size_t(Ly) + 15) & ~size_t(15);
-  const size_t smem = size_t(stage) + cta_tab + size_t(threads / 32) * wscr16;
+  const size_t cta_tab = 32 * size_t(Ly) + 16 * size_t(Ly);  // R tables (8 B aligned: 16 L is a multiple of 8)
+  const uint32_t item_table = uint32_t((12 * size_t(L.tr.K) + 15) & ~size_t(15));
+  const size_t smem = size_t(stage) + ((cta_tab + 15) & ~size_t(15)) + item_table + size_t(threads / 32) * wscr16;
   if (smem > 220 * 1024)
     CHM_FAIL(CHM_E_INVAL, "chm_eval_policies: trace image + scratch (%zu B) exceeds shared memory", smem);
   const bool narrow = L.tr.f0_narrow != 0;
-  auto kern = fp ? (narrow ? replay_kernel<true, true> : replay_kernel<true, false>) : replay_kernel<false, false>;
-  const int var = fp ? (narrow ? 2 : 1) : 0;
+  int P2 = 32, e_log = 0;
+  while (P2 < Ly) { P2 *= 2; e_log++; }  // E = P2 / 32 = 2^e_log (L <= 256: e_log <= 3)
+  using KernelFn = void (*)(EvalParams);
+  static const KernelFn table[3][4] = {
+      {replay_kernel<false, false, 1>, replay_kernel<false, false, 2>, replay_kernel<false, false, 4>,
+       replay_kernel<false, false, 8>},
+      {replay_kernel<true, false, 1>, replay_kernel<true, false, 2>, replay_kernel<true, false, 4>,
+       replay_kernel<true, false, 8>},
+      {replay_kernel<true, true, 1>, replay_kernel<true, true, 2>, replay_kernel<true, true, 4>,
+       replay_kernel<true, true, 8>}};
+  const int base_var = fp ? (narrow ? 2 : 1) : 0;
+  auto kern = table[base_var][e_log];
+  const int var = base_var * 4 + e_log;
   int per_sm = 0;
   CHM_CUDA(ensure_dyn_smem(reinterpret_cast<const void *>(kern), smem));
   if (ctx->eval_attr_smem[var] == smem) {
@@ -503,11 +556,8 @@ chm_status launch_eval(chm_ctx *ctx, const EvalLaunch &L, cudaStream_t stream) {
   p.stage_bytes = stage;
   p.warp_scratch = wscr16;
   p.row_pairs = (N + 1) / 2;
-  {
-    int P2 = 32;
-    while (P2 < Ly) P2 *= 2;
-    p.lay_per_lane = P2 / 32;
-  }
+  p.lay_per_lane = P2 / 32;
+  p.item_table = item_table;
   p.first = L.first;
   p.count = L.count;
   p.seed = L.seed;

@@ -240,7 +240,7 @@ chm_status chm::build_trace(chm_ctx *ctx, const IterRecord &R, const chm_trace_p
   const size_t n128 = (size_t(N) + 127) / 128 * 128;
   if (D.f0_narrow) {
     D.o_f0 = uint32_t(o); o += al(4 * n128);
-    D.o_lay4 = uint32_t(o); o += al(n128);
+    D.o_lay4 = uint32_t(o); o += al(2 * n128);  // per (block, lane): two pairs' D offsets
     D.full_bytes = uint32_t(o);
     D.o_lay = uint32_t(o); o += al(2 * size_t(N));  // EXPLICIT replay only (global memory)
   } else {
@@ -275,7 +275,9 @@ chm_status chm::build_trace(chm_ctx *ctx, const IterRecord &R, const chm_trace_p
       const size_t at = blk * 128 + 4 * lane + slot;
       const size_t src = std::min(i, size_t(N) - 1);  // padding: the last op's layer, F0 0
       f0u[at] = i < size_t(N) ? int32_t(tr->F0[i] >> D.f0_shift) : 0;
-      h[D.o_lay4 + at] = uint8_t(tr->lay_of_op[src]);  // L <= 256 (checked above)
+      // u16 byte offset 8 x layer of op i into the warp's D row, at (block, lane, slot)
+      const uint16_t off = uint16_t(8 * tr->lay_of_op[src]);  // L <= 256 (checked above)
+      std::memcpy(h + D.o_lay4 + 2 * at, &off, 2);
     }
     std::memcpy(h + D.o_f0, f0u.data(), 4 * n128);
   } else {
