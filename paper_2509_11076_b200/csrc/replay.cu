@@ -255,10 +255,11 @@ __global__ void __launch_bounds__(kEvalThreads, CHM_EVAL_MINB) replay_kernel(con
     const uint64_t g = p.first + c;
     // decode: only the items whose bit differs from R add a signed delta to their layers
     if (seeded) {  // one hash word per 4 items (reading R-seeded); flips are ~flip_thr rare
-      const uint64_t J = (uint64_t(K) + 3) >> 2;
+      const int J = (K + 3) >> 2;
       const unsigned thr16 = unsigned(p.flip_thr >> 48);
-      for (int q = lane; q < int(J); q += 32) {
-        const uint64_t w = mix64(p.seed ^ mix64(g * J + uint64_t(q)));
+      const uint64_t gJ = g * uint64_t(J);  // word q of candidate g hashes g * J + q
+      for (int q = lane; q < J; q += 32) {
+        const uint64_t w = mix64(p.seed ^ mix64(gJ + uint64_t(q)));
         unsigned f4 = 0;
 #pragma unroll
         for (int e = 0; e < 4; e++) f4 |= (unsigned((w >> (16 * e)) & 0xffffull) < thr16 ? 1u : 0u) << e;
