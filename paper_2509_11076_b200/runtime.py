@@ -1011,7 +1011,13 @@ class Runtime:
         self._join_prepin()
         t0 = time.perf_counter()
         gf, gb = self.groups
-        pt = self.ctx.trace_build(self.hbm_budget, self.m0, self.bw, gf, gb, t_iter=t_iter, omega=self.omega)
+        # C++ hook (above autograd): tensors a composite op creates and keeps past its end (e.g.
+        # cross-entropy's saved log-softmax, attention's logsumexp) are not records of their own,
+        # so the no-swap footprint comes from the allocator's bytes measured at every op of the
+        # Detailed step (Fig. 3; f0_source = 1) instead of the recorded events
+        f0_source = 1 if (self._nh is not None and not self.host_only) else 0
+        pt = self.ctx.trace_build(self.hbm_budget, self.m0, self.bw, gf, gb, t_iter=t_iter, omega=self.omega,
+                                  f0_source=f0_source)
         plan = dict(n_ops=pt.N, K=pt.K, peak0=pt.peak0, budget=pt.budget, t_iter=t_iter,
                     trace_ms=(time.perf_counter() - t0) * 1e3)
         if pt.K == 0 or pt.peak0 <= pt.budget:
