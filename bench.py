@@ -534,6 +534,65 @@ def _c1_block(chm, dev, reps):
     return res
 
 
+def _runtime_plan_block(chm, ctx, tr, pt, sd, C, dev, comp, compute, alone_ms, budget_pin):
+    """the runtime's planner on the step's trace (Algo. 2's grid, SEEDED around the empty mask,
+    the argmax-window base and Algo. 2's best, descent from each base's best; R-stall), then two
+    executed iterations of its plan under the step's compute"""
+    import torch
+    from paper_2509_11076_b200.runtime import _generate_all, _key3, default_bases, descend, seeded_multibase
+    t0 = time.perf_counter()
+    gen = _generate_all(pt)
+    best = torch.empty(5, dtype=torch.int64, device=dev)
+    gkeys = []
+    for g in gen:
+        ctx.eval_policies(pt, chm.EXPLICIT, 0, 1, best=best, item_offsets=np.array([0, len(g)], np.uint64), items=g)
+        gkeys.append(best.cpu().numpy().view(chm.BEST_DTYPE)[0].copy())
+    k, w, name, per = seeded_multibase(ctx, pt, default_bases(pt, gen, gkeys), C, sd["seed"], sd["flip_thr"], dev)
+    ends = [descend(ctx, pt, kx, wx, dev) for kx, wx in per.values()]
+    kd, wd, _ = min(ends, key=lambda e: _key3(e[0]))
+    plan_ms = (time.perf_counter() - t0) * 1e3
+    tb = pt.tables()
+    keep = [j for j in range(pt.K) if (int(wd[j // 64]) >> (j % 64)) & 1]
+    need = sum((int(tb["nbytes"][j]) + 511) // 512 * 512 for j in keep)
+    out = {"what": "the runtime's planner (SEEDED around 3 bases + descent from each, R-stall) on the step's trace, "
+                   "executed for 2 iterations under the same compute",
+           "plan_ms": plan_ms, "items": len(keep), "swap_bytes_per_direction": int(kd["swapped_bytes"]),
+           "excess": int(kd["excess"]), "predicted_stall_s": float(kd["stall"]),
+           "seeded_best": {"base": name, "stall_s": float(k["stall"]), "swapped": int(k["swapped_bytes"])}}
+    if need > budget_pin:
+        out["executed"] = f"skipped: the plan needs {need} B pinned"
+        return out
+    ctx.arena_reserve(max(need, 1 << 20))
+    ctx.policy_install(pt, wd)
+    pr = PolicyRun(chm, ctx, tr, pt, wd, keep, dev, 77)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    pr.execute(comp, chm.SWAP_KERNEL, compute)  # warm-up
+    ms, d2h, h2d = [], [], []
+    for _ in range(2):
+        torch.cuda.synchronize()
+        ev0.record(comp)
+        _, outs, ins = pr.execute(comp, chm.SWAP_KERNEL, compute)
+        ev1.record(comp)
+        torch.cuda.synchronize()
+        ms.append(ev0.elapsed_time(ev1))
+        d2h.append(sum(ctx.batch_elapsed_ms(b) for b in outs))
+        h2d.append(sum(ctx.batch_elapsed_ms(b) for b in ins))
+    bsw = pr.bytes_swap
+    rate = 2 * bsw / ((np.mean(d2h) + np.mean(h2d)) * 1e-3) if bsw else 0.0
+    items = pt.mask_items(wd)
+    ptm = ctx.trace_build(tr.budget, tr.static_bytes, rate if rate else tr.bw, tr.groups_fwd, tr.groups_bwd,
+                          t_iter=tr.t_iter)
+    out.update(exec_ms=float(np.mean(ms)), measured_stall_s=(float(np.mean(ms)) - alone_ms) * 1e-3,
+               estimated_at_measured_B=dict(zip(("r_stall", "per_direction", "timeline"),
+                                                ptm.stall_models(items).tolist())),
+               swap_GBps={"d2h": bsw / (np.mean(d2h) * 1e-3) / 1e9 if bsw else None,
+                          "h2d": bsw / (np.mean(h2d) * 1e-3) / 1e9 if bsw else None},
+               byte_exact_sample=pr.intact())
+    ptm.free()
+    pr.close()
+    return out
+
+
 def _swap_only_block(chm, args, dev, name, steps):
     """A config's policy executed without compute (swap-bound steps), kernel and copy engines:
     the r01 headline kept as a block (C2) beside the C3h line"""
@@ -877,6 +936,12 @@ def main():
     # release this run's HBM storage and pinned arena before the C2 block pins its own
     pr.close()
     arena_info = ctx.arena_placement()
+    # ---- the plan the runtime would install on this trace (reading R-bases + R-search: SEEDED
+    # around three bases, steepest descent from each base's best, R-stall ranking), executed
+    # under the same compute: its measured stall against its estimate (rank 0, N = 1)
+    if rank == 0 and P == 1 and not args.no_extras and compute is not None:
+        extras["runtime_plan"] = _runtime_plan_block(chm, ctx, tr, pt, sd, C, dev, comp, compute, alone[0],
+                                                     budget_pin)
     ctx.close()
     del fp, peak, stall
     torch.cuda.empty_cache()
