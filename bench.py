@@ -529,8 +529,37 @@ def _c1_block(chm, dev, reps):
             x.zero_()
         res[name] = {"us_per_round_trip": ms * 1e3, "GBps": 2 * total / (ms * 1e-3) / 1e9, "byte_exact": ok,
                      "calls_per_direction": 1 if flags == chm.SWAP_KERNEL else len(sizes)}
-    ctx.close()
+    # C1's evaluation measurement: all 2^K subsets in search mode, and full mode
+    # (64-op footprint rows) in a batch of 2^20 -- the oracle's brute force is in cpu_baseline
     res["kernel_speedup"] = res["copy_engines"]["us_per_round_trip"] / res["kernel"]["us_per_round_trip"]
+    ctx.close()
+    ev_ctx = chm.Context(device=dev.index)
+    ev_ctx.set_detailed(True)
+    chm.record_iteration(ev_ctx, tr)
+    ev_ctx.detect_seq_change(tr.t_iter)
+    ptd = ev_ctx.trace_build(tr.budget, tr.static_bytes, tr.bw, tr.groups_fwd, tr.groups_bwd, t_iter=tr.t_iter)
+    best = torch.empty(5, dtype=torch.int64, device=dev)
+    n_all = 1 << ptd.K
+    ld = (ptd.N + 1) // 2 * 2
+    fpb = torch.empty((1 << 20, ld), dtype=torch.int64, device=dev)
+    tm = {}
+    for name, cnt, fp_ in (("search_all_subsets", n_all, None), ("full_2^20", 1 << 20, fpb)):
+        ts = []
+        for it in range(4):
+            torch.cuda.synchronize()
+            e0.record(comp)
+            ev_ctx.eval_policies(ptd, chm.EXHAUSTIVE, 0, cnt, best=best, footprint=fp_, ld=ld if fp_ is not None else 0,
+                                 stream=comp)
+            e1.record(comp)
+            torch.cuda.synchronize()
+            if it:
+                ts.append(e0.elapsed_time(e1))
+        ms = float(np.median(ts))
+        tm[name] = {"candidates": cnt, "ms": ms, "candidates_per_s": cnt / (ms * 1e-3)}
+    bk = best.cpu().numpy().view(chm.BEST_DTYPE)[0]
+    res["eval"] = dict(tm, K=ptd.K, best_index=int(bk["index"]), best_excess=int(bk["excess"]))
+    ptd.free()
+    ev_ctx.close()
     return res
 
 

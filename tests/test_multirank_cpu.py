@@ -145,3 +145,32 @@ def test_runtime_under_ddp_two_ranks():
         per_step = np.diff([0] + o["matched"])
         assert set(per_step.tolist()) <= {0, o["items"]} and per_step[-1] == o["items"], o
         assert o["replicas_equal"]
+
+
+def _stagger_worker(rank, world, port, out):
+    import sys
+    import time
+    sys.path.insert(0, ROOT)
+    from paper_2509_11076_b200 import dist as D
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    def pin():  # stands in for the arena reservation: records when this rank ran
+        t0 = time.monotonic()
+        time.sleep(0.2)
+        return (t0, time.monotonic())
+    out[rank] = D.staggered(rank, world, pin, 2, dist.barrier)
+    dist.destroy_process_group()
+
+
+def test_staggered_pins_two_ranks_at_a_time():
+    """bench.py pins the arenas of a node's ranks two at a time (concurrent cudaHostRegister calls
+    of tens of GB serialise in the driver): with 4 ranks, ranks {0,1} run before {2,3}"""
+    world = 4
+    mgr = mp.get_context("spawn").Manager()
+    out = mgr.dict()
+    mp.spawn(_stagger_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    first_end = max(out[0][1], out[1][1])
+    second_start = min(out[2][0], out[3][0])
+    assert second_start >= first_end - 1e-3, dict(out)
