@@ -22,7 +22,7 @@ namespace {
 
 constexpr int kSwapThreads = 512;
 constexpr int kUnroll = 8;
-constexpr int kMisUnroll = 4;  // misaligned views: words per thread per pass
+constexpr int kMisUnroll = 8;  // misaligned views: words per thread per pass
 constexpr int kChunkShift = 16;  // 64 KiB = 512 threads x 8 x 16 B
 constexpr uint64_t kChunk = 1ull << kChunkShift;
 
@@ -107,47 +107,57 @@ __device__ __forceinline__ void copy_misaligned(const char *s, char *d, uint64_t
   const uint32_t r = uint32_t(reinterpret_cast<uintptr_t>(sb) & 15u);
   const int lane = threadIdx.x & 31;
   // kMisUnroll words per thread in flight per pass (zero-copy reads from host memory are
-  // latency-bound: 8 CTAs x 32 KiB in flight cover the link's bandwidth-delay product); words
-  // idx = pass + threadIdx.x + k * kSwapThreads
+  // latency-bound); words idx = pass + threadIdx.x + k * kSwapThreads.  The word after a
+  // warp's last lane is the next warp's lane-0 word (exchanged through shared memory), after
+  // the CTA's last thread the next k's thread-0 word; one extra load per pass for the last.
+  __shared__ int4 s_edge[kMisUnroll][kSwapThreads / 32];
+  const int warp = threadIdx.x >> 5, nwarp = kSwapThreads / 32;
   if (r == 0) {
     for (uint32_t p0 = 0; p0 < nvec; p0 += kMisUnroll * kSwapThreads) {
-    int4 v[kMisUnroll];
+      int4 v[kMisUnroll];
 #pragma unroll
-    for (int k = 0; k < kMisUnroll; k++) {
-      const uint32_t idx = p0 + threadIdx.x + k * kSwapThreads;
-      if (idx < nvec) v[k] = ld_nc_na(sb + 16ull * idx);
-    }
+      for (int k = 0; k < kMisUnroll; k++) {
+        const uint32_t idx = p0 + threadIdx.x + k * kSwapThreads;
+        if (idx < nvec) v[k] = ld_nc_na(sb + 16ull * idx);
+      }
 #pragma unroll
-    for (int k = 0; k < kMisUnroll; k++) {
-      const uint32_t idx = p0 + threadIdx.x + k * kSwapThreads;
-      if (idx < nvec) st_plain(db + 16ull * idx, v[k]);
-    }
+      for (int k = 0; k < kMisUnroll; k++) {
+        const uint32_t idx = p0 + threadIdx.x + k * kSwapThreads;
+        if (idx < nvec) st_plain(db + 16ull * idx, v[k]);
+      }
     }
   } else {
     const char *as = sb - r;  // aligned source words as[0 .. nvec] hold the body's bytes
     const int q = int(r >> 2);
     const unsigned sh = 8u * (r & 3u);
     for (uint32_t p0 = 0; p0 < nvec; p0 += kMisUnroll * kSwapThreads) {
-    int4 a[kMisUnroll], e[kMisUnroll];  // e: the word after the warp's last one (lane 31 only)
+      int4 a[kMisUnroll];
+      int4 last = make_int4(0, 0, 0, 0);
 #pragma unroll
-    for (int k = 0; k < kMisUnroll; k++) {
-      const uint32_t idx = p0 + threadIdx.x + k * kSwapThreads;
-      a[k] = make_int4(0, 0, 0, 0);
-      e[k] = a[k];
-      if (idx <= nvec) a[k] = ld_nc_na(as + 16ull * idx);
-      if (lane == 31 && idx + 1 <= nvec) e[k] = ld_nc_na(as + 16ull * (idx + 1));
-    }
+      for (int k = 0; k < kMisUnroll; k++) {
+        const uint32_t idx = p0 + threadIdx.x + k * kSwapThreads;
+        a[k] = make_int4(0, 0, 0, 0);
+        if (idx <= nvec) a[k] = ld_nc_na(as + 16ull * idx);
+      }
+      const uint32_t after = p0 + kMisUnroll * kSwapThreads;  // the word after the pass
+      if (threadIdx.x == kSwapThreads - 1 && after <= nvec) last = ld_nc_na(as + 16ull * after);
+      if (lane == 0) {
 #pragma unroll
-    for (int k = 0; k < kMisUnroll; k++) {
-      const uint32_t idx = p0 + threadIdx.x + k * kSwapThreads;
-      int4 b;
-      b.x = __shfl_down_sync(0xffffffffu, a[k].x, 1);
-      b.y = __shfl_down_sync(0xffffffffu, a[k].y, 1);
-      b.z = __shfl_down_sync(0xffffffffu, a[k].z, 1);
-      b.w = __shfl_down_sync(0xffffffffu, a[k].w, 1);
-      if (lane == 31) b = e[k];
-      if (idx < nvec) st_plain(db + 16ull * idx, shift_combine(a[k], b, q, sh));
-    }
+        for (int k = 0; k < kMisUnroll; k++) s_edge[k][warp] = a[k];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < kMisUnroll; k++) {
+        const uint32_t idx = p0 + threadIdx.x + k * kSwapThreads;
+        int4 b;
+        b.x = __shfl_down_sync(0xffffffffu, a[k].x, 1);
+        b.y = __shfl_down_sync(0xffffffffu, a[k].y, 1);
+        b.z = __shfl_down_sync(0xffffffffu, a[k].z, 1);
+        b.w = __shfl_down_sync(0xffffffffu, a[k].w, 1);
+        if (lane == 31) b = warp + 1 < nwarp ? s_edge[k][warp + 1] : (k + 1 < kMisUnroll ? s_edge[k + 1][0] : last);
+        if (idx < nvec) st_plain(db + 16ull * idx, shift_combine(a[k], b, q, sh));
+      }
+      __syncthreads();  // s_edge is rewritten by the next pass
     }
   }
   const uint32_t tail = uint32_t(body & 15);
