@@ -488,6 +488,48 @@ class PolicyRun:
         self.storage.clear()
 
 
+def _eval_strong_block(chm, D, dev, comp, rank, P, use_dist, barrier, max_over_ranks, total=10_000_000):
+    """the evaluation's strong scaling: C5's trace, `total` SEEDED candidates (search mode)
+    sharded over the P ranks, the per-rank launch + the argmin exchange timed with CUDA events,
+    the slowest rank's time"""
+    import torch
+    tr = W.CONFIGS["C5"]()
+    sd = W.SEEDED["C5"]
+    ctx = chm.Context(device=dev.index)
+    ctx.set_detailed(True)
+    chm.record_iteration(ctx, tr)
+    ctx.detect_seq_change(tr.t_iter)
+    pt = ctx.trace_build(tr.budget, tr.static_bytes, tr.bw, tr.groups_fwd, tr.groups_bwd, t_iter=tr.t_iter)
+    lo, cnt = D.shard(total, P, rank)
+    bl = torch.empty(5, dtype=torch.int64, device=dev)
+    ga = torch.empty(5 * P, dtype=torch.int64, device=dev)
+    bg = torch.empty(5, dtype=torch.int64, device=dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ts = []
+    for it in range(5):
+        barrier()
+        torch.cuda.synchronize()
+        torch.cuda._sleep(1_000_000)
+        e0.record(comp)
+        ctx.eval_policies(pt, chm.SEEDED, lo, cnt, best=bl, seed=sd["seed"], flip_thr=sd["flip_thr"], stream=comp)
+        if use_dist:
+            D.argmin_exchange(ctx, bl, ga, bg, P, stream=comp)
+        else:
+            bg.copy_(bl)
+        e1.record(comp)
+        torch.cuda.synchronize()
+        if it:
+            ts.append(e0.elapsed_time(e1))
+    t = max_over_ranks(float(np.median(ts)))
+    b = bg.cpu().numpy().view(chm.BEST_DTYPE)[0]
+    ctx.release_scratch()
+    pt.free()
+    ctx.close()
+    return {"workload": tr.meta["config"], "candidates_total": total, "candidates_per_rank": cnt,
+            "mode": "search", "ms": t, "candidates_per_s": total / (t * 1e-3), "scaling": "strong",
+            "best_index": int(b["index"]), "includes": "each rank's launch + NCCL all-gather + device argmin (N > 1)"}
+
+
 def _c1_block(chm, dev, reps):
     """C1's execution measurement: the 24 activations of the tiny trace (4 KiB -
     4 MiB) out and back in as one batch per direction, `reps` times: the swap kernel (one launch
@@ -906,6 +948,10 @@ def main():
     est["at_measured_B"] = dict(zip(("r_stall", "per_direction", "timeline"), ptm.stall_models(items).tolist()))
     ptm.free()
 
+    # ---- candidate policies evaluated / s at this N (the metric's second half):
+    # C5's per-rank trace, 10^7 SEEDED candidates in search mode split over the ranks
+    # (strong scaling), each rank's shard + the NCCL argmin, max over ranks
+    strong = _eval_strong_block(chm, D, dev, comp, rank, P, use_dist, barrier, max_over_ranks)
     # ---- rank-0 blocks beside the line: Algo. 2's grid, the timeline ranking, the C4 re-plan,
     # C1's small tensors, C2 (N = 1: host RAM)
     extras = {}
@@ -1048,6 +1094,7 @@ def main():
         },
         "argmin_exchange_us": t_argmin * 1e3 if use_dist else None,
         "eval": {"candidates_per_s": C / (t_eval * 1e-3), "ms_per_launch": t_eval, "unit": "candidates/s"},
+        "eval_strong": strong,
         "overlap": {
             "exec_ms": {"kernel": t_exec, "copy_engines": ce[0], "compute_alone": alone[0]},
             "swap_GBps_during_overlap": {"kernel": {"d2h": per_dir[0], "h2d": per_dir[1]},
