@@ -1075,6 +1075,8 @@ def main():
             "peak_source": "nominal PCIe Gen5 x16 per direction (no measured host-link peak in MEASURED_PEAKS.json)",
             "d2h_GBps": per_dir[0], "h2d_GBps": per_dir[1],
             "what": "swap-stream busy time of the kernel's batches during the overlapped step",
+            "per_step_GBps": {"d2h": [round(bytes_swap / (x * 1e-3) / 1e9, 2) for x in d2h_ms],
+                              "h2d": [round(bytes_swap / (x * 1e-3) / 1e9, 2) for x in h2d_ms]},
             "frac_of_copy_engines": ({"d2h": per_dir[0] / ce_dir[0], "h2d": per_dir[1] / ce_dir[1],
                                       "what": "vs the same batches on the copy engines (one cudaMemcpyAsync per "
                                               "tensor) under the same compute, this run"} if ce_dir else None),
