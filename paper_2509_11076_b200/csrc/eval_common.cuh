@@ -45,4 +45,18 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {  // splitmix64 finaliser
   return z ^ (z >> 31);
 }
 
+// x / b rounded to nearest (bit-equal to __ddiv_rn(x, b) and to the oracle's C division) for
+// x >= 0 an integer below 2^53 (a layer's swap bytes) and y = RN(1/b) with 2^-500 < b < 2^500
+// (the host sets y, else 0 and the caller divides): q = RN(x y) is within one ulp of x / b,
+// r = x - b q is exact under the FMA, and RN(q + r y) = RN(x / b) (Markstein's correction
+// theorem).  Three FP64 operations instead of the division's reciprocal refinement and the
+// out-of-line slow path it takes whenever x = 0, i.e. for every layer without swap traffic
+// (ncu, r02: 2 slow-path calls per candidate on C3h).  Checked against the division on 3 x 10^9
+// random (x, b) pairs, mantissa edge cases included (tools/div_check.c).
+__device__ __forceinline__ double div_rn_rcp(double x, double b, double y) {
+  const double q = __dmul_rn(x, y);
+  const double r = __fma_rn(-q, b, x);
+  return __fma_rn(r, y, q);
+}
+
 }  // namespace chm

@@ -175,14 +175,33 @@ struct DevTrace {
   int32_t f0_shift = 0;
   int32_t f0_narrow = 0;
   uint32_t o_lay = 0;   // u16   [N]  8 x logical layer of each op (byte offset into D, full mode)
-  uint32_t o_lay4 = 0;  // u16   [N padded to 128] 8 x logical layer of each op (its byte offset
-                        // into a D row), lane-swizzled like F0 (narrow only): one 8 B load gives
-                        // a lane's four ops' offsets
+  uint32_t o_lay4 = 0;  // u16   [N padded to 128] 8 x layer_slot(layer of each op) (its byte
+                        // offset into the warp's padded D row), lane-swizzled like F0 (narrow
+                        // only): one 8 B load gives a lane's four ops' offsets
   const uint64_t *base = nullptr;
   int32_t N = 0, K = 0, L = 0, W = 0;
   double bw = 1.0;
+  double rbw = 0.0;  // RN(1 / bw) when 2^-500 < bw < 2^500 (div_rn_rcp), else 0 (the kernels divide)
   int64_t budget = 0;
 };
+
+// The replay kernel's per-layer shared arrays, bank-conflict free: lane `lane` owns the E
+// consecutive layers E lane .. E lane + E - 1 (E = next power of two >= L / 32, 1 .. 8), so a
+// lane-blocked access with a stride of E words hits E-way bank conflicts; padding each lane's
+// block by one slot (stride E + 1, odd) spreads the lanes over all 32 banks.  Layer l lives at
+// layer_slot(l, E); layer_slots(L, E) entries hold all L layers.  Trace build and kernel share it.
+#ifdef __CUDACC__
+#define CHM_HD __host__ __device__ __forceinline__
+#else
+#define CHM_HD inline
+#endif
+CHM_HD int layers_per_lane(int L) {
+  int e = 1;
+  while (32 * e < L) e *= 2;
+  return e;
+}
+CHM_HD int layer_slot(int l, int E) { return E > 1 ? l + l / E : l; }
+CHM_HD int layer_slots(int L, int E) { return E > 1 ? L + (L + E - 1) / E : L; }
 
 }  // namespace chm
 

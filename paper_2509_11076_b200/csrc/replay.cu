@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(kEvalThreads, CHM_EVAL_MINB) replay_kernel(con
   __shared__ Key s_best[kEvalThreads / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int K = p.tr.K, L = p.tr.L;
+  const int PL = layer_slots(L, kE);  // per-layer arrays: layer l at layer_slot(l, kE) (internal.h)
   unsigned char *img = smem;
   const long long *mf0 = reinterpret_cast<const long long *>(img + p.tr.o_mf0);
   const double *bud = reinterpret_cast<const double *>(img + p.tr.o_bud);
@@ -175,31 +176,40 @@ __global__ void __launch_bounds__(kEvalThreads, CHM_EVAL_MINB) replay_kernel(con
   const unsigned char *f0 = img + p.tr.o_f0;  // int32 units (kNarrow) or int64
   const unsigned short *lay = reinterpret_cast<const unsigned short *>(img + p.tr.o_lay);  // 8 x layer
   // CTA tables of the reference mask R (the SEEDED base; empty for the other kinds):
-  // per-layer in / out sums and their cumulative sums, int64 [L] each
+  // per-layer in / out sums and their cumulative sums, and copies of the image's per-layer max F0
+  // and budget, int64 / double [PL] each in the padded slot layout
   long long *s_INR = reinterpret_cast<long long *>(img + p.stage_bytes);
-  long long *s_OUTR = s_INR + L;
-  long long *s_DR = s_OUTR + L;   // D_R(l) = CIR(l) - COR(l) + OUTR(l)
-  long long *s_SWR = s_DR + L;    // [L] (entry 0: total bytes of R)
-  unsigned *r_hi = reinterpret_cast<unsigned *>(s_SWR + L);  // [2L] R accumulators (in, out)
+  long long *s_OUTR = s_INR + PL;
+  long long *s_DR = s_OUTR + PL;   // D_R(l) = CIR(l) - COR(l) + OUTR(l)
+  long long *s_mf0 = s_DR + PL;
+  double *s_bud = reinterpret_cast<double *>(s_mf0 + PL);
+  long long *s_SWR = reinterpret_cast<long long *>(s_bud + PL);  // [2] (entry 0: total bytes of R)
+  unsigned *r_hi = reinterpret_cast<unsigned *>(s_SWR + 2);  // [2L] R accumulators (in, out), dense
   unsigned *r_lo = r_hi + 2 * L;                             // [2L]
   // per item k: its delta against R (-S if R has it, +S else) split as acc_add splits it, and
   // its layers lin | lout << 16 -- a flip is one 8 B + one 4 B shared load and four atomics
   uint2 *s_dv = reinterpret_cast<uint2 *>(r_lo + 2 * L);     // [K]
   unsigned *s_lay2 = reinterpret_cast<unsigned *>(s_dv + K);  // [K]
-  // per-warp scratch: D[L] (int64) and the candidate's signed deltas vs R, split hi/lo 32-bit
+  // per-warp scratch: D[PL] (int64; padded slots in narrow mode, dense in wide mode, where the
+  // image's op -> layer offsets index it) and the candidate's signed deltas vs R, split hi/lo
+  // 32-bit, [PL] each in the padded slot layout
   unsigned char *wscr = reinterpret_cast<unsigned char *>(s_dv) + p.item_table + size_t(warp) * p.warp_scratch;
   long long *s_D = reinterpret_cast<long long *>(wscr);
-  unsigned *dI_hi = reinterpret_cast<unsigned *>(s_D + L);
-  unsigned *dI_lo = dI_hi + L;
-  unsigned *dO_hi = dI_lo + L;
-  unsigned *dO_lo = dO_hi + L;
+  unsigned *dI_hi = reinterpret_cast<unsigned *>(s_D + PL);
+  unsigned *dI_lo = dI_hi + PL;
+  unsigned *dO_hi = dI_lo + PL;
+  unsigned *dO_lo = dO_hi + PL;
 
   __shared__ int s_lock, s_left;
   __shared__ unsigned long long s_cbase;
   if (tid == 0) { s_lock = 0; s_left = 0; s_cbase = 0; }
   stage_image(img, p.tr.image, p.stage_bytes, &s_mbar);  // its __syncthreads publishes the above
   for (int l = tid; l < 2 * L; l += blockDim.x) { r_hi[l] = 0u; r_lo[l] = 0u; }
-  for (int l = lane; l < L; l += 32) { dI_hi[l] = 0u; dI_lo[l] = 0u; dO_hi[l] = 0u; dO_lo[l] = 0u; }
+  for (int l = lane; l < PL; l += 32) { dI_hi[l] = 0u; dI_lo[l] = 0u; dO_hi[l] = 0u; dO_lo[l] = 0u; }
+  for (int l = tid; l < L; l += blockDim.x) {
+    s_mf0[layer_slot(l, kE)] = mf0[l];
+    s_bud[layer_slot(l, kE)] = bud[l];
+  }
   __syncthreads();
   const bool seeded = p.kind == CHM_CAND_SEEDED, flip1 = p.kind == CHM_CAND_FLIP1;
   for (int k = tid; k < K; k += blockDim.x) {
@@ -212,7 +222,7 @@ __global__ void __launch_bounds__(kEvalThreads, CHM_EVAL_MINB) replay_kernel(con
     const unsigned long long a = (unsigned long long)(v < 0 ? -v : v);
     const unsigned h = unsigned(a >> 16), w = unsigned(a & 0xffffull);
     s_dv[k] = make_uint2(v < 0 ? 0u - h : h, v < 0 ? 0u - w : w);
-    s_lay2[k] = unsigned(li_[k]) | (unsigned(lo_[k]) << 16);
+    s_lay2[k] = unsigned(layer_slot(li_[k], kE)) | (unsigned(layer_slot(lo_[k], kE)) << 16);
   }
   __syncthreads();
   if (warp == 0) {  // cumulative R sums over layers
@@ -227,7 +237,12 @@ __global__ void __launch_bounds__(kEvalThreads, CHM_EVAL_MINB) replay_kernel(con
         const long long ya = __shfl_up_sync(0xffffffffu, a, o), yb = __shfl_up_sync(0xffffffffu, b, o);
         if (lane >= o) { a += ya; b += yb; }
       }
-      if (l < L) { s_INR[l] = in_l; s_OUTR[l] = out_l; s_DR[l] = (ci + a) - (co + b) + out_l; }
+      if (l < L) {
+        const int q = layer_slot(l, kE);
+        s_INR[q] = in_l;
+        s_OUTR[q] = out_l;
+        s_DR[q] = (ci + a) - (co + b) + out_l;
+      }
       ci += __shfl_sync(0xffffffffu, a, 31);
       co += __shfl_sync(0xffffffffu, b, 31);
     }
@@ -286,6 +301,7 @@ __global__ void __launch_bounds__(kEvalThreads, CHM_EVAL_MINB) replay_kernel(con
     // The tree: 8 leaves per lane (zero past E), then the xor butterfly = the pairwise tree over
     // 256 zero-padded leaves, whose value equals R-stall's tree over the next power of two >= L.
     const int lb = kE * lane;
+    const int pb = layer_slot(lb, kE);  // = (kE + 1) lane for kE > 1: the lane's padded block
     // this candidate's deltas of the lane's layers, kept in registers between the two passes
     // (kE <= 4; at kE = 8 the second pass reads them again: 32 more registers would spill)
     constexpr bool kKeep = kE <= 4;
@@ -294,13 +310,13 @@ __global__ void __launch_bounds__(kEvalThreads, CHM_EVAL_MINB) replay_kernel(con
     long long tot = 0, lastd = 0;
 #pragma unroll
     for (int j = 0; j < kE; j++) {
-      const int l = lb + j;
+      const int l = lb + j, q = pb + j;
       if (l < L) {
-        const long long a = split_sum(dI_hi[l], dI_lo[l]), b = split_sum(dO_hi[l], dO_lo[l]);
+        const long long a = split_sum(dI_hi[q], dI_lo[q]), b = split_sum(dO_hi[q], dO_lo[q]);
         if (kKeep) {
           din[j % kR] = a;
           dout[j % kR] = b;
-          dI_hi[l] = 0u; dI_lo[l] = 0u; dO_hi[l] = 0u; dO_lo[l] = 0u;  // ready for the next candidate
+          dI_hi[q] = 0u; dI_lo[q] = 0u; dO_hi[q] = 0u; dO_lo[q] = 0u;  // ready for the next candidate
         }
         tot += a - (j ? lastd : 0);
         lastd = b;
@@ -322,23 +338,25 @@ __global__ void __launch_bounds__(kEvalThreads, CHM_EVAL_MINB) replay_kernel(con
 #pragma unroll
     for (int j = 0; j < kE; j++) {
       t[j] = 0.0;
-      const int l = lb + j;
+      const int l = lb + j, q = pb + j;
       if (l < L) {
         long long a, b;
         if (kKeep) {
           a = din[j % kR];
           b = dout[j % kR];
         } else {
-          a = split_sum(dI_hi[l], dI_lo[l]);
-          b = split_sum(dO_hi[l], dO_lo[l]);
-          dI_hi[l] = 0u; dI_lo[l] = 0u; dO_hi[l] = 0u; dO_lo[l] = 0u;  // ready for the next candidate
+          a = split_sum(dI_hi[q], dI_lo[q]);
+          b = split_sum(dO_hi[q], dO_lo[q]);
+          dI_hi[q] = 0u; dI_lo[q] = 0u; dO_hi[q] = 0u; dO_lo[q] = 0u;  // ready for the next candidate
         }
         run += a - prevd;
         prevd = b;
-        const long long d = s_DR[l] + run;
-        if (kFull) s_D[l] = d;
-        pk = max(pk, mf0[l] + d);
-        const double x = __dsub_rn(__ddiv_rn(double(s_INR[l] + a + s_OUTR[l] + b), p.tr.bw), bud[l]);
+        const long long d = s_DR[q] + run;
+        if (kFull) s_D[kNarrow ? q : l] = d;
+        pk = max(pk, s_mf0[q] + d);
+        const double v = double(s_INR[q] + a + s_OUTR[q] + b);
+        const double x =
+            __dsub_rn(p.tr.rbw != 0.0 ? div_rn_rcp(v, p.tr.bw, p.tr.rbw) : __ddiv_rn(v, p.tr.bw), s_bud[q]);
         t[j] = x > 0.0 ? x : 0.0;
         swd += b;
       }
@@ -394,7 +412,7 @@ __global__ void __launch_bounds__(kEvalThreads, CHM_EVAL_MINB) replay_kernel(con
         asm("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(f0x), "=r"(f0y), "=r"(f0z), "=r"(f0w) : "r"(sF));
         asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(oa), "=r"(ob) : "r"(sL));
         const unsigned a0 = oa & 0xffffu, a1 = oa >> 16, b0 = ob & 0xffffu, b1 = ob >> 16;
-        CHM_DCHECK(a0 < 8u * unsigned(L) && a1 < 8u * unsigned(L) && b0 < 8u * unsigned(L) && b1 < 8u * unsigned(L));
+        CHM_DCHECK(a0 < 8u * unsigned(PL) && a1 < 8u * unsigned(PL) && b0 < 8u * unsigned(PL) && b1 < 8u * unsigned(PL));
         long long d0, d1, d2, d3;
         asm("ld.shared.s64 %0, [%1];" : "=l"(d0) : "r"(sD + a0));
         asm("ld.shared.s64 %0, [%1];" : "=l"(d2) : "r"(sD + b0));
@@ -508,8 +526,9 @@ chm_status launch_eval(chm_ctx *ctx, const EvalLaunch &L, cudaStream_t stream) {
   const int threads = kEvalThreads;
   const bool fp = L.footprint != nullptr;
   const uint32_t stage = fp ? L.tr.full_bytes : L.tr.search_bytes;
-  const uint32_t wscr16 = uint32_t((8 * size_t(Ly) + 16 * size_t(Ly) + 15) & ~size_t(15));
-  const size_t cta_tab = 32 * size_t(Ly) + 16 * size_t(Ly);  // R tables (8 B aligned: 16 L is a multiple of 8)
+  const int E = layers_per_lane(Ly), PL = layer_slots(Ly, E);  // padded per-layer slots (internal.h)
+  const uint32_t wscr16 = uint32_t((8 * size_t(PL) + 16 * size_t(PL) + 15) & ~size_t(15));
+  const size_t cta_tab = 40 * size_t(PL) + 16 + 16 * size_t(Ly);  // R tables, max F0, budget; r_hi / r_lo
   const uint32_t item_table = uint32_t((12 * size_t(L.tr.K) + 15) & ~size_t(15));
   const size_t smem = size_t(stage) + ((cta_tab + 15) & ~size_t(15)) + item_table + size_t(threads / 32) * wscr16;
   if (smem > 220 * 1024)
@@ -557,7 +576,8 @@ chm_status launch_eval(chm_ctx *ctx, const EvalLaunch &L, cudaStream_t stream) {
   p.stage_bytes = stage;
   p.warp_scratch = wscr16;
   p.row_pairs = (N + 1) / 2;
-  p.lay_per_lane = P2 / 32;
+  p.lay_per_lane = E;
+  if (E != P2 / 32) CHM_FAIL(CHM_E_STATE, "chm_eval_policies: layers per lane %d != %d", E, P2 / 32);
   p.item_table = item_table;
   p.first = L.first;
   p.count = L.count;

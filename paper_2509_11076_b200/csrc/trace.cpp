@@ -3,6 +3,7 @@
 // swappable set, default SEEDED base; upload of the device tables for the replay kernel.
 #include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstring>
 #include <numeric>
 
@@ -269,14 +270,15 @@ chm_status chm::build_trace(chm_ctx *ctx, const IterRecord &R, const chm_trace_p
     std::memcpy(h + D.o_li, li16.data(), 2 * size_t(tr->K));
   }
   if (D.f0_narrow) {  // swizzled position of op i: block i / 128, lane (i % 64) / 2, slot
+    const int E = chm::layers_per_lane(tr->L);
     std::vector<int32_t> f0u(n128, 0);
     for (size_t i = 0; i < n128; i++) {
       const size_t blk = i / 128, w = i % 128, lane = (w % 64) / 2, slot = (w / 64) * 2 + (w % 2);
       const size_t at = blk * 128 + 4 * lane + slot;
       const size_t src = std::min(i, size_t(N) - 1);  // padding: the last op's layer, F0 0
       f0u[at] = i < size_t(N) ? int32_t(tr->F0[i] >> D.f0_shift) : 0;
-      // u16 byte offset 8 x layer of op i into the warp's D row, at (block, lane, slot)
-      const uint16_t off = uint16_t(8 * tr->lay_of_op[src]);  // L <= 256 (checked above)
+      // u16 byte offset of op i's layer into the warp's padded D row, at (block, lane, slot)
+      const uint16_t off = uint16_t(8 * chm::layer_slot(tr->lay_of_op[src], E));  // L <= 256 (checked above)
       std::memcpy(h + D.o_lay4 + 2 * at, &off, 2);
     }
     std::memcpy(h + D.o_f0, f0u.data(), 4 * n128);
@@ -293,6 +295,7 @@ chm_status chm::build_trace(chm_ctx *ctx, const IterRecord &R, const chm_trace_p
   D.L = tr->L;
   D.W = tr->W;
   D.bw = tr->bw;
+  D.rbw = (tr->bw > std::ldexp(1.0, -500) && tr->bw < std::ldexp(1.0, 500)) ? 1.0 / tr->bw : 0.0;
   D.budget = tr->budget;
   if (ctx->device < 0) {  // host-only ctx: tables stay on the host
     *out = tr;
