@@ -258,6 +258,36 @@ def eval_explicit(model: "Model", lists, budget: int = None, first_index: int = 
     return dict(peak=peak, stall=stall, swapped=sw, footprint=F, best=best)
 
 
+def descend(model: "Model", words, max_rounds: int = 4096, budget: Optional[int] = None, nthreads: int = 16):
+    """Steepest single-flip descent from a mask (reading R-search; the planner's
+    search around the evaluator, "selects the one with the best runtime performance"),
+    written out plainly: each round builds the K masks that differ from the current one in one
+    bit, scores them all with the oracle's MASKS evaluation (R-stall, §8(c).5) and takes the
+    argmin of (excess, stall, swapped, k) (§8(c).6); it moves there if that key's first three
+    fields are lexicographically smaller than the current mask's, else it stops.  Returns
+    (end words, end key (excess, stall, swapped), rounds)."""
+    K = model.K
+    W = (K + 63) // 64
+    cur = np.array(words, np.uint64).reshape(W).copy()
+    b = int(model.trace.budget if budget is None else budget)
+    k0 = model.eval(MASKS, 0, 1, words=cur, budget=b)["best"]
+    key = (int(k0.excess), float(k0.stall), int(k0.swapped))
+    rounds = 0
+    while rounds < max_rounds and K > 0:
+        nb = np.repeat(cur[None, :], K, axis=0)
+        for k in range(K):
+            nb[k, k // 64] ^= np.uint64(1 << (k % 64))
+        best = model.eval(MASKS, 0, K, words=nb.reshape(-1), budget=b, nthreads=nthreads)["best"]
+        nk = (int(best.excess), float(best.stall), int(best.swapped))
+        if not nk < key:
+            break
+        k = int(best.index)
+        cur[k // 64] ^= np.uint64(1 << (k % 64))
+        key = nk
+        rounds += 1
+    return cur, key, rounds
+
+
 def splitmix64(z: int) -> int:
     return lib().orc_splitmix64(z)
 
