@@ -342,12 +342,16 @@ class Compute:
         return float(sum(a.elapsed_time(b) for a, b in self.ev))
 
 
+def _k3(k):
+    return (int(k["excess"]), float(k["stall"]), int(k["swapped_bytes"]))
+
+
 def _replan_c4(chm, dev, comp):
     """C4 (Llama-2 13B, s = 8192 after a switch): record one Detailed iteration through
     chm_record_op, build the trace, evaluate 10^5 SEEDED candidates, run Algo. 2's grid (replayed
-    as EXPLICIT candidates), refine by steepest descent (MASKS), install -- each step timed"""
+    as EXPLICIT candidates), refine by steepest descent (chm_descend), install -- each step timed"""
     import torch
-    from paper_2509_11076_b200.runtime import _generate_all, descend
+    from paper_2509_11076_b200.runtime import _generate_all, descend, device_descend
     tr = W.llama2_13b(8192)
     ctx = chm.Context(device=dev.index, host_arena_bytes=1 << 20)
     ids = np.array([(1 << 60) + int(p) for p in tr.ptr], np.uint64)
@@ -381,9 +385,13 @@ def _replan_c4(chm, dev, comp):
     gk = gbest.cpu().numpy().view(chm.BEST_DTYPE)[0]
     out["generator_ms"] = (time.perf_counter() - t0) * 1e3
     t0 = time.perf_counter()
-    words = pt.candidate_mask(chm.SEEDED, int(bk["index"]), seed=sd["seed"], flip_thr=sd["flip_thr"])
-    dk, words, rounds = descend(ctx, pt, bk, words, dev)
+    w0 = pt.candidate_mask(chm.SEEDED, int(bk["index"]), seed=sd["seed"], flip_thr=sd["flip_thr"])
+    dk, words, rounds = device_descend(ctx, pt, [w0], dev)[0]  # one chm_descend launch
     out["descent_ms"] = (time.perf_counter() - t0) * 1e3
+    t0 = time.perf_counter()
+    hk, _, _ = descend(ctx, pt, bk, w0, dev)  # the same walk as a host loop of FLIP1 launches
+    out["descent_host_loop_ms"] = (time.perf_counter() - t0) * 1e3
+    out["descent_host_loop_same_key"] = bool(_k3(hk) == _k3(dk))
     hctx = chm.Context(device=-1)  # the trigger tables; the arena is reserved ahead in a real run
     t0 = time.perf_counter()
     hctx.policy_install(pt, words)
@@ -610,7 +618,7 @@ def _runtime_plan_block(chm, ctx, tr, pt, sd, C, dev, comp, compute, alone_ms, b
     the argmax-window base and Algo. 2's best, descent from each base's best; R-stall), then two
     executed iterations of its plan under the step's compute"""
     import torch
-    from paper_2509_11076_b200.runtime import _generate_all, _key3, default_bases, descend, seeded_multibase
+    from paper_2509_11076_b200.runtime import _generate_all, _key3, default_bases, device_descend, seeded_multibase
     t0 = time.perf_counter()
     gen = _generate_all(pt)
     best = torch.empty(5, dtype=torch.int64, device=dev)
@@ -619,13 +627,14 @@ def _runtime_plan_block(chm, ctx, tr, pt, sd, C, dev, comp, compute, alone_ms, b
         ctx.eval_policies(pt, chm.EXPLICIT, 0, 1, best=best, item_offsets=np.array([0, len(g)], np.uint64), items=g)
         gkeys.append(best.cpu().numpy().view(chm.BEST_DTYPE)[0].copy())
     k, w, name, per = seeded_multibase(ctx, pt, default_bases(pt, gen, gkeys), C, sd["seed"], sd["flip_thr"], dev)
-    ends = [descend(ctx, pt, kx, wx, dev) for kx, wx in per.values()]
+    ends = device_descend(ctx, pt, [wx for _, wx in per.values()], dev)  # one chm_descend launch
     kd, wd, _ = min(ends, key=lambda e: _key3(e[0]))
     plan_ms = (time.perf_counter() - t0) * 1e3
     tb = pt.tables()
     keep = [j for j in range(pt.K) if (int(wd[j // 64]) >> (j % 64)) & 1]
     need = sum((int(tb["nbytes"][j]) + 511) // 512 * 512 for j in keep)
-    out = {"what": "the runtime's planner (SEEDED around 3 bases + descent from each, R-stall) on the step's trace, "
+    out = {"what": "the runtime's planner (SEEDED around 3 bases + descent from each in one chm_descend launch, "
+                   "R-stall) on the step's trace, "
                    "executed for 2 iterations under the same compute",
            "plan_ms": plan_ms, "items": len(keep), "swap_bytes_per_direction": int(kd["swapped_bytes"]),
            "excess": int(kd["excess"]), "predicted_stall_s": float(kd["stall"]),

@@ -307,6 +307,23 @@ chm_status chm_best_reduce(const chm_best *keys, uint32_t n, chm_best *out);
  * step after the NCCL all-gather of per-rank keys, without a host round trip. */
 chm_status chm_best_reduce_device(chm_ctx *ctx, const chm_best *keys, uint32_t n, chm_best *out,
                                   cudaStream_t stream);
+/* Steepest single-flip descent over swap masks on the device (reading R-search, DESIGN.md §3;
+ * the planner's search around the evaluator), one CTA per start, all rounds on the device.
+ * From each start mask a round scores the K masks that differ from it in one bit under R-stall
+ * (the chm_eval_policies definitions above, bit for bit) and moves to the argmin of (excess,
+ * stall, swapped, k) if its (excess, stall, swapped) is lexicographically smaller than the
+ * current mask's; it stops when no flip improves or after max_rounds moves (0: score the starts
+ * only).  Enqueued on `stream`; every pointer is device memory, caller-owned:
+ *   starts  uint64 [n_starts][W] (W = ceil(K / 64), mask-bit order, bits >= K zero), read;
+ *   ends    uint64 [n_starts][W], written: the end masks (may be `starts` itself, in place; any
+ *           other overlap is CHM_E_INVAL);
+ *   keys    chm_best [n_starts], written: each end mask's key, index = the start's position;
+ *   rounds  int32 [n_starts] or NULL: moves made per start;
+ *   best    chm_best or NULL: the min of keys (chm_best_reduce_device).
+ * CHM_E_STATE on a host-only ctx; CHM_E_INVAL if the trace's tables exceed shared memory. */
+chm_status chm_descend(chm_ctx *ctx, const chm_trace *t, const uint64_t *starts, uint32_t n_starts,
+                       uint32_t max_rounds, uint64_t *ends, chm_best *keys, int32_t *rounds, chm_best *best,
+                       cudaStream_t stream);
 /* Algo. 2 policy generation on the trace's recorded iteration: MRL -> candidate
  * list with Eq. 2 scores -> simulated swap-in placement, backward search with the
  * highest-score fallback -> SetFreeTime forward search.  Writes up to

@@ -13,7 +13,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libchm.so")
 LIB_DEBUG = os.path.join(HERE, "libchm_debug.so")  # device-side bounds checks (CHM_DEBUG)
-SOURCES = ["core.cpp", "trace.cpp", "executor.cpp", "generator.cpp", "oom.cpp", "trace_io.cpp", "stall.cpp", "arena.cpp", "swap.cu", "replay.cu", "timeline.cu", "explicit.cu"]
+SOURCES = ["core.cpp", "trace.cpp", "executor.cpp", "generator.cpp", "oom.cpp", "trace_io.cpp", "stall.cpp", "arena.cpp", "swap.cu", "replay.cu", "timeline.cu", "explicit.cu", "descend.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

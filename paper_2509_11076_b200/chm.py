@@ -175,7 +175,7 @@ EXPORTS = [
     "chm_policy_install", "chm_policy_install_items", "chm_generate_policy", "chm_exec_stats_get", "chm_host_arena", "chm_swap_out", "chm_swap_in",
     "chm_batch_wait", "chm_batch_query", "chm_batch_elapsed", "chm_arena_reserve", "chm_issue_swap_out", "chm_issue_swap_in", "chm_item_wait",
     "chm_oom_release", "chm_passive_swap", "chm_passive_restore", "chm_trace_load", "chm_record_save",
-    "chm_stall_models", "chm_record_tokens", "chm_arena_placement", "chm_release_scratch",
+    "chm_stall_models", "chm_record_tokens", "chm_arena_placement", "chm_release_scratch", "chm_descend",
 ]
 
 _lib = None
@@ -214,6 +214,7 @@ def load(path: str = LIB_PATH):
         "chm_policy_install_items": (i32, [vp, vp, vp, u32]),
         "chm_best_reduce": (i32, [vp, u32, P(Best)]),
         "chm_best_reduce_device": (i32, [vp, vp, u32, vp, vp]),
+        "chm_descend": (i32, [vp, vp, vp, u32, u32, vp, vp, vp, vp, vp]),
         "chm_candidate_mask": (i32, [vp, P(Candidates), u64, vp]),
         "chm_policy_install": (i32, [vp, vp, vp]),
         "chm_exec_stats_get": (i32, [vp, P(ExecStats)]),
@@ -473,6 +474,14 @@ class Context:
 
     def best_reduce_device(self, keys, n: int, out, stream=None):
         _check(load().chm_best_reduce_device(self.h, _ptr(keys), n, _ptr(out), _stream(stream)))
+
+    def descend(self, trace: Trace, starts, n_starts: int, *, ends, keys, max_rounds: int = 4096, rounds=None,
+                best=None, stream=None):
+        """chm_descend: steepest single-flip descent from n_starts device masks [n][W] (uint64 /
+        int64 tensors); writes the end masks, their keys (chm_best [n]), optional rounds (int32
+        [n]) and the best key -- all device buffers, enqueued on `stream`"""
+        _check(load().chm_descend(self.h, trace.h, _ptr(starts), n_starts, max_rounds, _ptr(ends), _ptr(keys),
+                                  _ptr(rounds), _ptr(best), _stream(stream)))
 
     # ---------------------------------------------------------------------- swap
     def host_arena(self):

@@ -208,6 +208,21 @@ def items_to_mask(pt, items, tables=None):
     return w[:pt.W]
 
 
+def device_descend(ctx, pt, starts, dev, max_rounds: int = 4096):
+    """descend (batch 1, R-stall) from every mask in `starts` in one chm_descend launch: one CTA
+    per start, every round on the device, bit-identical end points (tests/test_gpu_descend.py).
+    Returns [(key, words, rounds)] in start order."""
+    n = len(starts)
+    st = torch.from_numpy(np.stack([np.ascontiguousarray(w, np.uint64) for w in starts]).view(np.int64)).to(dev)
+    keys = torch.empty((n, 5), dtype=torch.int64, device=dev)
+    rounds = torch.empty(n, dtype=torch.int32, device=dev)
+    ctx.descend(pt, st, n, ends=st, keys=keys, max_rounds=max_rounds, rounds=rounds)
+    ends = st.cpu().numpy().view(np.uint64).reshape(n, pt.W)
+    ks = keys.cpu().numpy().view(chm.BEST_DTYPE).reshape(n)
+    rs = rounds.cpu().numpy()
+    return [(ks[i].copy(), ends[i].copy(), int(rs[i])) for i in range(n)]
+
+
 def seeded_multibase(ctx, pt, bases, count: int, seed: int, flip_thr: int, dev,
                      stall_model: int = chm.STALL_LAYER):
     """SEEDED candidates around several base masks (reading R-bases): `bases` is a list of
@@ -1080,15 +1095,24 @@ class Runtime:
                 for c in gen_c:  # the generator's best as a mask (solo timing) to descend from
                     starts.append((c[0] + "->mask", None, items_to_mask(pt, c[2]), False))
                 rounds = 0
-                for name, k0, w0, _ in starts:
-                    if k0 is None:
-                        kb = torch.empty(5, dtype=torch.int64, device=self.dev)
-                        self.ctx.eval_policies(pt, chm.FLIP1, pt.K, 1, best=kb, base=w0,  # the mask itself
-                                               stall_model=self.stall_model)
-                        k0 = kb.cpu().numpy().view(chm.BEST_DTYPE)[0]
-                    k, w, r = self._local_search(pt, k0, w0)
-                    rounds += r
-                    cands.append((name + "+search", k, w, False))
+                if self.stall_model == chm.STALL_LAYER and self.search_batch <= 1 and starts:
+                    # every start's descent in one chm_descend launch (one CTA per start, all
+                    # rounds on the device): the same end points as the FLIP1 loop below
+                    for (name, _, _, _), (k, w, r) in zip(starts, device_descend(
+                            self.ctx, pt, [c[2] for c in starts], self.dev, self.search_rounds)):
+                        rounds += r
+                        cands.append((name + "+search", k, w, False))
+                    plan["search_device"] = True
+                else:
+                    for name, k0, w0, _ in starts:
+                        if k0 is None:
+                            kb = torch.empty(5, dtype=torch.int64, device=self.dev)
+                            self.ctx.eval_policies(pt, chm.FLIP1, pt.K, 1, best=kb, base=w0,  # the mask itself
+                                                   stall_model=self.stall_model)
+                            k0 = kb.cpu().numpy().view(chm.BEST_DTYPE)[0]
+                        k, w, r = self._local_search(pt, k0, w0)
+                        rounds += r
+                        cands.append((name + "+search", k, w, False))
                 plan["search_rounds"] = rounds
             plan["search_ms"] = (time.perf_counter() - t1) * 1e3
             if not cands:  # K > 4096 and no generator lists: nothing to choose from

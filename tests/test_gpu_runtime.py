@@ -161,6 +161,31 @@ def test_runtime_ranks_plans_by_the_timeline(reference):
     assert plan["stall"] == float(rt.policy[0].stall_models(rt.policy_items)[2])
 
 
+def test_runtime_r_stall_planner_descends_on_the_device(reference):
+    """stall_model = R-stall: the planner's descents from every start run as one chm_descend
+    launch; its plan's key equals the host FLIP1 loop's from the same starts and training stays
+    bit-exact"""
+    from paper_2509_11076_b200 import chm
+    from paper_2509_11076_b200.runtime import descend
+    rt = Runtime(0, hbm_budget=_budget(reference[2]), groups_fwd=6, groups_bwd=6, trials=1,
+                 stall_model=chm.STALL_LAYER)
+    run = _train(rt)
+    _check_exact(run, reference)
+    plan = rt.plans[0]
+    assert plan.get("search_device") and plan["items"] > 0
+    pt = rt.policy[0]
+    k0 = torch.empty(5, dtype=torch.int64, device="cuda:0")
+    w = pt.candidate_mask(chm.FLIP1, pt.K)
+    rt.ctx.eval_policies(pt, chm.FLIP1, pt.K, 1, best=k0, base=w)
+    hk, hw, _ = descend(rt.ctx, pt, k0.cpu().numpy().view(chm.BEST_DTYPE)[0], w, torch.device("cuda:0"))
+    from paper_2509_11076_b200.runtime import device_descend
+    dk, dw, _ = device_descend(rt.ctx, pt, [w], torch.device("cuda:0"))[0]
+    assert (int(dk["excess"]), float(dk["stall"]), int(dk["swapped_bytes"])) == \
+        (int(hk["excess"]), float(hk["stall"]), int(hk["swapped_bytes"]))
+    assert list(dw) == list(hw)
+    rt.close()
+
+
 def test_sequence_length_switch_replans_and_stays_exact():
     """C4 (configs[3]) on a real model: the sequence length switches 128 -> 256 -> 128 mid-run.
     The op sequence stays the same, so Algo. 1 needs reading Q4's byte signature (detect_bytes)
