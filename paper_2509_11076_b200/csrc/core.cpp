@@ -91,6 +91,16 @@ extern "C" chm_status chm_create(const chm_config *cfg, chm_ctx **out) {
   ctx->arena_mode = c.arena_mode;
   ctx->arena_numa = c.arena_numa;
   ctx->arena_threads = c.arena_threads;
+  {
+    cudaError_t (*pre[])() = {preload_swap, preload_replay, preload_descend, preload_timeline, preload_explicit};
+    for (auto f : pre) {
+      const cudaError_t e = f();
+      if (e != cudaSuccess) {
+        delete ctx;
+        CHM_FAIL(CHM_E_CUDA, "chm_create: loading the kernels: %s", cudaGetErrorString(e));
+      }
+    }
+  }
   ctx->events.resize(kEventRing, nullptr);
   ctx->fences.resize(kEventRing, nullptr);
   for (int i = 0; i < kEventRing; i++) {

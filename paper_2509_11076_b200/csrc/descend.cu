@@ -299,3 +299,10 @@ extern "C" chm_status chm_descend(chm_ctx *ctx, const chm_trace *t, const uint64
   if (best) return chm_best_reduce_device(ctx, keys, n_starts, best, stream);
   return CHM_OK;
 }
+
+namespace chm {
+cudaError_t preload_descend() {
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(descend_kernel));
+}
+}  // namespace chm

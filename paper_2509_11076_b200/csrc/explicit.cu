@@ -235,3 +235,12 @@ chm_status launch_eval_explicit(chm_ctx *ctx, const chm_trace *t, const chm_cand
 }
 
 }  // namespace chm
+
+namespace chm {
+cudaError_t preload_explicit() {
+  cudaFuncAttributes a;
+  cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(replay_explicit_kernel));
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(xkey_reduce_kernel));
+  return e;
+}
+}  // namespace chm

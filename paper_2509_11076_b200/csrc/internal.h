@@ -201,6 +201,14 @@ CHM_HD int layers_per_lane(int L) {
   return e;
 }
 CHM_HD int layer_slot(int l, int E) { return E > 1 ? l + l / E : l; }
+// each kernel TU's preload: cudaFuncGetAttributes on every kernel it launches, which loads its
+// code now (lazy module loading would otherwise charge the first launch -- e.g. the first
+// re-plan -- a few ms); chm_create calls them for a device ctx
+cudaError_t preload_replay();
+cudaError_t preload_descend();
+cudaError_t preload_timeline();
+cudaError_t preload_explicit();
+cudaError_t preload_swap();
 CHM_HD int layer_slots(int L, int E) { return E > 1 ? L + (L + E - 1) / E : L; }
 
 }  // namespace chm

@@ -725,3 +725,22 @@ extern "C" chm_status chm_release_scratch(chm_ctx *ctx) {
   }
   return CHM_OK;
 }
+
+namespace chm {
+cudaError_t preload_replay() {
+  const void *k[] = {
+      reinterpret_cast<const void *>(replay_kernel<false, false, 1>), reinterpret_cast<const void *>(replay_kernel<false, false, 2>),
+      reinterpret_cast<const void *>(replay_kernel<false, false, 4>), reinterpret_cast<const void *>(replay_kernel<false, false, 8>),
+      reinterpret_cast<const void *>(replay_kernel<true, false, 1>), reinterpret_cast<const void *>(replay_kernel<true, false, 2>),
+      reinterpret_cast<const void *>(replay_kernel<true, false, 4>), reinterpret_cast<const void *>(replay_kernel<true, false, 8>),
+      reinterpret_cast<const void *>(replay_kernel<true, true, 1>), reinterpret_cast<const void *>(replay_kernel<true, true, 2>),
+      reinterpret_cast<const void *>(replay_kernel<true, true, 4>), reinterpret_cast<const void *>(replay_kernel<true, true, 8>),
+      reinterpret_cast<const void *>(best_reduce_kernel)};
+  cudaFuncAttributes a;
+  for (const void *f : k) {
+    const cudaError_t e = cudaFuncGetAttributes(&a, f);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+}  // namespace chm

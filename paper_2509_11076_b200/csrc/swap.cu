@@ -468,3 +468,13 @@ extern "C" chm_status chm_arena_reserve(chm_ctx *ctx, uint64_t bytes) {
   }
   return st;
 }
+
+namespace chm {
+cudaError_t preload_swap() {
+  cudaFuncAttributes a;
+  cudaError_t e = cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(swap_copy_kernel<true>));
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(swap_copy_kernel<false>));
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(swap_bulk_kernel));
+  return e;
+}
+}  // namespace chm

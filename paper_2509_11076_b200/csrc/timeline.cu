@@ -430,3 +430,17 @@ chm_status launch_timeline(chm_ctx *ctx, const chm_trace *t, const EvalLaunch &L
 }
 
 }  // namespace chm
+
+namespace chm {
+cudaError_t preload_timeline() {
+  const void *k[] = {reinterpret_cast<const void *>(timeline_kernel<32, true, 1>),
+                     reinterpret_cast<const void *>(timeline_kernel<kTlThreads, false, 1>),
+                     reinterpret_cast<const void *>(timeline_kernel<kTlThreads2, false, 2>)};
+  cudaFuncAttributes a;
+  for (const void *f : k) {
+    const cudaError_t e = cudaFuncGetAttributes(&a, f);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+}  // namespace chm
