@@ -90,6 +90,11 @@ enum { CHM_ARENA_AUTO = 0, CHM_ARENA_HOSTALLOC = 1, CHM_ARENA_REGISTER = 2 };
 /* fills the paper's defaults */
 void chm_config_default(chm_config *cfg);
 
+/* Creates a context (*out, freed by chm_destroy).  A device ctx (cfg->device >= 0) checks for an
+ * sm_100 device (else CHM_E_NOKERNEL), loads every kernel of the library now (so the first
+ * evaluation or descent after a sequence change pays no module loading), creates its event rings
+ * and, if cfg->host_arena_bytes > 0, pins the host arena.  CHM_E_INVAL on a bad config,
+ * CHM_E_NOMEM / CHM_E_CUDA when an allocation or CUDA call fails (nothing is left allocated). */
 chm_status chm_create(const chm_config *cfg, chm_ctx **out);
 void chm_destroy(chm_ctx *ctx);
 const char *chm_last_error(void);
