@@ -132,3 +132,20 @@ def test_descend_zero_rounds_scores_the_starts_and_runs_in_place():
     assert np.array_equal(e1, e2) and np.array_equal(r1, r2)
     assert all(_key3(k1[i]) == _key3(k2[i]) for i in range(n))
     ctx.close()
+
+
+@pytest.mark.parametrize("max_rounds", [1, 7, 40])
+def test_descend_stops_after_max_rounds_like_the_oracle(max_rounds):
+    """a bounded descent ends where the oracle's bounded descent ends (C5, from the argmax-window
+    base and two SEEDED starts)"""
+    tr = W.CONFIGS["C5"]()
+    ctx, pt = _build(tr)
+    m = O.Model(tr)
+    starts = _starts(pt, 2)[1:]
+    ends, keys, rounds, _ = _run(ctx, pt, starts, max_rounds=max_rounds)
+    for i, s in enumerate(starts):
+        oe, okey, orounds = O.descend(m, s, max_rounds=max_rounds)
+        assert np.array_equal(ends[i], oe) and _key3(keys[i]) == okey and int(rounds[i]) == orounds
+        assert orounds <= max_rounds
+    ctx.close()
+
