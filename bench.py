@@ -81,6 +81,10 @@ def parse(argv=None):
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--force-dist", action="store_true", help="NCCL argmin path even at N = 1 (one-rank group)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: collectives on host tensors (a functional check of the N > 1 path, not a measurement)")
+    ap.add_argument("--same-device", action="store_true",
+                    help="every rank on cuda:0 (with --dist-backend gloo: the N > 1 path on one GPU, functional only)")
     return ap.parse_args(argv)
 
 
@@ -497,7 +501,22 @@ class PolicyRun:
         self.storage.clear()
 
 
-def _eval_strong_block(chm, D, dev, comp, rank, P, use_dist, barrier, max_over_ranks, total=10_000_000):
+def _exchange(D, ctx, bl, ga, bg, P, stream, backend):
+    """the argmin exchange: NCCL on device keys (all_gather_into_tensor + chm_best_reduce_device
+    on `stream`), or gloo on host copies (all-gather + chm_best_reduce; functional runs)"""
+    if backend == "nccl":
+        D.argmin_exchange(ctx, bl, ga, bg, P, stream=stream)
+        return
+    import torch
+    stream.synchronize()
+    gh = torch.empty(5 * P, dtype=torch.int64)
+    bh = torch.empty(5, dtype=torch.int64)
+    D.argmin_exchange(None, bl.cpu(), gh, bh, P)
+    bg.copy_(bh)
+
+
+def _eval_strong_block(chm, D, dev, comp, rank, P, use_dist, barrier, max_over_ranks, total=10_000_000,
+                       backend="nccl"):
     """the evaluation's strong scaling: C5's trace, `total` SEEDED candidates (search mode)
     sharded over the P ranks, the per-rank launch + the argmin exchange timed with CUDA events,
     the slowest rank's time"""
@@ -522,7 +541,7 @@ def _eval_strong_block(chm, D, dev, comp, rank, P, use_dist, barrier, max_over_r
         e0.record(comp)
         ctx.eval_policies(pt, chm.SEEDED, lo, cnt, best=bl, seed=sd["seed"], flip_thr=sd["flip_thr"], stream=comp)
         if use_dist:
-            D.argmin_exchange(ctx, bl, ga, bg, P, stream=comp)
+            _exchange(D, ctx, bl, ga, bg, P, comp, backend)
         else:
             bg.copy_(bl)
         e1.record(comp)
@@ -727,7 +746,7 @@ def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if args.same_device else int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank)
         return
@@ -748,7 +767,11 @@ def main():
             os.environ.setdefault("NCCL_DEBUG", "INFO")
             os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    host_coll = use_dist and args.dist_backend == "gloo"  # collectives on host tensors
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     P = world
@@ -761,14 +784,14 @@ def main():
     def max_over_ranks(x: float) -> float:
         if not use_dist:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if host_coll else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(x: float) -> float:
         if not use_dist:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if host_coll else dev)
         dist.all_reduce(t)
         return float(t.item())
 
@@ -787,7 +810,7 @@ def main():
     ctx.detect_seq_change(tr.t_iter)
     ctx.set_detailed(False)
     pt = ctx.trace_build(tr.budget, tr.static_bytes, tr.bw, tr.groups_fwd, tr.groups_bwd, t_iter=tr.t_iter)
-    digest = D.check_same_trace(pt, device=dev) if use_dist else pt.digest()  # ranks shard one trace
+    digest = D.check_same_trace(pt, device=None if host_coll else dev) if use_dist else pt.digest()  # one trace
     C = args.candidates
     lo, cnt = D.shard(C, P, rank)
     full = not args.search_mode
@@ -806,7 +829,7 @@ def main():
         if ev_kernel is not None:
             ev_kernel.record(comp)  # replay kernel done; the rest is the argmin exchange
         if use_dist:
-            D.argmin_exchange(ctx, best_local, gathered, best_global, P, stream=comp)
+            _exchange(D, ctx, best_local, gathered, best_global, P, comp, args.dist_backend)
         else:
             best_global.copy_(best_local)
 
@@ -961,7 +984,8 @@ def main():
     # ---- candidate policies evaluated / s at this N (the metric's second half):
     # C5's per-rank trace, 10^7 SEEDED candidates in search mode split over the ranks
     # (strong scaling), each rank's shard + the NCCL argmin, max over ranks
-    strong = _eval_strong_block(chm, D, dev, comp, rank, P, use_dist, barrier, max_over_ranks)
+    strong = _eval_strong_block(chm, D, dev, comp, rank, P, use_dist, barrier, max_over_ranks,
+                                backend=args.dist_backend)
     # ---- rank-0 blocks beside the line: Algo. 2's grid, the timeline ranking, the C4 re-plan,
     # C1's small tensors, C2 (N = 1: host RAM)
     extras = {}
@@ -1071,7 +1095,10 @@ def main():
                         {"what": f"one bf16 GEMM [{compute.M}, {GEMM_N}] x [{GEMM_N}, {GEMM_N}] per op on the compute "
                                  f"stream, calibrated to T_iter / N = {tr.t_iter / pt.N * 1e3:.3f} ms",
                          "gflop_per_step": gflop}),
-            "parallelism": f"dp{P}: per-rank swapping, candidates sharded, NCCL argmin all-gather",
+            "parallelism": f"dp{P}: per-rank swapping, candidates sharded, "
+                           + ("NCCL argmin all-gather" if args.dist_backend == "nccl" else
+                              "gloo argmin all-gather on host copies" + (", every rank on cuda:0 -- a functional "
+                                                                         "check, not a measurement" if args.same_device else "")),
             "l2": "inputs larger than L2 (swap set and footprint rows are GBs per step)",
             "swap_ctas": args.swap_ctas, "arena_pin_s": round(t_pin, 2), "arena": dict(arena_info, **arena_pages),
             "host": host_info(),
