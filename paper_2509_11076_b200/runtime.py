@@ -349,7 +349,14 @@ class Runtime:
     swappable tensor there, while above autograd those stay invisible to the executor and a
     retry re-runs the whole composite (measured: under a 60% cap the C++ hook runs out of
     passive candidates against allocator fragmentation, tools/debug_oom.py).  record_log needs
-    the Python hook."""
+    the Python hook.
+    defrag: Algo. 3 step (iii) "MemoryPool.Defragment()" (GMLake's stitched virtual
+    memory): switch PyTorch's caching allocator to expandable segments (physical 2 MiB pages
+    mapped into one growing virtual range with cuMemMap, unmapped when freed), so the blocks a
+    passive swap frees serve the failed request wherever they lie.  It is what makes the C++ hook
+    usable with OOM handling (native_hook=True, oom_host_bytes > 0): under 60% / 70% caps it then
+    trains bit-exactly where it ran out of candidates without (tools/oom_defrag.py,
+    profiles/r02_oom_defrag_hooks.jsonl).  Affects segments allocated after construction."""
 
     def __init__(self, device: Optional[int] = 0, *, hbm_budget: int, bw: Optional[float] = None,
                  groups_fwd: int = 0, groups_bwd: int = 0, omega: float = 1.0, candidates: int = 1 << 16,
@@ -357,7 +364,7 @@ class Runtime:
                  min_swap_bytes: int = 0, search_rounds: int = 4096, host_arena_bytes: int = 0,
                  swap_flags: int = chm.SWAP_AUTO, oom_host_bytes: int = 0, trials: int = 5,
                  stall_model: int = chm.STALL_TIMELINE, search_batch: int = 1, prepin: bool = True,
-                 host_pin_budget: int = 0, native_hook: Optional[bool] = None, **algo1):
+                 host_pin_budget: int = 0, native_hook: Optional[bool] = None, defrag: bool = False, **algo1):
         self.host_only = device is None
         self.dev = torch.device("cpu") if self.host_only else torch.device("cuda", device)
         self.ctx = chm.Context(device=-1 if self.host_only else device, swap_ctas=swap_ctas,
@@ -422,6 +429,9 @@ class Runtime:
         if native_hook is None:
             native_hook = not self.oom_host_bytes
         self._nh = globals()["native_hook"]() if native_hook else None
+        self.defrag = bool(defrag) and not self.host_only
+        if self.defrag:  # Algo. 3 step (iii): the pool's segments from here on are expandable
+            torch.cuda.memory._set_allocator_settings("expandable_segments:True")
 
     def _attach_hook(self):
         """hands this runtime's ctx and callbacks to the C++ hook for one step"""

@@ -48,7 +48,10 @@ def main():
     torch.cuda.empty_cache()
     total = torch.cuda.get_device_properties(0).total_memory
     budget = (1 << 62) if budget_frac is None else torch.cuda.memory_allocated() + int(budget_frac * peak)
-    rt = Runtime(0, hbm_budget=budget, groups_fwd=6, groups_bwd=6, oom_host_bytes=1 << 30, trials=1)
+    hook = os.environ.get("CHM_OOM_HOOK")  # "native" / "python": force the hook (default: the runtime's choice)
+    rt = Runtime(0, hbm_budget=budget, groups_fwd=6, groups_bwd=6, oom_host_bytes=1 << 30, trials=1,
+                 native_hook=None if hook is None else hook == "native",
+                 defrag=os.environ.get("CHM_OOM_DEFRAG") == "1")
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
     cap = torch.cuda.memory_reserved() + int(frac * peak)

@@ -38,3 +38,21 @@ def test_runtime_policy_under_a_tighter_cap_releases_early():
     st = out["stats"]
     assert out["plans"] and out["plans"][0]["items"] > 0 and st["release"] > 0, out
     assert st["oom"] > 0 and st["oom_released"] + st["passive"] > 0, st
+
+
+@pytest.mark.parametrize("frac", [0.6, 0.7])
+def test_native_hook_with_defrag_survives_a_memory_cap(frac):
+    """Algo. 3 with the C++ hook needs step (iii): Runtime(defrag=True) switches the caching
+    allocator to expandable segments, and the passive swaps' freed pages then serve the failed
+    requests -- bit-identical training under the cap"""
+    child = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_oom_child.py")
+    env = dict(os.environ, CHM_OOM_HOOK="native", CHM_OOM_DEFRAG="1")
+    env.pop("PYTORCH_CUDA_ALLOC_CONF", None)
+    r = subprocess.run([sys.executable, child, str(frac)], capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out["plain_under_cap"] == "oom", out
+    assert out["losses_equal"] and out["params_equal"], out
+    st = out["stats"]
+    assert st["oom"] > 0 and st["passive"] > 0 and st["passive_restored"] == st["passive"], st
+

@@ -18,9 +18,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def main():
     fracs = [float(a) for a in sys.argv[1:]] or [0.5, 0.6, 0.7, 0.8]
     child = os.path.join(ROOT, "tests", "_oom_child.py")
-    for frac in fracs:
+    hooks = [h for h in os.environ.get("HOOKS", "default").split(",")]
+    for frac, hook in [(f, h) for f in fracs for h in hooks]:
         for conf in ("", "expandable_segments:True"):
             env = dict(os.environ)
+            if hook != "default":
+                env["CHM_OOM_HOOK"] = hook
             if conf:
                 env["PYTORCH_CUDA_ALLOC_CONF"] = conf
             else:
@@ -31,7 +34,7 @@ def main():
             except (IndexError, ValueError):
                 out = {"error": r.stderr[-500:]}
             st = out.get("stats", {})
-            print(json.dumps({"cap_frac": frac, "alloc_conf": conf or "default", "rc": r.returncode,
+            print(json.dumps({"cap_frac": frac, "hook": hook, "alloc_conf": conf or "default", "rc": r.returncode,
                               "plain_under_cap": out.get("plain_under_cap"), "oom": st.get("oom"),
                               "passive": st.get("passive"), "passive_restored": st.get("passive_restored"),
                               "losses_equal": out.get("losses_equal"), "params_equal": out.get("params_equal"),
