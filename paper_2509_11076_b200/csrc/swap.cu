@@ -20,10 +20,18 @@
 namespace chm {
 namespace {
 
-constexpr int kSwapThreads = 512;
+#ifndef CHM_SWAP_THREADS
+#define CHM_SWAP_THREADS 512
+#endif
+constexpr int kSwapThreads = CHM_SWAP_THREADS;  // threads per swap CTA (A/B knob: tools/build_variant.py)
 constexpr int kUnroll = 8;
 constexpr int kMisUnroll = 8;  // misaligned views: words per thread per pass
-constexpr int kChunkShift = 16;  // 64 KiB = 512 threads x 8 x 16 B
+#ifndef CHM_SWAP_MINB
+#define CHM_SWAP_MINB 1
+#endif
+// a chunk is one pass of the CTA: threads x 8 x 16 B (64 KiB at 512 threads)
+constexpr int kChunkShift = kSwapThreads == 512 ? 16 : kSwapThreads == 256 ? 15 : 14;
+static_assert(kSwapThreads == 512 || kSwapThreads == 256 || kSwapThreads == 128, "swap CTA size");
 constexpr uint64_t kChunk = 1ull << kChunkShift;
 
 struct SwapParams {
@@ -99,11 +107,11 @@ __device__ __forceinline__ void copy_misaligned(const char *s, char *d, uint64_t
     h0 = h1 + ((16u - ((ua + h1) & 15u)) & 15u);
   }
   const uint32_t h = uint32_t(h0 < len ? h0 : len);
-  if (threadIdx.x < h) d[threadIdx.x] = s[threadIdx.x];
+  for (uint32_t i = threadIdx.x; i < h; i += kSwapThreads) d[i] = s[i];
   const char *sb = s + h;
   char *db = d + h;
   const uint64_t body = len - h;
-  const uint32_t nvec = uint32_t(body >> 4);  // <= 4096 (64 KiB chunk)
+  const uint32_t nvec = uint32_t(body >> 4);  // <= kSwapThreads x 8 (one chunk)
   const uint32_t r = uint32_t(reinterpret_cast<uintptr_t>(sb) & 15u);
   const int lane = threadIdx.x & 31;
   // kMisUnroll words per thread in flight per pass (zero-copy reads from host memory are
@@ -165,7 +173,7 @@ __device__ __forceinline__ void copy_misaligned(const char *s, char *d, uint64_t
 }
 
 template <bool kPrefetch256>
-__global__ void __launch_bounds__(kSwapThreads) swap_copy_kernel(const __grid_constant__ SwapParams p) {
+__global__ void __launch_bounds__(kSwapThreads, CHM_SWAP_MINB) swap_copy_kernel(const __grid_constant__ SwapParams p) {
   for (uint64_t c = blockIdx.x; c < p.total_chunks; c += gridDim.x) {
     uint32_t lo = 0, hi = p.n;  // chunk_begin[lo] <= c < chunk_begin[hi]
     while (hi - lo > 1) {
