@@ -196,6 +196,57 @@ def descend(ctx, pt, key, words, dev, max_rounds: int = 4096, stall_model: int =
     return key, cur, rounds
 
 
+def descend_many(ctx, pt, starts, dev, max_rounds: int = 4096, stall_model: int = chm.STALL_TIMELINE):
+    """descend (batch 1) from every (key, words) in `starts` in lockstep: each round scores the
+    one-bit neighbourhoods of all still-moving masks in one MASKS launch (per-candidate keys back,
+    the argmin of (excess, stall, swapped, k) within each start's K neighbours on the host), so
+    the descents share launches instead of running one after the other -- the same trajectories
+    as descend() per start (tests/test_gpu_descend.py).  For the timeline stall model, whose
+    rounds are latency-bound launches of one chain per candidate; R-stall descents run entirely
+    on the device (device_descend).  Returns [(key, words, rounds)] in start order."""
+    K, W = pt.K, pt.W
+    cur = [np.array(w, np.uint64).copy() for _, w in starts]
+    keys = [k for k, _ in starts]
+    rounds = [0] * len(starts)
+    active = [i for i in range(len(starts)) if K and max_rounds > 0]
+    eye = np.zeros((K, W), np.uint64)
+    for k in range(K):
+        eye[k, k // 64] = np.uint64(1 << (k % 64))
+    best = torch.empty(5, dtype=torch.int64, device=dev)
+    nmax = len(active) * K
+    pinned = dev.type == "cuda"
+    hmask = torch.empty((max(nmax, 1), max(W, 1)), dtype=torch.int64, pin_memory=pinned)
+    dmask = torch.empty_like(hmask, device=dev)
+    out = torch.empty((3, max(nmax, 1)), dtype=torch.int64, device=dev)  # peak, stall (f64 bits), swapped
+    hm = hmask.numpy().view(np.uint64)
+    while active:
+        n = len(active) * K
+        for j, i in enumerate(active):
+            np.bitwise_xor(cur[i][None, :], eye, out=hm[j * K:(j + 1) * K, :W])
+        dmask[:n].copy_(hmask[:n], non_blocking=pinned)
+        ctx.eval_policies(pt, chm.MASKS, 0, n, best=best, masks=dmask[:n], peak=out[0, :n],
+                          stall=out[1, :n].view(torch.float64), swapped=out[2, :n], stall_model=stall_model)
+        res = out[:, :n].cpu().numpy()  # one copy back
+        pkh, stl, swp = res[0], res[1].view(np.float64), res[2]
+        ex = np.maximum(pkh - pt.budget, 0)
+        nxt = []
+        for j, i in enumerate(active):
+            sl = slice(j * K, (j + 1) * K)
+            k = int(np.lexsort((np.arange(K), swp[sl], stl[sl], ex[sl]))[0])
+            g = j * K + k
+            if not (int(ex[g]), float(stl[g]), int(swp[g])) < _key3(keys[i]):
+                continue
+            cur[i][k // 64] ^= np.uint64(1 << (k % 64))
+            kk = np.zeros(1, chm.BEST_DTYPE)[0]
+            kk["excess"], kk["stall"], kk["swapped_bytes"], kk["index"], kk["peak"] = ex[g], stl[g], swp[g], k, pkh[g]
+            keys[i] = kk
+            rounds[i] += 1
+            if rounds[i] < max_rounds:
+                nxt.append(i)
+        active = nxt
+    return [(keys[i], cur[i], rounds[i]) for i in range(len(starts))]
+
+
 def items_to_mask(pt, items, tables=None):
     """the swappable-set mask of an item list's tensors (their solo timing)"""
     tb = tables if tables is not None else pt.tables()
@@ -1114,13 +1165,19 @@ class Runtime:
                         cands.append((name + "+search", k, w, False))
                     plan["search_device"] = True
                 else:
+                    sk = []
                     for name, k0, w0, _ in starts:
                         if k0 is None:
                             kb = torch.empty(5, dtype=torch.int64, device=self.dev)
                             self.ctx.eval_policies(pt, chm.FLIP1, pt.K, 1, best=kb, base=w0,  # the mask itself
                                                    stall_model=self.stall_model)
                             k0 = kb.cpu().numpy().view(chm.BEST_DTYPE)[0]
-                        k, w, r = self._local_search(pt, k0, w0)
+                        sk.append((k0, w0))
+                    if self.search_batch <= 1:  # the descents in lockstep: shared launches
+                        ends = descend_many(self.ctx, pt, sk, self.dev, self.search_rounds, self.stall_model)
+                    else:
+                        ends = [self._local_search(pt, k0, w0) for k0, w0 in sk]
+                    for (name, _, _, _), (k, w, r) in zip(starts, ends):
                         rounds += r
                         cands.append((name + "+search", k, w, False))
                 plan["search_rounds"] = rounds

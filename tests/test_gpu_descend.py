@@ -149,3 +149,24 @@ def test_descend_stops_after_max_rounds_like_the_oracle(max_rounds):
         assert orounds <= max_rounds
     ctx.close()
 
+
+@pytest.mark.parametrize("model", [chm.STALL_TIMELINE, chm.STALL_LAYER])
+def test_lockstep_descents_equal_one_by_one(model):
+    """runtime.descend_many (all starts' neighbourhoods in one MASKS launch per round) follows
+    each start's descend() trajectory exactly, under either stall model"""
+    from paper_2509_11076_b200.runtime import descend_many
+    tr = W.CONFIGS["C5"]()
+    ctx, pt = _build(tr)
+    starts = _starts(pt, 2)[1:]
+    best = torch.empty(5, dtype=torch.int64, device=DEV)
+    sk = []
+    for w in starts:
+        ctx.eval_policies(pt, chm.FLIP1, pt.K, 1, best=best, base=w, stall_model=model)
+        sk.append((best.cpu().numpy().view(chm.BEST_DTYPE)[0].copy(), w))
+    many = descend_many(ctx, pt, sk, torch.device(DEV), 4096, model)
+    for (k0, w0), (k, w, r) in zip(sk, many):
+        hk, hw, hr = host_descend(ctx, pt, k0, w0, torch.device(DEV), 4096, model)
+        assert np.array_equal(np.asarray(hw, np.uint64), w) and r == hr and _key3(hk) == _key3(k)
+        assert int(hk["index"]) == int(k["index"]) and int(hk["peak"]) == int(k["peak"])
+    ctx.close()
+
