@@ -409,7 +409,7 @@ static int cand_bit(const eval_job *j, uint64_t c, uint64_t idx, int32_t k) {
     const uint64_t *base = j->words ? j->words : m->base;
     int b = (int)((base[k / 64] >> (k % 64)) & 1ull);
     uint64_t J = ((uint64_t)m->K + 3) / 4;
-    uint64_t w = orc_splitmix64(j->seed ^ orc_splitmix64(c * J + (uint64_t)(k / 4)));
+    uint64_t w = orc_splitmix64(j->seed ^ (c * J + (uint64_t)(k / 4)));  /* reading R-seeded (r02: one mix) */
     uint64_t field = (w >> (16 * (k % 4))) & 0xffffull;
     return b ^ (field < (j->flip_thr >> 48) ? 1 : 0);
   }

@@ -26,7 +26,7 @@ def _policy(name, tr, m):
     base = m.base_mask()
     sel = []
     for k in range(m.K):
-        w = O.splitmix64(sd["seed"] ^ O.splitmix64((best.index * J + k // 4) % 2 ** 64))
+        w = O.splitmix64(sd["seed"] ^ ((best.index * J + k // 4) % 2 ** 64))
         bit = ((int(base[k // 64]) >> (k % 64)) & 1) ^ int(((w >> (16 * (k % 4))) & 0xFFFF) < (sd["flip_thr"] >> 48))
         if bit:
             sel.append(k)

@@ -288,7 +288,7 @@ def test_seeded_bits_and_masks_agree():
     for j in range(50):
         c = 5 + j
         for k in range(K):
-            w = O.splitmix64(seed ^ O.splitmix64((c * J + k // 4) % 2 ** 64))
+            w = O.splitmix64(seed ^ ((c * J + k // 4) % 2 ** 64))
             field = (w >> (16 * (k % 4))) & 0xFFFF
             bit = int((int(base[k // 64]) >> (k % 64)) & 1) ^ int(field < (thr >> 48))
             if bit:
@@ -296,6 +296,35 @@ def test_seeded_bits_and_masks_agree():
     res2 = m.eval(O.MASKS, 5, 50, words=masks)
     assert np.array_equal(res["peak"], res2["peak"]) and np.array_equal(res["stall"], res2["stall"])
     assert res["best"].key() == res2["best"].key()
+
+
+def _mix_np(z):
+    # splitmix64's finaliser, vectorised (wrapping uint64), checked against the oracle's below
+    z = z + np.uint64(0x9E3779B97F4A7C15)
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+@pytest.mark.parametrize("p", [0.02, 0.3])
+def test_seeded_flip_statistics(p):
+    """reading R-seeded draws one splitmix64 finaliser per 4 items, w = mix(seed ^ (c J + q)):
+    over 20,000 candidates x 120 words the 16-bit fields fall below flip_thr >> 48 at rate p
+    (within 5 standard errors), and flips of neighbouring fields, words and candidates are
+    uncorrelated (|r| < 0.01) -- the counter's structure does not leak through the finaliser"""
+    seed, J, n = 0x5EED, 120, 20_000
+    with np.errstate(over="ignore"):
+        ctr = (np.arange(n, dtype=np.uint64)[:, None] * np.uint64(J) + np.arange(J, dtype=np.uint64)[None, :])
+        w = _mix_np(np.uint64(seed) ^ ctr)
+    assert all(int(w[c, q]) == O.splitmix64(seed ^ (c * J + q)) for c, q in ((0, 0), (17, 3), (n - 1, J - 1)))
+    thr = int(p * 2 ** 16)
+    f = np.stack([((w >> np.uint64(16 * e)) & np.uint64(0xFFFF)) < np.uint64(thr) for e in range(4)], axis=-1)
+    f = f.reshape(n, 4 * J).astype(np.float64)
+    rate, q16 = f.mean(), thr / 2 ** 16
+    assert abs(rate - q16) < 5 * np.sqrt(q16 * (1 - q16) / f.size), (rate, q16)
+    for a, b in ((f[:, :-1], f[:, 1:]), (f[:, :-4], f[:, 4:]), (f[:-1, :], f[1:, :])):
+        r = np.corrcoef(a.ravel(), b.ravel())[0, 1]
+        assert abs(r) < 0.01, r
 
 
 def test_default_base_mask_contains_argmax():
