@@ -236,7 +236,7 @@ typedef struct {
 typedef enum {
   CHM_CAND_EXHAUSTIVE = 0, /* swap set of candidate c = bits of c; requires K <= 63        */
   CHM_CAND_SEEDED = 1,     /* bit t = base[t] ^ [f_t < flip_thr >> 48], f_t = 16-bit field
-                              t mod 4 of w = mix(seed ^ mix(c*J + t/4)), J = ceil(K/4),
+                              t mod 4 of w = mix(seed ^ (c*J + t/4)), J = ceil(K/4),
                               mix = splitmix64 finaliser (reading R-seeded)     */
   CHM_CAND_MASKS = 2,      /* device masks [count][mask_words], little-endian u64 words  */
   CHM_CAND_EXPLICIT = 3,   /* host item lists: candidate c = items[item_offsets[c] ..

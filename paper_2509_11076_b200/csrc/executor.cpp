@@ -32,7 +32,7 @@ extern "C" chm_status chm_candidate_mask(const chm_trace *t, const chm_candidate
       const uint64_t J = (uint64_t(K) + 3) / 4, thr16 = c->flip_thr >> 48;
       for (int32_t k = 0; k < K; k++) {
         uint64_t bit = (base[k / 64] >> (k % 64)) & 1ull;
-        const uint64_t w = splitmix64(c->seed ^ splitmix64(index * J + uint64_t(k / 4)));
+        const uint64_t w = splitmix64(c->seed ^ (index * J + uint64_t(k / 4)));
         bit ^= ((w >> (16 * (k % 4))) & 0xffffull) < thr16 ? 1ull : 0ull;
         words[k / 64] |= bit << (k % 64);
       }

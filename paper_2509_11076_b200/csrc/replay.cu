@@ -59,7 +59,7 @@ __device__ __forceinline__ bool cand_bit(const EvalParams &p, uint64_t g, uint64
   if (p.kind == CHM_CAND_SEEDED) {
     const bool b = (p.base[k >> 6] >> (k & 63)) & 1ull;
     const uint64_t J = (uint64_t(p.tr.K) + 3) >> 2;
-    const uint64_t w = mix64(p.seed ^ mix64(g * J + uint64_t(k >> 2)));
+    const uint64_t w = mix64(p.seed ^ (g * J + uint64_t(k >> 2)));
     return b != (((w >> (16 * (k & 3))) & 0xffffull) < (p.flip_thr >> 48));
   }
   return (__ldg(p.masks + c * uint64_t(p.tr.W) + uint64_t(k >> 6)) >> (k & 63)) & 1ull;
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(kEvalThreads, CHM_EVAL_MINB) replay_kernel(con
       const unsigned thr16 = unsigned(p.flip_thr >> 48);
       const uint64_t gJ = g * uint64_t(J);  // word q of candidate g hashes g * J + q
       for (int q = lane; q < J; q += 32) {
-        const uint64_t w = mix64(p.seed ^ mix64(gJ + uint64_t(q)));
+        const uint64_t w = mix64(p.seed ^ (gJ + uint64_t(q)));
         unsigned f4 = 0;
 #pragma unroll
         for (int e = 0; e < 4; e++) f4 |= (unsigned((w >> (16 * e)) & 0xffffull) < thr16 ? 1u : 0u) << e;

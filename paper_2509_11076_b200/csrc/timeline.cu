@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kT) timeline_kernel(const __grid_constant__ Tl
           const uint64_t J = (uint64_t(p.K) + 3) >> 2;
           const unsigned thr16 = unsigned(p.flip_thr >> 48);
           for (uint64_t q = 0; q < J; q++) {
-            const uint64_t w = mix64(p.seed ^ mix64(g * J + q));
+            const uint64_t w = mix64(p.seed ^ (g * J + q));
 #pragma unroll
             for (int e = 0; e < 4; e++) {
               const unsigned k = unsigned(4 * q) + e;
