@@ -24,7 +24,7 @@ def main():
     chm.record_iteration(ctx, tr)
     ctx.detect_seq_change(tr.t_iter)
     pt = ctx.trace_build(tr.budget, tr.static_bytes, tr.bw, tr.groups_fwd, tr.groups_bwd, t_iter=tr.t_iter)
-    n, ld = 100_000, (pt.N + 1) // 2 * 2
+    n, ld = int(os.environ.get("EVAL_N", "100000")), (pt.N + 1) // 2 * 2
     dev = torch.device("cuda:0")
     peak = torch.empty(n, dtype=torch.int64, device=dev)
     stall = torch.empty(n, dtype=torch.float64, device=dev)
