@@ -270,7 +270,7 @@ def descend(model: "Model", words, max_rounds: int = 4096, budget: Optional[int]
     W = (K + 63) // 64
     cur = np.array(words, np.uint64).reshape(W).copy()
     b = int(model.trace.budget if budget is None else budget)
-    k0 = model.eval(MASKS, 0, 1, words=cur, budget=b)["best"]
+    k0 = model.eval(MASKS, 0, 1, words=cur if W else np.zeros(1, np.uint64), budget=b)["best"]  # K = 0: no bits
     key = (int(k0.excess), float(k0.stall), int(k0.swapped))
     rounds = 0
     while rounds < max_rounds and K > 0:

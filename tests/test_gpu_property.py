@@ -128,3 +128,31 @@ def test_timeline_matches_oracle(ctx, tr, kind, first, count, seed, flip, path):
         os.environ.pop("CHM_TL_SMEM", None)
         if old is not None:
             os.environ["CHM_TL_SMEM"] = old
+
+
+@settings(max_examples=60, deadline=None)
+@given(tr=traces, seed=st.integers(0, 2 ** 32), n_starts=st.integers(1, 6), max_rounds=st.sampled_from([0, 1, 3, 4096]))
+def test_descend_matches_oracle(ctx, tr, seed, n_starts, max_rounds):
+    """chm_descend from random start masks (any K, including K = 0) = the oracle's descend"""
+    pt = product_trace(ctx, tr)
+    m = O.Model(tr)
+    if m.L < 1:
+        return
+    W_ = max(m.W, 1)
+    rng = np.random.default_rng(seed)
+    starts = rng.integers(0, 2 ** 63, size=(n_starts, W_), dtype=np.int64).astype(np.uint64)
+    if m.K % 64:
+        starts[:, -1] &= np.uint64((1 << (m.K % 64)) - 1)
+    if m.K == 0:
+        starts[:] = 0
+    st_ = torch.from_numpy(starts.view(np.int64).copy()).cuda()
+    keys = torch.empty((n_starts, 5), dtype=torch.int64, device="cuda")
+    rounds = torch.empty(n_starts, dtype=torch.int32, device="cuda")
+    ctx.descend(pt, st_, n_starts, ends=st_, keys=keys, rounds=rounds, max_rounds=max_rounds)
+    ends = st_.cpu().numpy().view(np.uint64)
+    ks = keys.cpu().numpy().view(chm.BEST_DTYPE).reshape(-1)
+    for i in range(n_starts):
+        oe, okey, orr = O.descend(m, starts[i, :m.W] if m.W else np.zeros(0, np.uint64), max_rounds=max_rounds,
+                                  nthreads=2)
+        assert np.array_equal(ends[i, :m.W], oe[:m.W]) and int(rounds.cpu()[i]) == orr
+        assert (int(ks[i]["excess"]), float(ks[i]["stall"]), int(ks[i]["swapped_bytes"])) == okey
