@@ -296,8 +296,10 @@ __global__ void __launch_bounds__(kEvalThreads, CHM_EVAL_MINB) replay_kernel(con
     // layer l: in_l / out_l = R sums + deltas; D_l = CI(l) - CO(l) + out_l (CI / CO cumulative)
     //   = D_R(l) + sum_{l' <= l} (din_l' - dout_{l'-1}),  D_R(l) = CIR(l) - COR(l) + OUTR(l);
     // term_l = max(0, (in_l + out_l) / B - Bud_l), pairwise tree (reading R-stall).
-    // Blocked layers: lane owns E = lay_per_lane (1, 2, 4 or 8) consecutive layers E*lane + j;
-    // its partial sum, one warp scan of the lane totals, then D, peak and the terms per layer.
+    // Blocked layers: lane owns E = lay_per_lane (1, 2, 4 or 8) consecutive layers E*lane + j,
+    // held at slots (E + 1) lane + j of the padded per-layer arrays (layer_slot: an odd stride,
+    // no bank conflicts); its partial sum, one warp scan of the lane totals, then D, peak and the
+    // terms per layer.
     // The tree: 8 leaves per lane (zero past E), then the xor butterfly = the pairwise tree over
     // 256 zero-padded leaves, whose value equals R-stall's tree over the next power of two >= L.
     const int lb = kE * lane;
