@@ -965,6 +965,19 @@ def main():
         e2e_ms.append(max(ev[0].elapsed_time(ev[3]), (time.perf_counter() - t0) * 1e3))
         pt2.free()
     ok = ok and pr.intact()
+    # ---- the box's best pinned large-block copy-engine rate ("the fraction of the
+    # box's best pinned large-block cudaMemcpyAsync"): one 2 GiB copy per direction, best of 3
+    ce_big = {"d2h": 0.0, "h2d": 0.0}
+    if ctx.host_arena()[1] >= (2 << 30):
+        big = torch.empty(2 << 30, dtype=torch.uint8, device=dev)
+        s_big = torch.cuda.Stream(dev)
+        for _ in range(3):
+            for d, fn in (("d2h", ctx.swap_out), ("h2d", ctx.swap_in)):
+                b = fn([(big.data_ptr(), 0, big.numel())], comp, s_big, chm.SWAP_CE)
+                ctx.batch_wait(b, comp)
+                torch.cuda.synchronize()
+                ce_big[d] = max(ce_big[d], big.numel() / (ctx.batch_elapsed_ms(b) * 1e-3) / 1e9)
+        del big
 
     # ---- the policy's estimated stall (the models chm_stall_models evaluates), at the trace's B
     # and at the B this run's kernel measured, against the measured one: step with swaps minus
@@ -1117,6 +1130,11 @@ def main():
             "frac_of_copy_engines": ({"d2h": per_dir[0] / ce_dir[0], "h2d": per_dir[1] / ce_dir[1],
                                       "what": "vs the same batches on the copy engines (one cudaMemcpyAsync per "
                                               "tensor) under the same compute, this run"} if ce_dir else None),
+            "copy_engine_large_block_GBps": ce_big if ce_big["d2h"] else None,
+            "frac_of_copy_engine_large_block": ({"d2h": per_dir[0] / ce_big["d2h"], "h2d": per_dir[1] / ce_big["h2d"],
+                                                 "what": "vs one 2 GiB pinned cudaMemcpyAsync per direction (best of 3), "
+                                                         "the box's large-block copy-engine rate"}
+                                                if ce_big["d2h"] else None),
         },
         "roofline_replay": {
             "bound": "hbm", "kernel": "replay_kernel<%s>" % ("true" if full else "false"),
