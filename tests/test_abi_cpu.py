@@ -83,3 +83,24 @@ def test_arena_config_validation():
     assert ctx.arena_placement() == {"numa_node": -1, "mode": -1, "pin_s": 0.0}
     ctx.release_scratch()  # a host-only ctx holds no device scratch: a no-op
     assert chm.load().chm_release_scratch(None) == -1  # CHM_E_INVAL
+
+
+def test_descend_argument_and_state_errors():
+    """chm_descend checks its arguments and refuses a host-only ctx / trace (CHM_E_STATE) before
+    it touches any pointer: no CPU fallback"""
+    from workloads import traces as W
+    tr = W.tiny()
+    ctx = chm.Context(device=-1)
+    ctx.set_detailed(True)
+    chm.record_iteration(ctx, tr)
+    ctx.detect_seq_change(tr.t_iter)
+    pt = ctx.trace_build(tr.budget, tr.static_bytes, tr.bw, tr.groups_fwd, tr.groups_bwd, t_iter=tr.t_iter)
+    L = chm.load()
+    dummy = ctypes.c_void_p(16)
+    assert L.chm_descend(ctx.h, pt.h, dummy, 1, 10, dummy, dummy, None, None, None) == -3  # CHM_E_STATE
+    assert b"host-only" in L.chm_last_error()
+    assert L.chm_descend(ctx.h, pt.h, None, 1, 10, dummy, dummy, None, None, None) == -1  # CHM_E_INVAL
+    assert L.chm_descend(ctx.h, pt.h, dummy, 0, 10, dummy, dummy, None, None, None) == -1  # no starts
+    assert L.chm_descend(None, pt.h, dummy, 1, 10, dummy, dummy, None, None, None) == -1
+    with pytest.raises(chm.ChmError):
+        ctx.descend(pt, 16, 1, ends=16, keys=16)
