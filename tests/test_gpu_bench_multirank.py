@@ -40,3 +40,21 @@ def test_bench_two_ranks_functional():
     assert "gloo" in d["config"]["parallelism"] and "functional" in d["config"]["parallelism"]
     assert d["config"]["policy"]["executed_items"] == d["config"]["policy"]["items"]
     assert d["eval_strong"]["candidates_per_rank"] == d["eval_strong"]["candidates_total"] // 2
+    _check_contract(d)
+
+
+def _check_contract(d):
+    """the driver's JSON-line contract: every key it reads, with the right types"""
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
+        assert k in d, k
+    assert isinstance(d["config"]["workload"], str) and d["higher_is_better"] is True and d["scaling"] == "weak"
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in d["roofline"], k
+    assert abs(d["roofline"]["frac"] - d["roofline"]["achieved"] / d["roofline"]["peak"]) < 1e-9
+    for k in ("value", "unit", "cores", "kind", "sample"):
+        assert k in d["cpu_baseline"], k
+    assert d["cpu_baseline"]["kind"] == "oracle"
+    for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"):
+        assert k in d["e2e"], k
+    assert d["gpu_launches"] > 0
