@@ -106,7 +106,8 @@ __global__ void __launch_bounds__(kDescThreads) descend_kernel(const __grid_cons
     uint32_t round = 0;
     Key cur;
     while (true) {
-      // ---- this mask's tables: D, P, prefix / suffix max (warp 0), stall leaves (the rest)
+      // ---- this mask's tables, warp-synchronous (one CTA barrier per rebuild): warp 0 builds D,
+      // P, its prefix / suffix maxima and the sparse table, warp 1 the stall tree
       if (warp == 0) {
         long long ci = 0, co = 0, pmax = LLONG_MIN;
         for (int l0 = 0; l0 < L; l0 += 32) {
@@ -144,20 +145,22 @@ __global__ void __launch_bounds__(kDescThreads) descend_kernel(const __grid_cons
           if (l < L) SM[l] = max64(smax, m);
           smax = max64(smax, __shfl_sync(0xffffffffu, m, 0));
         }
-      } else {
-        for (int l = tid - 32; l < P2; l += blockDim.x - 32)
-          tree[P2 + l] = l < L ? stall_term(IN[l] + OUT[l], p.tr, bud[l]) : 0.0;
+        __syncwarp();
+        // the sparse table of P, level by level inside the warp (no CTA barrier per level)
+        for (int it = 1; it <= p.LG; it++) {
+          const int half = 1 << (it - 1), n = L - (1 << it) + 1;
+          for (int l = lane; l < n; l += 32) ST[(it - 1) * L + l] = max64(st_at(it - 1, l), st_at(it - 1, l + half));
+          __syncwarp();
+        }
+      } else if (warp == 1) {  // the stall tree: leaves, then the pairwise levels (left + right)
+        for (int l = lane; l < P2; l += 32) tree[P2 + l] = l < L ? stall_term(IN[l] + OUT[l], p.tr, bud[l]) : 0.0;
+        __syncwarp();
+        for (int h = P2 >> 1; h >= 1; h >>= 1) {
+          for (int i = lane; i < h; i += 32) tree[h + i] = __dadd_rn(tree[2 * (h + i)], tree[2 * (h + i) + 1]);
+          __syncwarp();
+        }
       }
       __syncthreads();
-      // ---- the pairwise tree, level by level (left + right), and the sparse table of P
-      for (int it = 1, h = P2 >> 1; h >= 1 || it <= p.LG; it++, h >>= 1) {
-        for (int i = tid; i < h; i += blockDim.x) tree[h + i] = __dadd_rn(tree[2 * (h + i)], tree[2 * (h + i) + 1]);
-        if (it <= p.LG) {
-          const int half = 1 << (it - 1), n = L - (1 << it) + 1;
-          for (int l = tid; l < n; l += blockDim.x) ST[(it - 1) * L + l] = max64(st_at(it - 1, l), st_at(it - 1, l + half));
-        }
-        __syncthreads();
-      }
       const long long pk0 = PM[L - 1], sw0 = s_swapped;
       cur.excess = pk0 > p.tr.budget ? pk0 - p.tr.budget : 0;
       cur.stall = P2 > 0 ? tree[1] : 0.0;
