@@ -105,6 +105,11 @@ int main(void) {
   /* errors come back as codes with a message, never as a crash */
   chm_status bad = chm_trace_build(ctx, NULL, &t);
   printf("null params -> %d (%s)\n", bad, chm_last_error());
+  /* device-only calls on this host-only ctx: a state error, no CPU fallback */
+  uint64_t w[2] = {0, 0};
+  chm_best k[2];
+  bad = chm_descend(ctx, t, w, 1, 8, w, k, NULL, NULL, NULL);
+  printf("descend on a host-only ctx -> %d\n", bad);
   chm_trace_free(t);
   chm_destroy(ctx);
   printf("ok\n");

@@ -33,3 +33,4 @@ def test_plain_c_client(tmp_path):
     e = re.search(r"executed items (\d+) matched (\d+) actions (\d+)", out)
     assert int(g.group(1)) > 0 and int(e.group(1)) == int(e.group(2)) == int(g.group(1)) and int(e.group(3)) > 0
     assert "null params -> -1" in out
+    assert "descend on a host-only ctx -> -3" in out  # CHM_E_STATE
