@@ -264,11 +264,15 @@ def device_descend(ctx, pt, starts, dev, max_rounds: int = 4096):
     per start, every round on the device, bit-identical end points (tests/test_gpu_descend.py).
     Returns [(key, words, rounds)] in start order."""
     n = len(starts)
-    st = torch.from_numpy(np.stack([np.ascontiguousarray(w, np.uint64) for w in starts]).view(np.int64)).to(dev)
+    W = max(pt.W, 1)  # K = 0: no mask words (a one-word buffer keeps the pointers valid)
+    host = np.zeros((n, W), np.uint64)
+    for i, w in enumerate(starts):
+        host[i, :pt.W] = np.asarray(w, np.uint64)[:pt.W]
+    st = torch.from_numpy(host.view(np.int64)).to(dev)
     keys = torch.empty((n, 5), dtype=torch.int64, device=dev)
     rounds = torch.empty(n, dtype=torch.int32, device=dev)
     ctx.descend(pt, st, n, ends=st, keys=keys, max_rounds=max_rounds, rounds=rounds)
-    ends = st.cpu().numpy().view(np.uint64).reshape(n, pt.W)
+    ends = st.cpu().numpy().view(np.uint64).reshape(n, W)[:, :pt.W]
     ks = keys.cpu().numpy().view(chm.BEST_DTYPE).reshape(n)
     rs = rounds.cpu().numpy()
     return [(ks[i].copy(), ends[i].copy(), int(rs[i])) for i in range(n)]

@@ -170,3 +170,21 @@ def test_lockstep_descents_equal_one_by_one(model):
         assert int(hk["index"]) == int(k["index"]) and int(hk["peak"]) == int(k["peak"])
     ctx.close()
 
+
+
+def test_device_descend_without_swappables():
+    """K = 0: runtime.device_descend returns each start's (empty) mask and the no-swap key"""
+    from paper_2509_11076_b200.runtime import device_descend
+    from tests.helpers import make_trace
+    ins = [[], [0], [1], [], [], []]
+    outs = [[0], [1], [2], [3], [], []]
+    frees = [[], [0], [1, 2], [3], [], []]
+    tr = make_trace([0, 0, 0, 1, 1, 1], [512, 1024, 2048, 4096], ins, outs, frees, 512, 1.0, 1e9, 2048, 2, 2)
+    ctx, pt = _build(tr)
+    assert pt.K == 0 and pt.W == 0
+    (k, w, r), = device_descend(ctx, pt, [np.zeros(0, np.uint64)], torch.device(DEV))
+    assert r == 0 and w.size == 0
+    m = O.Model(tr)
+    ok = m.eval(O.MASKS, 0, 1, words=np.zeros(1, np.uint64))["best"]
+    assert _key3(k) == (int(ok.excess), float(ok.stall), int(ok.swapped))
+    ctx.close()
