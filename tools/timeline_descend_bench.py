@@ -16,7 +16,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2509_11076_b200 import chm  # noqa: E402
 from paper_2509_11076_b200.runtime import (_generate_all, _key3, default_bases, descend, descend_many,  # noqa: E402
-                                           seeded_multibase)
+                                           device_descend, seeded_multibase)
 from workloads import traces as W  # noqa: E402
 
 DEV = torch.device("cuda:0")
@@ -53,10 +53,28 @@ def main():
             lock_t.append(time.perf_counter() - t0)
         same = all(_key3(a[0]) == _key3(b[0]) and a[2] == b[2] for a, b in zip(seq, lock))
         kb = min((e[0] for e in lock), key=_key3)
+        # extra starts: the R-stall descents' end points (chm_descend), scored under the timeline
+        ext_t = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rs = device_descend(ctx, pt, [w for _, w in starts], DEV)
+            extra = []
+            for _, w, _ in rs:
+                ctx.eval_policies(pt, chm.FLIP1, pt.K, 1, best=best, base=w, stall_model=TL)
+                extra.append((best.cpu().numpy().view(chm.BEST_DTYPE)[0].copy(), np.array(w, np.uint64)))
+            lock2 = descend_many(ctx, pt, starts + extra, DEV, 4096, TL)
+            ext_t.append(time.perf_counter() - t0)
+        kb2 = min((e[0] for e in lock2), key=_key3)
         print(json.dumps({"config": name, "K": pt.K, "starts": len(starts), "rounds": [e[2] for e in lock],
                           "sequential_ms": float(np.median(seq_t)) * 1e3, "lockstep_ms": float(np.median(lock_t)) * 1e3,
                           "same_ends": same, "best_stall_s": float(kb["stall"]),
-                          "best_excess_gib": int(kb["excess"]) / 2 ** 30}), flush=True)
+                          "best_excess_gib": int(kb["excess"]) / 2 ** 30,
+                          "with_rstall_starts": {"ms": float(np.median(ext_t)) * 1e3, "rounds": [e[2] for e in lock2],
+                                                 "best_stall_s": float(kb2["stall"]),
+                                                 "best_excess_gib": int(kb2["excess"]) / 2 ** 30,
+                                                 "best_swapped_gb": int(kb2["swapped_bytes"]) / 1e9},
+                          "best_swapped_gb": int(kb["swapped_bytes"]) / 1e9}), flush=True)
         ctx.close()
 
 
